@@ -337,10 +337,12 @@ class Rng:
         self._c._fn("rng_sign")(self._h, _U64(n), _ptr(out))
         return out
 
-    def index(self, n, count=1):
-        out = np.empty(count, np.uint64)
-        self._c._fn("rng_index")(self._h, _U64(n), _U64(count), _ptr(out))
-        return out
+    def index(self, n, count=None):
+        """rng.index(n) (rng.hpp:52): an int, or an array of `count` draws."""
+        k = 1 if count is None else count
+        out = np.empty(k, np.uint64)
+        self._c._fn("rng_index")(self._h, _U64(n), _U64(k), _ptr(out))
+        return int(out[0]) if count is None else out
 
     def matrix(self, rows, cols):
         """random_matrix (test_support.hpp:52-56)."""

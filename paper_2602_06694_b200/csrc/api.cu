@@ -1,0 +1,572 @@
+// api.cu — extern "C" entry points of libnqb (include/nqb.h): context,
+// packing, layers and the forward.  ADMM entry points live in admm.cu.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace nqb {
+
+// pack.cu
+void launch_binarize(nqb_context*, const double*, double*, uint64_t, int*);
+void launch_pack_rows(nqb_context*, const double*, uint32_t, uint32_t, uint32_t*, int, int*);
+void launch_check_padding(nqb_context*, const uint32_t*, uint32_t, uint32_t, uint32_t, int*);
+void launch_unpack(nqb_context*, const uint32_t*, uint32_t, uint32_t, double*);
+void launch_bit_transpose(nqb_context*, const uint32_t*, uint32_t, uint32_t, uint32_t,
+                          uint32_t*, uint32_t);
+void launch_reconstruct(nqb_context*, const nqb_layer*, const uint32_t*, uint32_t, double*);
+void launch_rel_error(nqb_context*, const nqb_layer*, const uint32_t*, uint32_t, const double*,
+                      double*, double*, const double* = nullptr, const double* = nullptr);
+uint64_t rel_error_partial_count(const nqb_layer*);
+// forward_simt.cu
+template <typename Acc, typename In>
+void simt_gemv(nqb_context*, const nqb_layer*, const In*, Acc*);
+void simt_gemm_f64(nqb_context*, const nqb_layer*, const double*, uint32_t, double*);
+// decode.cu / prefill.cu
+void decode_gemv_f32(nqb_context*, const nqb_layer*, const float*, float*);
+void decode_gemv_f16(nqb_context*, const nqb_layer*, const __half*, __half*);
+void prefill_gemm_f16(nqb_context*, const nqb_layer*, const __half*, uint32_t, __half*);
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void fail(int code, const std::string& msg) { throw Failure{code, msg}; }
+
+void* scratch(nqb_context* ctx, int slot, size_t bytes) {
+  Scratch& s = ctx->scratch[slot];
+  if (s.bytes < bytes) {
+    if (s.ptr) NQB_CUDA(cudaFreeAsync(s.ptr, ctx->stream));
+    s.ptr = nullptr;
+    s.bytes = 0;
+    const size_t want = bytes < 256 ? 256 : bytes;
+    NQB_CUDA(cudaMallocAsync(&s.ptr, want, ctx->stream));
+    s.bytes = want;
+  }
+  return s.ptr;
+}
+
+uint16_t host_double_to_half(double x) {
+  const __half h = __float2half_rn((float)x);
+  uint16_t bits;
+  std::memcpy(&bits, &h, 2);
+  return bits;
+}
+
+double host_half_to_double(uint16_t bits) {
+  __half_raw raw;
+  raw.x = bits;
+  return (double)__half2float(__half(raw));
+}
+
+// RAII device buffer on the context stream.
+struct DevBuf {
+  nqb_context* ctx;
+  void* p = nullptr;
+  DevBuf(nqb_context* c, size_t bytes) : ctx(c) {
+    if (bytes) NQB_CUDA(cudaMallocAsync(&p, bytes, ctx->stream));
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, ctx->stream);
+  }
+  template <typename T>
+  T* as() const { return (T*)p; }
+};
+
+// Device-side flag word read back synchronously.
+struct Flags {
+  nqb_context* ctx;
+  int* d;
+  explicit Flags(nqb_context* c) : ctx(c) {
+    d = (int*)scratch(ctx, 7, 64);
+    NQB_CUDA(cudaMemsetAsync(d, 0, sizeof(int), ctx->stream));
+  }
+  int read() {
+    int h = 0;
+    NQB_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return h;
+  }
+};
+
+void check_ctx(nqb_context* ctx) {
+  NQB_REQUIRE(ctx != nullptr, NQB_E_VALIDATION, "null context");
+  NQB_CUDA(cudaSetDevice(ctx->device));
+}
+
+void check_layer(const nqb_layer* L) {
+  NQB_REQUIRE(L != nullptr, NQB_E_VALIDATION, "null layer");
+}
+
+}  // namespace nqb
+
+using namespace nqb;
+
+#define API_BEGIN try {
+#define API_END                   \
+  return NQB_OK;                  \
+  }                               \
+  catch (const Failure& f) {      \
+    set_error(f.msg);             \
+    return f.code;                \
+  }                               \
+  catch (const std::exception& e) { \
+    set_error(e.what());          \
+    return NQB_E_INTERNAL;        \
+  }
+
+extern "C" {
+
+int nqb_status_kind(int status) {
+  if (status == NQB_OK) return 0;
+  if (status < 32) return 1;
+  if (status < 64) return 2;
+  return 3;
+}
+
+const char* nqb_last_error(void) { return g_last_error.c_str(); }
+
+const char* nqb_version(void) {
+#ifdef NQB_GIT_DESCRIBE
+  return "libnqb sm_100a " NQB_GIT_DESCRIBE;
+#else
+  return "libnqb sm_100a";
+#endif
+}
+
+int nqb_create(int device, nqb_context** out) {
+  API_BEGIN
+  NQB_REQUIRE(out != nullptr, NQB_E_VALIDATION, "null output");
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    fail(NQB_E_NO_DEVICE, "no CUDA device: libnqb has no CPU path");
+  }
+  NQB_REQUIRE(device >= 0 && device < count, NQB_E_NO_DEVICE, "device index out of range");
+  NQB_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  NQB_CUDA(cudaGetDeviceProperties(&prop, device));
+  NQB_REQUIRE(prop.major == 10, NQB_E_NO_DEVICE,
+              std::string("libnqb needs an sm_100 (B200) device, found ") + prop.name);
+  auto* ctx = new nqb_context();
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  NQB_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+  ctx->stream = ctx->own_stream;
+  NQB_CUDA(cudaMalloc(&ctx->barrier, 64 * sizeof(unsigned)));
+  NQB_CUDA(cudaMemset(ctx->barrier, 0, 64 * sizeof(unsigned)));
+  NQB_CUDA(cudaEventCreate(&ctx->ev0));
+  NQB_CUDA(cudaEventCreate(&ctx->ev1));
+  *out = ctx;
+  API_END
+}
+
+int nqb_destroy(nqb_context* ctx) {
+  API_BEGIN
+  if (!ctx) return NQB_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& s : ctx->scratch)
+    if (s.ptr) cudaFree(s.ptr);
+  if (ctx->barrier) cudaFree(ctx->barrier);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  API_END
+}
+
+int nqb_set_stream(nqb_context* ctx, void* stream) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  API_END
+}
+
+void* nqb_get_stream(nqb_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int nqb_synchronize(nqb_context* ctx) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+uint64_t nqb_kernel_launches(const nqb_context* ctx) { return ctx ? ctx->launches : 0; }
+
+// storage.cpp:124-141 (host arithmetic; no device work).
+int nqb_rank_for_target_bpw(uint64_t n, uint64_t m, double t, uint32_t* rank) {
+  API_BEGIN
+  NQB_REQUIRE(n > 0 && m > 0, NQB_E_VALIDATION, "layer dims must be positive");
+  NQB_REQUIRE(t > 0.0, NQB_E_TARGET_TOO_SMALL, "target BPW must be positive");
+  const double nm = (double)n * (double)m;
+  const long long rounded = std::llround(t * nm / (double)(n + m) - 16.0);
+  if (rounded < 1) {
+    const double bpw1 = (double)(17 * (n + m)) / (double)(n * m);
+    NQB_REQUIRE(!(bpw1 > 2.0 * t), NQB_E_TARGET_TOO_SMALL,
+                "even rank 1 overshoots the target by more than 2x");
+    *rank = 1;
+    return NQB_OK;
+  }
+  const uint64_t cap = n < m ? n : m;
+  *rank = (uint32_t)((uint64_t)rounded < cap ? (uint64_t)rounded : cap);
+  API_END
+}
+
+// ---------------------------------------------------------------------------
+// binarize / pack / unpack
+// ---------------------------------------------------------------------------
+int nqb_binarize(nqb_context* ctx, const double* latent, uint64_t count, double* out,
+                 int on_device) {
+  API_BEGIN
+  check_ctx(ctx);
+  Flags flags(ctx);
+  if (on_device) {
+    launch_binarize(ctx, latent, out, count, flags.d);
+  } else {
+    DevBuf buf(ctx, 2 * count * sizeof(double));
+    double* din = buf.as<double>();
+    NQB_CUDA(cudaMemcpyAsync(din, latent, count * 8, cudaMemcpyHostToDevice, ctx->stream));
+    launch_binarize(ctx, din, din + count, count, flags.d);
+    NQB_CUDA(cudaMemcpyAsync(out, din + count, count * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  NQB_REQUIRE(!(flags.read() & 1), NQB_E_NON_FINITE_INPUT, "binarize: non-finite input");
+  API_END
+}
+
+static int pack_impl(nqb_context* ctx, const double* in, uint32_t rows, uint32_t cols,
+                     uint32_t* words, int on_device, int latent) {
+  API_BEGIN
+  check_ctx(ctx);
+  Flags flags(ctx);
+  const uint64_t elems = (uint64_t)rows * cols;
+  const uint64_t nwords = (uint64_t)rows * ceil_div(cols, 32);
+  if (on_device) {
+    launch_pack_rows(ctx, in, rows, cols, words, latent, flags.d);
+  } else {
+    DevBuf buf(ctx, elems * 8 + nwords * 4);
+    double* din = buf.as<double>();
+    uint32_t* dw = (uint32_t*)(din + elems);
+    NQB_CUDA(cudaMemcpyAsync(din, in, elems * 8, cudaMemcpyHostToDevice, ctx->stream));
+    launch_pack_rows(ctx, din, rows, cols, dw, latent, flags.d);
+    NQB_CUDA(cudaMemcpyAsync(words, dw, nwords * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  const int f = flags.read();
+  NQB_REQUIRE(!(f & 1), NQB_E_NON_FINITE_INPUT, "pack: non-finite latent");
+  NQB_REQUIRE(!(f & 2), NQB_E_NON_BINARY_ENTRY, "pack_signs: entries must be exactly +-1");
+  API_END
+}
+
+int nqb_pack_signs(nqb_context* ctx, const double* signs, uint32_t rows, uint32_t cols,
+                   uint32_t* words, int on_device) {
+  return pack_impl(ctx, signs, rows, cols, words, on_device, 0);
+}
+
+int nqb_pack_latent(nqb_context* ctx, const double* latent, uint32_t rows, uint32_t cols,
+                    uint32_t* words, int on_device) {
+  return pack_impl(ctx, latent, rows, cols, words, on_device, 1);
+}
+
+int nqb_unpack_signs(nqb_context* ctx, const uint32_t* words, uint32_t rows, uint32_t cols,
+                     double* signs, int on_device) {
+  API_BEGIN
+  check_ctx(ctx);
+  Flags flags(ctx);
+  const uint32_t wpr = ceil_div(cols, 32);
+  const uint64_t elems = (uint64_t)rows * cols, nwords = (uint64_t)rows * wpr;
+  if (on_device) {
+    launch_check_padding(ctx, words, rows, cols, wpr, flags.d);
+    NQB_REQUIRE(!(flags.read() & 4), NQB_E_CORRUPT_PADDING, "padding bits beyond cols are set");
+    launch_unpack(ctx, words, rows, cols, signs);
+  } else {
+    DevBuf buf(ctx, nwords * 4 + elems * 8);
+    uint32_t* dw = buf.as<uint32_t>();
+    double* dout = (double*)(buf.as<char>() + ((nwords * 4 + 7) / 8) * 8);
+    NQB_CUDA(cudaMemcpyAsync(dw, words, nwords * 4, cudaMemcpyHostToDevice, ctx->stream));
+    launch_check_padding(ctx, dw, rows, cols, wpr, flags.d);
+    NQB_REQUIRE(!(flags.read() & 4), NQB_E_CORRUPT_PADDING, "padding bits beyond cols are set");
+    launch_unpack(ctx, dw, rows, cols, dout);
+    NQB_CUDA(cudaMemcpyAsync(signs, dout, elems * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  API_END
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Layers
+// ---------------------------------------------------------------------------
+namespace nqb {
+
+// Builds a device layer from reference-layout words already on the device.
+// d_u / d_v: n x wpr and m x wpr words (row stride wpr).
+nqb_layer* layer_from_device_words(nqb_context* ctx, uint32_t n, uint32_t m, uint32_t r,
+                                   const uint32_t* d_u, const uint32_t* d_v,
+                                   const __half* d_s1h, const __half* d_s2h) {
+  const uint32_t wpr = ceil_div(r, 32);
+  auto* L = new nqb_layer();
+  L->n = n;
+  L->m = m;
+  L->r = r;
+  L->device = ctx->device;
+  L->u_words = round_up(wpr, 4);
+  L->vt_words = round_up(ceil_div(m, 32), 4);
+  try {
+    NQB_CUDA(cudaMalloc(&L->u, (size_t)n * L->u_words * 4));
+    NQB_CUDA(cudaMalloc(&L->vt, (size_t)r * L->vt_words * 4));
+    NQB_CUDA(cudaMalloc(&L->s1h, (size_t)n * 2));
+    NQB_CUDA(cudaMalloc(&L->s2h, (size_t)m * 2));
+    NQB_CUDA(cudaMemsetAsync(L->u, 0, (size_t)n * L->u_words * 4, ctx->stream));
+    NQB_CUDA(cudaMemsetAsync(L->vt, 0, (size_t)r * L->vt_words * 4, ctx->stream));
+    NQB_CUDA(cudaMemcpy2DAsync(L->u, L->u_words * 4, d_u, wpr * 4, wpr * 4, n,
+                               cudaMemcpyDeviceToDevice, ctx->stream));
+    launch_bit_transpose(ctx, d_v, m, r, wpr, L->vt, L->vt_words);
+    NQB_CUDA(cudaMemcpyAsync(L->s1h, d_s1h, (size_t)n * 2, cudaMemcpyDeviceToDevice, ctx->stream));
+    NQB_CUDA(cudaMemcpyAsync(L->s2h, d_s2h, (size_t)m * 2, cudaMemcpyDeviceToDevice, ctx->stream));
+  } catch (...) {
+    cudaFree(L->u);
+    cudaFree(L->vt);
+    cudaFree(L->s1h);
+    cudaFree(L->s2h);
+    delete L;
+    throw;
+  }
+  return L;
+}
+
+// V back to the reference orientation (m x stride words) in device memory.
+void layer_v_reference(nqb_context* ctx, const nqb_layer* L, uint32_t* d_vr, uint32_t stride) {
+  NQB_CUDA(cudaMemsetAsync(d_vr, 0, (size_t)L->m * stride * 4, ctx->stream));
+  launch_bit_transpose(ctx, L->vt, L->r, L->m, L->vt_words, d_vr, stride);
+}
+
+}  // namespace nqb
+
+extern "C" {
+
+static int upload_impl(nqb_context* ctx, uint32_t n, uint32_t m, uint32_t r,
+                       const uint32_t* u_words, const uint32_t* v_words,
+                       const uint16_t* s1h, const uint16_t* s2h, nqb_layer** out) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_REQUIRE(out != nullptr, NQB_E_VALIDATION, "null output");
+  *out = nullptr;
+  NQB_REQUIRE(n > 0 && m > 0 && r > 0, NQB_E_DIMENSION_MISMATCH, "zero layer dimension");
+  const uint32_t wpr = ceil_div(r, 32);
+  const uint32_t tail = r % 32;
+  if (tail) {  // unpack_signs' padding rule (packed.cpp:85-93), checked on upload
+    const uint32_t pad = ~0u << tail;
+    for (uint64_t i = 0; i < n; ++i)
+      NQB_REQUIRE(!(u_words[i * wpr + wpr - 1] & pad), NQB_E_CORRUPT_PADDING,
+                  "U: padding bits beyond r are set");
+    for (uint64_t j = 0; j < m; ++j)
+      NQB_REQUIRE(!(v_words[j * wpr + wpr - 1] & pad), NQB_E_CORRUPT_PADDING,
+                  "V: padding bits beyond r are set");
+  }
+  const size_t ub = (size_t)n * wpr * 4, vb = (size_t)m * wpr * 4;
+  DevBuf buf(ctx, ub + vb + 2 * (size_t)(n + m) + 16);
+  uint32_t* du = buf.as<uint32_t>();
+  uint32_t* dv = du + (size_t)n * wpr;
+  __half* ds = (__half*)(dv + (size_t)m * wpr);
+  NQB_CUDA(cudaMemcpyAsync(du, u_words, ub, cudaMemcpyHostToDevice, ctx->stream));
+  NQB_CUDA(cudaMemcpyAsync(dv, v_words, vb, cudaMemcpyHostToDevice, ctx->stream));
+  NQB_CUDA(cudaMemcpyAsync(ds, s1h, 2 * (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
+  NQB_CUDA(cudaMemcpyAsync(ds + n, s2h, 2 * (size_t)m, cudaMemcpyHostToDevice, ctx->stream));
+  *out = layer_from_device_words(ctx, n, m, r, du, dv, ds, ds + n);
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+int nqb_layer_upload_f16(nqb_context* ctx, uint32_t n, uint32_t m, uint32_t r,
+                         const uint32_t* u_words, const uint32_t* v_words,
+                         const uint16_t* s1_half, const uint16_t* s2_half, nqb_layer** out) {
+  return upload_impl(ctx, n, m, r, u_words, v_words, s1_half, s2_half, out);
+}
+
+int nqb_layer_upload(nqb_context* ctx, uint32_t n, uint32_t m, uint32_t r,
+                     const uint32_t* u_words, const uint32_t* v_words, const double* s1,
+                     const double* s2, nqb_layer** out) {
+  std::vector<uint16_t> h1(n), h2(m);
+  for (uint32_t i = 0; i < n; ++i) h1[i] = host_double_to_half(s1[i]);
+  for (uint32_t j = 0; j < m; ++j) h2[j] = host_double_to_half(s2[j]);
+  return upload_impl(ctx, n, m, r, u_words, v_words, h1.data(), h2.data(), out);
+}
+
+int nqb_layer_free(nqb_layer* L) {
+  API_BEGIN
+  if (!L) return NQB_OK;
+  cudaSetDevice(L->device);
+  cudaFree(L->u);
+  cudaFree(L->vt);
+  cudaFree(L->s1h);
+  cudaFree(L->s2h);
+  delete L;
+  API_END
+}
+
+int nqb_layer_shape(const nqb_layer* L, uint32_t* n, uint32_t* m, uint32_t* r) {
+  API_BEGIN
+  check_layer(L);
+  if (n) *n = L->n;
+  if (m) *m = L->m;
+  if (r) *r = L->r;
+  API_END
+}
+
+uint64_t nqb_layer_device_bytes(const nqb_layer* L) {
+  if (!L) return 0;
+  return (uint64_t)L->r * L->vt_words * 4 + (uint64_t)L->n * L->u_words * 4 +
+         2ull * (L->n + L->m);
+}
+
+int nqb_layer_download(nqb_context* ctx, const nqb_layer* L, uint32_t* u_words,
+                       uint32_t* v_words, double* s1, double* s2) {
+  API_BEGIN
+  check_ctx(ctx);
+  check_layer(L);
+  const uint32_t wpr = ceil_div(L->r, 32);
+  if (u_words) {
+    NQB_CUDA(cudaMemcpy2DAsync(u_words, wpr * 4, L->u, L->u_words * 4, wpr * 4, L->n,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (v_words) {
+    DevBuf buf(ctx, (size_t)L->m * wpr * 4);
+    layer_v_reference(ctx, L, buf.as<uint32_t>(), wpr);
+    NQB_CUDA(cudaMemcpyAsync(v_words, buf.p, (size_t)L->m * wpr * 4, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  if (s1 || s2) {
+    std::vector<uint16_t> h1(L->n), h2(L->m);
+    NQB_CUDA(cudaMemcpyAsync(h1.data(), L->s1h, 2 * (size_t)L->n, cudaMemcpyDeviceToHost, ctx->stream));
+    NQB_CUDA(cudaMemcpyAsync(h2.data(), L->s2h, 2 * (size_t)L->m, cudaMemcpyDeviceToHost, ctx->stream));
+    NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (s1)
+      for (uint32_t i = 0; i < L->n; ++i) s1[i] = host_half_to_double(h1[i]);
+    if (s2)
+      for (uint32_t j = 0; j < L->m; ++j) s2[j] = host_half_to_double(h2[j]);
+  }
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+// ---------------------------------------------------------------------------
+// Forward
+// ---------------------------------------------------------------------------
+int nqb_gemv_f32_device(nqb_context* ctx, const nqb_layer* L, const float* d_x, float* d_y) {
+  API_BEGIN
+  check_layer(L);
+  decode_gemv_f32(ctx, L, d_x, d_y);
+  API_END
+}
+
+int nqb_gemv_f16_device(nqb_context* ctx, const nqb_layer* L, const uint16_t* d_x,
+                        uint16_t* d_y) {
+  API_BEGIN
+  check_layer(L);
+  decode_gemv_f16(ctx, L, (const __half*)d_x, (__half*)d_y);
+  API_END
+}
+
+int nqb_gemv_f32_host(nqb_context* ctx, const nqb_layer* L, const float* x, float* y) {
+  API_BEGIN
+  check_ctx(ctx);
+  check_layer(L);
+  DevBuf buf(ctx, 4 * ((size_t)L->m + L->n));
+  float* dx = buf.as<float>();
+  float* dy = dx + L->m;
+  NQB_CUDA(cudaMemcpyAsync(dx, x, 4 * (size_t)L->m, cudaMemcpyHostToDevice, ctx->stream));
+  decode_gemv_f32(ctx, L, dx, dy);
+  NQB_CUDA(cudaMemcpyAsync(y, dy, 4 * (size_t)L->n, cudaMemcpyDeviceToHost, ctx->stream));
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+int nqb_gemv_f64_host(nqb_context* ctx, const nqb_layer* L, const double* x, double* y) {
+  API_BEGIN
+  check_ctx(ctx);
+  check_layer(L);
+  DevBuf buf(ctx, 8 * ((size_t)L->m + L->n));
+  double* dx = buf.as<double>();
+  double* dy = dx + L->m;
+  NQB_CUDA(cudaMemcpyAsync(dx, x, 8 * (size_t)L->m, cudaMemcpyHostToDevice, ctx->stream));
+  simt_gemv<double, double>(ctx, L, dx, dy);
+  NQB_CUDA(cudaMemcpyAsync(y, dy, 8 * (size_t)L->n, cudaMemcpyDeviceToHost, ctx->stream));
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+int nqb_gemm_f64_host(nqb_context* ctx, const nqb_layer* L, const double* x, uint32_t b,
+                      double* y) {
+  API_BEGIN
+  check_ctx(ctx);
+  check_layer(L);
+  if (b == 0) return NQB_OK;
+  const size_t xb = (size_t)L->m * b * 8, yb = (size_t)L->n * b * 8;
+  DevBuf buf(ctx, xb + yb);
+  double* dx = buf.as<double>();
+  double* dy = dx + (size_t)L->m * b;
+  NQB_CUDA(cudaMemcpyAsync(dx, x, xb, cudaMemcpyHostToDevice, ctx->stream));
+  simt_gemm_f64(ctx, L, dx, b, dy);
+  NQB_CUDA(cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, ctx->stream));
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+int nqb_gemm_f16_device(nqb_context* ctx, const nqb_layer* L, const uint16_t* d_x, uint32_t b,
+                        uint16_t* d_y) {
+  API_BEGIN
+  check_ctx(ctx);
+  check_layer(L);
+  if (b == 0) return NQB_OK;
+  prefill_gemm_f16(ctx, L, (const __half*)d_x, b, (__half*)d_y);
+  API_END
+}
+
+int nqb_reconstruct_dense_host(nqb_context* ctx, const nqb_layer* L, double* w) {
+  API_BEGIN
+  check_ctx(ctx);
+  check_layer(L);
+  const uint32_t wpr = ceil_div(L->r, 32);
+  const size_t wb = (size_t)L->n * L->m * 8;
+  DevBuf buf(ctx, wb + (size_t)L->m * L->u_words * 4);
+  double* dw = buf.as<double>();
+  uint32_t* dvr = (uint32_t*)(dw + (size_t)L->n * L->m);
+  layer_v_reference(ctx, L, dvr, L->u_words);
+  (void)wpr;
+  launch_reconstruct(ctx, L, dvr, L->u_words, dw);
+  NQB_CUDA(cudaMemcpyAsync(w, dw, wb, cudaMemcpyDeviceToHost, ctx->stream));
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+int nqb_layer_rel_error(nqb_context* ctx, const nqb_layer* L, const double* w, int on_device,
+                        double* rel_error) {
+  API_BEGIN
+  check_ctx(ctx);
+  check_layer(L);
+  const size_t wb = on_device ? 0 : (size_t)L->n * L->m * 8;
+  const uint64_t parts = rel_error_partial_count(L);
+  DevBuf buf(ctx, wb + (size_t)L->m * L->u_words * 4 + parts * 16 + 64);
+  char* base = buf.as<char>();
+  const double* dw = on_device ? w : (const double*)base;
+  if (!on_device) {
+    NQB_CUDA(cudaMemcpyAsync((void*)dw, w, wb, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  double* part = (double*)(base + wb);
+  double* sums = part + 2 * parts;
+  uint32_t* dvr = (uint32_t*)(sums + 2);
+  layer_v_reference(ctx, L, dvr, L->u_words);
+  launch_rel_error(ctx, L, dvr, L->u_words, dw, part, sums);
+  double h[2];
+  NQB_CUDA(cudaMemcpyAsync(h, sums, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double num = std::sqrt(h[0]), den = std::sqrt(h[1]);
+  *rel_error = den == 0.0 ? (num == 0.0 ? 0.0 : INFINITY) : num / den;
+  API_END
+}
+
+}  // extern "C"

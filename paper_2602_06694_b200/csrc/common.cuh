@@ -1,0 +1,154 @@
+// common.cuh — shared internals of libnqb (B200 / sm_100a only).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "nqb.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libnqb is written for sm_100a (B200) only"
+#endif
+
+namespace nqb {
+
+// ---------------------------------------------------------------------------
+// Status plumbing: every C-ABI entry point catches nqb::Failure and returns
+// its code; the message goes to a thread-local buffer (nqb_last_error).
+// ---------------------------------------------------------------------------
+struct Failure {
+  int code;
+  std::string msg;
+};
+
+void set_error(const std::string& msg);
+[[noreturn]] void fail(int code, const std::string& msg);
+
+#define NQB_CUDA(call)                                                           \
+  do {                                                                           \
+    cudaError_t e_ = (call);                                                     \
+    if (e_ != cudaSuccess) {                                                     \
+      ::nqb::fail(e_ == cudaErrorMemoryAllocation ? NQB_E_OUT_OF_MEMORY : NQB_E_CUDA, \
+                  std::string(#call) + ": " + cudaGetErrorString(e_) + " @" +    \
+                      __FILE__ + ":" + std::to_string(__LINE__));                \
+    }                                                                            \
+  } while (0)
+
+#define NQB_REQUIRE(cond, code, msg) \
+  do {                               \
+    if (!(cond)) ::nqb::fail(code, msg); \
+  } while (0)
+
+// Kernel launch bookkeeping: every kernel launch goes through NQB_LAUNCHED so
+// the context counts them (nqb_kernel_launches; bench.py reports it).
+#define NQB_LAUNCHED(ctx)                                   \
+  do {                                                      \
+    NQB_CUDA(cudaGetLastError());                           \
+    (ctx)->launches++;                                      \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Device scratch arena owned by a context (grows, never shrinks).
+// ---------------------------------------------------------------------------
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace nqb
+
+struct nqb_context {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;     // active stream
+  cudaStream_t own_stream = nullptr;  // created by nqb_create
+  uint64_t launches = 0;
+  nqb::Scratch scratch[16];
+  unsigned* barrier = nullptr;  // grid-barrier words (zeroed), 64 entries
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+// Device-resident factorized layer.  Layout:
+//   vt  : r rows x vt_words u32 — V^T, bit (k, j) = sign of V[j][k]; row k is
+//         all m inputs, LSB-first, zero padded to a 16-byte row multiple
+//   u   : n rows x u_words u32  — U as in the reference (bits along r), rows
+//         padded to 16 bytes
+//   s1h : n binary16, s2h : m binary16
+struct nqb_layer {
+  uint32_t n = 0, m = 0, r = 0;
+  uint32_t vt_words = 0;  // words per V^T row (multiple of 4)
+  uint32_t u_words = 0;   // words per U row (multiple of 4)
+  uint32_t* vt = nullptr;
+  uint32_t* u = nullptr;
+  __half* s1h = nullptr;
+  __half* s2h = nullptr;
+  int device = 0;
+};
+
+namespace nqb {
+
+// Returns a device buffer of at least `bytes` from slot `slot` of the arena.
+void* scratch(nqb_context* ctx, int slot, size_t bytes);
+
+inline uint32_t ceil_div(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
+inline uint32_t round_up(uint32_t a, uint32_t b) { return (a + b - 1) / b * b; }
+
+// IEEE binary16 RNE from double via float (same rounding chain as the
+// reference's double_to_half: double -> float (RNE) -> half (RNE)).
+uint16_t host_double_to_half(double x);
+double host_half_to_double(uint16_t h);
+
+// ---------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum with a fixed reduction tree (deterministic).  `red` must hold
+// blockDim.x/32 elements.  Result is broadcast to every thread.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T s = T(0);
+  for (int w = 0; w < nw; ++w) s += red[w];  // same order in every thread
+  return s;
+}
+
+// Sense-reversing software grid barrier for persistent kernels whose grid is
+// sized to be fully co-resident (launched with cudaLaunchCooperativeKernel).
+// bar[0] = arrival count, bar[1] = generation.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned gen = *vgen;
+    __threadfence();
+    const unsigned arrived = atomicAdd(bar, 1u);
+    if (arrived == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicExch(bar + 1, gen + 1u);
+    } else {
+      while (*vgen == gen) {
+        __nanosleep(32);
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+}  // namespace nqb

@@ -1,0 +1,297 @@
+// pack.cu — sign binarisation, packing, unpacking and the device bit layout.
+//
+// Reference semantics (packed.cpp):
+//   binarize      :51-58   x < 0 ? -1 : +1 (so -0.0 -> +1); NonFiniteInput
+//   pack_signs    :60-78   LSB-first u32 words, 1 <=> +1; NonBinaryEntry
+//   unpack_signs  :80-103  inverse; CorruptPadding when pad bits are set
+//   reconstruct   :126-149 W^_ij = s1_i (2 popc(~(u_i ^ v_j) & mask) - r) s2_j
+//
+// Device layout of a layer: U keeps the reference orientation
+// (bits along r, rows padded to 16 B) because the decode stage 2 streams U by
+// rows; V is stored TRANSPOSED (V^T: r rows of m bits) so decode stage 1 also
+// streams contiguous rows.  The transposition is a warp-ballot 32x32 bit
+// transpose, so upload/download are bit-exact inverses.
+#include "common.cuh"
+
+namespace nqb {
+
+// ---------------------------------------------------------------------------
+// binarize / pack / unpack
+// ---------------------------------------------------------------------------
+__global__ void k_binarize(const double* __restrict__ in, double* __restrict__ out, uint64_t n,
+                           int* __restrict__ flags) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double x = in[i];
+    if (!isfinite(x)) atomicOr(flags, 1);
+    out[i] = x < 0.0 ? -1.0 : 1.0;
+  }
+}
+
+// One warp per (row, word).  latent != 0: bit = !(x < 0) (binarize fused);
+// latent == 0: exact +-1 required (pack_signs).  flags bit0 = non-finite,
+// bit1 = non-binary.
+__global__ void k_pack_rows(const double* __restrict__ in, uint32_t rows, uint32_t cols,
+                            uint32_t wpr, uint32_t* __restrict__ words, int latent,
+                            int* __restrict__ flags) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint64_t total = (uint64_t)rows * wpr;
+  for (uint64_t wi = warp; wi < total; wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint64_t row = wi / wpr;
+    const uint32_t w = (uint32_t)(wi % wpr);
+    const uint32_t j = w * 32 + lane;
+    bool bit = false;
+    if (j < cols) {
+      const double x = in[row * cols + j];
+      if (latent) {
+        if (!isfinite(x)) atomicOr(flags, 1);
+        bit = !(x < 0.0);
+      } else {
+        if (x == 1.0) bit = true;
+        else if (x != -1.0) atomicOr(flags, 2);
+      }
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, bit);
+    if (lane == 0) words[row * wpr + w] = word;
+  }
+}
+
+__global__ void k_check_padding(const uint32_t* __restrict__ words, uint32_t rows, uint32_t wpr,
+                                uint32_t stride, uint32_t pad_mask, int* __restrict__ flags) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+       i += gridDim.x * blockDim.x) {
+    if (words[(uint64_t)i * stride + wpr - 1] & pad_mask) atomicOr(flags, 4);
+  }
+}
+
+__global__ void k_unpack(const uint32_t* __restrict__ words, uint32_t rows, uint32_t cols,
+                         uint32_t wpr, double* __restrict__ out) {
+  const uint64_t total = (uint64_t)rows * cols;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = e / cols;
+    const uint32_t j = (uint32_t)(e % cols);
+    out[e] = (words[i * wpr + j / 32] >> (j % 32)) & 1u ? 1.0 : -1.0;
+  }
+}
+
+// 32x32 bit-tile transpose with warp ballots.
+//   src: src_rows x src_stride words, bit (i, c) = column c of row i
+//   dst: dst_rows x dst_stride words, bit (c, i) = src bit (i, c)
+// dst_rows = number of valid columns in src (c < src_cols); rows of src beyond
+// src_rows contribute zero bits (padding stays zero).
+__global__ void k_bit_transpose(const uint32_t* __restrict__ src, uint32_t src_rows,
+                                uint32_t src_words, uint32_t src_stride, uint32_t src_cols,
+                                uint32_t* __restrict__ dst, uint32_t dst_stride,
+                                uint32_t dst_words) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps_per_block = blockDim.x >> 5;
+  const uint32_t row_tiles = dst_words;  // 32-row groups of src = words of dst rows
+  const uint64_t tiles = (uint64_t)row_tiles * src_words;
+  for (uint64_t t = blockIdx.x * (uint64_t)warps_per_block + (threadIdx.x >> 5); t < tiles;
+       t += (uint64_t)gridDim.x * warps_per_block) {
+    const uint32_t rt = (uint32_t)(t / src_words);  // which 32 src rows
+    const uint32_t w = (uint32_t)(t % src_words);   // which src word column
+    const uint32_t i = rt * 32 + lane;
+    const uint32_t word = (i < src_rows) ? src[(uint64_t)i * src_stride + w] : 0u;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+      const uint32_t col = __ballot_sync(0xffffffffu, (word >> b) & 1u);
+      if ((int)lane == b) mine = col;
+    }
+    const uint32_t c = w * 32 + lane;
+    if (c < src_cols) dst[(uint64_t)c * dst_stride + rt] = mine;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// reconstruct_dense and relative error (packed.cpp:126-149, dense.cpp:141-146)
+// ---------------------------------------------------------------------------
+// vr: V in reference orientation (m rows x stride words along r).
+// If w_ref != nullptr, accumulates per-block sum((W - W^)^2) and sum(W^2)
+// into partial[2*block + {0,1}] and does not write the dense matrix.
+template <bool kError>
+__global__ void __launch_bounds__(256) k_reconstruct(
+    const uint32_t* __restrict__ u, const uint32_t* __restrict__ vr, uint32_t stride,
+    uint32_t n, uint32_t m, uint32_t r, const __half* __restrict__ s1h,
+    const __half* __restrict__ s2h, double* __restrict__ w_out,
+    const double* __restrict__ w_ref, double* __restrict__ partial,
+    const double* __restrict__ s1d, const double* __restrict__ s2d) {
+  __shared__ uint32_t us[16][64 + 1];
+  __shared__ uint32_t vs[16][64 + 1];
+  __shared__ double red[2][8];
+  const uint32_t tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const uint32_t i = blockIdx.y * 16 + ty, j = blockIdx.x * 16 + tx;
+  const uint32_t wpr = (r + 31) / 32;
+  const uint32_t tail = r % 32;
+  int agree = 0;
+  for (uint32_t w0 = 0; w0 < wpr; w0 += 64) {
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < 16 * 64; e += 256) {
+      const uint32_t rr = e / 64, ww = e % 64;
+      const uint32_t gi = blockIdx.y * 16 + rr, gj = blockIdx.x * 16 + rr;
+      us[rr][ww] = (gi < n && w0 + ww < wpr) ? u[(uint64_t)gi * stride + w0 + ww] : 0u;
+      vs[rr][ww] = (gj < m && w0 + ww < wpr) ? vr[(uint64_t)gj * stride + w0 + ww] : 0u;
+    }
+    __syncthreads();
+    const uint32_t lim = min(64u, wpr - w0);
+    for (uint32_t ww = 0; ww < lim; ++ww) {
+      uint32_t same = ~(us[ty][ww] ^ vs[tx][ww]);
+      if (w0 + ww + 1 == wpr && tail != 0) same &= (1u << tail) - 1u;
+      agree += __popc(same);
+    }
+  }
+  double err = 0.0, ref = 0.0;
+  if (i < n && j < m) {
+    const long long inner = 2LL * agree - (long long)r;
+    // fp64 scales when given (the pipeline's metric, pipeline.cpp:152-153, is
+    // taken before the binary16 snap), else the stored binary16 scales.
+    const double a = s1d ? s1d[i] : (double)__half2float(s1h[i]);
+    const double b = s2d ? s2d[j] : (double)__half2float(s2h[j]);
+    const double v = a * (double)inner * b;
+    if (kError) {
+      const double x = w_ref[(uint64_t)i * m + j];
+      const double d = x - v;
+      err = d * d;
+      ref = x * x;
+    } else {
+      w_out[(uint64_t)i * m + j] = v;
+    }
+  }
+  if (kError) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    err = warp_sum(err);
+    ref = warp_sum(ref);
+    if (lane == 0) {
+      red[0][wid] = err;
+      red[1][wid] = ref;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0, b = 0.0;
+      for (int k = 0; k < 8; ++k) {
+        a += red[0][k];
+        b += red[1][k];
+      }
+      const uint64_t blk = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
+      partial[2 * blk] = a;
+      partial[2 * blk + 1] = b;
+    }
+  }
+}
+
+// Deterministic final sum of `count` pairs (single block).
+__global__ void k_sum_pairs(const double* __restrict__ partial, uint64_t count,
+                            double* __restrict__ out) {
+  __shared__ double red[2][32];
+  double a = 0.0, b = 0.0;
+  for (uint64_t k = threadIdx.x; k < count; k += blockDim.x) {
+    a += partial[2 * k];
+    b += partial[2 * k + 1];
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = a;
+    red[1][wid] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      x += red[0][k];
+      y += red[1][k];
+    }
+    out[0] = x;
+    out[1] = y;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host-side helpers used by api.cu
+// ---------------------------------------------------------------------------
+static int grid_for(nqb_context* ctx, uint64_t work, int block) {
+  const uint64_t want = (work + block - 1) / block;
+  const uint64_t cap = (uint64_t)ctx->num_sms * 16;
+  return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+void launch_binarize(nqb_context* ctx, const double* d_in, double* d_out, uint64_t n,
+                     int* d_flags) {
+  if (n == 0) return;
+  k_binarize<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(d_in, d_out, n, d_flags);
+  NQB_LAUNCHED(ctx);
+}
+
+void launch_pack_rows(nqb_context* ctx, const double* d_in, uint32_t rows, uint32_t cols,
+                      uint32_t* d_words, int latent, int* d_flags) {
+  const uint32_t wpr = ceil_div(cols, 32);
+  const uint64_t warps = (uint64_t)rows * wpr;
+  if (warps == 0) return;
+  k_pack_rows<<<grid_for(ctx, warps * 32, 256), 256, 0, ctx->stream>>>(d_in, rows, cols, wpr,
+                                                                       d_words, latent, d_flags);
+  NQB_LAUNCHED(ctx);
+}
+
+void launch_check_padding(nqb_context* ctx, const uint32_t* d_words, uint32_t rows,
+                          uint32_t cols, uint32_t stride, int* d_flags) {
+  const uint32_t tail = cols % 32;
+  if (tail == 0 || rows == 0) return;
+  const uint32_t wpr = ceil_div(cols, 32);
+  k_check_padding<<<grid_for(ctx, rows, 256), 256, 0, ctx->stream>>>(d_words, rows, wpr, stride,
+                                                                     ~0u << tail, d_flags);
+  NQB_LAUNCHED(ctx);
+}
+
+void launch_unpack(nqb_context* ctx, const uint32_t* d_words, uint32_t rows, uint32_t cols,
+                   double* d_out) {
+  const uint64_t total = (uint64_t)rows * cols;
+  if (total == 0) return;
+  k_unpack<<<grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(d_words, rows, cols,
+                                                               ceil_div(cols, 32), d_out);
+  NQB_LAUNCHED(ctx);
+}
+
+void launch_bit_transpose(nqb_context* ctx, const uint32_t* d_src, uint32_t src_rows,
+                          uint32_t src_cols, uint32_t src_stride, uint32_t* d_dst,
+                          uint32_t dst_stride) {
+  const uint32_t src_words = ceil_div(src_cols, 32);
+  const uint32_t dst_words = ceil_div(src_rows, 32);
+  const uint64_t tiles = (uint64_t)src_words * dst_words;
+  if (tiles == 0) return;
+  k_bit_transpose<<<grid_for(ctx, tiles * 32, 256), 256, 0, ctx->stream>>>(
+      d_src, src_rows, src_words, src_stride, src_cols, d_dst, dst_stride, dst_words);
+  NQB_LAUNCHED(ctx);
+}
+
+void launch_reconstruct(nqb_context* ctx, const nqb_layer* L, const uint32_t* d_vr,
+                        uint32_t stride, double* d_w) {
+  dim3 grid(ceil_div(L->m, 16), ceil_div(L->n, 16));
+  k_reconstruct<false><<<grid, 256, 0, ctx->stream>>>(L->u, d_vr, stride, L->n, L->m, L->r,
+                                                      L->s1h, L->s2h, d_w, nullptr, nullptr,
+                                                      nullptr, nullptr);
+  NQB_LAUNCHED(ctx);
+}
+
+// Returns (sum (W - W^)^2, sum W^2) into d_out2 (device, 2 doubles).  With
+// d_s1 / d_s2 (fp64, device) the scales are taken from there instead.
+void launch_rel_error(nqb_context* ctx, const nqb_layer* L, const uint32_t* d_vr,
+                      uint32_t stride, const double* d_w, double* d_partial, double* d_out2,
+                      const double* d_s1, const double* d_s2) {
+  dim3 grid(ceil_div(L->m, 16), ceil_div(L->n, 16));
+  k_reconstruct<true><<<grid, 256, 0, ctx->stream>>>(L->u, d_vr, stride, L->n, L->m, L->r,
+                                                     L->s1h, L->s2h, nullptr, d_w, d_partial,
+                                                     d_s1, d_s2);
+  NQB_LAUNCHED(ctx);
+  k_sum_pairs<<<1, 1024, 0, ctx->stream>>>(d_partial, (uint64_t)grid.x * grid.y, d_out2);
+  NQB_LAUNCHED(ctx);
+}
+
+uint64_t rel_error_partial_count(const nqb_layer* L) {
+  return (uint64_t)ceil_div(L->m, 16) * ceil_div(L->n, 16);
+}
+
+}  // namespace nqb

@@ -1,0 +1,636 @@
+"""Host-side mirror of the NanoQuant reference API for the BLR hot path.
+
+Same names, argument meaning and error behaviour as the reference C++ value
+API (``namespace nanoquant``), every call executed on the B200 through the C ABI
+of libnqb (include/nqb.h):
+
+  packed.hpp:49-102    binarize, pack_signs, unpack_signs, make_factorized_layer,
+                       reconstruct_dense, gemv_packed, gemv_packed_f32, gemm_packed
+  storage.hpp:82-91    rank_for_target_bpw
+  linalg.hpp:35-51     cholesky_solve, top_singular_pair, spectral_norm_estimate,
+                       truncated_svd_factors
+  admm.hpp:30-85       svid, admm_factor_solve, augmented_lagrangian,
+                       admm_factorize, monotone_rho
+  balance.hpp:38-41    balance_and_extract_scales
+  errors.hpp:25-114    Error and its subclasses (raised from nqb status codes)
+
+Matrices are numpy float64 arrays (the reference DenseMatrix is row-major fp64);
+packed sign matrices are uint32 arrays of shape (rows, ceil(cols/32)) in the
+reference PackedBitMatrix layout.  There is no CPU path: every function needs
+libnqb.so and a B200.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+
+# ---------------------------------------------------------------------------
+# errors.hpp:25-114
+# ---------------------------------------------------------------------------
+KIND_VALIDATION = "validation"
+KIND_NUMERICAL = "numerical"
+KIND_RUNTIME = "runtime"
+
+
+class Error(RuntimeError):
+    """nanoquant::Error; `kind` is validation / numerical (CLI exit 2 / 3)."""
+
+    kind = KIND_VALIDATION
+    code = 9
+
+    def __init__(self, what: str = "", code: Optional[int] = None):
+        super().__init__(what)
+        if code is not None:
+            self.code = code
+
+
+class DimensionMismatch(Error):
+    code = 1
+
+
+class NonFiniteInput(Error):
+    code = 2
+
+
+class NonBinaryEntry(Error):
+    code = 3
+
+
+class CorruptPadding(Error):
+    code = 4
+
+
+class RankTooLarge(Error):
+    code = 5
+
+
+class InvalidRank(Error):
+    code = 6
+
+
+class NotSymmetric(Error):
+    code = 7
+
+
+class TargetTooSmall(Error):
+    code = 8
+
+
+class ParseError(Error):
+    code = 10
+
+
+class IoError(Error):
+    code = 11
+
+
+class ZeroMatrix(Error):
+    kind = KIND_NUMERICAL
+    code = 32
+
+
+class NotPositiveDefinite(Error):
+    kind = KIND_NUMERICAL
+    code = 33
+
+
+class DeviceError(Error):
+    """CUDA / allocation / missing-device failures (no reference counterpart)."""
+
+    kind = KIND_RUNTIME
+    code = 64
+
+
+_BY_CODE = {cls.code: cls for cls in (DimensionMismatch, NonFiniteInput, NonBinaryEntry,
+                                       CorruptPadding, RankTooLarge, InvalidRank,
+                                       NotSymmetric, TargetTooSmall, ParseError, IoError,
+                                       ZeroMatrix, NotPositiveDefinite)}
+
+
+def _check(status: int, where: str):
+    if status == 0:
+        return
+    msg = L.load().nqb_last_error().decode(errors="replace")
+    cls = _BY_CODE.get(status)
+    if cls is None:
+        cls = Error if status == 9 else DeviceError
+    raise cls(f"{where}: {msg}", code=status)
+
+
+# ---------------------------------------------------------------------------
+# Context
+# ---------------------------------------------------------------------------
+class Context:
+    """One device, one stream, the library's workspaces (nqb_context)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = L.load()
+        h = C.c_void_p()
+        _check(self.lib.nqb_create(device, C.byref(h)), "nqb_create")
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            self.lib.nqb_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int | None):
+        _check(self.lib.nqb_set_stream(self.handle, C.c_void_p(stream_ptr or 0)),
+               "nqb_set_stream")
+
+    def synchronize(self):
+        _check(self.lib.nqb_synchronize(self.handle), "nqb_synchronize")
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self.lib.nqb_kernel_launches(self.handle))
+
+
+_CONTEXTS: dict = {}
+
+
+def context(device: int = 0) -> Context:
+    if device not in _CONTEXTS:
+        _CONTEXTS[device] = Context(device)
+    return _CONTEXTS[device]
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _u32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+def _mat(a) -> np.ndarray:
+    a = _f64(a)
+    if a.ndim != 2:
+        raise DimensionMismatch("expected a 2-D matrix")
+    return a
+
+
+def words_per_row(cols: int) -> int:
+    return (cols + 31) // 32
+
+
+# ---------------------------------------------------------------------------
+# storage.cpp:124-141
+# ---------------------------------------------------------------------------
+def rank_for_target_bpw(n: int, m: int, target_bpw: float) -> int:
+    out = C.c_uint32()
+    _check(L.load().nqb_rank_for_target_bpw(n, m, float(target_bpw), C.byref(out)),
+           "rank_for_target_bpw")
+    return out.value
+
+
+# ---------------------------------------------------------------------------
+# packed.hpp
+# ---------------------------------------------------------------------------
+def binarize(latent, ctx: Context | None = None) -> np.ndarray:
+    ctx = ctx or context()
+    x = _f64(latent)
+    out = np.empty_like(x)
+    _check(ctx.lib.nqb_binarize(ctx.handle, _ptr(x), x.size, _ptr(out), 0), "binarize")
+    return out
+
+
+def pack_signs(signs, ctx: Context | None = None) -> np.ndarray:
+    ctx = ctx or context()
+    s = _mat(signs)
+    rows, cols = s.shape
+    words = np.zeros((rows, words_per_row(cols)), np.uint32)
+    _check(ctx.lib.nqb_pack_signs(ctx.handle, _ptr(s), rows, cols, _ptr(words), 0),
+           "pack_signs")
+    return words
+
+
+def unpack_signs(words, rows: int, cols: int, ctx: Context | None = None) -> np.ndarray:
+    ctx = ctx or context()
+    w = _u32(words)
+    if w.size != rows * words_per_row(cols):
+        raise DimensionMismatch("unpack_signs: word count mismatch")
+    out = np.empty((rows, cols), np.float64)
+    _check(ctx.lib.nqb_unpack_signs(ctx.handle, _ptr(w), rows, cols, _ptr(out), 0),
+           "unpack_signs")
+    return out
+
+
+@dataclass
+class FactorizedLayer:
+    """FactorizedLayer (packed.hpp:57-72): packed U (n x r), V (m x r), s1, s2.
+
+    The device copy (re-laid-out, binary16 scales) is created on first use and
+    cached; `device_layer()` returns it.
+    """
+
+    n: int
+    m: int
+    r: int
+    u: np.ndarray
+    v: np.ndarray
+    s1: np.ndarray
+    s2: np.ndarray
+    _dev: Optional["DeviceLayer"] = field(default=None, repr=False, compare=False)
+
+    def payload_bits(self) -> int:  # packed.hpp:65-68
+        return self.r * (self.n + self.m) + 16 * (self.n + self.m)
+
+    def device_layer(self, ctx: Context | None = None) -> "DeviceLayer":
+        if self._dev is None:
+            self._dev = DeviceLayer.upload(self, ctx)
+        return self._dev
+
+
+class DeviceLayer:
+    """A factorized layer resident in HBM (nqb_layer)."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p):
+        self.ctx = ctx
+        self.handle = handle
+        n, m, r = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _check(ctx.lib.nqb_layer_shape(handle, C.byref(n), C.byref(m), C.byref(r)),
+               "nqb_layer_shape")
+        self.n, self.m, self.r = n.value, m.value, r.value
+
+    @classmethod
+    def upload(cls, layer: FactorizedLayer, ctx: Context | None = None) -> "DeviceLayer":
+        ctx = ctx or context()
+        h = C.c_void_p()
+        u, v = _u32(layer.u), _u32(layer.v)
+        s1, s2 = _f64(layer.s1), _f64(layer.s2)
+        if u.size != layer.n * words_per_row(layer.r) or v.size != layer.m * words_per_row(
+                layer.r) or s1.size != layer.n or s2.size != layer.m:
+            raise DimensionMismatch("layer arrays do not match (n, m, r)")
+        _check(ctx.lib.nqb_layer_upload(ctx.handle, layer.n, layer.m, layer.r, _ptr(u),
+                                        _ptr(v), _ptr(s1), _ptr(s2), C.byref(h)),
+               "nqb_layer_upload")
+        return cls(ctx, h)
+
+    @classmethod
+    def upload_f16(cls, n, m, r, u, v, s1_half, s2_half, ctx: Context | None = None):
+        ctx = ctx or context()
+        h = C.c_void_p()
+        u, v = _u32(u), _u32(v)
+        s1h = np.ascontiguousarray(s1_half, dtype=np.uint16)
+        s2h = np.ascontiguousarray(s2_half, dtype=np.uint16)
+        _check(ctx.lib.nqb_layer_upload_f16(ctx.handle, n, m, r, _ptr(u), _ptr(v), _ptr(s1h),
+                                            _ptr(s2h), C.byref(h)), "nqb_layer_upload_f16")
+        return cls(ctx, h)
+
+    def free(self):
+        if self.handle:
+            self.ctx.lib.nqb_layer_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self.ctx.lib.nqb_layer_device_bytes(self.handle))
+
+    def download(self) -> FactorizedLayer:
+        k = words_per_row(self.r)
+        u = np.zeros((self.n, k), np.uint32)
+        v = np.zeros((self.m, k), np.uint32)
+        s1, s2 = np.empty(self.n), np.empty(self.m)
+        _check(self.ctx.lib.nqb_layer_download(self.ctx.handle, self.handle, _ptr(u), _ptr(v),
+                                               _ptr(s1), _ptr(s2)), "nqb_layer_download")
+        return FactorizedLayer(self.n, self.m, self.r, u, v, s1, s2)
+
+    # -- forward on host buffers (drop-in) --------------------------------
+    def gemv_f32(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        if x.size != self.m:
+            raise DimensionMismatch("gemv_packed: |x| != m")
+        y = np.empty(self.n, np.float32)
+        _check(self.ctx.lib.nqb_gemv_f32_host(self.ctx.handle, self.handle, _ptr(x), _ptr(y)),
+               "gemv_packed_f32")
+        return y
+
+    def gemv_f64(self, x) -> np.ndarray:
+        x = _f64(x)
+        if x.size != self.m:
+            raise DimensionMismatch("gemv_packed: |x| != m")
+        y = np.empty(self.n, np.float64)
+        _check(self.ctx.lib.nqb_gemv_f64_host(self.ctx.handle, self.handle, _ptr(x), _ptr(y)),
+               "gemv_packed")
+        return y
+
+    def gemm_f64(self, x) -> np.ndarray:
+        x = _mat(x)
+        if x.shape[0] != self.m:
+            raise DimensionMismatch("gemm_packed: rows(X) != m")
+        y = np.empty((self.n, x.shape[1]), np.float64)
+        _check(self.ctx.lib.nqb_gemm_f64_host(self.ctx.handle, self.handle, _ptr(x),
+                                              x.shape[1], _ptr(y)), "gemm_packed")
+        return y
+
+    def reconstruct_dense(self) -> np.ndarray:
+        w = np.empty((self.n, self.m), np.float64)
+        _check(self.ctx.lib.nqb_reconstruct_dense_host(self.ctx.handle, self.handle, _ptr(w)),
+               "reconstruct_dense")
+        return w
+
+    def rel_error(self, w) -> float:
+        w = _mat(w)
+        out = C.c_double()
+        _check(self.ctx.lib.nqb_layer_rel_error(self.ctx.handle, self.handle, _ptr(w), 0,
+                                                C.byref(out)), "nqb_layer_rel_error")
+        return out.value
+
+    # -- forward on device buffers (torch tensors; the hot path) -----------
+    def _bind_stream(self, tensor):
+        import torch
+        self.ctx.set_stream(torch.cuda.current_stream(tensor.device).cuda_stream)
+
+    def gemv_device(self, x, y):
+        """x: (m,) fp32/fp16 CUDA tensor, y: (n,) same dtype; async on torch's stream."""
+        import torch
+        self._bind_stream(x)
+        if x.dtype == torch.float32:
+            fn = self.ctx.lib.nqb_gemv_f32_device
+        elif x.dtype == torch.float16:
+            fn = self.ctx.lib.nqb_gemv_f16_device
+        else:
+            raise Error("gemv_device: dtype must be float32 or float16")
+        _check(fn(self.ctx.handle, self.handle, C.c_void_p(x.data_ptr()),
+                  C.c_void_p(y.data_ptr())), "gemv_device")
+
+    def gemm_device(self, x, y):
+        """x: (b, m) fp16 token-major CUDA tensor -> y: (b, n) fp16."""
+        self._bind_stream(x)
+        _check(self.ctx.lib.nqb_gemm_f16_device(self.ctx.handle, self.handle,
+                                                C.c_void_p(x.data_ptr()), x.shape[0],
+                                                C.c_void_p(y.data_ptr())), "gemm_device")
+
+
+def make_factorized_layer(latent_u, latent_v, s1, s2, ctx: Context | None = None):
+    """packed.cpp:105-124: binarize + pack both latents on the device."""
+    ctx = ctx or context()
+    lu, lv = _mat(latent_u), _mat(latent_v)
+    if lu.shape[1] != lv.shape[1]:
+        raise DimensionMismatch("make_factorized_layer: ranks differ")
+    s1, s2 = _f64(s1).ravel(), _f64(s2).ravel()
+    if s1.size != lu.shape[0] or s2.size != lv.shape[0]:
+        raise DimensionMismatch("make_factorized_layer: scale lengths")
+    r = lu.shape[1]
+    u = np.zeros((lu.shape[0], words_per_row(r)), np.uint32)
+    v = np.zeros((lv.shape[0], words_per_row(r)), np.uint32)
+    _check(ctx.lib.nqb_pack_latent(ctx.handle, _ptr(lu), lu.shape[0], r, _ptr(u), 0),
+           "make_factorized_layer")
+    _check(ctx.lib.nqb_pack_latent(ctx.handle, _ptr(lv), lv.shape[0], r, _ptr(v), 0),
+           "make_factorized_layer")
+    return FactorizedLayer(lu.shape[0], lv.shape[0], r, u, v, s1, s2)
+
+
+def reconstruct_dense(layer: FactorizedLayer, ctx: Context | None = None) -> np.ndarray:
+    return layer.device_layer(ctx).reconstruct_dense()
+
+
+def gemv_packed(layer: FactorizedLayer, x, ctx: Context | None = None) -> np.ndarray:
+    return layer.device_layer(ctx).gemv_f64(x)
+
+
+def gemv_packed_f32(layer: FactorizedLayer, x, ctx: Context | None = None) -> np.ndarray:
+    return layer.device_layer(ctx).gemv_f32(x)
+
+
+def gemm_packed(layer: FactorizedLayer, x, ctx: Context | None = None) -> np.ndarray:
+    return layer.device_layer(ctx).gemm_f64(x)
+
+
+def relative_frobenius_error(reference, approx) -> float:
+    """dense.cpp:141-146 (host arithmetic on already-computed matrices)."""
+    reference, approx = _mat(reference), _mat(approx)
+    denom = float(np.sqrt(np.sum(reference * reference)))
+    d = reference - approx
+    num = float(np.sqrt(np.sum(d * d)))
+    if denom == 0.0:
+        return 0.0 if num == 0.0 else float("inf")
+    return num / denom
+
+
+# ---------------------------------------------------------------------------
+# linalg.hpp / admm.hpp / balance.hpp
+# ---------------------------------------------------------------------------
+@dataclass
+class SingularPair:  # linalg.hpp:27-32
+    sigma: float
+    left: np.ndarray
+    right: np.ndarray
+    converged: bool
+
+
+def top_singular_pair(m, max_iters: int = 500, tol: float = 1e-12,
+                      ctx: Context | None = None) -> SingularPair:
+    ctx = ctx or context()
+    a = _mat(m)
+    rows, cols = a.shape
+    sigma, conv = C.c_double(), C.c_int32()
+    left, right = np.empty(rows), np.empty(cols)
+    _check(ctx.lib.nqb_top_singular_pair_host(ctx.handle, _ptr(a), rows, cols, max_iters, tol,
+                                              C.byref(sigma), _ptr(left), _ptr(right),
+                                              C.byref(conv)), "top_singular_pair")
+    return SingularPair(sigma.value, left, right, bool(conv.value))
+
+
+def spectral_norm_estimate(m, iters: int = 200, ctx: Context | None = None) -> float:
+    ctx = ctx or context()
+    a = _mat(m)
+    out = C.c_double()
+    _check(ctx.lib.nqb_spectral_norm_host(ctx.handle, _ptr(a), a.shape[0], a.shape[1], iters,
+                                          C.byref(out)), "spectral_norm_estimate")
+    return out.value
+
+
+def truncated_svd_factors(m, rank: int, ctx: Context | None = None):
+    ctx = ctx or context()
+    a = _mat(m)
+    u = np.empty((a.shape[0], rank))
+    v = np.empty((a.shape[1], rank))
+    _check(ctx.lib.nqb_truncated_svd_host(ctx.handle, _ptr(a), a.shape[0], a.shape[1], rank,
+                                          _ptr(u), _ptr(v)), "truncated_svd_factors")
+    return u, v
+
+
+def cholesky_solve(a, b, ctx: Context | None = None) -> np.ndarray:
+    ctx = ctx or context()
+    a, b = _mat(a), _mat(b)
+    if a.shape[0] != a.shape[1]:
+        raise DimensionMismatch("cholesky_solve: A is not square")
+    if a.shape[0] != b.shape[0]:
+        raise DimensionMismatch("cholesky_solve: rows(B) != rows(A)")
+    x = np.empty_like(b)
+    _check(ctx.lib.nqb_cholesky_solve_host(ctx.handle, _ptr(a), a.shape[0], _ptr(b),
+                                           b.shape[1], _ptr(x)), "cholesky_solve")
+    return x
+
+
+def svid(p, ctx: Context | None = None) -> np.ndarray:
+    ctx = ctx or context()
+    a = _mat(p)
+    z = np.empty_like(a)
+    _check(ctx.lib.nqb_svid_host(ctx.handle, _ptr(a), a.shape[0], a.shape[1], _ptr(z)), "svid")
+    return z
+
+
+def admm_factor_solve(target, fixed, z, l, rho: float, ridge: float,
+                      ctx: Context | None = None) -> np.ndarray:
+    ctx = ctx or context()
+    target, fixed, z, l = map(_mat, (target, fixed, z, l))
+    r = fixed.shape[1]
+    if z.shape[1] != r or l.shape[1] != r:
+        raise DimensionMismatch("admm_factor_solve: proxy rank mismatch")
+    if z.shape[0] != target.shape[0] or l.shape[0] != target.shape[0]:
+        raise DimensionMismatch("admm_factor_solve: proxy rows mismatch")
+    if fixed.shape[0] != target.shape[1]:
+        raise DimensionMismatch("admm_factor_solve: rows(fixed) != cols(target)")
+    x = np.empty((target.shape[0], r))
+    _check(ctx.lib.nqb_admm_factor_solve_host(ctx.handle, _ptr(target), target.shape[0],
+                                              target.shape[1], _ptr(fixed), r, _ptr(z), _ptr(l),
+                                              rho, ridge, _ptr(x)), "admm_factor_solve")
+    return x
+
+
+@dataclass
+class AdmmConfig:  # admm.hpp:41-51
+    rank: int = 1
+    max_iters: int = 400
+    rho_start: float = 0.0
+    rho_end: float = 0.0
+    ridge: float = 1e-4
+    tol: float = 1e-4
+    seed: int = 0
+    record_trace: bool = True
+
+    def c(self) -> L.AdmmConfig:
+        return L.AdmmConfig(self.rank, self.max_iters, self.rho_start, self.rho_end, self.ridge,
+                            self.tol, self.seed, 1 if self.record_trace else 0, 0)
+
+
+@dataclass
+class AdmmState:  # admm.hpp:53-62 (scalars; matrices stay on the device)
+    rho: float
+    iteration: int
+    lagrangian_trace: list
+    primal_residual: float
+    converged: bool
+    stats: dict
+
+
+@dataclass
+class AdmmResult:  # admm.hpp:69-73
+    state: AdmmState
+    consensus_u: np.ndarray
+    consensus_v: np.ndarray
+
+
+def admm_factorize(target, config: AdmmConfig, ctx: Context | None = None) -> AdmmResult:
+    ctx = ctx or context()
+    w = _mat(target)
+    n, m = w.shape
+    cfg = config.c()
+    cu = np.empty((n, config.rank))
+    cv = np.empty((m, config.rank))
+    trace = np.empty(max(config.max_iters, 1) + 1)
+    res = L.AdmmResultC()
+    _check(ctx.lib.nqb_admm_factorize_host(ctx.handle, _ptr(w), n, m, C.byref(cfg), _ptr(cu),
+                                           _ptr(cv), _ptr(trace), C.byref(res)),
+           "admm_factorize")
+    d = res.as_dict()
+    state = AdmmState(res.rho, res.iteration, list(trace[: res.trace_len]),
+                      res.primal_residual, bool(res.converged), d)
+    return AdmmResult(state, cu, cv)
+
+
+def augmented_lagrangian(u, v, z_u, z_v, l_u, l_v, rho, target, ridge,
+                         ctx: Context | None = None) -> float:
+    ctx = ctx or context()
+    u, v, z_u, z_v, l_u, l_v, target = map(_mat, (u, v, z_u, z_v, l_u, l_v, target))
+    if u.shape[0] != target.shape[0] or v.shape[0] != target.shape[1]:
+        raise DimensionMismatch("augmented_lagrangian: state does not match target")
+    out = C.c_double()
+    _check(ctx.lib.nqb_augmented_lagrangian_host(ctx.handle, _ptr(u), _ptr(v), _ptr(z_u),
+                                                 _ptr(z_v), _ptr(l_u), _ptr(l_v), u.shape[0],
+                                                 v.shape[0], u.shape[1], rho, _ptr(target),
+                                                 ridge, C.byref(out)), "augmented_lagrangian")
+    return out.value
+
+
+def monotone_rho(target, ctx: Context | None = None) -> float:
+    """admm.cpp:98-100."""
+    return 16.0 * max(spectral_norm_estimate(target, ctx=ctx), 1e-12)
+
+
+@dataclass
+class BalancedLatents:  # balance.hpp:28-34
+    latent_u: np.ndarray
+    latent_v: np.ndarray
+    s1: np.ndarray
+    s2: np.ndarray
+    eta: float
+
+
+def balance_and_extract_scales(consensus_u, consensus_v, diag_out=None, diag_in=None,
+                               scale_floor: float = 1e-12,
+                               ctx: Context | None = None) -> BalancedLatents:
+    ctx = ctx or context()
+    pu, pv = _mat(consensus_u), _mat(consensus_v)
+    n, r = pu.shape
+    m = pv.shape[0]
+    if diag_out is not None and len(diag_out) not in (0, n):
+        raise DimensionMismatch("balance: rows(P_U) != |diag_out|")
+    if diag_in is not None and len(diag_in) not in (0, m):
+        raise DimensionMismatch("balance: rows(P_V) != |diag_in|")
+    if pv.shape[1] != r:
+        raise DimensionMismatch("balance: factor ranks differ")
+    do = _f64(diag_out) if diag_out is not None and len(diag_out) else None
+    di = _f64(diag_in) if diag_in is not None and len(diag_in) else None
+    lu, lv = np.empty_like(pu), np.empty_like(pv)
+    s1, s2 = np.empty(n), np.empty(m)
+    eta = C.c_double()
+    _check(ctx.lib.nqb_balance_host(ctx.handle, _ptr(pu), _ptr(pv), n, m, r, _ptr(do),
+                                    _ptr(di), scale_floor, _ptr(lu), _ptr(lv), _ptr(s1),
+                                    _ptr(s2), C.byref(eta)), "balance_and_extract_scales")
+    return BalancedLatents(lu, lv, s1, s2, eta.value)
+
+
+def factorize_layer(w, config: AdmmConfig, scale_floor: float = 1e-12,
+                    ctx: Context | None = None):
+    """One matrix through pipeline.cpp:95-110 + :150-153 on the device.
+
+    Returns (DeviceLayer, rel_fro_error, AdmmState)."""
+    ctx = ctx or context()
+    w = _mat(w)
+    n, m = w.shape
+    cfg = config.c()
+    h = C.c_void_p()
+    res = L.AdmmResultC()
+    err = C.c_double()
+    _check(ctx.lib.nqb_factorize_layer(ctx.handle, _ptr(w), n, m, C.byref(cfg), scale_floor, 0,
+                                       C.byref(h), C.byref(res), C.byref(err)),
+           "factorize_layer")
+    d = res.as_dict()
+    state = AdmmState(res.rho, res.iteration, [], res.primal_residual, bool(res.converged), d)
+    return DeviceLayer(ctx, h), err.value, state

@@ -1,0 +1,256 @@
+"""GPU parity of the on-device fp64 LB-ADMM initialisation and its parts.
+
+Bars (BASELINE.json north_star): ADMM reconstruction error within 1e-4
+relative of the reference's, with >= 99.9% sign agreement (pooled over U and V,
+as pipeline.cpp:139-148 pools them), on identical inputs.  Building blocks are
+compared with the reference's own tolerances (test_linalg.cpp, test_admm.cpp).
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import GOLDEN, bits_of, rel
+
+pytestmark = pytest.mark.gpu
+
+ERR_TOL = 1e-4       # |e_gpu - e_ref| <= 1e-4 * e_ref
+SIGN_AGREEMENT = 0.999
+
+
+# --------------------------------------------------------------- DMMA GEMM --
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("mnk", [(1, 1, 1), (7, 13, 5), (128, 64, 16), (300, 257, 129),
+                                 (1000, 33, 700)])
+def test_dgemm_vs_numpy(nq, ctx, chk, ta, tb, mnk):
+    import torch
+    M, N, K = mnk
+    rng = chk.rng(M * 131 + N * 7 + K)
+    A = rng.gaussian(M * K).reshape((K, M) if ta else (M, K))
+    B = rng.gaussian(K * N).reshape((N, K) if tb else (K, N))
+    C0 = rng.gaussian(M * N).reshape(M, N)
+    want = 0.5 * ((A.T if ta else A) @ (B.T if tb else B)) - 2.0 * C0
+    dA, dB, dC = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (A, B, C0))
+    lib = nq._lib.load()
+    st = lib.nqb_dgemm_device(ctx.handle, ta, tb, M, N, K, 0.5, dA.data_ptr(), A.shape[1],
+                              dB.data_ptr(), B.shape[1], -2.0, dC.data_ptr(), N)
+    torch.cuda.synchronize()
+    assert st == 0
+    assert rel(dC.cpu().numpy(), want) <= 1e-13
+
+
+# ---------------------------------------------------------------- linalg --
+def test_cholesky_kats_and_errors(nq, ctx):  # test_linalg.cpp:26-84
+    x = nq.cholesky_solve(np.array([[4.0, 2], [2, 3]]), np.array([[1.0], [0.0]]))
+    assert np.allclose(x[:, 0], [0.375, -0.25], rtol=1e-12)
+    b = np.arange(1, 7, dtype=float).reshape(3, 2)
+    assert np.array_equal(nq.cholesky_solve(np.eye(3), b), b)
+    with pytest.raises(nq.NotSymmetric):
+        nq.cholesky_solve(np.array([[1.0, 5], [2, 1]]), np.zeros((2, 1)))
+    with pytest.raises(nq.NotPositiveDefinite):
+        nq.cholesky_solve(np.array([[1.0, 0], [0, -5]]), np.zeros((2, 1)))
+    with pytest.raises(nq.DimensionMismatch):
+        nq.cholesky_solve(np.eye(3), np.zeros((2, 1)))
+    x = nq.cholesky_solve(np.ones((2, 2)), np.ones((2, 1)))  # jitter rescue
+    assert np.all(np.isfinite(x)) and np.linalg.norm(np.ones((2, 2)) @ x - 1) <= 1e-3
+
+
+@pytest.mark.parametrize("n,k", [(3, 5), (40, 4), (100, 100), (333, 17), (1000, 9)])
+def test_cholesky_vs_reference(nq, ctx, chk, n, k):
+    v = chk.rng(n).matrix(n + 5, n)
+    a = v.T @ v + 0.5 * np.eye(n)
+    b = chk.rng(n + 1).matrix(n, k)
+    want = chk.cholesky_solve(a, b)
+    got = nq.cholesky_solve(a, b)
+    assert rel(got, want) <= 1e-10
+    assert np.linalg.norm(a @ got - b) <= 1e-8 * (1 + np.linalg.norm(b))
+
+
+def test_top_singular_pair_kats(nq, ctx):  # test_linalg.cpp:86-103, 155-160
+    p = nq.top_singular_pair(np.full((2, 2), 2.0), 200, 1e-12)
+    assert abs(p.sigma - 4.0) <= 4e-10
+    assert np.allclose(p.left, 2 ** -0.5, rtol=1e-9) and np.allclose(p.right, 2 ** -0.5, rtol=1e-9)
+    p = nq.top_singular_pair(np.array([[3.0, 0], [0, 1]]), 500, 1e-13)
+    assert abs(p.sigma - 3.0) <= 3e-8 and abs(abs(p.left[0]) - 1) <= 1e-6
+    with pytest.raises(nq.ZeroMatrix):
+        nq.top_singular_pair(np.zeros((3, 3)), 10, 1e-6)
+    assert nq.spectral_norm_estimate(np.zeros((4, 4))) == 0.0
+
+
+@pytest.mark.parametrize("shape", [(16, 5), (64, 48), (300, 120), (1000, 700)])
+def test_top_singular_pair_vs_reference(nq, ctx, chk, shape):
+    w = O.synthetic_weight(chk, shape[0], *shape)
+    s, l, r, conv = chk.top_singular_pair(w, 1000, 1e-13)
+    p = nq.top_singular_pair(w, 1000, 1e-13)
+    assert abs(p.sigma - s) <= 1e-12 * s
+    assert rel(p.left, l) <= 1e-9 and rel(p.right, r) <= 1e-9
+    assert p.converged == conv
+
+
+def test_nonnegative_input_keeps_nonnegative_vectors(nq, ctx, chk):  # test_linalg.cpp:137-150
+    rng = chk.rng(5)
+    for _ in range(10):
+        m = np.abs(rng.matrix(1 + rng.index(12), 1 + rng.index(12)))
+        p = nq.top_singular_pair(m, 500, 1e-12)
+        assert np.all(p.left >= 0) and np.all(p.right >= 0)
+
+
+@pytest.mark.parametrize("shape,rank", [((12, 9), 3), ((64, 48), 11), ((256, 256), 112)])
+def test_truncated_svd_vs_reference(nq, ctx, chk, shape, rank):
+    w = O.synthetic_weight(chk, 7, *shape)
+    ua, va = chk.truncated_svd_factors(w, rank)
+    ub, vb = nq.truncated_svd_factors(w, rank)
+    assert rel(ub, ua) <= 1e-8 and rel(vb, va) <= 1e-8
+
+
+def test_truncated_svd_low_rank_exact(nq, ctx, chk):  # test_linalg.cpp:162-175
+    a, b = chk.rng(7).matrix(12, 3), chk.rng(8).matrix(9, 3)
+    w = a @ b.T
+    u, v = nq.truncated_svd_factors(w, 3)
+    assert rel(u @ v.T, w) <= 1e-8
+    assert abs(np.linalg.norm(u) - np.linalg.norm(v)) <= 1e-8 * np.linalg.norm(u)
+
+
+# ------------------------------------------------------------------ ADMM --
+def test_svid_exact_and_vs_reference(nq, ctx, chk):  # test_admm.cpp:50-78
+    p = np.array([[2.0, -2], [-2, 2]])
+    assert rel(nq.svid(p), p) <= 1e-10
+    assert rel(nq.svid(np.full((3, 5), 2.5)), np.full((3, 5), 2.5)) <= 1e-10
+    with pytest.raises(nq.ZeroMatrix):
+        nq.svid(np.zeros((2, 2)))
+    for shape in [(8, 3), (400, 100), (2000, 300)]:
+        p = chk.rng(shape[0]).matrix(*shape)
+        assert rel(nq.svid(p), chk.svid(p)) <= 1e-10
+
+
+def test_factor_solve_limits_and_reference(nq, ctx, chk):  # test_admm.cpp:80-119
+    rng = chk.rng(22)
+    t, f, z, l = rng.matrix(6, 4), rng.matrix(4, 2), rng.matrix(6, 2), rng.matrix(6, 2)
+    x = nq.admm_factor_solve(t, f, z, l, 1e9, 0.0)
+    assert rel(x, z - l) <= 1e-6
+    t = chk.rng(23).matrix(5, 7)
+    e1 = np.zeros((7, 1))
+    e1[0, 0] = 1.0
+    x = nq.admm_factor_solve(t, e1, np.zeros((5, 1)), np.zeros((5, 1)), 1e-12, 0.0)
+    assert rel(x, t @ e1) <= 1e-8
+    for shape in [(50, 40, 8), (300, 200, 64)]:
+        n, m, r = shape
+        rng = chk.rng(n)
+        t, f, z, l = rng.matrix(n, m), rng.matrix(m, r), rng.matrix(n, r), rng.matrix(n, r)
+        assert rel(nq.admm_factor_solve(t, f, z, l, 0.7, 1e-3),
+                   chk.admm_factor_solve(t, f, z, l, 0.7, 1e-3)) <= 1e-10
+
+
+def test_lagrangian_vs_reference(nq, ctx, chk):  # test_admm.cpp:121-183
+    rng = chk.rng(26)
+    u, v, zu, zv, lu, lv = (rng.matrix(5, 2), rng.matrix(4, 2), rng.matrix(5, 2),
+                            rng.matrix(4, 2), rng.matrix(5, 2), rng.matrix(4, 2))
+    t = rng.matrix(5, 4)
+    want = chk.augmented_lagrangian(u, v, zu, zv, lu, lv, 0.37, t, 0.021)
+    got = nq.augmented_lagrangian(u, v, zu, zv, lu, lv, 0.37, t, 0.021)
+    assert abs(got - want) <= 1e-10 * abs(want)
+    # zero at exact consensus and fit
+    u, v = chk.rng(25).matrix(4, 2), chk.rng(26).matrix(3, 2)
+    val = nq.augmented_lagrangian(u, v, u, v, np.zeros((4, 2)), np.zeros((3, 2)), 1.3, u @ v.T, 0.0)
+    assert abs(val) <= 1e-12
+
+
+def test_admm_validation(nq, ctx):  # test_admm.cpp:287-293
+    with pytest.raises(nq.RankTooLarge):
+        nq.admm_factorize(np.ones((3, 3)), nq.AdmmConfig(rank=5))
+    with pytest.raises(nq.ZeroMatrix):
+        nq.admm_factorize(np.zeros((3, 3)), nq.AdmmConfig(rank=1))
+    with pytest.raises(nq.InvalidRank):
+        nq.admm_factorize(np.ones((3, 3)), nq.AdmmConfig(rank=0))
+    with pytest.raises(nq.NonFiniteInput):
+        nq.admm_factorize(np.array([[1.0, np.nan], [0, 1]]), nq.AdmmConfig(rank=1))
+
+
+def test_admm_degenerate_run_returns_svd_init(nq, ctx, chk):  # test_admm.cpp:205-220
+    w = chk.rng(28).matrix(6, 5)
+    res = nq.admm_factorize(w, nq.AdmmConfig(rank=2, max_iters=1, tol=1e9))
+    assert res.state.iteration == 0 and len(res.state.lagrangian_trace) >= 1
+    u0, v0 = chk.truncated_svd_factors(w, 2)
+    assert rel(res.consensus_u, u0) <= 1e-12 and rel(res.consensus_v, v0) <= 1e-12
+
+
+def test_admm_monotone_descent(nq, ctx, chk):  # test_admm.cpp:222-235
+    w = chk.rng(29).matrix(16, 12)
+    rho = nq.monotone_rho(w)
+    res = nq.admm_factorize(w, nq.AdmmConfig(rank=2, max_iters=120, rho_start=rho, rho_end=rho))
+    t = np.array(res.state.lagrangian_trace)
+    assert len(t) >= 2 and np.all(t[1:] <= t[:-1] + 1e-8 * (1 + np.abs(t[:-1])))
+
+
+def test_admm_trace_and_consensus_vs_reference(nq, ctx, chk):
+    w = O.synthetic_weight(chk, 12345, 64, 48)
+    cfg = nq.AdmmConfig(rank=11)
+    cu, cv, trace, res = chk.admm_factorize(w, O.AdmmConfig.make(rank=11))
+    got = nq.admm_factorize(w, cfg)
+    assert got.state.iteration == res["iteration"]
+    assert rel(got.consensus_u, cu) <= 1e-8 and rel(got.consensus_v, cv) <= 1e-8
+    assert rel(got.state.lagrangian_trace, trace) <= 1e-10
+
+
+def test_admm_deterministic_bitwise(nq, ctx, chk):  # test_admm.cpp:237-251
+    w = O.synthetic_weight(chk, 30, 100, 80)
+    a = nq.admm_factorize(w, nq.AdmmConfig(rank=20, max_iters=60))
+    b = nq.admm_factorize(w, nq.AdmmConfig(rank=20, max_iters=60))
+    assert a.state.lagrangian_trace == b.state.lagrangian_trace
+    assert np.array_equal(a.consensus_u, b.consensus_u)
+    assert np.array_equal(a.consensus_v, b.consensus_v)
+
+
+def test_admm_in_class_rank1(nq, ctx, chk):  # test_admm.cpp:185-203 (subset)
+    rng = chk.rng(27)
+    hits = 0
+    for _ in range(20):
+        n, m = 2 + rng.index(63), 2 + rng.index(63)
+        w = np.outer(rng.sign(n) * rng.uniform(0.5, 2.0, n), rng.sign(m) * rng.uniform(0.5, 2.0, m))
+        _, err, _ = nq.factorize_layer(w, nq.AdmmConfig(rank=1))
+        hits += err <= 1e-3
+    assert hits >= 19
+
+
+def test_balance_vs_reference(nq, ctx, chk):  # test_balance.cpp
+    rng = chk.rng(42)
+    for _ in range(20):
+        n, m, r = 1 + rng.index(24), 1 + rng.index(24), 1 + rng.index(4)
+        pu = rng.matrix(n, r) * 3.0
+        pv = rng.matrix(m, r) * 0.2
+        do, di = rng.uniform(0.25, 3.0, n), rng.uniform(0.25, 3.0, m)
+        want = chk.balance_and_extract_scales(pu, pv, do, di)
+        got = nq.balance_and_extract_scales(pu, pv, do, di)
+        assert rel(got.latent_u, want[0]) <= 1e-13 and rel(got.latent_v, want[1]) <= 1e-13
+        assert rel(got.s1, want[2]) <= 1e-13 and rel(got.s2, want[3]) <= 1e-13
+        assert abs(got.eta - want[4]) <= 1e-13 * want[4]
+    lat = nq.balance_and_extract_scales(np.zeros((3, 1)), np.ones((2, 1)))
+    assert lat.eta == 1.0
+
+
+# --------------------------------------------- pipeline parity (fixtures) --
+FIXTURES = sorted(glob.glob(os.path.join(GOLDEN, "admm_*.npz")))
+
+
+def _pooled_sign_agreement(got, g, n, m, r):
+    au = bits_of(got.u, r) == bits_of(g["u"], r)
+    av = bits_of(got.v, r) == bits_of(g["v"], r)
+    return (au.sum() + av.sum()) / (au.size + av.size)
+
+
+@pytest.mark.parametrize("path", FIXTURES, ids=os.path.basename)
+def test_factorize_layer_matches_reference_fixture(nq, ctx, chk, path):
+    g = np.load(path)
+    n, m, r = int(g["n"]), int(g["m"]), int(g["r"])
+    w = O.synthetic_weight(chk, int(g["seed"]), n, m)
+    assert abs(float(np.sum(w * w)) - float(g["w_sumsq"])) == 0.0  # same inputs
+    layer, err, state = nq.factorize_layer(w, nq.AdmmConfig(rank=r, max_iters=int(g["max_iters"])))
+    e_ref = float(g["rel_err"])
+    assert abs(err - e_ref) <= ERR_TOL * e_ref, (err, e_ref)
+    got = layer.download()
+    agree = _pooled_sign_agreement(got, g, n, m, r)
+    assert agree >= SIGN_AGREEMENT, agree
+    assert abs(state.iteration - int(g["iteration"])) <= 2
+    assert rel(got.s1, g["s1"]) <= 1e-3 and rel(got.s2, g["s2"]) <= 1e-3  # binary16 snap

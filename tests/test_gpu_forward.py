@@ -1,0 +1,213 @@
+"""GPU parity of packing, the device layout and the forward, through the C ABI.
+
+Bars (BASELINE.json north_star): packing/unpacking/relayout bit-exact; forward
+within 1e-3 relative (norm-wise) of the reference's fp32 result
+(gemv_packed_f32) on the same binary16-snapped scales; the fp64 drop-in paths
+within 1e-10 like the reference's own tests (test_packed.cpp:143-217).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import bits_of, rel
+
+pytestmark = pytest.mark.gpu
+
+FWD_TOL = 1e-3  # north_star: forward within 1e-3 relative of gemv_packed_f32
+
+
+def to_nq(nq, lay):
+    return nq.FactorizedLayer(lay.n, lay.m, lay.r, lay.u, lay.v, lay.s1, lay.s2)
+
+
+# ---------------------------------------------------------------- packing --
+def test_pack_kats(nq, ctx):
+    assert nq.pack_signs(np.array([[1, -1, 1, -1.0]])).tolist() == [[5]]
+    assert nq.pack_signs(np.ones((1, 33))).tolist() == [[0xFFFFFFFF, 1]]
+    assert nq.pack_signs(-np.ones((1, 32))).tolist() == [[0]]
+    with pytest.raises(nq.NonBinaryEntry):
+        nq.pack_signs(np.full((1, 3), 0.5))
+    assert nq.unpack_signs(np.array([[5]], np.uint32), 1, 4).tolist() == [[1, -1, 1, -1]]
+    with pytest.raises(nq.CorruptPadding):
+        nq.unpack_signs(np.array([[5 | (1 << 10)]], np.uint32), 1, 4)
+    assert nq.binarize(np.array([[0.3, -0.2, 0.0, -0.0, -5.0]])).tolist() == [[1, -1, 1, 1, -1]]
+    with pytest.raises(nq.NonFiniteInput):
+        nq.binarize(np.array([[1.0, np.inf]]))
+
+
+@pytest.mark.parametrize("cols", [1, 31, 32, 33, 64, 67, 100, 1000])
+def test_pack_roundtrip_bitwise(nq, chk, cols):  # test_packed.cpp:86-92
+    rng = chk.rng(72 + cols)
+    rows = 1 + rng.index(40)
+    s = rng.sign(rows * cols).reshape(rows, cols)
+    words = nq.pack_signs(s)
+    assert np.array_equal(words, chk.pack_signs(s))
+    assert np.array_equal(nq.unpack_signs(words, rows, cols), s)
+    lat = rng.gaussian(rows * cols).reshape(rows, cols)
+    lat[0, 0] = -0.0
+    lay = nq.make_factorized_layer(lat, lat[:, :], np.ones(rows), np.ones(rows))
+    assert np.array_equal(lay.u, chk.pack_signs(chk.binarize(lat)))
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (3, 5, 31), (33, 65, 32), (100, 37, 33),
+                                   (257, 129, 100), (4096, 4096, 1622), (1024, 8192, 485)])
+def test_layer_upload_download_bit_exact(nq, chk, shape):
+    n, m, r = shape
+    lay = O.synthetic_layer(chk, 0xB1A5E100 + n, n, m, r)
+    dev = nq.DeviceLayer.upload(to_nq(nq, lay))
+    back = dev.download()
+    assert np.array_equal(back.u, lay.u) and np.array_equal(back.v, lay.v)
+    assert np.array_equal(back.s1, lay.s1) and np.array_equal(back.s2, lay.s2)
+    assert dev.device_bytes >= r * (n + m) // 8
+
+
+def test_upload_rejects_corrupt_padding(nq, chk):
+    lay = O.synthetic_layer(chk, 3, 8, 8, 20)
+    lay.v[3, 0] |= np.uint32(1 << 25)
+    with pytest.raises(nq.CorruptPadding):
+        nq.DeviceLayer.upload(to_nq(nq, lay))
+
+
+def test_scale_snap_matches_reference_half(nq, chk):
+    n, m, r = 64, 48, 16
+    lay = O.synthetic_layer(chk, 5, n, m, r)
+    raw1 = chk.rng(6).uniform(1e-6, 70000.0, n)
+    raw2 = chk.rng(7).uniform(0.25, 2.0, m)
+    dev = nq.DeviceLayer.upload(nq.FactorizedLayer(n, m, r, lay.u, lay.v, raw1, raw2))
+    back = dev.download()
+    assert np.array_equal(back.s1, chk.snap_half(raw1))
+    assert np.array_equal(back.s2, chk.snap_half(raw2))
+
+
+# ------------------------------------------------------------ reconstruct --
+@pytest.mark.parametrize("shape", [(20, 18, 9), (97, 131, 64), (300, 200, 77)])
+def test_reconstruct_dense_bitwise(nq, chk, shape):
+    n, m, r = shape
+    lay = O.synthetic_layer(chk, 11 * n, n, m, r)
+    dev = nq.DeviceLayer.upload(to_nq(nq, lay))
+    assert np.array_equal(dev.reconstruct_dense(), chk.reconstruct_dense(lay))
+    w = O.synthetic_weight(chk, 3, n, m)
+    assert abs(dev.rel_error(w) - chk.layer_rel_error(lay, w)) <= 1e-12
+
+
+# ------------------------------------------------------------------ GEMV --
+def test_gemv_closed_form(nq, chk):  # test_packed.cpp:125-141
+    ones = nq.make_factorized_layer(np.ones((3, 1)), np.ones((5, 1)), [1] * 3, [1] * 5)
+    x = chk.rng(74).gaussian(5)
+    assert np.allclose(nq.gemv_packed(ones, x), x.sum(), rtol=1e-12)
+    assert np.all(nq.gemv_packed(ones, np.zeros(5)) == 0.0)
+    with pytest.raises(nq.DimensionMismatch):
+        nq.gemv_packed(ones, np.zeros(4))
+
+
+def test_gemv_f64_vs_dense_random_layers(nq, chk):  # test_packed.cpp:143-163 (200 layers)
+    rng = chk.rng(75)
+    for trial in range(200):
+        n, m = 1 + rng.index(512), 1 + rng.index(512)
+        r = 1 + rng.index(64)
+        lay = O.synthetic_layer(chk, 5000 + trial, n, m, r)
+        x = chk.rng(6000 + trial).gaussian(m)
+        expect = chk.reconstruct_dense(lay) @ x
+        y = nq.gemv_packed(to_nq(nq, lay), x)
+        assert np.linalg.norm(expect - y) <= 1e-10 * (1 + np.linalg.norm(expect))
+
+
+SHAPES_DECODE = {
+    "l7_q_0.8": (4096, 4096, 1622),
+    "l7_gate_0.8": (11008, 4096, 2372),
+    "l7_down_0.8": (4096, 11008, 2372),
+    "l13_q_0.55": (5120, 5120, 1392),
+    "l70_q_0.55": (8192, 8192, 2237),
+    "l70_gate_0.55": (28672, 8192, 3488),
+    "l70_down_0.55": (8192, 28672, 3488),
+    "ragged": (1000, 777, 45),
+    "tiny": (1, 1, 1),
+}
+
+
+@pytest.mark.parametrize("name", list(SHAPES_DECODE))
+def test_decode_gemv_f32_vs_reference_f32(nq, chk, name):
+    n, m, r = SHAPES_DECODE[name]
+    lay = O.synthetic_layer(chk, 0xB1A5E100 + n + m, n, m, r)
+    x = chk.rng(0xB1A5E002).gaussian(m).astype(np.float32)
+    want = chk.gemv_packed_f32(lay, x)
+    dev = nq.DeviceLayer.upload(to_nq(nq, lay))
+    got = dev.gemv_f32(x)
+    assert rel(got, want) <= FWD_TOL
+    # device-buffer entry point (the bench path) agrees with the host one
+    import torch
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty(n, dtype=torch.float32, device="cuda")
+    dev.gemv_device(xd, yd)
+    torch.cuda.synchronize()
+    assert rel(yd.cpu().numpy(), want) <= FWD_TOL
+
+
+@pytest.mark.parametrize("name", ["l7_q_0.8", "l70_gate_0.55", "ragged"])
+def test_decode_gemv_f16_vs_reference(nq, chk, name):
+    import torch
+    n, m, r = SHAPES_DECODE[name]
+    lay = O.synthetic_layer(chk, 77 + n, n, m, r)
+    x16 = chk.rng(8).gaussian(m).astype(np.float16)
+    want = chk.gemv_packed_f32(lay, x16.astype(np.float32))
+    dev = nq.DeviceLayer.upload(to_nq(nq, lay))
+    y = torch.empty(n, dtype=torch.float16, device="cuda")
+    dev.gemv_device(torch.from_numpy(x16).cuda(), y)
+    torch.cuda.synchronize()
+    assert rel(y.float().cpu().numpy(), want) <= FWD_TOL
+
+
+def test_decode_gemv_deterministic(nq, chk):
+    lay = O.synthetic_layer(chk, 42, 8192, 8192, 2237)
+    x = chk.rng(1).gaussian(8192).astype(np.float32)
+    dev = nq.DeviceLayer.upload(to_nq(nq, lay))
+    a, b = dev.gemv_f32(x), dev.gemv_f32(x)
+    assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ GEMM --
+def test_gemm_f64_equals_reference(nq, chk):  # test_packed.cpp:199-217 analogue
+    rng = chk.rng(78)
+    for trial in range(12):
+        n, m = 1 + rng.index(60), 1 + rng.index(60)
+        r, b = 1 + rng.index(48), 1 + rng.index(40)
+        lay = O.synthetic_layer(chk, 7000 + trial, n, m, r)
+        X = chk.rng(8000 + trial).matrix(m, b)
+        want = chk.gemm_packed(lay, X)
+        got = nq.gemm_packed(to_nq(nq, lay), X)
+        assert np.linalg.norm(got - want) <= 1e-10 * (1 + np.linalg.norm(want))
+
+
+def test_gemm_identity_probe(nq, chk):  # test_packed.cpp:219-225
+    lay = O.synthetic_layer(chk, 79, 24, 18, 9)
+    out = nq.gemm_packed(to_nq(nq, lay), np.eye(18))
+    assert rel(out, chk.reconstruct_dense(lay)) <= 1e-12
+
+
+@pytest.mark.parametrize("shape", [(8192, 8192, 2237, 64), (1024, 8192, 485, 256),
+                                   (300, 200, 77, 33)])
+def test_prefill_gemm_f16_vs_reference(nq, chk, shape):
+    import torch
+    n, m, r, b = shape
+    lay = O.synthetic_layer(chk, 99 + n, n, m, r)
+    X16 = chk.rng(10).gaussian(m * b).reshape(b, m).astype(np.float16)  # token-major
+    want = chk.gemm_packed(lay, X16.astype(np.float64).T)  # n x b, fp64 on fp16 inputs
+    dev = nq.DeviceLayer.upload(to_nq(nq, lay))
+    y = torch.empty((b, n), dtype=torch.float16, device="cuda")
+    dev.gemm_device(torch.from_numpy(X16).cuda(), y)
+    torch.cuda.synchronize()
+    assert rel(y.float().cpu().numpy().T, want) <= FWD_TOL
+
+
+def test_kernel_launch_counter_moves(nq, chk):
+    ctx = nq.context(0)
+    before = ctx.kernel_launches
+    lay = O.synthetic_layer(chk, 1, 64, 64, 32)
+    nq.DeviceLayer.upload(to_nq(nq, lay)).gemv_f32(np.ones(64, np.float32))
+    assert ctx.kernel_launches > before
+
+
+def test_sign_bits_helper_on_device_layer(nq, chk):
+    lay = O.synthetic_layer(chk, 2, 40, 70, 45)
+    back = nq.DeviceLayer.upload(to_nq(nq, lay)).download()
+    assert np.array_equal(bits_of(back.u, 45), bits_of(lay.u, 45))
