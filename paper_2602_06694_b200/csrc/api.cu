@@ -281,9 +281,10 @@ int nqb_unpack_signs(nqb_context* ctx, const uint32_t* words, uint32_t rows, uin
     NQB_REQUIRE(!(flags.read() & 4), NQB_E_CORRUPT_PADDING, "padding bits beyond cols are set");
     launch_unpack(ctx, words, rows, cols, signs);
   } else {
-    DevBuf buf(ctx, nwords * 4 + elems * 8);
+    const uint64_t wbytes = ((nwords * 4 + 15) / 16) * 16;
+    DevBuf buf(ctx, wbytes + elems * 8);
     uint32_t* dw = buf.as<uint32_t>();
-    double* dout = (double*)(buf.as<char>() + ((nwords * 4 + 7) / 8) * 8);
+    double* dout = (double*)(buf.as<char>() + wbytes);
     NQB_CUDA(cudaMemcpyAsync(dw, words, nwords * 4, cudaMemcpyHostToDevice, ctx->stream));
     launch_check_padding(ctx, dw, rows, cols, wpr, flags.d);
     NQB_REQUIRE(!(flags.read() & 4), NQB_E_CORRUPT_PADDING, "padding bits beyond cols are set");

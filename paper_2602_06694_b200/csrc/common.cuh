@@ -32,6 +32,7 @@ void set_error(const std::string& msg);
   do {                                                                           \
     cudaError_t e_ = (call);                                                     \
     if (e_ != cudaSuccess) {                                                     \
+      cudaGetLastError(); /* clear a non-sticky error so later checks are clean */ \
       ::nqb::fail(e_ == cudaErrorMemoryAllocation ? NQB_E_OUT_OF_MEMORY : NQB_E_CUDA, \
                   std::string(#call) + ": " + cudaGetErrorString(e_) + " @" +    \
                       __FILE__ + ":" + std::to_string(__LINE__));                \
@@ -142,8 +143,12 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks) {
       __threadfence();
       atomicExch(bar + 1, gen + 1u);
     } else {
+      // Watchdog: a block that waits ~4 s means the grid diverged; trap so the
+      // launch fails with an error instead of hanging the device.
+      unsigned long long spins = 0;
       while (*vgen == gen) {
-        __nanosleep(32);
+        __nanosleep(64);
+        if (++spins > (1ull << 26)) __trap();
       }
     }
     __threadfence();

@@ -171,8 +171,11 @@ struct PowerArgs {
   double* left;        // [rows] out: left vector (M v / sigma)
   double* wpart;       // [grid][cols]
   double* w;           // [cols]
-  double* sspart;      // [grid]
-  double* wsspart;     // [grid]
+  // [3][grid]: slot (it & 1) for iteration it, slot 2 for the final pass.  Phase
+  // A of iteration it+1 runs before any barrier, so it must not overwrite the
+  // values slower blocks are still reading in phase C of iteration it.
+  double* sspart;
+  double* wsspart;     // [grid] (written after a barrier: single slot is safe)
   double* out;         // [0] sigma, [1] converged, [2] iterations
   unsigned* bar;
 };
@@ -268,7 +271,8 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
         else a.wpart[(uint64_t)bid * a.cols + j] = wloc[c];
       }
     }
-    if (tid == 0) a.sspart[bid] = ss;
+    double* ssp = a.sspart + (size_t)(it & 1) * G;
+    if (tid == 0) ssp[bid] = ss;
     grid_sync(a.bar, G);
 
     // ---- phase B: w = sum_b wpart[b] (fixed order), ||w||^2 partials --------
@@ -286,7 +290,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
     // ---- phase C (every block, identical): sigma, normalise, stop rule ------
     double s2 = 0.0, w2 = 0.0;
     for (uint32_t b = 0; b < G; ++b) {
-      s2 += __ldcg(a.sspart + b);
+      s2 += __ldcg(ssp + b);
       w2 += __ldcg(a.wsspart + b);
     }
     sigma = sqrt(s2);
@@ -324,10 +328,11 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
       ss += s * s;
     }
   }
-  if (tid == 0) a.sspart[bid] = ss;
+  double* ssf = a.sspart + 2 * (size_t)G;
+  if (tid == 0) ssf[bid] = ss;
   grid_sync(a.bar, G);
   double s2 = 0.0;
-  for (uint32_t b = 0; b < G; ++b) s2 += __ldcg(a.sspart + b);
+  for (uint32_t b = 0; b < G; ++b) s2 += __ldcg(ssf + b);
   const double fsig = sqrt(s2);
   for (uint32_t i = r0 + tid; i < r1; i += PI_THREADS) {
     a.left[i] = fsig > 0.0 ? a.left[i] / fsig : 0.0;
@@ -370,7 +375,7 @@ void power_iterate_device(nqb_context* ctx, const double* d_m, uint32_t rows, ui
   NQB_REQUIRE(cols <= PI_MAX_COLS, NQB_E_VALIDATION,
               "power iteration supports at most 14336 columns");
   const uint32_t grid = std::max(1u, std::min<uint32_t>(rows, ctx->num_sms));
-  double* base = (double*)scratch(ctx, 5, sizeof(double) * ((size_t)grid * cols + cols + 2 * grid + 8));
+  double* base = (double*)scratch(ctx, 5, sizeof(double) * ((size_t)grid * cols + cols + 4 * grid + 8));
   PowerArgs a;
   a.M = d_m;
   a.rows = rows;
@@ -383,7 +388,7 @@ void power_iterate_device(nqb_context* ctx, const double* d_m, uint32_t rows, ui
   a.wpart = base;
   a.w = base + (size_t)grid * cols;
   a.sspart = a.w + cols;
-  a.wsspart = a.sspart + grid;
+  a.wsspart = a.sspart + 3 * grid;
   a.out = a.wsspart + grid;
   a.bar = ctx->barrier;
   const uint32_t cpt = ceil_div(cols, PI_THREADS);

@@ -87,7 +87,8 @@ def test_reconstruct_dense_bitwise(nq, chk, shape):
     dev = nq.DeviceLayer.upload(to_nq(nq, lay))
     assert np.array_equal(dev.reconstruct_dense(), chk.reconstruct_dense(lay))
     w = O.synthetic_weight(chk, 3, n, m)
-    assert abs(dev.rel_error(w) - chk.layer_rel_error(lay, w)) <= 1e-12
+    want = chk.layer_rel_error(lay, w)
+    assert abs(dev.rel_error(w) - want) <= 1e-13 * want
 
 
 # ------------------------------------------------------------------ GEMV --
