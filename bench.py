@@ -4,8 +4,11 @@ One step = one batch-1 decode pass through all 224 linear layers of a
 Llama-2-7B-shaped model (32 blocks x q,k,v,o 4096x4096 r=1622; gate,up
 11008x4096 r=2372; down 4096x11008 r=2372; ranks from rank_for_target_bpw at
 0.8 bit, BASELINE.json configs[1]).  Weights are random packed sign bits with
-binary16 scales (synthetic, seeded); every layer gets its own fp16 activation
-vector.  The 224 layers occupy ~0.65 GB, > 5x the 126 MB L2, so every step
+binary16 scales (synthetic, seeded).  A decode pass is issued the way a
+decoder issues it: per block q/k/v as one fused launch (they share the
+attention input), o, gate/up as one launch (shared MLP input), down; each
+launch reads its own fp16 input vector.  The 128 launches of a pass are one
+CUDA graph (nqb_graph_*), consecutive kernels overlapped with PDL.  The 224 layers occupy ~0.65 GB, > 5x the 126 MB L2, so every step
 streams the bits from HBM (no L2 flush needed; stated in `config`).
 
   value   = algorithmic bytes of the step / device time (CUDA events, max over
@@ -196,38 +199,64 @@ def cpu_reference_gbs(seconds_target=15.0, threads=None):
 # GPU side
 # ---------------------------------------------------------------------------
 def build_model(nq, ctx, seed):
+    """32 Llama-2-7B blocks; per block the four decode launches a decoder makes:
+    q/k/v as one group (shared attention input), o, gate/up as one group
+    (shared MLP input), down.  Returns [(launch, [layers])]."""
     rng = np.random.default_rng(seed)
-    layers = []
-    shapes = {}
-    for name, n, m in L7_BLOCK:
-        shapes[name] = (n, m, rank_for(n, m, BPW))
+    ranks = {name: rank_for(n, m, BPW) for name, n, m in L7_BLOCK}
+    launches = []
     for blk in range(32):
+        lay = {}
         for name, n, m in L7_BLOCK:
-            r = shapes[name][2]
+            r = ranks[name]
             u, v, s1, s2 = random_layer_arrays(rng, n, m, r)
-            layers.append((f"b{blk}.{name}", nq.DeviceLayer.upload_f16(n, m, r, u, v, s1, s2, ctx)))
-    return layers
+            lay[name] = nq.DeviceLayer.upload_f16(n, m, r, u, v, s1, s2, ctx)
+        launches.append((nq.DecodeGroup([lay["q"], lay["k"], lay["v"]]), [lay["q"], lay["k"], lay["v"]]))
+        launches.append((None, [lay["o"]]))
+        launches.append((nq.DecodeGroup([lay["gate"], lay["up"]]), [lay["gate"], lay["up"]]))
+        launches.append((None, [lay["down"]]))
+    return launches
 
 
-def time_device(torch, fn, steps, warmup):
-    for _ in range(warmup):
-        fn()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / 1e3
+def make_step(launches, xs, ys):
+    def step():
+        for (grp, lays), x, y in zip(launches, xs, ys):
+            if grp is None:
+                lays[0].gemv_device(x, y[0])
+            else:
+                grp.gemv_device(x, y)
+    return step
 
 
-def shape_roofline(nq, ctx, torch, n, m, r, reps=20, copies=None):
-    """Back-to-back decode GEMVs of one shape over distinct layer copies whose
-    total size exceeds L2 (cold HBM reads).  Returns seconds per call."""
+def graph_time(torch, ctx, stream, fn, reps, warmup=3):
+    """Captures fn() into one CUDA graph (library graph API) and times `reps`
+    replays with CUDA events on the capturing stream.  Returns (seconds per
+    replay, kernel launches per replay)."""
+    with torch.cuda.stream(stream):
+        ctx.bind_torch_stream()
+        fn()  # eager warm-up (also proves the path outside a graph)
+        l0 = ctx.kernel_launches
+        with ctx.capture() as cap:
+            fn()
+        per = ctx.kernel_launches - l0
+        for _ in range(warmup):
+            cap.graph.launch()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            cap.graph.launch()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps, per, cap.graph
+
+
+def shape_roofline(nq, ctx, torch, stream, n, m, r, reps=20):
+    """Back-to-back single-layer decode GEMVs over distinct copies totalling
+    > 4x L2 (every call reads its bits from HBM), captured in one graph."""
     per = algo_bytes(n, m, r)
-    copies = copies or max(4, int(np.ceil(4 * 126e6 / per)))
+    copies = max(4, int(np.ceil(4 * 126e6 / per)))
     rng = np.random.default_rng(n + m + r)
     lays = [nq.DeviceLayer.upload_f16(n, m, r, *random_layer_arrays(rng, n, m, r), ctx)
             for _ in range(copies)]
@@ -237,8 +266,9 @@ def shape_roofline(nq, ctx, torch, n, m, r, reps=20, copies=None):
     def step():
         for lay, x, y in zip(lays, xs, ys):
             lay.gemv_device(x, y)
-    secs = time_device(torch, step, reps, 2)
-    return secs / (reps * copies), per
+    sec, _, g = graph_time(torch, ctx, stream, step, reps)
+    g.free()
+    return sec / copies, per
 
 
 def main():
@@ -249,6 +279,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-shapes", action="store_true", help="skip the per-shape roofline sweep")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     ws, rank, local = dist_env()
@@ -278,36 +309,42 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = nq.context(local)
-    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    stream = torch.cuda.Stream()
 
-    layers = build_model(nq, ctx, seed=1234 + rank)
+    launch_list = build_model(nq, ctx, seed=1234 + rank)
     xs, ys, step_bytes = [], [], 0.0
-    for name, lay in layers:
-        xs.append(torch.randn(lay.m, device="cuda", dtype=torch.float16))
-        ys.append(torch.empty(lay.n, device="cuda", dtype=torch.float16))
-        step_bytes += algo_bytes(lay.n, lay.m, lay.r)
+    for grp, lays in launch_list:
+        xs.append(torch.randn(lays[0].m, device="cuda", dtype=torch.float16))
+        ys.append([torch.empty(l.n, device="cuda", dtype=torch.float16) for l in lays])
+        # x is read once per launch, even when the launch serves 2-3 layers
+        step_bytes += sum(algo_bytes(l.n, l.m, l.r) for l in lays) - 2 * lays[0].m * (len(lays) - 1)
+    step = make_step(launch_list, xs, ys)
 
-    def step():
-        for (name, lay), x, y in zip(layers, xs, ys):
-            lay.gemv_device(x, y)
-
-    for _ in range(args.warmup):
+    # one decode pass = one CUDA graph of 128 fused launches (PDL between them)
+    with torch.cuda.stream(stream):
+        ctx.bind_torch_stream()
         step()
-    torch.cuda.synchronize()
+        l0 = ctx.kernel_launches
+        with ctx.capture() as cap:
+            step()
+        launches_per_step = ctx.kernel_launches - l0
+        graph = cap.graph
+        for _ in range(args.warmup):
+            graph.launch()
+        torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
-    launches0 = ctx.kernel_launches
     with Clocks(local) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        e0.record()
+        e0.record(stream)
         for _ in range(args.steps):
-            step()
-        e1.record()
+            graph.launch()
+        e1.record(stream)
         torch.cuda.synchronize()
     secs = e0.elapsed_time(e1) / 1e3
-    launches = ctx.kernel_launches - launches0
+    launches = launches_per_step * args.steps
     if ws > 1:
         t = torch.tensor([secs], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -315,16 +352,18 @@ def main():
         torch.distributed.barrier()
     value = ws * step_bytes * args.steps / secs / 1e9
 
-    # ---- e2e: drop-in host entry point, H2D + D2H inside the timed region ----
-    e2e = None
-    h2d = sum(4 * lay.m for _, lay in layers)
-    d2h = sum(4 * lay.n for _, lay in layers)
-    hx = [torch.randn(lay.m, dtype=torch.float32).pin_memory().numpy() for _, lay in layers]
-    hy = [torch.empty(lay.n, dtype=torch.float32).pin_memory().numpy() for _, lay in layers]
+    # ---- e2e: the reference-facing drop-in (gemv_packed_f32 -> nqb_gemv_f32_host),
+    #      per layer: pinned host x -> device -> kernel -> host y, synchronous ----
+    all_layers = [l for _, lays in launch_list for l in lays]
+    h2d = sum(4 * l.m for l in all_layers)
+    d2h = sum(4 * l.n for l in all_layers)
+    hx = [torch.randn(l.m, dtype=torch.float32).pin_memory().numpy() for l in all_layers]
+    hy = [torch.empty(l.n, dtype=torch.float32).pin_memory().numpy() for l in all_layers]
+    ctx.set_stream(None)
 
     def e2e_step():
-        for (name, lay), x, y in zip(layers, hx, hy):
-            y[:] = lay.gemv_f32(x)
+        for l, x, y in zip(all_layers, hx, hy):
+            y[:] = l.gemv_f32(x)
     e2e_step()
     e2e_steps = max(1, min(args.steps, 5))
     t0 = time.perf_counter()
@@ -335,33 +374,31 @@ def main():
         t = torch.tensor([e2e_secs], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_secs = float(t.item())
-    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     e2e = {"value": ws * step_bytes * e2e_steps / e2e_secs / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "api": "nqb_gemv_f32_host (pinned host buffers)", "steps": e2e_steps}
+           "api": "nqb_gemv_f32_host per layer (gemv_packed_f32 drop-in, pinned host buffers)",
+           "steps": e2e_steps}
 
     peak, peak_kind = measured_peaks()
     extra = {}
     roof = None
     if rank == 0:
-        # per-shape cold-L2 timing (7B shapes of the step + the 70B target shapes)
         shapes = {}
-        for name, n, m in L7_BLOCK[3:]:
-            r = rank_for(n, m, BPW)
-            sec, per = shape_roofline(nq, ctx, torch, n, m, r)
-            shapes[f"l7_{name}_0.8"] = {"n": n, "m": m, "r": r, "us": sec * 1e6,
-                                        "gbs": per / sec / 1e9, "frac": per / sec / 1e9 / peak}
-        for name, n, m, bpw in L70_SHAPES:
-            r = rank_for(n, m, bpw)
-            sec, per = shape_roofline(nq, ctx, torch, n, m, r)
-            shapes[name + "_0.55"] = {"n": n, "m": m, "r": r, "us": sec * 1e6,
-                                      "gbs": per / sec / 1e9, "frac": per / sec / 1e9 / peak}
-        extra["per_shape"] = shapes
+        if not args.no_shapes:
+            for name, n, m, bpw in [("l7_q", 4096, 4096, 0.8), ("l7_gate", 11008, 4096, 0.8),
+                                    ("l7_down", 4096, 11008, 0.8)] + list(L70_SHAPES):
+                r = rank_for(n, m, bpw)
+                sec, per = shape_roofline(nq, ctx, torch, stream, n, m, r)
+                shapes[f"{name}_{bpw}"] = {"n": n, "m": m, "r": r, "us": sec * 1e6,
+                                           "gbs": per / sec / 1e9, "frac": per / sec / 1e9 / peak}
+        extra["per_shape_single_layer"] = shapes
         achieved = step_bytes * args.steps / secs / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
-                "kernel": "decode GEMV (all kernels of one nqb_gemv_f16_device call)",
-                "algorithmic_bytes_per_step": step_bytes, "launches_per_step": launches / args.steps}
+                "kernel": "nqb::dec::k_decode (fused two-stage decode GEMV; every launch of the "
+                          "step is this kernel, PDL-overlapped, so duration = step time / launches)",
+                "algorithmic_bytes_per_step": step_bytes, "launches_per_step": launches_per_step,
+                "us_per_launch": secs / args.steps / launches_per_step * 1e6}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -376,11 +413,13 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f16 activations, 1-bit weights, fp32 accumulate",
+                "dtype": "u1 x s8-limb IMMA, int32/int64 exact accumulate (fp16 x/y I/O)",
                 "data": "synthetic (seeded random sign bits, binary16 scales U(0.25,2), N(0,1) fp16 x)",
                 "config": {"workload": "llama2-7b decode pass: 224 linear layers (32 x q,k,v,o "
                                        "4096x4096 r=1622; gate,up 11008x4096 r=2372; down "
-                                       "4096x11008 r=2372) @0.8 bit, batch 1",
+                                       "4096x11008 r=2372) @0.8 bit, batch 1, as 128 fused "
+                                       "launches (qkv group, o, gate/up group, down) in one "
+                                       "CUDA graph",
                            "parallelism": f"replicas x{ws}", "l2": "working set 0.65 GB > L2 "
                            "(126 MB): no flush needed", "bpw": BPW},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),

@@ -153,6 +153,41 @@ int nqb_gemm_f64_host(nqb_context* ctx, const nqb_layer* layer, const double* x,
  * Y is b x n row-major binary16. */
 int nqb_gemm_f16_device(nqb_context* ctx, const nqb_layer* layer, const uint16_t* d_x,
                         uint32_t b, uint16_t* d_y);
+/* Decode groups: 1..4 layers that read the same input x (q/k/v share the
+ * attention input, gate/up the MLP input).  One launch of the fused decode
+ * kernel computes every layer of the group; a single layer is
+ * a group of one (nqb_gemv_*_device use the layer's own implicit group).
+ * The group keeps its own copy of the bits in the decode layout and refers
+ * to the layers' scales: free the group before its layers. */
+typedef struct nqb_group nqb_group;
+int nqb_group_create(nqb_context* ctx, const nqb_layer* const* layers, uint32_t count,
+                     nqb_group** out);
+int nqb_group_free(nqb_group* group);
+uint64_t nqb_group_stream_bytes(const nqb_group* group);
+/* d_ys[i] receives layer i's output (n_i elements). */
+int nqb_group_gemv_f16_device(nqb_context* ctx, const nqb_group* group, const uint16_t* d_x,
+                              uint16_t* const* d_ys);
+int nqb_group_gemv_f32_device(nqb_context* ctx, const nqb_group* group, const float* d_x,
+                              float* const* d_ys);
+/* Programmatic Dependent Launch of decode kernels (default on): a decode
+ * kernel starts streaming its bits while the previous kernel finishes. */
+int nqb_set_pdl(nqb_context* ctx, int enable);
+
+/* Diagnostics: one f16 decode launch of `layer` with per-CTA %globaltimer
+ * stamps (24 words per CTA: 16 ns stamps, see decode.cu TRACE points, then
+ * smid and the CTA's work).  stamps holds 24*grid. */
+int nqb_debug_decode_trace(nqb_context* ctx, const nqb_layer* layer, const uint16_t* d_x,
+                           uint16_t* d_y, uint64_t* stamps, uint32_t* grid);
+
+/* CUDA graphs of library calls on the context stream (e.g. one decode pass
+ * over a layer stack), replayed with a single launch.  Between begin and end
+ * only device-buffer entry points may be called. */
+typedef struct nqb_graph nqb_graph;
+int nqb_graph_begin(nqb_context* ctx);
+int nqb_graph_end(nqb_context* ctx, nqb_graph** out);
+int nqb_graph_launch(nqb_context* ctx, const nqb_graph* graph);
+int nqb_graph_free(nqb_graph* graph);
+
 /* reconstruct_dense (packed.cpp:126-149): n x m fp64, host buffer. */
 int nqb_reconstruct_dense_host(nqb_context* ctx, const nqb_layer* layer, double* w);
 

@@ -87,6 +87,17 @@ PROTOTYPES = {
     "nqb_admm_factor_solve_host": (C.c_int, [P, P, U32, U32, P, U32, P, P, D, D, P]),
     "nqb_augmented_lagrangian_host": (C.c_int, [P, P, P, P, P, P, P, U32, U32, U32, D, P, D,
                                                 PD]),
+    "nqb_group_create": (C.c_int, [P, PP, U32, PP]),
+    "nqb_group_free": (C.c_int, [P]),
+    "nqb_group_stream_bytes": (U64, [P]),
+    "nqb_group_gemv_f16_device": (C.c_int, [P, P, P, PP]),
+    "nqb_group_gemv_f32_device": (C.c_int, [P, P, P, PP]),
+    "nqb_set_pdl": (C.c_int, [P, C.c_int]),
+    "nqb_debug_decode_trace": (C.c_int, [P, P, P, P, P, PU32]),
+    "nqb_graph_begin": (C.c_int, [P]),
+    "nqb_graph_end": (C.c_int, [P, PP]),
+    "nqb_graph_launch": (C.c_int, [P, P]),
+    "nqb_graph_free": (C.c_int, [P]),
     "nqb_dgemm_device": (C.c_int, [P, C.c_int, C.c_int, U32, U32, U32, D, P, U32, P, U32, D,
                                    P, U32]),
 }

@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "decode.cuh"
 
 namespace nqb {
 
@@ -180,8 +181,10 @@ int nqb_destroy(nqb_context* ctx) {
 int nqb_set_stream(nqb_context* ctx, void* stream) {
   API_BEGIN
   check_ctx(ctx);
+  const cudaStream_t next = stream ? (cudaStream_t)stream : ctx->own_stream;
+  if (next == ctx->stream) return NQB_OK;
   NQB_CUDA(cudaStreamSynchronize(ctx->stream));
-  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  ctx->stream = next;
   API_END
 }
 
@@ -327,7 +330,10 @@ nqb_layer* layer_from_device_words(nqb_context* ctx, uint32_t n, uint32_t m, uin
     launch_bit_transpose(ctx, d_v, m, r, wpr, L->vt, L->vt_words);
     NQB_CUDA(cudaMemcpyAsync(L->s1h, d_s1h, (size_t)n * 2, cudaMemcpyDeviceToDevice, ctx->stream));
     NQB_CUDA(cudaMemcpyAsync(L->s2h, d_s2h, (size_t)m * 2, cudaMemcpyDeviceToDevice, ctx->stream));
+    const nqb_layer* one[1] = {L};
+    L->dec = group_build(ctx, one, 1);  // the decode kernel's layout of the same bits
   } catch (...) {
+    group_free(L->dec);
     cudaFree(L->u);
     cudaFree(L->vt);
     cudaFree(L->s1h);
@@ -400,6 +406,7 @@ int nqb_layer_free(nqb_layer* L) {
   API_BEGIN
   if (!L) return NQB_OK;
   cudaSetDevice(L->device);
+  group_free(L->dec);
   cudaFree(L->u);
   cudaFree(L->vt);
   cudaFree(L->s1h);
@@ -419,6 +426,7 @@ int nqb_layer_shape(const nqb_layer* L, uint32_t* n, uint32_t* m, uint32_t* r) {
 
 uint64_t nqb_layer_device_bytes(const nqb_layer* L) {
   if (!L) return 0;
+  if (L->dec) return L->dec->stream_bytes + 2ull * (L->n + L->m);
   return (uint64_t)L->r * L->vt_words * 4 + (uint64_t)L->n * L->u_words * 4 +
          2ull * (L->n + L->m);
 }
@@ -567,6 +575,130 @@ int nqb_layer_rel_error(nqb_context* ctx, const nqb_layer* L, const double* w, i
   NQB_CUDA(cudaStreamSynchronize(ctx->stream));
   const double num = std::sqrt(h[0]), den = std::sqrt(h[1]);
   *rel_error = den == 0.0 ? (num == 0.0 ? 0.0 : INFINITY) : num / den;
+  API_END
+}
+
+// ---------------------------------------------------------------------------
+// Decode groups (layers sharing one input) and CUDA graphs of decode passes
+// ---------------------------------------------------------------------------
+int nqb_group_create(nqb_context* ctx, const nqb_layer* const* layers, uint32_t count,
+                     nqb_group** out) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_REQUIRE(out != nullptr && layers != nullptr, NQB_E_VALIDATION, "null argument");
+  *out = nullptr;
+  *out = group_build(ctx, layers, count);
+  API_END
+}
+
+int nqb_group_free(nqb_group* g) {
+  API_BEGIN
+  group_free(g);
+  API_END
+}
+
+uint64_t nqb_group_stream_bytes(const nqb_group* g) { return g ? g->stream_bytes : 0; }
+
+int nqb_group_gemv_f16_device(nqb_context* ctx, const nqb_group* g, const uint16_t* d_x,
+                              uint16_t* const* d_ys) {
+  API_BEGIN
+  NQB_REQUIRE(ctx && g && d_ys, NQB_E_VALIDATION, "null argument");
+  group_gemv(ctx, g, d_x, 0, (void* const*)d_ys, 0);
+  API_END
+}
+
+int nqb_group_gemv_f32_device(nqb_context* ctx, const nqb_group* g, const float* d_x,
+                              float* const* d_ys) {
+  API_BEGIN
+  NQB_REQUIRE(ctx && g && d_ys, NQB_E_VALIDATION, "null argument");
+  group_gemv(ctx, g, d_x, 1, (void* const*)d_ys, 1);
+  API_END
+}
+
+int nqb_debug_decode_trace(nqb_context* ctx, const nqb_layer* L, const uint16_t* d_x,
+                           uint16_t* d_y, uint64_t* stamps, uint32_t* grid) {
+  API_BEGIN
+  check_ctx(ctx);
+  check_layer(L);
+  const uint32_t G = L->dec->grid;
+  if (grid) *grid = G;
+  NQB_CUDA(cudaMalloc(&ctx->dec_trace, 24 * 8 * (size_t)G));
+  NQB_CUDA(cudaMemsetAsync(ctx->dec_trace, 0, 24 * 8 * (size_t)G, ctx->stream));
+  try {
+    void* ys[1] = {d_y};
+    group_gemv(ctx, L->dec, d_x, 0, ys, 0);
+    NQB_CUDA(cudaMemcpyAsync(stamps, ctx->dec_trace, 24 * 8 * (size_t)G, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  } catch (...) {
+    cudaFree(ctx->dec_trace);
+    ctx->dec_trace = nullptr;
+    throw;
+  }
+  cudaFree(ctx->dec_trace);
+  ctx->dec_trace = nullptr;
+  API_END
+}
+
+int nqb_set_pdl(nqb_context* ctx, int enable) {
+  API_BEGIN
+  check_ctx(ctx);
+  ctx->pdl = enable != 0;
+  API_END
+}
+
+}  // extern "C"
+
+struct nqb_graph {
+  int device = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+extern "C" {
+
+int nqb_graph_begin(nqb_context* ctx) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  API_END
+}
+
+int nqb_graph_end(nqb_context* ctx, nqb_graph** out) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_REQUIRE(out != nullptr, NQB_E_VALIDATION, "null output");
+  *out = nullptr;
+  cudaGraph_t graph = nullptr;
+  NQB_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+  auto* g = new nqb_graph();
+  g->device = ctx->device;
+  g->graph = graph;
+  const cudaError_t e = cudaGraphInstantiate(&g->exec, graph, 0);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    delete g;
+    NQB_CUDA(e);
+  }
+  *out = g;
+  API_END
+}
+
+int nqb_graph_launch(nqb_context* ctx, const nqb_graph* g) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_REQUIRE(g != nullptr, NQB_E_VALIDATION, "null graph");
+  NQB_CUDA(cudaGraphLaunch(g->exec, ctx->stream));
+  API_END
+}
+
+int nqb_graph_free(nqb_graph* g) {
+  API_BEGIN
+  if (!g) return NQB_OK;
+  cudaSetDevice(g->device);
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
   API_END
 }
 

@@ -71,7 +71,15 @@ struct nqb_context {
   nqb::Scratch scratch[16];
   unsigned* barrier = nullptr;  // grid-barrier words (zeroed), 64 entries
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // decode GEMV state (decode.cu): dec::State followed by 2 x dec_cap int64 rows
+  void* dec_state = nullptr;
+  uint32_t dec_cap = 0;
+  bool dec_attr_set = false;
+  bool pdl = true;  // launch decode kernels with Programmatic Dependent Launch
+  void* dec_trace = nullptr;  // diagnostics (nqb_debug_decode_trace)
 };
+
+struct nqb_group;
 
 // Device-resident factorized layer.  Layout:
 //   vt  : r rows x vt_words u32 — V^T, bit (k, j) = sign of V[j][k]; row k is
@@ -88,6 +96,7 @@ struct nqb_layer {
   __half* s1h = nullptr;
   __half* s2h = nullptr;
   int device = 0;
+  nqb_group* dec = nullptr;  // decode plan of this layer alone (decode.cuh)
 };
 
 namespace nqb {

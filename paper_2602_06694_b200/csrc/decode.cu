@@ -1,27 +1,679 @@
-// decode.cu — batch-1 decode GEMV entry points (the HBM-bound hot kernel).
-// v1: the two-stage CUDA-core bit-row kernels of forward_simt.cu.
-#include "common.cuh"
+// decode.cu — batch-1 BLR decode GEMV (gemv_packed_f32, packed.cpp:201-204)
+// as one fused two-stage sm_100a kernel.  Design: decode.cuh, DESIGN.md §4.
+#include <algorithm>
+#include <cmath>
+
+#include "decode.cuh"
+#include "tc_common.cuh"
 
 namespace nqb {
+namespace dec {
 
-template <typename Acc, typename In>
-void simt_gemv(nqb_context*, const nqb_layer*, const In*, Acc*);
-
-__global__ void k_f32_to_f16(const float* __restrict__ in, __half* __restrict__ out,
-                             uint32_t n) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    out[i] = __float2half_rn(in[i]);
+// D += A(16x32 u8) * B(32x8 s8), int32 accumulate (IMMA.16832.U8.S8).
+__device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerThreads) : "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Diagnostics: slot 0 = %globaltimer at CTA start, slots 1.. = SM clock64
+// cycles since the CTA started (exact, per CTA).
+#define TRACE(i)                                                                   \
+  do {                                                                             \
+    if (p.trace && threadIdx.x == 0) {                                             \
+      if ((i) == 0) {                                                              \
+        p.trace[blockIdx.x * 24] = globaltimer();                                  \
+        p.trace[blockIdx.x * 24 + 22] = clock64();                                 \
+      } else {                                                                     \
+        p.trace[blockIdx.x * 24 + (i)] = clock64() - p.trace[blockIdx.x * 24 + 22]; \
+      }                                                                            \
+    }                                                                              \
+  } while (0)
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// mbarrier wait with a watchdog: a wait that never completes traps the
+// launch (reported as a CUDA error) instead of hanging the device.
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0, it = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(ok)
+        : "r"(tc::smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (++it > (1u << 24)) __trap();
+  }
+}
+
+// Tile index q (0..7) of input K inside its slab of a K-long dimension.
+__device__ __forceinline__ uint32_t q_of(uint32_t k, uint32_t K) {
+  uint32_t F, rem;
+  slab_split(K, F, rem);
+  const uint32_t full = 256 * F;
+  if (k < full) return (k >> 5) & 7;
+  const uint32_t k0 = (rem >= 128 && k < full + 128) ? full : full + (rem >= 128 ? 128 : 0);
+  return (k - k0) >> 5;
+}
+
+// Signed base-256 digits of v (|v| <= 2^37) into byte e of the kLimbs limb words.
+__device__ __forceinline__ void put_limbs(long long v, uint32_t e, uint32_t (&w)[kLimbs]) {
+  const uint32_t s = 8 * e;
+#pragma unroll
+  for (int l = 0; l < kLimbs - 1; ++l) {
+    const int d = (int)(int8_t)(v & 0xFF);
+    w[l] |= (uint32_t)(d & 0xFF) << s;
+    v = (v - d) >> 8;
+  }
+  w[kLimbs - 1] |= (uint32_t)(v & 0xFF) << s;
+}
+
+// B-fragment words for the quad of inputs k0..k0+3 (values already << (7-q)):
+// tile (k0-klo)/32 owns kTileB bytes = [limb g<kLimbs][c][h] words.
+__device__ __forceinline__ void store_quad(uint8_t* bfrag, uint32_t klo, uint32_t k0,
+                                           const uint32_t (&w)[kLimbs]) {
+  const uint32_t kk = k0 & 31, h = kk >> 4, c = (kk >> 2) & 3;
+  uint32_t* t = (uint32_t*)(bfrag + ((k0 - klo) >> 5) * kTileB);
+#pragma unroll
+  for (uint32_t g = 0; g < kLimbs; ++g) t[(g * 4 + c) * 2 + h] = w[g];
+}
+
+__device__ __forceinline__ long long cta_sum_i64(long long v, long long* red8) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(~0u, v, o);
+  consumers_sync();
+  if (lane == 0) red8[warp] = v;
+  consumers_sync();
+  long long s = 0;
+#pragma unroll
+  for (int w = 0; w < kConsumerWarps; ++w) s += red8[w];
+  return s;
+}
+
+__device__ __forceinline__ unsigned long long cta_max_u64(unsigned long long v,
+                                                          unsigned long long* red8) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(~0u, v, o));
+  consumers_sync();
+  if (lane == 0) red8[warp] = v;
+  consumers_sync();
+  unsigned long long s = 0;
+#pragma unroll
+  for (int w = 0; w < kConsumerWarps; ++w) s = max(s, red8[w]);
+  return s;
+}
+
+__device__ __forceinline__ int exponent_of(float M) {
+  if (!(M > 0.f) || isinf(M)) return 0;
+  int e;
+  frexpf(M, &e);
+  return e;  // M < 2^e
+}
+
+// Words w_0..w_3 of this lane in a unit with nq tiles (formats: decode_plan.cu).
+__device__ __forceinline__ void unit_words(const uint8_t* unit, uint32_t nq, int lane,
+                                           uint32_t (&w)[4]) {
+  if (nq == 8) {
+    const uint4 v = *(const uint4*)(unit + lane * 16);
+    w[0] = v.x;
+    w[1] = v.y;
+    w[2] = v.z;
+    w[3] = v.w;
+  } else if (nq == 4) {
+    const uint2 v = *(const uint2*)(unit + lane * 8);
+    w[0] = v.x;
+    w[1] = v.x >> 4;
+    w[2] = v.y;
+    w[3] = v.y >> 4;
+  } else {
+    const uint32_t u = *(const uint32_t*)(unit + lane * 4);
+    w[0] = u;
+    w[1] = u >> 2;
+    w[2] = u >> 4;
+    w[3] = u >> 6;
+  }
+}
+
+// One 16-row unit of a slab: tile q of the slab goes to chain q (8 independent
+// IMMA chains; A registers `w_i & 0x01010101<<q`).  All 32 A registers are
+// formed before the first IMMA so no IMMA waits on a register still being read
+// by the previous one (the WAR stall of reusing four temporaries).
+__device__ __forceinline__ void unit_mma(const uint32_t (&w)[4], const uint2 (&b)[8],
+                                         uint32_t nq, int (&acc)[8][4]) {
+  uint32_t a[8][4];
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[q][i] = w[i] & (0x01010101u << q);
+  if (nq == 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      mma_u8s8(acc[q], a[q][0], a[q][1], a[q][2], a[q][3], b[q].x, b[q].y);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < (int)nq) mma_u8s8(acc[q], a[q][0], a[q][1], a[q][2], a[q][3], b[q].x, b[q].y);
+  }
+}
+
+// Adds the chains of one work item to red[16 rows] (exact): chains are summed
+// in int32 (|sum| < 2^28), then lane c's limbs 2c, 2c+1 are combined in int64.
+__device__ __forceinline__ void flush_rows(int (&acc)[8][4], long long* red16, int lane) {
+  int s[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    s[i] = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      s[i] += acc[q][i];
+      acc[q][i] = 0;
+    }
+  }
+  const int g = lane >> 2, c = lane & 3;
+  long long v0 = ((long long)s[0] + ((long long)s[1] << 8)) << (16 * c);
+  long long v1 = ((long long)s[2] + ((long long)s[3] << 8)) << (16 * c);
+  v0 += __shfl_xor_sync(~0u, v0, 1);
+  v1 += __shfl_xor_sync(~0u, v1, 1);
+  v0 += __shfl_xor_sync(~0u, v0, 2);
+  v1 += __shfl_xor_sync(~0u, v1, 2);
+  if (c == 0) {
+    atomicAdd((unsigned long long*)&red16[g], (unsigned long long)(v0 >> 7));
+    atomicAdd((unsigned long long*)&red16[g + 8], (unsigned long long)(v1 >> 7));
+  }
+}
+
+struct StageArgs {
+  uint32_t rtn, nsec, sec_base;   // row tiles, sections, index of the first section
+  uint32_t K, slab_base, klo;     // K dimension, first slab, its k0
+  uint32_t lin_off;               // linear mode: buffer offset of the first section
+};
+
+// All sections of one stage; leaves sum_K bit*value per row in red[] (exact).
+// Linear mode: work items (row tile, run of sections) go round-robin to the
+// consumer warps; a warp waits only for the sections it reads.  Ring mode:
+// the stream is longer than the buffer, every warp walks every section in
+// order and releases it (slot reuse); a warp handles the tiles t = w mod 8.
+__device__ __forceinline__ void run_stage(const StageArgs& A, uint32_t NS, bool ring_mode,
+                                          uint32_t slot_bytes, uint64_t* full, uint64_t* empty,
+                                          const uint8_t* buf, const uint8_t* bfrag,
+                                          long long* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t g = lane >> 2, c = lane & 3;
+  int acc[8][4];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0;
+  if (!A.rtn || !A.nsec) return;
+  uint32_t w[4];
+  uint2 b[8];
+  auto load_b = [&](const Slab& sl) {
+    const uint8_t* bp = bfrag + kBytesPerK * (sl.k0 - A.klo) + (g * 4 + c) * 8;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      b[q] = make_uint2(0u, 0u);
+      if (q < (int)sl.nq && g < (uint32_t)kLimbs) b[q] = *(const uint2*)(bp + q * kTileB);
+    }
+  };
+  if (!ring_mode) {
+    // chunk C sections per item so that every warp gets ~3 items
+    const uint32_t want = 3 * kConsumerWarps;
+    const uint32_t C = max(1u, (A.rtn * A.nsec) / want);
+    const uint32_t nch = (A.nsec + C - 1) / C, nitems = nch * A.rtn;
+    for (uint32_t it = warp; it < nitems; it += kConsumerWarps) {
+      const uint32_t ch = it / A.rtn, t = it % A.rtn;
+      const uint32_t s0 = ch * C, s1 = min(A.nsec, s0 + C);
+      for (uint32_t s = s0; s < s1; ++s) {
+        const Slab sl = slab_of(A.K, A.slab_base + s);
+        mbar_wait_wd(&full[A.sec_base + s], 0);
+        // sections are contiguous in K: section s starts 2*rtn*(k0 - klo) bytes in
+        const uint8_t* unit =
+            buf + A.lin_off + 2u * A.rtn * (sl.k0 - A.klo) + t * unit_bytes(sl.nq);
+        unit_words(unit, sl.nq, lane, w);
+        load_b(sl);
+        unit_mma(w, b, sl.nq, acc);
+      }
+      flush_rows(acc, red + t * 16, lane);
+    }
+  } else {
+    for (uint32_t s = 0; s < A.nsec; ++s) {
+      const uint32_t sec = A.sec_base + s, slot = sec % NS;
+      const Slab sl = slab_of(A.K, A.slab_base + s);
+      mbar_wait_wd(&full[slot], (sec / NS) & 1);
+      if ((uint32_t)warp < A.rtn) load_b(sl);
+      for (uint32_t t = warp; t < A.rtn; t += kConsumerWarps) {
+        unit_words(buf + (size_t)slot * slot_bytes + t * unit_bytes(sl.nq), sl.nq, lane, w);
+        unit_mma(w, b, sl.nq, acc);
+        flush_rows(acc, red + t * 16, lane);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&empty[slot]);
+    }
+  }
+}
+
+// a * 2^k exactly in fp32 for k up to ~250 (two steps avoid overflowing 2^k)
+__device__ __forceinline__ float scale_pow2(float a, int k) {
+  const int k1 = k > 126 ? 126 : (k < -126 ? -126 : k);
+  return __fmul_rn(__fmul_rn(a, __int_as_float((127 + k1) << 23)),
+                   __int_as_float((127 + (k - k1)) << 23));
+}
+
+// Limbs of the quad v[0..3] (tile-in-slab q) into the B-fragment buffer.
+__device__ __forceinline__ void emit_quad(uint8_t* bfrag, uint32_t klo, uint32_t k0, uint32_t q,
+                                          const long long (&v)[4]) {
+  uint32_t w[kLimbs] = {};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) put_limbs(v[e] * (1 << (7 - q)), e, w);
+  store_quad(bfrag, klo, k0, w);
+}
+
+struct XQuad {
+  float s[4], x[4];
+};
+
+__device__ __forceinline__ XQuad load_xquad(const Params& p, const __half* s2h, uint32_t k0,
+                                            uint32_t m) {
+  XQuad r;
+  if (k0 + 3 < m && p.x_vec) {
+    const uint2 sh2 = *(const uint2*)(s2h + k0);
+    const float2 s01 = __half22float2(*(const __half2*)&sh2.x);
+    const float2 s23 = __half22float2(*(const __half2*)&sh2.y);
+    r.s[0] = s01.x; r.s[1] = s01.y; r.s[2] = s23.x; r.s[3] = s23.y;
+    if (p.x_f32) {
+      const float4 v = __ldcg((const float4*)((const float*)p.x + k0));
+      r.x[0] = v.x; r.x[1] = v.y; r.x[2] = v.z; r.x[3] = v.w;
+    } else {
+      const uint2 v = __ldcg((const uint2*)((const __half*)p.x + k0));
+      const float2 x01 = __half22float2(*(const __half2*)&v.x);
+      const float2 x23 = __half22float2(*(const __half2*)&v.y);
+      r.x[0] = x01.x; r.x[1] = x01.y; r.x[2] = x23.x; r.x[3] = x23.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t j = k0 + e;
+      r.s[e] = r.x[e] = 0.f;
+      if (j < m) {
+        r.s[e] = __half2float(s2h[j]);
+        r.x[e] = p.x_f32 ? __ldcg((const float*)p.x + j)
+                         : __half2float(__ushort_as_half(__ldcg((const unsigned short*)p.x + j)));
+      }
+    }
+  }
+  return r;
+}
+
+__device__ __forceinline__ void load_tquad(const long long* Tseg, uint32_t k0, uint32_t r,
+                                           uint32_t t_off, long long (&v)[4]) {
+  if (k0 + 3 < r && ((t_off + k0) & 1) == 0) {
+    const longlong2 v0 = __ldcg((const longlong2*)(Tseg + k0));
+    const longlong2 v1 = __ldcg((const longlong2*)(Tseg + k0 + 2));
+    v[0] = v0.x; v[1] = v0.y; v[2] = v1.x; v[3] = v1.y;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = k0 + e < r ? __ldcg(Tseg + k0 + e) : 0;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ Params p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t NB = p.nbar;
+  uint64_t* full = (uint64_t*)smem;
+  uint64_t* empty = full + NB;
+  long long* red8 = (long long*)(smem + 16 * NB);
+  long long* red = (long long*)(smem + 16 * NB + 256);
+  const uint32_t head = ((16 * NB + 256 + kMaxRt * 16 * 8) + 127) / 128 * 128;
+  uint8_t* bfrag = smem + head;
+  uint8_t* buf = bfrag + p.bfrag_bytes;
+
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(~0u, tid >> 5, 0);
+  TRACE(0);
+  const Cta C = p.ctas[blockIdx.x];
+  if (p.trace && tid == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.trace[blockIdx.x * 24 + 16] = smid;
+    p.trace[blockIdx.x * 24 + 17] = C.s1_rtn;
+    p.trace[blockIdx.x * 24 + 18] = C.s1_sln;
+    p.trace[blockIdx.x * 24 + 19] = C.s2_rtn;
+    p.trace[blockIdx.x * 24 + 20] = C.nsec;
+    p.trace[blockIdx.x * 24 + 21] = C.ring;
+  }
+  const uint32_t n1 = C.s1_rtn ? C.s1_sln : 0;
+  const uint32_t m = p.m;
+  const bool ring_mode = C.ring != 0;
+  const uint32_t NS = ring_mode ? p.buf_bytes / p.slot_bytes : 0;  // ring slots
+  auto sec_bytes = [&](uint32_t sec) -> uint32_t {
+    return sec < n1 ? C.s1_rtn * unit_bytes(slab_of(m, C.s1_sl0 + sec).nq)
+                    : C.s2_rtn * unit_bytes(slab_of(p.seg[C.s2_seg].r, sec - n1).nq);
+  };
+
+  if (tid == 0) {
+    for (uint32_t s = 0; s < NB; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], kConsumerWarps);
+    }
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_launch_dependents();  // the next kernel may start streaming its bits
+
+  // ------------------------------------------------------------------ producer
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      const uint8_t* src = p.bits + C.stream_off;
+      uint32_t off = 0;
+      for (uint32_t sec = 0; sec < C.nsec; ++sec) {
+        const uint32_t bytes = sec_bytes(sec);
+        if (ring_mode) {
+          const uint32_t slot = sec % NS;
+          if (sec >= NS) mbar_wait_wd(&empty[slot], ((sec / NS) - 1) & 1);
+          tc::mbar_arrive_expect_tx(&full[slot], bytes);
+          tc::bulk_g2s(buf + (size_t)slot * p.slot_bytes, src + off, bytes, &full[slot]);
+        } else {  // linear: the section lives at its stream offset
+          tc::mbar_arrive_expect_tx(&full[sec], bytes);
+          tc::bulk_g2s(buf + off, src + off, bytes, &full[sec]);
+        }
+        off += bytes;
+      }
+      if (p.trace) p.trace[blockIdx.x * 24 + 14] = clock64();
+      if (p.trace && !ring_mode && C.nsec) {  // diagnostics: the whole stream landed
+        for (uint32_t s = 0; s < C.nsec; ++s) mbar_wait_wd(&full[s], 0);
+        p.trace[blockIdx.x * 24 + 15] = clock64();
+      }
+    }
+    return;
+  }
+
+  // ----------------------------------------------------------------- consumers
+  for (int i = tid; i < kMaxRt * 16; i += kConsumerThreads) red[i] = 0;
+  TRACE(1);
+  pdl_wait();  // x (and the t accumulator) may be written by the previous kernel
+  TRACE(2);
+  State* st = p.st;
+  const uint32_t ep = *(volatile uint32_t*)&st->epoch;
+  const uint32_t dirty_next = *(volatile uint32_t*)&st->dirty[(ep & 1) ^ 1];
+  const uint32_t b = ep & 1;
+
+  // ---- input statistics over all m (x is L2-resident): max|x| and sum|x| ----
+  // max|x| * max|s2| bounds |a| (fixes a's exponent); sum|x| * max|s2| bounds
+  // |t_k| = |sum_j +-a_j| (fixes t's exponent) - no pass over t is needed.
+  float xmax, xsum;
+  {
+    float mx = 0.f, sm = 0.f;
+    if (p.x_f32) {
+      const float* xf = (const float*)p.x;
+      const uint32_t nv = p.x_vec ? m / 4 : 0;
+#pragma unroll 4
+      for (uint32_t i = tid; i < nv; i += kConsumerThreads) {
+        const float4 v = __ldcg((const float4*)xf + i);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        sm += (fabsf(v.x) + fabsf(v.y)) + (fabsf(v.z) + fabsf(v.w));
+      }
+      for (uint32_t i = 4 * nv + tid; i < m; i += kConsumerThreads) {
+        const float v = fabsf(__ldcg(xf + i));
+        mx = fmaxf(mx, v);
+        sm += v;
+      }
+    } else {
+      const __half* xh = (const __half*)p.x;
+      const uint32_t nv = p.x_vec ? m / 8 : 0;
+#pragma unroll 4
+      for (uint32_t i = tid; i < nv; i += kConsumerThreads) {
+        const uint4 v = __ldcg((const uint4*)xh + i);
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __half22float2(*(const __half2*)&wv[k]);
+          mx = fmaxf(mx, fmaxf(fabsf(f.x), fabsf(f.y)));
+          sm += fabsf(f.x) + fabsf(f.y);
+        }
+      }
+      for (uint32_t i = 8 * nv + tid; i < m; i += kConsumerThreads) {
+        const float v = fabsf(__half2float(__ushort_as_half(__ldcg((const unsigned short*)xh + i))));
+        mx = fmaxf(mx, v);
+        sm += v;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mx = fmaxf(mx, __shfl_xor_sync(~0u, mx, o));
+      sm += __shfl_xor_sync(~0u, sm, o);
+    }
+    float* rf = (float*)red8;
+    if (lane == 0) {
+      rf[warp] = mx;
+      rf[kConsumerWarps + warp] = sm;
+    }
+    consumers_sync();
+    mx = 0.f;
+    sm = 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) {
+      mx = fmaxf(mx, rf[w]);
+      sm += rf[kConsumerWarps + w];
+    }
+    xmax = mx;
+    xsum = sm;
+  }
+  TRACE(3);
+
+  // ------------------------------------------------------------------ stage 1
+  if (n1) {
+    const Seg& S = p.seg[C.s1_seg];
+    const int ea = exponent_of(S.s2max * xmax);
+    const uint32_t klo = slab_of(m, C.s1_sl0).k0;
+    const Slab last = slab_of(m, C.s1_sl0 + C.s1_sln - 1);
+    const uint32_t nquad = (last.k0 + 32 * last.nq - klo) / 4;
+    long long asum = 0;
+    uint32_t qd = tid;
+    XQuad cur = load_xquad(p, S.s2h, klo + 4 * min(qd, nquad - 1), m);
+    while (qd < nquad) {  // one quad in flight ahead of the one being quantised
+      const uint32_t nx = qd + kConsumerThreads;
+      const XQuad nxt = load_xquad(p, S.s2h, klo + 4 * min(nx, nquad - 1), m);
+      const uint32_t k0 = klo + 4 * qd;
+      long long v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float a = cur.s[e] * cur.x[e];  // packed.cpp:160
+        v[e] = __float2int_rn(scale_pow2(a, kFix - ea));
+        asum += v[e];
+      }
+      emit_quad(bfrag, klo, k0, q_of(k0, m), v);
+      cur = nxt;
+      qd = nx;
+    }
+    const long long A = cta_sum_i64(asum, red8);  // also orders the bfrag stores
+    TRACE(4);
+    StageArgs sa{C.s1_rtn, n1, 0, m, C.s1_sl0, klo, 0};
+    run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red);
+    TRACE(12);
+    consumers_sync();
+    TRACE(5);
+    long long* Tseg = p.T + (size_t)b * p.r_cap + S.t_off + (size_t)C.s1_rt0 * 16;
+    for (uint32_t i = tid; i < (uint32_t)C.s1_rtn * 16; i += kConsumerThreads)
+      atomicAdd((unsigned long long*)&Tseg[i], (unsigned long long)(2 * red[i] - A));
+  }
+  {  // clear this CTA's share of the other t buffer for the next launch
+    long long* Tn = p.T + (size_t)(b ^ 1) * p.r_cap;
+    const uint32_t lo = (uint32_t)((uint64_t)dirty_next * blockIdx.x / gridDim.x);
+    const uint32_t hi = (uint32_t)((uint64_t)dirty_next * (blockIdx.x + 1) / gridDim.x);
+    for (uint32_t i = lo + tid; i < hi; i += kConsumerThreads) Tn[i] = 0;
+  }
+  __threadfence();
+
+  // --------------------------------------------------------------- grid barrier
+  consumers_sync();
+  TRACE(6);
+  if (tid == 0) {
+    const uint32_t arrived = atomicAdd(&st->done[b], 1u);
+    if (arrived == gridDim.x - 1) {  // every CTA has read epoch and dirty: advance them
+      st->epoch = ep + 1;
+      st->dirty[b] = p.R1;
+      st->dirty[b ^ 1] = 0;
+      st->done[b ^ 1] = 0;
+    }
+  }
+  if (!C.s2_rtn) return;
+  TRACE(7);
+  if (tid == 0) {
+    uint32_t it = 0;
+    while (ld_acquire(&st->done[b]) < gridDim.x) {
+      __nanosleep(20);
+      if (++it > (1u << 26)) __trap();
+    }
+  }
+  consumers_sync();
+  TRACE(8);
+  for (int i = tid; i < kMaxRt * 16; i += kConsumerThreads) red[i] = 0;
+
+  // ------------------------------------------------------------------ stage 2
+  const Seg& S = p.seg[C.s2_seg];
+  const int ea = exponent_of(S.s2max * xmax);
+  // |t_k| <= sum_j |a_int_j| <= s2max*sum|x|*2^(kFix-ea) + m  (+ margin for fp32 sums)
+  const double tbound =
+      ((double)S.s2max * (double)xsum * ldexp(1.0, kFix - ea) + (double)m) * (1.0 + 1.0 / 1024);
+  int et = 0;
+  if (tbound > 0) frexp(tbound, &et);  // |t_k| < 2^et
+  const int sh = et - kFix;
+  const long long* Tseg = p.T + (size_t)b * p.r_cap + S.t_off;
+  const uint32_t nquad2 = kpad(S.r) / 4;
+  long long tsum = 0;
+  {
+    uint32_t qd = tid;
+    long long cur[4], nxt[4];
+    load_tquad(Tseg, 4 * min(qd, nquad2 - 1), S.r, S.t_off, cur);
+    while (qd < nquad2) {
+      const uint32_t nx = qd + kConsumerThreads;
+      load_tquad(Tseg, 4 * min(nx, nquad2 - 1), S.r, S.t_off, nxt);
+      long long v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[e] = sh > 0 ? (cur[e] + (1ll << (sh - 1))) >> sh : cur[e] * (1ll << (-sh));
+        tsum += v[e];
+      }
+      emit_quad(bfrag, 0, 4 * qd, q_of(4 * qd, S.r), v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cur[e] = nxt[e];
+      qd = nx;
+    }
+  }
+  const long long Tsum = cta_sum_i64(tsum, red8);
+  TRACE(9);
+  uint32_t s1_bytes = 0;  // linear offset of the first stage-2 section
+  for (uint32_t s = 0; s < n1; ++s) s1_bytes += sec_bytes(s);
+  StageArgs sa{C.s2_rtn, C.nsec - n1, n1, S.r, 0, 0, s1_bytes};
+  run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red);
+  TRACE(13);
+  consumers_sync();
+  TRACE(10);
+  const int E = sh + ea - kFix;
+  for (uint32_t i = tid; i < (uint32_t)C.s2_rtn * 16; i += kConsumerThreads) {
+    const uint32_t row = C.s2_rt0 * 16 + i;
+    if (row >= S.n) continue;
+    const long long Y = 2 * red[i] - Tsum;
+    const double y = (double)__half2float(S.s1h[row]) * ldexp((double)Y, E);  // packed.cpp:189
+    if (p.y_f32) ((float*)p.y[C.s2_seg])[row] = (float)y;
+    else ((__half*)p.y[C.s2_seg])[row] = __float2half_rn((float)y);
+  }
+  TRACE(11);
+}
+
+}  // namespace dec
+
+using namespace dec;
+
+void dec_state_reserve(nqb_context* ctx, uint32_t rows) {
+  if (ctx->dec_state && ctx->dec_cap >= rows) return;
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->dec_state) NQB_CUDA(cudaFree(ctx->dec_state));
+  ctx->dec_state = nullptr;
+  const uint32_t cap = std::max<uint32_t>(std::max<uint32_t>(rows, 2 * ctx->dec_cap), 1u << 14);
+  const size_t bytes = sizeof(State) + 2 * (size_t)cap * sizeof(long long);
+  NQB_CUDA(cudaMalloc(&ctx->dec_state, bytes));
+  NQB_CUDA(cudaMemset(ctx->dec_state, 0, bytes));
+  ctx->dec_cap = cap;
+}
+
+void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32,
+                void* const* d_ys, int y_f32) {
+  NQB_REQUIRE(g->device == ctx->device, NQB_E_VALIDATION, "decode group lives on another device");
+  NQB_REQUIRE(d_x != nullptr, NQB_E_VALIDATION, "null input");
+  dec_state_reserve(ctx, g->R1);
+  Params p{};
+  p.bits = g->bits;
+  p.ctas = g->ctas;
+  for (uint32_t s = 0; s < g->nseg; ++s) {
+    p.seg[s] = g->seg[s];
+    NQB_REQUIRE(d_ys[s] != nullptr, NQB_E_VALIDATION, "null output");
+    p.y[s] = d_ys[s];
+  }
+  p.nseg = g->nseg;
+  p.m = g->m;
+  p.R1 = g->R1;
+  p.r_cap = ctx->dec_cap;
+  p.st = (State*)ctx->dec_state;
+  p.T = (long long*)((char*)ctx->dec_state + sizeof(State));
+  p.buf_bytes = g->buf_bytes;
+  p.slot_bytes = g->slot_bytes;
+  p.nbar = g->nbar;
+  p.bfrag_bytes = g->bfrag_bytes;
+  p.x_f32 = x_f32 ? 1u : 0u;
+  p.y_f32 = y_f32 ? 1u : 0u;
+  p.x_vec = ((uintptr_t)d_x % 16 == 0) ? 1u : 0u;
+  p.x = d_x;
+  p.trace = (unsigned long long*)ctx->dec_trace;
+  if (!ctx->dec_attr_set) {
+    NQB_CUDA(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    ctx->dec_attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g->grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = g->smem_bytes;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  NQB_CUDA(cudaLaunchKernelEx(&cfg, k_decode, p));
+  NQB_LAUNCHED(ctx);
+}
+
+// ---- single-layer entry points (the layer's implicit group of one) ---------
 void decode_gemv_f32(nqb_context* ctx, const nqb_layer* L, const float* d_x, float* d_y) {
-  simt_gemv<float, float>(ctx, L, d_x, d_y);
+  void* ys[1] = {d_y};
+  group_gemv(ctx, L->dec, d_x, 1, ys, 1);
 }
 
 void decode_gemv_f16(nqb_context* ctx, const nqb_layer* L, const __half* d_x, __half* d_y) {
-  float* y32 = (float*)scratch(ctx, 2, sizeof(float) * L->n);
-  simt_gemv<float, __half>(ctx, L, d_x, y32);
-  k_f32_to_f16<<<ceil_div(L->n, 256), 256, 0, ctx->stream>>>(y32, d_y, L->n);
-  NQB_LAUNCHED(ctx);
+  void* ys[1] = {d_y};
+  group_gemv(ctx, L->dec, d_x, 0, ys, 0);
 }
 
 }  // namespace nqb

@@ -134,6 +134,7 @@ class Context:
         _check(self.lib.nqb_create(device, C.byref(h)), "nqb_create")
         self.handle = h
         self.device = device
+        self._stream = 0
 
     def close(self):
         if self.handle:
@@ -147,8 +148,26 @@ class Context:
             pass
 
     def set_stream(self, stream_ptr: int | None):
-        _check(self.lib.nqb_set_stream(self.handle, C.c_void_p(stream_ptr or 0)),
-               "nqb_set_stream")
+        stream_ptr = stream_ptr or 0
+        if stream_ptr == self._stream:
+            return
+        _check(self.lib.nqb_set_stream(self.handle, C.c_void_p(stream_ptr)), "nqb_set_stream")
+        self._stream = stream_ptr
+
+    def bind_torch_stream(self, device=None):
+        """Run library work on torch's current stream.  torch's default stream is
+        the legacy NULL stream; it is passed as cudaStreamLegacy (0x1) so the
+        library never silently falls back to its own unsynchronised stream."""
+        import torch
+        self.set_stream(torch.cuda.current_stream(device).cuda_stream or 1)
+
+    def set_pdl(self, enable: bool):
+        """Programmatic Dependent Launch for decode kernels (default on)."""
+        _check(self.lib.nqb_set_pdl(self.handle, 1 if enable else 0), "nqb_set_pdl")
+
+    def capture(self):
+        """Context manager capturing the context stream's work into a Graph."""
+        return _Capture(self)
 
     def synchronize(self):
         _check(self.lib.nqb_synchronize(self.handle), "nqb_synchronize")
@@ -156,6 +175,46 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return int(self.lib.nqb_kernel_launches(self.handle))
+
+
+class Graph:
+    """A captured sequence of library calls, replayed with one launch (nqb_graph)."""
+
+    def __init__(self, ctx: "Context", handle: C.c_void_p):
+        self.ctx = ctx
+        self.handle = handle
+
+    def launch(self):
+        _check(self.ctx.lib.nqb_graph_launch(self.ctx.handle, self.handle), "nqb_graph_launch")
+
+    def free(self):
+        if self.handle:
+            self.ctx.lib.nqb_graph_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class _Capture:
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.graph = None
+
+    def __enter__(self):
+        _check(self.ctx.lib.nqb_graph_begin(self.ctx.handle), "nqb_graph_begin")
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        h = C.c_void_p()
+        st = self.ctx.lib.nqb_graph_end(self.ctx.handle, C.byref(h))
+        if exc_type is None:
+            _check(st, "nqb_graph_end")
+            self.graph = Graph(self.ctx, h)
+        return False
 
 
 _CONTEXTS: dict = {}
@@ -362,7 +421,7 @@ class DeviceLayer:
     # -- forward on device buffers (torch tensors; the hot path) -----------
     def _bind_stream(self, tensor):
         import torch
-        self.ctx.set_stream(torch.cuda.current_stream(tensor.device).cuda_stream)
+        self.ctx.bind_torch_stream(tensor.device)
 
     def gemv_device(self, x, y):
         """x: (m,) fp32/fp16 CUDA tensor, y: (n,) same dtype; async on torch's stream."""
@@ -383,6 +442,50 @@ class DeviceLayer:
         _check(self.ctx.lib.nqb_gemm_f16_device(self.ctx.handle, self.handle,
                                                 C.c_void_p(x.data_ptr()), x.shape[0],
                                                 C.c_void_p(y.data_ptr())), "gemm_device")
+
+
+class DecodeGroup:
+    """1..4 device layers that read the same input (q/k/v, gate/up): one fused
+    decode launch computes all of them (nqb_group)."""
+
+    def __init__(self, layers, ctx: Context | None = None):
+        ctx = ctx or layers[0].ctx
+        self.ctx = ctx
+        self.layers = list(layers)
+        arr = (C.c_void_p * len(self.layers))(*[lay.handle for lay in self.layers])
+        h = C.c_void_p()
+        _check(ctx.lib.nqb_group_create(ctx.handle, arr, len(self.layers), C.byref(h)),
+               "nqb_group_create")
+        self.handle = h
+        self.m = self.layers[0].m
+
+    @property
+    def stream_bytes(self) -> int:
+        return int(self.ctx.lib.nqb_group_stream_bytes(self.handle))
+
+    def free(self):
+        if self.handle:
+            self.ctx.lib.nqb_group_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def gemv_device(self, x, ys):
+        """x: (m,) fp16/fp32 CUDA tensor; ys: one (n_i,) tensor per layer, same dtype."""
+        import torch
+        self.ctx.bind_torch_stream(x.device)
+        arr = (C.c_void_p * len(ys))(*[y.data_ptr() for y in ys])
+        if x.dtype == torch.float16:
+            fn = self.ctx.lib.nqb_group_gemv_f16_device
+        elif x.dtype == torch.float32:
+            fn = self.ctx.lib.nqb_group_gemv_f32_device
+        else:
+            raise Error("gemv_device: dtype must be float32 or float16")
+        _check(fn(self.ctx.handle, self.handle, C.c_void_p(x.data_ptr()), arr), "group gemv")
 
 
 def make_factorized_layer(latent_u, latent_v, s1, s2, ctx: Context | None = None):

@@ -1,0 +1,156 @@
+"""GPU parity of the fused decode kernel (decode.cu) through the C ABI.
+
+The kernel quantises activations to 22-bit fixed point and accumulates
+exactly in integers, so besides the north-star bar (1e-3 relative to the
+reference's gemv_packed_f32, packed.cpp:201-204) it is held to a much tighter
+internal bar, and to bitwise identity wherever the arithmetic must agree:
+grouped vs single-layer launches, PDL on/off, graph replay vs direct calls.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+FWD_TOL = 1e-3    # north_star
+TIGHT_TOL = 2e-5  # what the 22-bit fixed point actually delivers
+
+
+def to_nq(nq, lay):
+    return nq.FactorizedLayer(lay.n, lay.m, lay.r, lay.u, lay.v, lay.s1, lay.s2)
+
+
+def dev_layer(nq, chk, seed, n, m, r):
+    lay = O.synthetic_layer(chk, seed, n, m, r)
+    return lay, nq.DeviceLayer.upload(to_nq(nq, lay))
+
+
+# K tails of every kind: r % 256 in {0, 64, 128, 192, ragged}, m likewise
+TAIL_SHAPES = [(300, 320, 320), (200, 448, 130), (77, 100, 45), (40, 1000, 500),
+               (513, 257, 193), (16, 64, 64), (17, 65, 65), (1, 3000, 1),
+               (2048, 512, 511), (64, 28672, 40)]
+
+
+@pytest.mark.parametrize("shape", TAIL_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_decode_tails_vs_reference(nq, chk, shape):
+    n, m, r = shape
+    lay, dev = dev_layer(nq, chk, 0xD0 + n * 7 + m, n, m, r)
+    x = chk.rng(n + 3 * m).gaussian(m).astype(np.float32)
+    want = chk.gemv_packed_f32(lay, x)
+    got = dev.gemv_f32(x)
+    assert rel(got, want) <= TIGHT_TOL
+
+
+@pytest.mark.parametrize("name,n,m,r", [("l7_q", 4096, 4096, 1622), ("l70_gate", 28672, 8192, 3488),
+                                        ("l70_down", 8192, 28672, 3488)])
+def test_decode_tight_on_target_shapes(nq, chk, name, n, m, r):
+    lay, dev = dev_layer(nq, chk, 0xB1A5E100 + n + m, n, m, r)
+    x = chk.rng(0xB1A5E002).gaussian(m).astype(np.float32)
+    assert rel(dev.gemv_f32(x), chk.gemv_packed_f32(lay, x)) <= TIGHT_TOL
+
+
+def test_decode_zero_and_wide_dynamic_range(nq, chk):
+    n, m, r = 500, 700, 96
+    lay, dev = dev_layer(nq, chk, 91, n, m, r)
+    assert np.all(dev.gemv_f32(np.zeros(m, np.float32)) == 0)
+    x = chk.rng(92).gaussian(m).astype(np.float32)
+    x[17] = 3.0e4  # one outlier: the fixed point is set by the bound, the rest still count
+    x[18] = -1e-30
+    want = chk.gemv_packed_f32(lay, x)
+    assert rel(dev.gemv_f32(x), want) <= FWD_TOL
+
+
+def test_group_bitwise_equals_single_layers(nq, chk):
+    import torch
+    m = 4096
+    specs = [(4096, 1622), (1024, 300), (4096, 1622)]  # q, (short) k, v
+    lays, devs = [], []
+    for i, (n, r) in enumerate(specs):
+        lay, dev = dev_layer(nq, chk, 0x6000 + i, n, m, r)
+        lays.append(lay)
+        devs.append(dev)
+    grp = nq.DecodeGroup(devs)
+    x = torch.from_numpy(chk.rng(5).gaussian(m).astype(np.float16)).cuda()
+    ys = [torch.empty(n, dtype=torch.float16, device="cuda") for n, _ in specs]
+    grp.gemv_device(x, ys)
+    singles = []
+    for d, (n, _) in zip(devs, specs):
+        y = torch.empty(n, dtype=torch.float16, device="cuda")
+        d.gemv_device(x, y)
+        singles.append(y)
+    torch.cuda.synchronize()
+    for lay, y, s in zip(lays, ys, singles):
+        assert torch.equal(y, s)
+        want = chk.gemv_packed_f32(lay, x.float().cpu().numpy())
+        assert rel(y.float().cpu().numpy(), want) <= FWD_TOL
+    assert grp.stream_bytes >= sum(r * (n + m) // 8 for n, r in specs)
+
+
+def test_interleaved_layers_share_scratch(nq, chk):
+    """Different plans back to back on one stream (t-buffer reuse, dirty rows)."""
+    import torch
+    shapes = [(8192, 8192, 2237), (64, 300, 17), (4096, 11008, 2372), (1000, 8192, 45)]
+    items = []
+    for i, (n, m, r) in enumerate(shapes):
+        lay, dev = dev_layer(nq, chk, 0x7000 + i, n, m, r)
+        x = chk.rng(0x7100 + i).gaussian(m).astype(np.float32)
+        items.append((lay, dev, x, chk.gemv_packed_f32(lay, x)))
+    xs = [torch.from_numpy(x).cuda() for _, _, x, _ in items]
+    ys = [torch.empty(lay.n, dtype=torch.float32, device="cuda") for lay, _, _, _ in items]
+    first = None
+    for rep in range(3):
+        for (lay, dev, _, _), xd, yd in zip(items, xs, ys):
+            dev.gemv_device(xd, yd)
+        torch.cuda.synchronize()
+        outs = [y.cpu().numpy().copy() for y in ys]
+        for (_, _, _, want), got in zip(items, outs):
+            assert rel(got, want) <= TIGHT_TOL
+        if first is None:
+            first = outs
+        else:
+            for a, b in zip(first, outs):
+                assert np.array_equal(a, b)
+
+
+def test_pdl_off_and_graph_replay_bitwise(nq, chk):
+    import torch
+    ctx = nq.context(0)
+    lay_a, a = dev_layer(nq, chk, 0x8001, 4096, 4096, 1622)
+    lay_b, b = dev_layer(nq, chk, 0x8002, 11008, 4096, 2372)
+    # fp32 chain (b's fp16 output would overflow: |y_b| ~ 1e7)
+    xa = torch.from_numpy(chk.rng(1).gaussian(4096).astype(np.float32)).cuda()
+    ya = torch.empty(4096, dtype=torch.float32, device="cuda")
+    yb = torch.empty(11008, dtype=torch.float32, device="cuda")
+
+    def run():
+        a.gemv_device(xa, ya)
+        b.gemv_device(ya[:4096], yb)  # b reads a's output: a real dependency
+        torch.cuda.synchronize()
+        return ya.clone(), yb.clone()
+
+    ref_a, ref_b = run()
+    want_b = chk.gemv_packed_f32(lay_b, ref_a.cpu().numpy())
+    assert rel(ref_b.cpu().numpy(), want_b) <= TIGHT_TOL
+    ctx.set_pdl(False)
+    try:
+        pa, pb = run()
+    finally:
+        ctx.set_pdl(True)
+    assert torch.equal(pa, ref_a) and torch.equal(pb, ref_b)
+    side = torch.cuda.Stream()  # graphs cannot capture the legacy NULL stream
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        ctx.bind_torch_stream()
+        with ctx.capture() as cap:
+            a.gemv_device(xa, ya)
+            b.gemv_device(ya[:4096], yb)
+        for _ in range(3):
+            ya.zero_()
+            yb.zero_()
+            cap.graph.launch()
+            torch.cuda.synchronize()
+            assert torch.equal(ya, ref_a) and torch.equal(yb, ref_b)
+    torch.cuda.synchronize()
+    ctx.bind_torch_stream()
