@@ -174,8 +174,8 @@ int nqb_group_gemv_f32_device(nqb_context* ctx, const nqb_group* group, const fl
 int nqb_set_pdl(nqb_context* ctx, int enable);
 
 /* Diagnostics: one f16 decode launch of `layer` with per-CTA %globaltimer
- * stamps (24 words per CTA: 16 ns stamps, see decode.cu TRACE points, then
- * smid and the CTA's work).  stamps holds 24*grid. */
+ * stamps (32 words per CTA: 16 ns stamps, see decode.cu TRACE points, then
+ * smid and the CTA's work).  stamps holds 32*grid. */
 int nqb_debug_decode_trace(nqb_context* ctx, const nqb_layer* layer, const uint16_t* d_x,
                            uint16_t* d_y, uint64_t* stamps, uint32_t* grid);
 

@@ -622,12 +622,12 @@ int nqb_debug_decode_trace(nqb_context* ctx, const nqb_layer* L, const uint16_t*
   check_layer(L);
   const uint32_t G = L->dec->grid;
   if (grid) *grid = G;
-  NQB_CUDA(cudaMalloc(&ctx->dec_trace, 24 * 8 * (size_t)G));
-  NQB_CUDA(cudaMemsetAsync(ctx->dec_trace, 0, 24 * 8 * (size_t)G, ctx->stream));
+  NQB_CUDA(cudaMalloc(&ctx->dec_trace, 32 * 8 * (size_t)G));
+  NQB_CUDA(cudaMemsetAsync(ctx->dec_trace, 0, 32 * 8 * (size_t)G, ctx->stream));
   try {
     void* ys[1] = {d_y};
     group_gemv(ctx, L->dec, d_x, 0, ys, 0);
-    NQB_CUDA(cudaMemcpyAsync(stamps, ctx->dec_trace, 24 * 8 * (size_t)G, cudaMemcpyDeviceToHost,
+    NQB_CUDA(cudaMemcpyAsync(stamps, ctx->dec_trace, 32 * 8 * (size_t)G, cudaMemcpyDeviceToHost,
                              ctx->stream));
     NQB_CUDA(cudaStreamSynchronize(ctx->stream));
   } catch (...) {

@@ -31,17 +31,17 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 // Diagnostics: slot 0 = %globaltimer at CTA start, slots 1.. = SM clock64
-// cycles since the CTA started (exact, per CTA).
-#define TRACE(i)                                                                   \
-  do {                                                                             \
-    if (p.trace && threadIdx.x == 0) {                                             \
-      if ((i) == 0) {                                                              \
-        p.trace[blockIdx.x * 24] = globaltimer();                                  \
-        p.trace[blockIdx.x * 24 + 22] = clock64();                                 \
-      } else {                                                                     \
-        p.trace[blockIdx.x * 24 + (i)] = clock64() - p.trace[blockIdx.x * 24 + 22]; \
-      }                                                                            \
-    }                                                                              \
+// cycles since the CTA started (exact, per CTA; the base stays in a register).
+#define TRACE(i)                                                                  \
+  do {                                                                            \
+    if (p.trace && threadIdx.x == 0) {                                            \
+      if ((i) == 0) {                                                             \
+        trace_t0 = clock64();                                                     \
+        p.trace[blockIdx.x * 32] = globaltimer();                                 \
+      } else {                                                                    \
+        p.trace[blockIdx.x * 32 + (i)] = clock64() - trace_t0;                    \
+      }                                                                           \
+    }                                                                             \
   } while (0)
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
@@ -157,40 +157,17 @@ __device__ __forceinline__ void unit_words(const uint8_t* unit, uint32_t nq, int
   }
 }
 
-// One 16-row unit of a slab: tile q of the slab goes to chain q (8 independent
-// IMMA chains; A registers `w_i & 0x01010101<<q`).  All 32 A registers are
-// formed before the first IMMA so no IMMA waits on a register still being read
-// by the previous one (the WAR stall of reusing four temporaries).
-__device__ __forceinline__ void unit_mma(const uint32_t (&w)[4], const uint2 (&b)[8],
-                                         uint32_t nq, int (&acc)[8][4]) {
-  uint32_t a[8][4];
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a[q][i] = w[i] & (0x01010101u << q);
-  if (nq == 8) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      mma_u8s8(acc[q], a[q][0], a[q][1], a[q][2], a[q][3], b[q].x, b[q].y);
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (q < (int)nq) mma_u8s8(acc[q], a[q][0], a[q][1], a[q][2], a[q][3], b[q].x, b[q].y);
-  }
-}
-
-// Adds the chains of one work item to red[16 rows] (exact): chains are summed
-// in int32 (|sum| < 2^28), then lane c's limbs 2c, 2c+1 are combined in int64.
-__device__ __forceinline__ void flush_rows(int (&acc)[8][4], long long* red16, int lane) {
+// Adds 4 accumulator chains of one row tile to red[16 rows] (exact): chains
+// are summed in int32 (|sum| < 2^30), then lane c's limbs 2c, 2c+1 are
+// combined in int64 (two's-complement wraparound is harmless: the true value
+// fits).
+__device__ __forceinline__ void flush_rows(int (&acc)[4][4], long long* red16, int lane) {
   int s[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    s[i] = 0;
+    s[i] = acc[0][i] + acc[1][i] + acc[2][i] + acc[3][i];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      s[i] += acc[q][i];
-      acc[q][i] = 0;
-    }
+    for (int q = 0; q < 4; ++q) acc[q][i] = 0;
   }
   const int g = lane >> 2, c = lane & 3;
   long long v0 = ((long long)s[0] + ((long long)s[1] << 8)) << (16 * c);
@@ -211,61 +188,101 @@ struct StageArgs {
   uint32_t lin_off;               // linear mode: buffer offset of the first section
 };
 
+// B fragments of one slab for this lane: b[q] = limbs g of the 4-input groups
+// 4c.. and 16+4c.. of tile q (lanes g >= kLimbs feed zero columns).
+__device__ __forceinline__ void load_b(const uint8_t* bfrag, uint32_t klo, const Slab& sl,
+                                       uint32_t g, uint32_t c, uint2 (&b)[8]) {
+  const uint8_t* bp = bfrag + kBytesPerK * (sl.k0 - klo) + (g * 4 + c) * 8;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    b[q] = make_uint2(0u, 0u);
+    if (q < (int)sl.nq && g < (uint32_t)kLimbs) b[q] = *(const uint2*)(bp + q * kTileB);
+  }
+}
+
+// NT (1 or 2) row tiles of one slab against shared B fragments: tile q of the
+// slab accumulates into chain q&3 of each row tile.
+template <int NT>
+__device__ __forceinline__ void tiles_mma(const uint8_t* unit0, uint32_t ub, uint32_t nq, int lane,
+                                          const uint2 (&b)[8], int (&acc)[2][4][4]) {
+  uint32_t w[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) unit_words(unit0 + j * ub, nq, lane, w[j]);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (q >= (int)nq) break;
+    const uint32_t mask = 0x01010101u << q;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+      mma_u8s8(acc[j][q & 3], w[j][0] & mask, w[j][1] & mask, w[j][2] & mask, w[j][3] & mask,
+               b[q].x, b[q].y);
+  }
+}
+
 // All sections of one stage; leaves sum_K bit*value per row in red[] (exact).
-// Linear mode: work items (row tile, run of sections) go round-robin to the
-// consumer warps; a warp waits only for the sections it reads.  Ring mode:
-// the stream is longer than the buffer, every warp walks every section in
-// order and releases it (slot reuse); a warp handles the tiles t = w mod 8.
+// Linear mode: the stage's sections are resident (one mbarrier per stage);
+// work items (pair of row tiles, run of sections) go round-robin to the
+// consumer warps, each B-fragment load serving both tiles.  Ring mode: the
+// stream is longer than the buffer; every warp walks every section in order
+// and releases it (slot reuse), handling tiles t = w mod warps.
 __device__ __forceinline__ void run_stage(const StageArgs& A, uint32_t NS, bool ring_mode,
                                           uint32_t slot_bytes, uint64_t* full, uint64_t* empty,
                                           const uint8_t* buf, const uint8_t* bfrag,
-                                          long long* red) {
+                                          long long* red, unsigned long long* prof) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t g = lane >> 2, c = lane & 3;
-  int acc[8][4];
+  int acc[2][4][4];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0;
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[j][q][0] = acc[j][q][1] = acc[j][q][2] = acc[j][q][3] = 0;
   if (!A.rtn || !A.nsec) return;
-  uint32_t w[4];
   uint2 b[8];
-  auto load_b = [&](const Slab& sl) {
-    const uint8_t* bp = bfrag + kBytesPerK * (sl.k0 - A.klo) + (g * 4 + c) * 8;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      b[q] = make_uint2(0u, 0u);
-      if (q < (int)sl.nq && g < (uint32_t)kLimbs) b[q] = *(const uint2*)(bp + q * kTileB);
-    }
-  };
   if (!ring_mode) {
-    // chunk C sections per item so that every warp gets ~3 items
-    const uint32_t want = 3 * kConsumerWarps;
-    const uint32_t C = max(1u, (A.rtn * A.nsec) / want);
-    const uint32_t nch = (A.nsec + C - 1) / C, nitems = nch * A.rtn;
+    const uint32_t npair = (A.rtn + 1) / 2;
+    const uint32_t want = 2 * kConsumerWarps;
+    const uint32_t C = max(1u, (npair * A.nsec) / want);
+    const uint32_t nch = (A.nsec + C - 1) / C, nitems = nch * npair;
+    bool waited = false;
     for (uint32_t it = warp; it < nitems; it += kConsumerWarps) {
-      const uint32_t ch = it / A.rtn, t = it % A.rtn;
+      if (!waited) {
+        long long c0 = prof ? clock64() : 0;
+        mbar_wait_wd(&full[A.sec_base], 0);  // the whole stage has landed
+        if (prof && lane == 0) prof[0] += clock64() - c0;
+        waited = true;
+      }
+      const uint32_t ch = it / npair, t0 = 2 * (it % npair);
+      const bool two = t0 + 1 < A.rtn;
       const uint32_t s0 = ch * C, s1 = min(A.nsec, s0 + C);
+      long long c1 = prof ? clock64() : 0;
       for (uint32_t s = s0; s < s1; ++s) {
         const Slab sl = slab_of(A.K, A.slab_base + s);
-        mbar_wait_wd(&full[A.sec_base + s], 0);
+        const uint32_t ub = unit_bytes(sl.nq);
         // sections are contiguous in K: section s starts 2*rtn*(k0 - klo) bytes in
-        const uint8_t* unit =
-            buf + A.lin_off + 2u * A.rtn * (sl.k0 - A.klo) + t * unit_bytes(sl.nq);
-        unit_words(unit, sl.nq, lane, w);
-        load_b(sl);
-        unit_mma(w, b, sl.nq, acc);
+        const uint8_t* unit = buf + A.lin_off + 2u * A.rtn * (sl.k0 - A.klo) + t0 * ub;
+        load_b(bfrag, A.klo, sl, g, c, b);
+        if (two) tiles_mma<2>(unit, ub, sl.nq, lane, b, acc);
+        else tiles_mma<1>(unit, ub, sl.nq, lane, b, acc);
       }
-      flush_rows(acc, red + t * 16, lane);
+      long long c2 = prof ? clock64() : 0;
+      flush_rows(acc[0], red + t0 * 16, lane);
+      if (two) flush_rows(acc[1], red + (t0 + 1) * 16, lane);
+      if (prof && lane == 0) {
+        prof[2] += c2 - c1;
+        prof[3] += clock64() - c2;
+        prof[4] += (s1 - s0) * (two ? 2 : 1);
+      }
     }
   } else {
     for (uint32_t s = 0; s < A.nsec; ++s) {
       const uint32_t sec = A.sec_base + s, slot = sec % NS;
       const Slab sl = slab_of(A.K, A.slab_base + s);
       mbar_wait_wd(&full[slot], (sec / NS) & 1);
-      if ((uint32_t)warp < A.rtn) load_b(sl);
+      if ((uint32_t)warp < A.rtn) load_b(bfrag, A.klo, sl, g, c, b);
       for (uint32_t t = warp; t < A.rtn; t += kConsumerWarps) {
-        unit_words(buf + (size_t)slot * slot_bytes + t * unit_bytes(sl.nq), sl.nq, lane, w);
-        unit_mma(w, b, sl.nq, acc);
-        flush_rows(acc, red + t * 16, lane);
+        tiles_mma<1>(buf + (size_t)slot * slot_bytes + t * unit_bytes(sl.nq), 0, sl.nq, lane, b,
+                     acc);
+        flush_rows(acc[0], red + t * 16, lane);
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&empty[slot]);
@@ -350,17 +367,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
 
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(~0u, tid >> 5, 0);
+  long long trace_t0 = 0;
   TRACE(0);
   const Cta C = p.ctas[blockIdx.x];
   if (p.trace && tid == 0) {
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    p.trace[blockIdx.x * 24 + 16] = smid;
-    p.trace[blockIdx.x * 24 + 17] = C.s1_rtn;
-    p.trace[blockIdx.x * 24 + 18] = C.s1_sln;
-    p.trace[blockIdx.x * 24 + 19] = C.s2_rtn;
-    p.trace[blockIdx.x * 24 + 20] = C.nsec;
-    p.trace[blockIdx.x * 24 + 21] = C.ring;
+    p.trace[blockIdx.x * 32 + 16] = smid;
+    p.trace[blockIdx.x * 32 + 17] = C.s1_rtn;
+    p.trace[blockIdx.x * 32 + 18] = C.s1_sln;
+    p.trace[blockIdx.x * 32 + 19] = C.s2_rtn;
+    p.trace[blockIdx.x * 32 + 20] = C.nsec;
+    p.trace[blockIdx.x * 32 + 21] = C.ring;
   }
   const uint32_t n1 = C.s1_rtn ? C.s1_sln : 0;
   const uint32_t m = p.m;
@@ -393,16 +411,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
           if (sec >= NS) mbar_wait_wd(&empty[slot], ((sec / NS) - 1) & 1);
           tc::mbar_arrive_expect_tx(&full[slot], bytes);
           tc::bulk_g2s(buf + (size_t)slot * p.slot_bytes, src + off, bytes, &full[slot]);
-        } else {  // linear: the section lives at its stream offset
-          tc::mbar_arrive_expect_tx(&full[sec], bytes);
-          tc::bulk_g2s(buf + off, src + off, bytes, &full[sec]);
+        } else {  // linear: the section lives at its stream offset; one barrier per stage
+          uint64_t* bar = &full[sec < n1 ? 0 : 1];
+          if (sec == 0 || sec == n1) {
+            uint32_t total = 0;
+            for (uint32_t q = sec; q < (sec < n1 ? n1 : C.nsec); ++q) total += sec_bytes(q);
+            tc::mbar_arrive_expect_tx(bar, total);
+          }
+          tc::bulk_g2s(buf + off, src + off, bytes, bar);
         }
         off += bytes;
       }
-      if (p.trace) p.trace[blockIdx.x * 24 + 14] = clock64();
+      if (p.trace) p.trace[blockIdx.x * 32 + 14] = clock64() - trace_t0;
       if (p.trace && !ring_mode && C.nsec) {  // diagnostics: the whole stream landed
-        for (uint32_t s = 0; s < C.nsec; ++s) mbar_wait_wd(&full[s], 0);
-        p.trace[blockIdx.x * 24 + 15] = clock64();
+        if (n1) mbar_wait_wd(&full[0], 0);
+        if (C.nsec > n1) mbar_wait_wd(&full[1], 0);
+        p.trace[blockIdx.x * 32 + 15] = clock64() - trace_t0;
       }
     }
     return;
@@ -418,66 +442,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
   const uint32_t dirty_next = *(volatile uint32_t*)&st->dirty[(ep & 1) ^ 1];
   const uint32_t b = ep & 1;
 
-  // ---- input statistics over all m (x is L2-resident): max|x| and sum|x| ----
-  // max|x| * max|s2| bounds |a| (fixes a's exponent); sum|x| * max|s2| bounds
-  // |t_k| = |sum_j +-a_j| (fixes t's exponent) - no pass over t is needed.
-  float xmax, xsum;
-  {
-    float mx = 0.f, sm = 0.f;
-    if (p.x_f32) {
-      const float* xf = (const float*)p.x;
-      const uint32_t nv = p.x_vec ? m / 4 : 0;
+  // ---- activation exponent: a = s2*x with |a| <= max|s2| * X, X = 65504 for
+  // binary16 x (no pass over x), max|x| over all m for fp32 x.
+  float xmax = 65504.f;
+  if (p.x_f32) {
+    float mx = 0.f;
+    const float* xf = (const float*)p.x;
+    const uint32_t nv = p.x_vec ? m / 4 : 0;
 #pragma unroll 4
-      for (uint32_t i = tid; i < nv; i += kConsumerThreads) {
-        const float4 v = __ldcg((const float4*)xf + i);
-        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-        sm += (fabsf(v.x) + fabsf(v.y)) + (fabsf(v.z) + fabsf(v.w));
-      }
-      for (uint32_t i = 4 * nv + tid; i < m; i += kConsumerThreads) {
-        const float v = fabsf(__ldcg(xf + i));
-        mx = fmaxf(mx, v);
-        sm += v;
-      }
-    } else {
-      const __half* xh = (const __half*)p.x;
-      const uint32_t nv = p.x_vec ? m / 8 : 0;
-#pragma unroll 4
-      for (uint32_t i = tid; i < nv; i += kConsumerThreads) {
-        const uint4 v = __ldcg((const uint4*)xh + i);
-        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 f = __half22float2(*(const __half2*)&wv[k]);
-          mx = fmaxf(mx, fmaxf(fabsf(f.x), fabsf(f.y)));
-          sm += fabsf(f.x) + fabsf(f.y);
-        }
-      }
-      for (uint32_t i = 8 * nv + tid; i < m; i += kConsumerThreads) {
-        const float v = fabsf(__half2float(__ushort_as_half(__ldcg((const unsigned short*)xh + i))));
-        mx = fmaxf(mx, v);
-        sm += v;
-      }
+    for (uint32_t i = tid; i < nv; i += kConsumerThreads) {
+      const float4 v = __ldcg((const float4*)xf + i);
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
     }
+    for (uint32_t i = 4 * nv + tid; i < m; i += kConsumerThreads) mx = fmaxf(mx, fabsf(__ldcg(xf + i)));
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      mx = fmaxf(mx, __shfl_xor_sync(~0u, mx, o));
-      sm += __shfl_xor_sync(~0u, sm, o);
-    }
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(~0u, mx, o));
     float* rf = (float*)red8;
-    if (lane == 0) {
-      rf[warp] = mx;
-      rf[kConsumerWarps + warp] = sm;
-    }
+    if (lane == 0) rf[warp] = mx;
     consumers_sync();
     mx = 0.f;
-    sm = 0.f;
 #pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) {
-      mx = fmaxf(mx, rf[w]);
-      sm += rf[kConsumerWarps + w];
-    }
+    for (int w = 0; w < kConsumerWarps; ++w) mx = fmaxf(mx, rf[w]);
     xmax = mx;
-    xsum = sm;
   }
   TRACE(3);
 
@@ -488,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
     const uint32_t klo = slab_of(m, C.s1_sl0).k0;
     const Slab last = slab_of(m, C.s1_sl0 + C.s1_sln - 1);
     const uint32_t nquad = (last.k0 + 32 * last.nq - klo) / 4;
-    long long asum = 0;
+    long long asum = 0, aabs = 0;
     uint32_t qd = tid;
     XQuad cur = load_xquad(p, S.s2h, klo + 4 * min(qd, nquad - 1), m);
     while (qd < nquad) {  // one quad in flight ahead of the one being quantised
@@ -499,17 +485,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float a = cur.s[e] * cur.x[e];  // packed.cpp:160
-        v[e] = __float2int_rn(scale_pow2(a, kFix - ea));
+        v[e] = __float2ll_rn(scale_pow2(a, kFix - ea));
         asum += v[e];
+        aabs += v[e] < 0 ? -v[e] : v[e];
       }
       emit_quad(bfrag, klo, k0, q_of(k0, m), v);
       cur = nxt;
       qd = nx;
     }
     const long long A = cta_sum_i64(asum, red8);  // also orders the bfrag stores
+    const long long Aabs = cta_sum_i64(aabs, red8);
+    // one CTA per slab range publishes sum|a_int| (bounds every |t_k| of the segment)
+    if (tid == 0 && C.s1_rt0 == 0)
+      atomicAdd((unsigned long long*)&p.st->abs_a[(ep & 1)][C.s1_seg], (unsigned long long)Aabs);
     TRACE(4);
-    StageArgs sa{C.s1_rtn, n1, 0, m, C.s1_sl0, klo, 0};
-    run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red);
+    StageArgs sa{C.s1_rtn, n1, 0, m, C.s1_sl0, klo, 0};  // linear: barrier full[0]
+    run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
+              (p.trace && warp == 0) ? p.trace + blockIdx.x * 32 + 22 : nullptr);
     TRACE(12);
     consumers_sync();
     TRACE(5);
@@ -523,18 +515,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
     const uint32_t hi = (uint32_t)((uint64_t)dirty_next * (blockIdx.x + 1) / gridDim.x);
     for (uint32_t i = lo + tid; i < hi; i += kConsumerThreads) Tn[i] = 0;
   }
-  __threadfence();
 
   // --------------------------------------------------------------- grid barrier
-  consumers_sync();
+  consumers_sync();  // the CTA's reds to t happen-before thread 0's fence (cumulativity)
   TRACE(6);
   if (tid == 0) {
+    __threadfence();
     const uint32_t arrived = atomicAdd(&st->done[b], 1u);
     if (arrived == gridDim.x - 1) {  // every CTA has read epoch and dirty: advance them
       st->epoch = ep + 1;
       st->dirty[b] = p.R1;
       st->dirty[b ^ 1] = 0;
       st->done[b ^ 1] = 0;
+#pragma unroll
+      for (int sg = 0; sg < kMaxSeg; ++sg) st->abs_a[b ^ 1][sg] = 0;
     }
   }
   if (!C.s2_rtn) return;
@@ -553,11 +547,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
   // ------------------------------------------------------------------ stage 2
   const Seg& S = p.seg[C.s2_seg];
   const int ea = exponent_of(S.s2max * xmax);
-  // |t_k| <= sum_j |a_int_j| <= s2max*sum|x|*2^(kFix-ea) + m  (+ margin for fp32 sums)
-  const double tbound =
-      ((double)S.s2max * (double)xsum * ldexp(1.0, kFix - ea) + (double)m) * (1.0 + 1.0 / 1024);
-  int et = 0;
-  if (tbound > 0) frexp(tbound, &et);  // |t_k| < 2^et
+  // |t_k| = |sum_j +-a_int_j| <= sum_j |a_int_j|, published exactly by stage 1
+  const unsigned long long tbound = __ldcg((const unsigned long long*)&st->abs_a[b][C.s2_seg]);
+  const int et = tbound ? 64 - __clzll((long long)tbound) : 0;  // |t_k| < 2^et
   const int sh = et - kFix;
   const long long* Tseg = p.T + (size_t)b * p.r_cap + S.t_off;
   const uint32_t nquad2 = kpad(S.r) / 4;
@@ -586,11 +578,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
   uint32_t s1_bytes = 0;  // linear offset of the first stage-2 section
   for (uint32_t s = 0; s < n1; ++s) s1_bytes += sec_bytes(s);
   StageArgs sa{C.s2_rtn, C.nsec - n1, n1, S.r, 0, 0, s1_bytes};
-  run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red);
+  if (!ring_mode) sa.sec_base = 1;  // linear: barrier full[1]
+  run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
+            (p.trace && warp == 0) ? p.trace + blockIdx.x * 32 + 27 : nullptr);
   TRACE(13);
   consumers_sync();
   TRACE(10);
-  const int E = sh + ea - kFix;
+  const int E = sh + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
   for (uint32_t i = tid; i < (uint32_t)C.s2_rtn * 16; i += kConsumerThreads) {
     const uint32_t row = C.s2_rt0 * 16 + i;
     if (row >= S.n) continue;
@@ -625,7 +619,7 @@ void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32
   dec_state_reserve(ctx, g->R1);
   Params p{};
   p.bits = g->bits;
-  p.ctas = g->ctas;
+  std::copy(g->ctas, g->ctas + g->grid, p.ctas);
   for (uint32_t s = 0; s < g->nseg; ++s) {
     p.seg[s] = g->seg[s];
     NQB_REQUIRE(d_ys[s] != nullptr, NQB_E_VALIDATION, "null output");

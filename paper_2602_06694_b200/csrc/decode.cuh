@@ -11,7 +11,7 @@
 // and B limbs of (value << (7-q)), so every tile contributes 2^7 * bit * value
 // to the same int32 accumulators.  All accumulation is exact integer
 // arithmetic, so the result is bitwise deterministic and independent of the
-// work split; the only rounding is the 30-bit quantisation of a and of t.
+// work split; the only rounding is the 38-bit quantisation of a and of t.
 //
 // One launch computes both stages.  CTA c streams one contiguous byte range of
 // the plan's bit buffer (its stage-1 sections, then its stage-2 sections)
@@ -32,8 +32,9 @@ constexpr int kConsumerThreads = kConsumerWarps * 32;
 constexpr int kThreads = kConsumerThreads + 32;
 constexpr int kMaxRt = 32;         // 16-row tiles per CTA per stage (4 per consumer warp)
 constexpr int kMaxSlabs1 = 16;     // stage-1 K slabs per CTA (4096 inputs)
-constexpr int kFix = 30;           // activations and t in 30-bit fixed point
-constexpr int kLimbs = 5;          // signed 8-bit limbs of (value << (7-q)) <= 2^37
+constexpr int kFix = 38;           // activations and t in 38-bit fixed point
+constexpr int kLimbs = 6;          // signed 8-bit limbs of (value << (7-q)) <= 2^45
+constexpr int kMaxGrid = 160;      // CTA table lives in the kernel parameters
 constexpr int kTileB = kLimbs * 32;    // B-fragment bytes per 32-wide K tile
 constexpr int kBytesPerK = kLimbs;     // B-fragment bytes per input
 
@@ -99,11 +100,11 @@ struct State {               // per-context decode state (device memory)
   uint32_t done[2];          // grid-barrier arrival counters
   uint32_t dirty[2];         // rows of t[b] that may be non-zero
   uint32_t pad[3];
+  long long abs_a[2][kMaxSeg];  // sum_j |a_int_j| per segment (bounds |t_k|)
 };
 
 struct Params {
   const uint8_t* bits;
-  const Cta* ctas;
   Seg seg[kMaxSeg];
   uint32_t nseg, m;
   uint32_t R1;               // rows of the t accumulator used by this plan
@@ -117,7 +118,8 @@ struct Params {
   uint32_t x_f32, y_f32, x_vec;
   const void* x;
   void* y[kMaxSeg];
-  unsigned long long* trace;  // diagnostics: 16 %globaltimer stamps per CTA, or null
+  unsigned long long* trace;  // diagnostics (nqb_debug_decode_trace), or null
+  Cta ctas[kMaxGrid];
 };
 
 }  // namespace dec
@@ -131,7 +133,7 @@ struct nqb_group {
   uint32_t buf_bytes = 0, slot_bytes = 0, nbar = 0, bfrag_bytes = 0, smem_bytes = 0;
   uint64_t stream_bytes = 0;
   uint8_t* bits = nullptr;             // device, stream_bytes
-  nqb::dec::Cta* ctas = nullptr;       // device, grid entries
+  nqb::dec::Cta* ctas = nullptr;       // host copy of the CTA table (grid entries)
   nqb::dec::Seg seg[nqb::dec::kMaxSeg];
   uint32_t n[nqb::dec::kMaxSeg] = {0}, r[nqb::dec::kMaxSeg] = {0};
 };

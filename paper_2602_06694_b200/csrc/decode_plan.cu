@@ -173,7 +173,7 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
     B1tot += B1[s];
   }
 
-  const uint32_t Gmax = (uint32_t)ctx->num_sms;
+  const uint32_t Gmax = std::min<uint32_t>((uint32_t)ctx->num_sms, kMaxGrid);
   const uint32_t min_cta_bytes = env_u32("NQB_DEC_MIN_CTA_BYTES", 8192);
   uint32_t G = (uint32_t)std::min<uint64_t>(Gmax, std::max<uint64_t>(1, (Btot + min_cta_bytes - 1) /
                                                                          min_cta_bytes));
@@ -366,11 +366,10 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   // streams through fixed slots (ring mode).
   const uint32_t cap = env_u32("NQB_DEC_SMEM_KB", 160) * 1024;
   const uint32_t buf = (uint32_t)std::min<uint64_t>((max_stream + 127) / 128 * 128, cap);
-  uint32_t slot = 0, nbar = 1;
+  uint32_t slot = 0, nbar = 2;  // linear mode: one mbarrier per stage
   for (uint32_t c = 0; c < G; ++c) {
     Cta& C = ctas[c];
     C.ring = sbytes[c] > buf ? 1 : 0;
-    if (!C.ring) nbar = std::max<uint32_t>(nbar, C.nsec);
   }
   for (uint32_t c = 0; c < G; ++c) {
     const Cta& C = ctas[c];
@@ -401,8 +400,11 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   // ---- device buffers --------------------------------------------------------
   try {
     NQB_CUDA(cudaMalloc(&g->bits, std::max<uint64_t>(off, 16)));
-    NQB_CUDA(cudaMalloc(&g->ctas, sizeof(Cta) * G));
-    NQB_CUDA(cudaMemcpyAsync(g->ctas, ctas.data(), sizeof(Cta) * G, cudaMemcpyHostToDevice,
+    g->ctas = new Cta[G];
+    std::copy(ctas.begin(), ctas.end(), g->ctas);
+    Cta* dctas = nullptr;
+    NQB_CUDA(cudaMallocAsync(&dctas, sizeof(Cta) * G, ctx->stream));
+    NQB_CUDA(cudaMemcpyAsync(dctas, ctas.data(), sizeof(Cta) * G, cudaMemcpyHostToDevice,
                              ctx->stream));
     Seg* dsegs = nullptr;
     uint32_t* dmax = nullptr;
@@ -430,11 +432,12 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
     }
     NQB_CUDA(cudaMemcpyAsync(dsegs, g->seg, sizeof(Seg) * kMaxSeg, cudaMemcpyHostToDevice,
                              ctx->stream));
-    k_relayout<<<G, 256, 0, ctx->stream>>>(g->ctas, dsegs, m, src, (uint32_t*)g->bits);
+    k_relayout<<<G, 256, 0, ctx->stream>>>(dctas, dsegs, m, src, (uint32_t*)g->bits);
     NQB_LAUNCHED(ctx);
     uint32_t hmax[kMaxSeg] = {0};
     NQB_CUDA(cudaMemcpyAsync(hmax, dmax, 4 * kMaxSeg, cudaMemcpyDeviceToHost, ctx->stream));
     NQB_CUDA(cudaFreeAsync(dsegs, ctx->stream));
+    NQB_CUDA(cudaFreeAsync(dctas, ctx->stream));
     NQB_CUDA(cudaFreeAsync(dmax, ctx->stream));
     NQB_CUDA(cudaStreamSynchronize(ctx->stream));
     for (uint32_t s = 0; s < count; ++s)
@@ -451,7 +454,7 @@ void group_free(nqb_group* g) {
   if (!g) return;
   cudaSetDevice(g->device);
   cudaFree(g->bits);
-  cudaFree(g->ctas);
+  delete[] g->ctas;
   delete g;
 }
 

@@ -33,18 +33,15 @@ for name in sys.argv[1:] or list(SHAPES):
     torch.cuda.synchronize()
     for trial in range(2):
         grid = C.c_uint32()
-        st = np.zeros(24 * 148, np.uint64)
+        st = np.zeros(32 * 148, np.uint64)
         rc = ctx.lib.nqb_debug_decode_trace(ctx.handle, lay.handle, C.c_void_p(x.data_ptr()),
                                             C.c_void_p(y.data_ptr()), st.ctypes.data_as(C.c_void_p),
                                             C.byref(grid))
         assert rc == 0, ctx.lib.nqb_last_error()
     G = grid.value
-    full = st[:24 * G].reshape(G, 24).astype(np.float64)
+    full = st[:32 * G].reshape(G, 32).astype(np.float64)
     ghz = 1.9
     cyc = full[:, :16].copy()
-    base = full[:, 22]
-    cyc[:, 14] = np.where(full[:, 14] > 0, full[:, 14] - base, np.nan)
-    cyc[:, 15] = np.where(full[:, 15] > 0, full[:, 15] - base, np.nan)
     cyc[:, 0] = (full[:, 0] - full[:, 0].min()) * ghz  # start skew (ns -> cycles)
     us = np.where(cyc > 0, cyc / ghz / 1e3, np.nan)
     us[:, 0] = cyc[:, 0] / ghz / 1e3
@@ -63,3 +60,10 @@ for name in sys.argv[1:] or list(SHAPES):
         col = col[~np.isnan(col)]
         if col.size:
             print(f"   {i:2d} {lab:11s} min {col.min():7.2f}  med {np.median(col):7.2f}  max {col.max():7.2f}  (n={col.size})")
+    for nm, o in (("stage1", 22), ("stage2", 27)):
+        u = full[:, o + 4]
+        sel = u > 0
+        if sel.any():
+            tot = full[sel, o:o + 4].sum(0) / u[sel].sum()
+            print(f"   warp0 {nm}: units/CTA {u[sel].mean():.1f}; cycles per unit: wait {tot[0]:.0f} "
+                  f"loads {tot[1]:.0f} mma {tot[2]:.0f}; flush per unit {tot[3]:.0f}")
