@@ -60,10 +60,14 @@ for name in sys.argv[1:] or list(SHAPES):
         col = col[~np.isnan(col)]
         if col.size:
             print(f"   {i:2d} {lab:11s} min {col.min():7.2f}  med {np.median(col):7.2f}  max {col.max():7.2f}  (n={col.size})")
-    for nm, o in (("stage1", 22), ("stage2", 27)):
-        u = full[:, o + 4]
-        sel = u > 0
-        if sel.any():
-            tot = full[sel, o:o + 4].sum(0) / u[sel].sum()
-            print(f"   warp0 {nm}: units/CTA {u[sel].mean():.1f}; cycles per unit: wait {tot[0]:.0f} "
-                  f"loads {tot[1]:.0f} mma {tot[2]:.0f}; flush per unit {tot[3]:.0f}")
+    sel = full[:, 26] > 0
+    if sel.any():
+        u = full[sel, 26].sum()
+        tot = full[sel, 22:26].sum(0) / u
+        print(f"   stage2 warp0 per pair ({u/sel.sum():.1f} pairs/CTA): loads {tot[0]:.0f} afree-wait {tot[1]:.0f} "
+              f"sttm {tot[2]:.0f} waitst+arrive {tot[3]:.0f} cycles")
+    sel = full[:, 30] > 0
+    if sel.any():
+        u = full[sel, 30].sum()
+        tot = full[sel, 28:30].sum(0) / u
+        print(f"   stage2 MMA thread per pair ({u/sel.sum():.1f} pairs/CTA): aready-wait {tot[0]:.0f} issue {tot[1]:.0f} cycles")
