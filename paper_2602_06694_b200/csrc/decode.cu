@@ -9,6 +9,15 @@
 namespace nqb {
 namespace dec {
 
+// D += A(16x32 u8) * B(32x8 s8), int32 accumulate (IMMA.16832.U8.S8).
+__device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
 __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerThreads) : "memory");
 }
@@ -80,25 +89,15 @@ __device__ __forceinline__ void put_limbs(long long v, uint32_t e, uint32_t (&w)
   w[kLimbs - 1] |= (uint32_t)(v & 0xFF) << s;
 }
 
-// B operand words for the quad of inputs k0..k0+3 (values already << (7-q)),
-// canonical K-major layout of one 32-wide K tile (16 rows = limbs x 32 bytes):
-// byte (limb n, k) at ((k/16)*2 + n/8)*128 + (n%8)*16 + k%16.  Limbs 0..7 are
-// written here (6, 7 zero); rows 8..15 are zeroed by zero_b_hi.
+// B-fragment words for the quad of inputs k0..k0+3 (values already << (7-q)):
+// tile (k0-klo)/32 owns kTileB bytes = [limb g<kLimbs][c][h] words.
 __device__ __forceinline__ void store_quad(uint8_t* bfrag, uint32_t klo, uint32_t k0,
                                            const uint32_t (&w)[kLimbs]) {
-  const uint32_t kk = k0 & 31;
-  uint8_t* t = bfrag + ((k0 - klo) >> 5) * kTileB + (kk >> 4) * 256 + (kk & 15);
+  // tiles 2i, 2i+1 interleave per (limb, c) so one 16-byte load feeds both
+  const uint32_t kk = k0 & 31, h = kk >> 4, c = (kk >> 2) & 3, tt = (k0 - klo) >> 5;
+  uint32_t* t = (uint32_t*)(bfrag + (tt >> 1) * 2 * kTileB) + (tt & 1) * 2 + h;
 #pragma unroll
-  for (uint32_t g = 0; g < 8; ++g) *(uint32_t*)(t + g * 16) = g < (uint32_t)kLimbs ? w[g] : 0u;
-}
-
-// Zeroes B rows 8..15 (the upper core-matrix group) of tiles [0, ntiles).
-__device__ __forceinline__ void zero_b_hi(uint8_t* bfrag, uint32_t ntiles, int tid) {
-  for (uint32_t i = tid; i < ntiles * 16; i += kConsumerThreads) {
-    const uint32_t tile = i >> 4, part = i & 15;  // 2 halves x 8 x 16 B
-    *(uint4*)(bfrag + tile * kTileB + (part >> 3) * 256 + 128 + (part & 7) * 16) =
-        make_uint4(0u, 0u, 0u, 0u);
-  }
+  for (uint32_t g = 0; g < kLimbs; ++g) t[(g * 4 + c) * 4] = w[g];
 }
 
 __device__ __forceinline__ long long cta_sum_i64(long long v, long long* red8) {
@@ -133,6 +132,185 @@ __device__ __forceinline__ int exponent_of(float M) {
   int e;
   frexpf(M, &e);
   return e;  // M < 2^e
+}
+
+// Words w_0..w_3 of this lane in a unit with nq tiles (formats: decode_plan.cu).
+__device__ __forceinline__ void unit_words(const uint8_t* unit, uint32_t nq, int lane,
+                                           uint32_t (&w)[4]) {
+  if (nq == 8) {
+    const uint4 v = *(const uint4*)(unit + lane * 16);
+    w[0] = v.x;
+    w[1] = v.y;
+    w[2] = v.z;
+    w[3] = v.w;
+  } else if (nq == 4) {
+    const uint2 v = *(const uint2*)(unit + lane * 8);
+    w[0] = v.x;
+    w[1] = v.x >> 4;
+    w[2] = v.y;
+    w[3] = v.y >> 4;
+  } else {
+    const uint32_t u = *(const uint32_t*)(unit + lane * 4);
+    w[0] = u;
+    w[1] = u >> 2;
+    w[2] = u >> 4;
+    w[3] = u >> 6;
+  }
+}
+
+// Adds 4 accumulator chains of one row tile to the per-limb row sums
+// red32[row][limb] (16 rows x kRedStride ints): chains are summed in int32
+// (|sum| < 2^30) and lane c adds limbs 2c, 2c+1 of rows g and g+8 with native
+// 32-bit shared atomics (the limb sums stay < 2^31: sum_K 2^q * |limb| <= K * 2^14).
+__device__ __forceinline__ void flush_rows(int (&acc)[4][4], int* red32, int lane) {
+  const int g = lane >> 2, c = lane & 3;
+  if (c >= (kLimbs + 1) / 2) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0;
+    return;
+  }
+  int s[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    s[i] = acc[0][i] + acc[1][i] + acc[2][i] + acc[3][i];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q][i] = 0;
+  }
+  int* r0 = red32 + g * kRedStride + 2 * c;
+  int* r1 = red32 + (g + 8) * kRedStride + 2 * c;
+  atomicAdd(r0, s[0]);
+  atomicAdd(r0 + 1, s[1]);
+  atomicAdd(r1, s[2]);
+  atomicAdd(r1 + 1, s[3]);
+}
+
+// sum_K bit * value of a row from its limb sums (exact; two's-complement
+// wraparound of the partial sums is harmless because the total fits).
+__device__ __forceinline__ long long row_value(const int* red32row) {
+  unsigned long long v = 0;
+#pragma unroll
+  for (int l = 0; l < kLimbs; ++l) v += (unsigned long long)(long long)red32row[l] << (8 * l);
+  return (long long)v >> 7;
+}
+
+struct StageArgs {
+  uint32_t rtn, nsec, sec_base;   // row tiles, sections, index of the first section
+  uint32_t K, slab_base, klo;     // K dimension, first slab, its k0
+  uint32_t lin_off;               // linear mode: buffer offset of the first section
+};
+
+// B fragments of one slab for this lane: b[q] = limbs g of the 4-input groups
+// 4c.. and 16+4c.. of tile q (lanes g >= kLimbs feed zero columns).
+__device__ __forceinline__ void load_b(const uint8_t* bfrag, uint32_t klo, const Slab& sl,
+                                       uint32_t g, uint32_t c, uint2 (&b)[8]) {
+  const uint8_t* bp = bfrag + kBytesPerK * (sl.k0 - klo) + (g * 4 + c) * 16;
+#pragma unroll
+  for (int q = 0; q < 8; q += 2) {
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (q < (int)sl.nq && g < (uint32_t)kLimbs) v = *(const uint4*)(bp + q * kTileB);
+    b[q] = make_uint2(v.x, v.y);
+    b[q + 1] = make_uint2(v.z, v.w);
+  }
+}
+
+// NT (1 or 2) row tiles of one slab against shared B fragments: tile q of the
+// slab accumulates into chain q&3 of each row tile.
+template <int NT>
+__device__ __forceinline__ void tiles_mma(const uint8_t* unit0, uint32_t ub, uint32_t nq, int lane,
+                                          const uint2 (&b)[8], int (&acc)[2][4][4]) {
+  uint32_t w[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) unit_words(unit0 + j * ub, nq, lane, w[j]);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (q >= (int)nq) break;
+    const uint32_t mask = 0x01010101u << q;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+      mma_u8s8(acc[j][q & 3], w[j][0] & mask, w[j][1] & mask, w[j][2] & mask, w[j][3] & mask,
+               b[q].x, b[q].y);
+  }
+}
+
+// All sections of one stage; leaves sum_K bit*value per row in red[] (exact).
+// Linear mode: the stage's sections are resident (one mbarrier per stage);
+// work items (pair of row tiles, run of sections) go round-robin to the
+// consumer warps, each B-fragment load serving both tiles.  Ring mode: the
+// stream is longer than the buffer; every warp walks every section in order
+// and releases it (slot reuse), handling tiles t = w mod warps.
+__device__ __forceinline__ void run_stage(const StageArgs& A, uint32_t NS, bool ring_mode,
+                                          uint32_t slot_bytes, uint64_t* full, uint64_t* empty,
+                                          const uint8_t* buf, const uint8_t* bfrag,
+                                          int* red, unsigned long long* prof) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t g = lane >> 2, c = lane & 3;
+  int acc[2][4][4];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[j][q][0] = acc[j][q][1] = acc[j][q][2] = acc[j][q][3] = 0;
+  if (!A.rtn || !A.nsec) return;
+  uint2 b[8];
+  if (!ring_mode) {
+    // warp w walks a contiguous range of the (tile pair, section) steps in
+    // pair-major order, so its accumulators persist across sections and it
+    // flushes only when the pair changes (at most a few times).
+    const uint32_t npair = (A.rtn + 1) / 2, U = npair * A.nsec;
+    const uint32_t f0 = (uint32_t)((uint64_t)U * warp / kConsumerWarps);
+    const uint32_t f1 = (uint32_t)((uint64_t)U * (warp + 1) / kConsumerWarps);
+    if (f0 < f1) {
+      long long c0 = prof ? clock64() : 0;
+      mbar_wait_wd(&full[A.sec_base], 0);  // the whole stage has landed
+      if (prof && lane == 0) prof[0] += clock64() - c0;
+    }
+    uint32_t cur = f0 < f1 ? f0 / A.nsec : 0;
+    long long c1 = prof ? clock64() : 0, tf = 0;
+    for (uint32_t f = f0; f < f1; ++f) {
+      const uint32_t pr = f / A.nsec, s = f % A.nsec;
+      if (pr != cur) {
+        const long long cf = prof ? clock64() : 0;
+        flush_rows(acc[0], red + 2 * cur * 16 * kRedStride, lane);
+        if (2 * cur + 1 < A.rtn) flush_rows(acc[1], red + (2 * cur + 1) * 16 * kRedStride, lane);
+        if (prof) tf += clock64() - cf;
+        cur = pr;
+      }
+      const uint32_t t0 = 2 * pr;
+      const Slab sl = slab_of(A.K, A.slab_base + s);
+      const uint32_t ub = unit_bytes(sl.nq);
+      // sections are contiguous in K: section s starts 2*rtn*(k0 - klo) bytes in
+      const uint8_t* unit = buf + A.lin_off + 2u * A.rtn * (sl.k0 - A.klo) + t0 * ub;
+      load_b(bfrag, A.klo, sl, g, c, b);
+      if (t0 + 1 < A.rtn) tiles_mma<2>(unit, ub, sl.nq, lane, b, acc);
+      else tiles_mma<1>(unit, ub, sl.nq, lane, b, acc);
+    }
+    if (f0 < f1) {
+      const long long cf = prof ? clock64() : 0;
+      flush_rows(acc[0], red + 2 * cur * 16 * kRedStride, lane);
+      if (2 * cur + 1 < A.rtn) flush_rows(acc[1], red + (2 * cur + 1) * 16 * kRedStride, lane);
+      if (prof && lane == 0) {
+        tf += clock64() - cf;
+        prof[2] += clock64() - c1 - tf;
+        prof[3] += tf;
+        uint32_t units = 0;
+        for (uint32_t f = f0; f < f1; ++f) units += (2 * (f / A.nsec) + 1 < A.rtn) ? 2 : 1;
+        prof[4] += units;
+      }
+    }
+  } else {
+    for (uint32_t s = 0; s < A.nsec; ++s) {
+      const uint32_t sec = A.sec_base + s, slot = sec % NS;
+      const Slab sl = slab_of(A.K, A.slab_base + s);
+      mbar_wait_wd(&full[slot], (sec / NS) & 1);
+      if ((uint32_t)warp < A.rtn) load_b(bfrag, A.klo, sl, g, c, b);
+      for (uint32_t t = warp; t < A.rtn; t += kConsumerWarps) {
+        tiles_mma<1>(buf + (size_t)slot * slot_bytes + t * unit_bytes(sl.nq), 0, sl.nq, lane, b,
+                     acc);
+        flush_rows(acc[0], red + t * 16 * kRedStride, lane);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&empty[slot]);
+    }
+  }
 }
 
 // a * 2^k exactly in fp32 for k up to ~250 (two steps avoid overflowing 2^k)
@@ -199,171 +377,15 @@ __device__ __forceinline__ void load_tquad(const long long* Tseg, uint32_t k0, u
   }
 }
 
-// ---------------------------------------------------------------------------
-// tcgen05 stage machinery
-// ---------------------------------------------------------------------------
-constexpr uint32_t kSlots = 7;  // (row block, slab) pairs in flight in TMEM (64 columns each, after D)
-
-// Shared-memory barriers of one CTA.
-struct Bars {
-  uint64_t full[2];          // stream landed: stage 1, stage 2 (TMA complete_tx)
-  uint64_t aready[kSlots];   // pair slot written (4 warp arrivals of one warpgroup)
-  uint64_t afree[kSlots];    // the MMAs reading the slot completed (tcgen05.commit)
-  uint64_t dready;           // all MMAs of a stage completed (tcgen05.commit)
-  uint32_t tmem;             // TMEM base address (tcgen05.alloc)
-  uint32_t pad;
-};
-static_assert(sizeof(Bars) <= 512, "barriers fit the smem head");
-
-// Geometry of one stage of one CTA.  Pairs (row block, slab) run slab-major,
-// numbered pi0 + p across stages; pair pi lives in TMEM slot pi % kSlots.
-struct Stage {
-  uint32_t rows;       // 16 * row tiles
-  uint32_t nrb;        // TMEM row blocks of 128 rows
-  uint32_t nsec;       // K slabs
-  uint32_t K, slab0, klo;
-  uint32_t off;        // buffer offset of the stage's first section
-  uint32_t pi0;        // pairs of earlier stages
-  __device__ uint32_t npairs() const { return nrb * nsec; }
-};
-
-__device__ __forceinline__ uint32_t tmem_d(uint32_t tmem, uint32_t rb) { return tmem + rb * kMmaN; }
-__device__ __forceinline__ uint32_t tmem_slot(uint32_t tmem, uint32_t slot, uint32_t q) {
-  return tmem + 64 + slot * 64 + q * 8;
-}
-
-// A registers of tile q for this thread's row (row-major stream formats:
-// nq=8: 8 words, bit 8b+q of word j = A[row][32q + 4j + b]; nq=4: 4 words,
-// word h packs words 2h (low nibbles) and 2h+1 (high nibbles); nq=2: 2 words,
-// word h packs words 4h+i at bit offset 2i).
-__device__ __forceinline__ void a_regs(const uint32_t (&u)[8], uint32_t nq, uint32_t q,
-                                       uint32_t (&v)[8]) {
-  const uint32_t mask = 0x01010101u << q;
-  if (nq == 8) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = u[j] & mask;
-  } else if (nq == 4) {
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      v[2 * h] = u[h] & mask;
-      v[2 * h + 1] = (u[h] >> 4) & mask;
-    }
-  } else {
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) v[4 * h + i] = (u[h] >> (2 * i)) & mask;
-  }
-}
-
-// Expander side of one stage: warpgroup e writes the A tiles of pairs
-// p = e, e+2, ... into their TMEM slots and hands them to the MMA thread.
-__device__ __forceinline__ void expand_stage(const Stage& S, const uint8_t* buf, Bars* bars,
-                                             uint32_t tmem, unsigned long long* prof) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t e = warp >> 2, wq = warp & 3;
-  const uint32_t rl = wq * 32 + lane;  // row inside a 128-row block = TMEM lane
-  const uint32_t lane_base = (wq * 32) << 16;
-  const uint32_t np = S.npairs();
-  for (uint32_t p = e; p < np; p += 2) {
-    const uint32_t rb = p % S.nrb, s = p / S.nrb;
-    const Slab sl = slab_of(S.K, S.slab0 + s);
-    const uint32_t row = rb * 128 + rl;
-    long long c0 = prof ? clock64() : 0;
-    uint32_t u[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    if (row < S.rows) {
-      const uint8_t* src = buf + S.off + S.rows * ((sl.k0 - S.klo) >> 3) + row * 4 * sl.nq;
-      if (sl.nq == 8) {
-        const uint4 x0 = *(const uint4*)src, x1 = *(const uint4*)(src + 16);
-        u[0] = x0.x; u[1] = x0.y; u[2] = x0.z; u[3] = x0.w;
-        u[4] = x1.x; u[5] = x1.y; u[6] = x1.z; u[7] = x1.w;
-      } else if (sl.nq == 4) {
-        const uint4 x0 = *(const uint4*)src;
-        u[0] = x0.x; u[1] = x0.y; u[2] = x0.z; u[3] = x0.w;
-      } else {
-        const uint2 x0 = *(const uint2*)src;
-        u[0] = x0.x; u[1] = x0.y;
-      }
-    }
-    const uint32_t pi = S.pi0 + p, slot = pi % kSlots, use = pi / kSlots;
-    if (prof) {
-      uint32_t z = u[0] ^ u[7];
-      asm volatile("" ::"r"(z));
-    }
-    long long c1 = prof ? clock64() : 0;
-    if (use > 0) mbar_wait_wd(&bars->afree[slot], (use - 1) & 1);
-    tc::fence_after_sync();
-    long long c2 = prof ? clock64() : 0;
-    for (uint32_t q = 0; q < sl.nq; ++q) {
-      uint32_t v[8];
-      a_regs(u, sl.nq, q, v);
-      tc::tmem_st_x8(tmem_slot(tmem, slot, q) + lane_base, v);
-    }
-    long long c3 = prof ? clock64() : 0;
-    tc::wait_st();
-    tc::fence_before_sync();
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(&bars->aready[slot]);
-    if (prof && lane == 0) {
-      long long c4 = clock64();
-      prof[0] += c1 - c0;
-      prof[1] += c2 - c1;
-      prof[2] += c3 - c2;
-      prof[3] += c4 - c3;
-      prof[4] += 1;
-    }
-  }
-}
-
-// MMA-issuer side of one stage (one thread): tile by tile, wait for the A
-// slot, issue one kind::i8 MMA (128 rows x 32 K x 16 limbs), release the slot.
-__device__ __forceinline__ void mma_stage(const Stage& S, uint32_t bfrag_u32, Bars* bars,
-                                          unsigned long long* prof) {
-  constexpr uint32_t idesc = tc::idesc_i8(128, kMmaN, false, true);
-  const uint32_t np = S.npairs();
-  uint32_t tmem = 0;
-  for (uint32_t p = 0; p < np; ++p) {
-    const uint32_t rb = p % S.nrb, s = p / S.nrb;
-    const Slab sl = slab_of(S.K, S.slab0 + s);
-    const uint32_t pi = S.pi0 + p, slot = pi % kSlots, tile0 = (sl.k0 - S.klo) >> 5;
-    long long c0 = prof ? clock64() : 0;
-    mbar_wait_wd(&bars->aready[slot], (pi / kSlots) & 1);
-    tc::fence_after_sync();
-    long long c1 = prof ? clock64() : 0;
-    if (prof) prof[0] += c1 - c0;
-    if (!tmem) tmem = *(volatile uint32_t*)&bars->tmem;  // allocated before any aready
-    for (uint32_t q = 0; q < sl.nq; ++q) {
-      const uint64_t bdesc =
-          tc::smem_desc_kmajor(bfrag_u32 + (tile0 + q) * kTileB, (kMmaN / 8) * 128, 128);
-      tc::mma_i8_ts(tmem_d(tmem, rb), tmem_slot(tmem, slot, q), bdesc, idesc, (s | q) ? 1u : 0u);
-    }
-    tc::mma_commit(&bars->afree[slot]);
-    if (prof) {
-      prof[1] += clock64() - c1;
-      prof[2] += 1;
-    }
-  }
-  tc::mma_commit(&bars->dready);
-}
-
-// Row sums of a finished stage for this thread's TMEM lane in row block rb:
-// D[row][l] = sum_K bit * 2^q * limb_l  ->  sum_K bit * value (exact int64;
-// two's-complement wraparound of the partial sums is harmless).
-__device__ __forceinline__ long long d_row(uint32_t tmem, uint32_t rb, uint32_t wq) {
-  uint32_t v[16];
-  tc::tmem_ld_x16(tmem_d(tmem, rb) + ((wq * 32) << 16), v);
-  tc::wait_ld();
-  unsigned long long acc = 0;
-#pragma unroll
-  for (int l = 0; l < kLimbs; ++l) acc += (unsigned long long)(long long)(int)v[l] << (8 * l);
-  return (long long)acc >> 7;
-}
-
-__global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ Params p) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  Bars* bars = (Bars*)smem;
-  long long* red8 = (long long*)(smem + 512);
-  uint8_t* bfrag = smem + kSmemHead;
+__global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_decode(const __grid_constant__ Params p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t NB = p.nbar;
+  uint64_t* full = (uint64_t*)smem;
+  uint64_t* empty = full + NB;
+  long long* red8 = (long long*)(smem + 16 * NB);
+  int* red = (int*)(smem + 16 * NB + 256);
+  const uint32_t head = ((16 * NB + 256 + kMaxRt * 16 * kRedStride * 4) + 127) / 128 * 128;
+  uint8_t* bfrag = smem + head;
   uint8_t* buf = bfrag + p.bfrag_bytes;
 
   const int tid = threadIdx.x, lane = tid & 31;
@@ -379,88 +401,65 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
     p.trace[blockIdx.x * 32 + 18] = C.s1_sln;
     p.trace[blockIdx.x * 32 + 19] = C.s2_rtn;
     p.trace[blockIdx.x * 32 + 20] = C.nsec;
+    p.trace[blockIdx.x * 32 + 21] = C.ring;
   }
   const uint32_t n1 = C.s1_rtn ? C.s1_sln : 0;
   const uint32_t m = p.m;
-  const Seg& S2seg = p.seg[C.s2_seg];
+  const bool ring_mode = C.ring != 0;
+  const uint32_t NS = ring_mode ? p.buf_bytes / p.slot_bytes : 0;  // ring slots
   auto sec_bytes = [&](uint32_t sec) -> uint32_t {
     return sec < n1 ? C.s1_rtn * unit_bytes(slab_of(m, C.s1_sl0 + sec).nq)
-                    : C.s2_rtn * unit_bytes(slab_of(S2seg.r, sec - n1).nq);
+                    : C.s2_rtn * unit_bytes(slab_of(p.seg[C.s2_seg].r, sec - n1).nq);
   };
-  Stage st1{}, st2{};
-  if (n1) {
-    st1.rows = 16u * C.s1_rtn;
-    st1.nrb = (st1.rows + 127) / 128;
-    st1.nsec = n1;
-    st1.K = m;
-    st1.slab0 = C.s1_sl0;
-    st1.klo = slab_of(m, C.s1_sl0).k0;
-    st1.off = 0;
-    st1.pi0 = 0;
-  }
-  uint32_t s1_bytes = 0;
-  for (uint32_t s = 0; s < n1; ++s) s1_bytes += sec_bytes(s);
-  if (C.s2_rtn) {
-    st2.rows = 16u * C.s2_rtn;
-    st2.nrb = (st2.rows + 127) / 128;
-    st2.nsec = C.nsec - n1;
-    st2.K = S2seg.r;
-    st2.slab0 = 0;
-    st2.klo = 0;
-    st2.off = s1_bytes;
-    st2.pi0 = n1 ? st1.nrb * n1 : 0;
-  }
 
   if (tid == 0) {
-    tc::mbar_init(&bars->full[0], 1);
-    tc::mbar_init(&bars->full[1], 1);
-    for (uint32_t i = 0; i < kSlots; ++i) {
-      tc::mbar_init(&bars->aready[i], 4);
-      tc::mbar_init(&bars->afree[i], 1);
+    for (uint32_t s = 0; s < NB; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], kConsumerWarps);
     }
-    tc::mbar_init(&bars->dready, 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
   pdl_launch_dependents();  // the next kernel may start streaming its bits
 
-  // --------------------------------------------------- producer / MMA issuer
+  // ------------------------------------------------------------------ producer
   if (warp == kConsumerWarps) {
     if (lane == 0) {
       const uint8_t* src = p.bits + C.stream_off;
       uint32_t off = 0;
       for (uint32_t sec = 0; sec < C.nsec; ++sec) {
         const uint32_t bytes = sec_bytes(sec);
-        uint64_t* bar = &bars->full[sec < n1 ? 0 : 1];
-        if (sec == 0 || sec == n1) {
-          uint32_t total = 0;
-          for (uint32_t q = sec; q < (sec < n1 ? n1 : C.nsec); ++q) total += sec_bytes(q);
-          tc::mbar_arrive_expect_tx(bar, total);
+        if (ring_mode) {
+          const uint32_t slot = sec % NS;
+          if (sec >= NS) mbar_wait_wd(&empty[slot], ((sec / NS) - 1) & 1);
+          tc::mbar_arrive_expect_tx(&full[slot], bytes);
+          tc::bulk_g2s(buf + (size_t)slot * p.slot_bytes, src + off, bytes, &full[slot]);
+        } else {  // linear: the section lives at its stream offset; one barrier per stage
+          uint64_t* bar = &full[sec < n1 ? 0 : 1];
+          if (sec == 0 || sec == n1) {
+            uint32_t total = 0;
+            for (uint32_t q = sec; q < (sec < n1 ? n1 : C.nsec); ++q) total += sec_bytes(q);
+            tc::mbar_arrive_expect_tx(bar, total);
+          }
+          tc::bulk_g2s(buf + off, src + off, bytes, bar);
         }
-        tc::bulk_g2s(buf + off, src + off, bytes, bar);
         off += bytes;
       }
-    }
-    // TMEM is allocated by warp 0 after griddepcontrol.wait; its base is read
-    // after the first aready wait (expanders only arrive after allocation).
-    if (lane == 0) {
-      const uint32_t b_u32 = tc::smem_u32(bfrag);
-      unsigned long long* pr = p.trace ? p.trace + blockIdx.x * 32 + 28 : nullptr;
-      if (n1) mma_stage(st1, b_u32, bars, nullptr);
-      if (C.s2_rtn) mma_stage(st2, b_u32, bars, pr);
+      if (p.trace) p.trace[blockIdx.x * 32 + 14] = clock64() - trace_t0;
+      if (p.trace && !ring_mode && C.nsec) {  // diagnostics: the whole stream landed
+        if (n1) mbar_wait_wd(&full[0], 0);
+        if (C.nsec > n1) mbar_wait_wd(&full[1], 0);
+        p.trace[blockIdx.x * 32 + 15] = clock64() - trace_t0;
+      }
     }
     return;
   }
 
   // ----------------------------------------------------------------- consumers
+  for (int i = tid; i < kMaxRt * 16 * kRedStride; i += kConsumerThreads) red[i] = 0;
   TRACE(1);
   pdl_wait();  // x (and the t accumulator) may be written by the previous kernel
   TRACE(2);
-  if (warp == 0) {
-    tc::tmem_alloc(&bars->tmem, kTmemCols);
-    tc::tmem_relinquish();
-    tc::fence_before_sync();
-  }
   State* st = p.st;
   const uint32_t ep = __ldcg(&st->epoch);
   const uint32_t dirty_next = __ldcg(&st->dirty[(ep & 1) ^ 1]);
@@ -487,59 +486,52 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
     mx = 0.f;
 #pragma unroll
     for (int w = 0; w < kConsumerWarps; ++w) mx = fmaxf(mx, rf[w]);
-    consumers_sync();
     xmax = mx;
   }
   TRACE(3);
-  const uint32_t wq = warp & 3, e = warp >> 2, rl = wq * 32 + lane;
-  uint32_t dphase = 0;   // dready completions consumed
 
   // ------------------------------------------------------------------ stage 1
   if (n1) {
     const Seg& S = p.seg[C.s1_seg];
     const int ea = exponent_of(S.s2max * xmax);
+    const uint32_t klo = slab_of(m, C.s1_sl0).k0;
     const Slab last = slab_of(m, C.s1_sl0 + C.s1_sln - 1);
-    const uint32_t nquad = (last.k0 + 32 * last.nq - st1.klo) / 4;
-    zero_b_hi(bfrag, nquad / 8, tid);
+    const uint32_t nquad = (last.k0 + 32 * last.nq - klo) / 4;
     long long asum = 0, aabs = 0;
     uint32_t qd = tid;
-    XQuad cur = load_xquad(p, S.s2h, st1.klo + 4 * min(qd, nquad - 1), m);
+    XQuad cur = load_xquad(p, S.s2h, klo + 4 * min(qd, nquad - 1), m);
     while (qd < nquad) {  // one quad in flight ahead of the one being quantised
       const uint32_t nx = qd + kConsumerThreads;
-      const XQuad nxt = load_xquad(p, S.s2h, st1.klo + 4 * min(nx, nquad - 1), m);
-      const uint32_t k0 = st1.klo + 4 * qd;
+      const XQuad nxt = load_xquad(p, S.s2h, klo + 4 * min(nx, nquad - 1), m);
+      const uint32_t k0 = klo + 4 * qd;
       long long v[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float a = cur.s[i] * cur.x[i];  // packed.cpp:160
-        v[i] = __float2ll_rn(scale_pow2(a, kFix - ea));
-        asum += v[i];
-        aabs += v[i] < 0 ? -v[i] : v[i];
+      for (int e = 0; e < 4; ++e) {
+        const float a = cur.s[e] * cur.x[e];  // packed.cpp:160
+        v[e] = __float2ll_rn(scale_pow2(a, kFix - ea));
+        asum += v[e];
+        aabs += v[e] < 0 ? -v[e] : v[e];
       }
-      emit_quad(bfrag, st1.klo, k0, q_of(k0, m), v);
+      emit_quad(bfrag, klo, k0, q_of(k0, m), v);
       cur = nxt;
       qd = nx;
     }
-    tc::fence_proxy_async_smem();  // B is read by the MMA through the async proxy
-    const long long A = cta_sum_i64(asum, red8);
+    const long long A = cta_sum_i64(asum, red8);  // also orders the bfrag stores
     const long long Aabs = cta_sum_i64(aabs, red8);
     // one CTA per slab range publishes sum|a_int| (bounds every |t_k| of the segment)
     if (tid == 0 && C.s1_rt0 == 0)
-      atomicAdd((unsigned long long*)&st->abs_a[b][C.s1_seg], (unsigned long long)Aabs);
+      atomicAdd((unsigned long long*)&p.st->abs_a[(ep & 1)][C.s1_seg], (unsigned long long)Aabs);
     TRACE(4);
-    mbar_wait_wd(&bars->full[0], 0);
-    expand_stage(st1, buf, bars, bars->tmem, nullptr);
+    StageArgs sa{C.s1_rtn, n1, 0, m, C.s1_sl0, klo, 0};  // linear: barrier full[0]
+    run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
+              (p.trace && warp == 0) ? p.trace + blockIdx.x * 32 + 22 : nullptr);
     TRACE(12);
-    mbar_wait_wd(&bars->dready, dphase & 1);
-    ++dphase;
-    tc::fence_after_sync();
+    consumers_sync();
     TRACE(5);
     long long* Tseg = p.T + (size_t)b * p.r_cap + S.t_off + (size_t)C.s1_rt0 * 16;
-    for (uint32_t rb = e; rb < st1.nrb; rb += 2) {
-      const long long P = d_row(bars->tmem, rb, wq);
-      const uint32_t row = rb * 128 + rl;
-      if (row < st1.rows) atomicAdd((unsigned long long*)&Tseg[row], (unsigned long long)(2 * P - A));
-    }
+    for (uint32_t i = tid; i < (uint32_t)C.s1_rtn * 16; i += kConsumerThreads)
+      atomicAdd((unsigned long long*)&Tseg[i],
+                (unsigned long long)(2 * row_value(red + i * kRedStride) - A));
   }
   {  // clear this CTA's share of the other t buffer for the next launch
     long long* Tn = p.T + (size_t)(b ^ 1) * p.r_cap;
@@ -549,7 +541,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
   }
 
   // --------------------------------------------------------------- grid barrier
-  tc::fence_before_sync();
   consumers_sync();  // the CTA's reds to t happen-before thread 0's fence (cumulativity)
   TRACE(6);
   if (tid == 0) {
@@ -564,10 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
       for (int sg = 0; sg < kMaxSeg; ++sg) st->abs_a[b ^ 1][sg] = 0;
     }
   }
-  if (!C.s2_rtn) {
-    if (warp == 0) tc::tmem_dealloc(bars->tmem, kTmemCols);
-    return;
-  }
+  if (!C.s2_rtn) return;
   TRACE(7);
   if (tid == 0) {
     uint32_t it = 0;
@@ -577,11 +565,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
     }
   }
   consumers_sync();
-  tc::fence_after_sync();
   TRACE(8);
+  for (int i = tid; i < kMaxRt * 16 * kRedStride; i += kConsumerThreads) red[i] = 0;
 
   // ------------------------------------------------------------------ stage 2
-  const Seg& S = S2seg;
+  const Seg& S = p.seg[C.s2_seg];
   const int ea = exponent_of(S.s2max * xmax);
   // |t_k| = |sum_j +-a_int_j| <= sum_j |a_int_j|, published exactly by stage 1
   const unsigned long long tbound = __ldcg((const unsigned long long*)&st->abs_a[b][C.s2_seg]);
@@ -589,7 +577,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
   const int sh = et - kFix;
   const long long* Tseg = p.T + (size_t)b * p.r_cap + S.t_off;
   const uint32_t nquad2 = kpad(S.r) / 4;
-  zero_b_hi(bfrag, nquad2 / 8, tid);
   long long tsum = 0;
   {
     uint32_t qd = tid;
@@ -600,42 +587,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
       load_tquad(Tseg, 4 * min(nx, nquad2 - 1), S.r, S.t_off, nxt);
       long long v[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        v[i] = sh > 0 ? (cur[i] + (1ll << (sh - 1))) >> sh : cur[i] * (1ll << (-sh));
-        tsum += v[i];
+      for (int e = 0; e < 4; ++e) {
+        v[e] = sh > 0 ? (cur[e] + (1ll << (sh - 1))) >> sh : cur[e] * (1ll << (-sh));
+        tsum += v[e];
       }
       emit_quad(bfrag, 0, 4 * qd, q_of(4 * qd, S.r), v);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
+      for (int e = 0; e < 4; ++e) cur[e] = nxt[e];
       qd = nx;
     }
   }
-  tc::fence_proxy_async_smem();
   const long long Tsum = cta_sum_i64(tsum, red8);
   TRACE(9);
-  mbar_wait_wd(&bars->full[1], 0);
-  expand_stage(st2, buf, bars, bars->tmem,
-               (p.trace && warp == 0) ? p.trace + blockIdx.x * 32 + 22 : nullptr);
+  uint32_t s1_bytes = 0;  // linear offset of the first stage-2 section
+  for (uint32_t s = 0; s < n1; ++s) s1_bytes += sec_bytes(s);
+  StageArgs sa{C.s2_rtn, C.nsec - n1, n1, S.r, 0, 0, s1_bytes};
+  if (!ring_mode) sa.sec_base = 1;  // linear: barrier full[1]
+  run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
+            (p.trace && warp == 0) ? p.trace + blockIdx.x * 32 + 27 : nullptr);
   TRACE(13);
-  mbar_wait_wd(&bars->dready, dphase & 1);
-  tc::fence_after_sync();
+  consumers_sync();
   TRACE(10);
   const int E = sh + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
-  for (uint32_t rb = e; rb < st2.nrb; rb += 2) {
-    const long long P = d_row(bars->tmem, rb, wq);
-    const uint32_t row = rb * 128 + rl;
-    if (row < st2.rows && C.s2_rt0 * 16 + row < S.n) {
-      const uint32_t orow = C.s2_rt0 * 16 + row;
-      const long long Y = 2 * P - Tsum;
-      const double y = (double)__half2float(S.s1h[orow]) * ldexp((double)Y, E);  // packed.cpp:189
-      if (p.y_f32) ((float*)p.y[C.s2_seg])[orow] = (float)y;
-      else ((__half*)p.y[C.s2_seg])[orow] = __float2half_rn((float)y);
-    }
+  for (uint32_t i = tid; i < (uint32_t)C.s2_rtn * 16; i += kConsumerThreads) {
+    const uint32_t row = C.s2_rt0 * 16 + i;
+    if (row >= S.n) continue;
+    const long long Y = 2 * row_value(red + i * kRedStride) - Tsum;
+    const double y = (double)__half2float(S.s1h[row]) * ldexp((double)Y, E);  // packed.cpp:189
+    if (p.y_f32) ((float*)p.y[C.s2_seg])[row] = (float)y;
+    else ((__half*)p.y[C.s2_seg])[row] = __float2half_rn((float)y);
   }
   TRACE(11);
-  tc::fence_before_sync();
-  consumers_sync();
-  if (warp == 0) tc::tmem_dealloc(bars->tmem, kTmemCols);
 }
 
 }  // namespace dec

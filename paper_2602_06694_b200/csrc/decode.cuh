@@ -3,23 +3,23 @@
 // y = s1 .* U (V^T (s2 .* x))  (gemv_two_stage, packed.cpp:153-192)
 //
 // The signs are consumed as {0,1} bits: sum_j sign_j a_j = 2 sum_j bit_j a_j -
-// sum_j a_j.  Activations are quantised once per call to 38-bit fixed point
-// against a per-segment power-of-two bound and split into six signed 8-bit
-// limbs: the B operand (N = 16 columns, limbs 0..5) of `tcgen05.mma kind::i8`.
-// The bits are the A operand (M = 128 rows x K = 32), written into TMEM by
-// expander warps with ONE LOP3 per four bits: tile q of a 256-wide K slab uses
-// A bytes {0, 2^q} (word & 0x01010101<<q) and B limbs of (value << (7-q)), so
-// every tile adds 2^7 * bit * value to the same int32 accumulators in TMEM.
-// All accumulation is exact integer arithmetic: the result is bitwise
-// deterministic and independent of the work split; the only rounding is the
-// 38-bit quantisation of a and of t.
+// sum_j a_j.  Activations are quantised once per call to 22-bit fixed point
+// against a per-segment power-of-two bound, split into four signed 8-bit limbs
+// and fed to the tensor cores as the B operand of `mma.sync m16n8k32 u8.s8`;
+// the bits are the A operand, expanded in registers with ONE LOP3 per four
+// bits: tile q of a 256-wide K slab uses A bytes {0, 2^q} (word & 0x01010101<<q)
+// and B limbs of (value << (7-q)), so every tile contributes 2^7 * bit * value
+// to the same int32 accumulators.  All accumulation is exact integer
+// arithmetic, so the result is bitwise deterministic and independent of the
+// work split; the only rounding is the 38-bit quantisation of a and of t.
 //
 // One launch computes both stages.  CTA c streams one contiguous byte range of
-// the plan's bit buffer (its stage-1 sections, then its stage-2 sections) into
-// shared memory with 1-D TMA bulk copies issued before griddepcontrol.wait, so
-// under Programmatic Dependent Launch they overlap the previous kernel.
-// Stage-1 partial sums are int64 red.add'ed into a global t accumulator; a
-// grid barrier (all CTAs co-resident: grid <= #SMs) separates the stages.
+// the plan's bit buffer (its stage-1 sections, then its stage-2 sections)
+// through a shared-memory ring filled by a producer warp with 1-D TMA bulk
+// copies; the first ring-full is issued before griddepcontrol.wait, so under
+// Programmatic Dependent Launch it overlaps the previous kernel.  Stage-1
+// partial sums are int64 red.add'ed into a global t accumulator; a grid
+// barrier (all CTAs co-resident: grid <= #SMs) separates the stages.
 #pragma once
 #include "common.cuh"
 
@@ -27,19 +27,20 @@ namespace nqb {
 namespace dec {
 
 constexpr int kMaxSeg = 4;         // layers sharing one input per launch
-constexpr int kConsumerWarps = 8;  // two expander warpgroups; + 1 producer/MMA warp
+#ifndef NQB_DEC_WARPS
+#define NQB_DEC_WARPS 16
+#endif
+constexpr int kConsumerWarps = NQB_DEC_WARPS;  // + 1 producer warp
 constexpr int kConsumerThreads = kConsumerWarps * 32;
 constexpr int kThreads = kConsumerThreads + 32;
-constexpr int kMaxRt = 32;         // 16-row tiles per CTA per stage (4 TMEM row blocks)
+constexpr int kMaxRt = 32;         // 16-row tiles per CTA per stage (4 per consumer warp)
 constexpr int kMaxSlabs1 = 16;     // stage-1 K slabs per CTA (4096 inputs)
 constexpr int kFix = 38;           // activations and t in 38-bit fixed point
 constexpr int kLimbs = 6;          // signed 8-bit limbs of (value << (7-q)) <= 2^45
 constexpr int kMaxGrid = 160;      // CTA table lives in the kernel parameters
-constexpr int kMmaN = 16;          // B columns (limbs 0..5, rest zero)
-constexpr int kTileB = kMmaN * 32;  // B bytes per 32-wide K tile (canonical K-major)
-constexpr int kBytesPerK = kMmaN;   // B bytes per input
-constexpr uint32_t kSmemHead = 1024;  // barriers + reduction scratch before the B operand
-constexpr uint32_t kTmemCols = 512;  // D: 4 row blocks x 16 columns; then 7 pair slots x 64
+constexpr int kTileB = kLimbs * 32;    // B-fragment bytes per 32-wide K tile
+constexpr int kBytesPerK = kLimbs;     // B-fragment bytes per input
+constexpr int kRedStride = 8;          // ints per row of the per-limb row sums
 
 // ---- K slabs: 256-wide (8 tiles of 32), then a 128 tail, then a 64 tail ----
 struct Slab {

@@ -30,25 +30,24 @@ struct RelayoutSrc {
   uint32_t u_words[kMaxSeg], vt_words[kMaxSeg];
 };
 
-// Stream format of one section (one K slab, the CTA's rows in order): each row
-// has nq words; bit 8b+bb of word wl is A[row][K = 32q + 4j + b] with
-//   nq=8: j = wl, q = bb;   nq=4: j = 2wl + bb/4, q = bb%4;   nq=2: j = 4wl + bb/2, q = bb%2
-// i.e. after `w & 0x01010101<<q` (and the shifts of decode.cu a_regs) the
-// eight 32-bit TMEM columns of a row hold its 32 A bytes {0, 2^q} of tile q.
-__host__ __device__ __forceinline__ uint32_t word_k(uint32_t nq, uint32_t wl, uint32_t p) {
+// Maps (lane, word, bit) of a unit with nq tiles to (row in tile, K in slab).
+__host__ __device__ __forceinline__ void unit_pos(uint32_t nq, uint32_t lane, uint32_t wl,
+                                                  uint32_t p, uint32_t& row, uint32_t& kk) {
   const uint32_t b = p >> 3, bb = p & 7;
-  uint32_t j, q;
+  uint32_t i, q;
   if (nq == 8) {
-    j = wl;
+    i = wl;
     q = bb;
   } else if (nq == 4) {
-    j = 2 * wl + (bb >> 2);
+    i = 2 * wl + (bb >> 2);
     q = bb & 3;
   } else {
-    j = 4 * wl + (bb >> 1);
+    i = bb >> 1;
     q = bb & 1;
   }
-  return 32 * q + 4 * j + b;
+  const uint32_t g = lane >> 2, c = lane & 3;
+  row = g + 8 * (i & 1);
+  kk = 32 * q + 16 * (i >> 1) + 4 * c + b;
 }
 
 // One block per CTA of the plan: writes that CTA's byte stream.
@@ -66,12 +65,16 @@ __global__ void k_relayout(const Cta* __restrict__ ctas, const Seg* __restrict__
     const Slab sl = slab_of(K, st1 ? C.s1_sl0 + sec : sec - n1);
     const uint32_t rtn = st1 ? C.s1_rtn : C.s2_rtn;
     const uint32_t rt0 = st1 ? C.s1_rt0 : C.s2_rt0;
-    const uint32_t words = rtn * 16 * sl.nq;
+    const uint32_t unit_words = 16 * sl.nq, lane_words = sl.nq / 2;
+    const uint32_t words = rtn * unit_words;
     for (uint32_t x = threadIdx.x; x < words; x += blockDim.x) {
-      const uint32_t row = x / sl.nq, wl = x % sl.nq;
+      const uint32_t t = x / unit_words, rem = x % unit_words;
+      const uint32_t lane = rem / lane_words, wl = rem % lane_words;
       uint32_t v = 0;
       for (uint32_t p = 0; p < 32; ++p) {
-        const uint32_t R = rt0 * 16 + row, k = sl.k0 + word_k(sl.nq, wl, p);
+        uint32_t row, kk;
+        unit_pos(sl.nq, lane, wl, p, row, kk);
+        const uint32_t R = (rt0 + t) * 16 + row, k = sl.k0 + kk;
         uint32_t bit = 0;
         if (st1) {  // V^T: row = rank index, K = input index j
           if (R < S.r && k < m)
@@ -361,14 +364,12 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   // Stream buffer: the whole per-CTA stream when it fits the cap (linear mode:
   // every copy issued up front, one mbarrier per section); otherwise the CTA
   // streams through fixed slots (ring mode).
-  const uint32_t cap = env_u32("NQB_DEC_SMEM_KB", 176) * 1024;
+  const uint32_t cap = env_u32("NQB_DEC_SMEM_KB", 160) * 1024;
   const uint32_t buf = (uint32_t)std::min<uint64_t>((max_stream + 127) / 128 * 128, cap);
   uint32_t slot = 0, nbar = 2;  // linear mode: one mbarrier per stage
   for (uint32_t c = 0; c < G; ++c) {
     Cta& C = ctas[c];
     C.ring = sbytes[c] > buf ? 1 : 0;
-    NQB_REQUIRE(!C.ring, NQB_E_DIMENSION_MISMATCH,
-                "decode plan: a CTA stream exceeds shared memory (layer too large)");
   }
   for (uint32_t c = 0; c < G; ++c) {
     const Cta& C = ctas[c];
@@ -390,8 +391,9 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   g->slot_bytes = slot;
   g->nbar = nbar;
   g->bfrag_bytes = (bfrag + 127) / 128 * 128;
-  // [barriers + scratch kSmemHead][B operand][stream buffer]
-  g->smem_bytes = kSmemHead + g->bfrag_bytes + buf;
+  // [mbarriers 2*nbar*8][misc 256][red kMaxRt*16*8][bfrag][stream buffer]
+  const uint32_t head = ((16 * nbar + 256 + kMaxRt * 16 * kRedStride * 4) + 127) / 128 * 128;
+  g->smem_bytes = head + g->bfrag_bytes + buf;
   NQB_REQUIRE(g->smem_bytes <= 227 * 1024, NQB_E_DIMENSION_MISMATCH,
               "decode plan exceeds shared memory (" + std::to_string(g->smem_bytes) + " B)");
 
