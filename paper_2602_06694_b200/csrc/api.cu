@@ -28,6 +28,7 @@ void simt_gemm_f64(nqb_context*, const nqb_layer*, const double*, uint32_t, doub
 void decode_gemv_f32(nqb_context*, const nqb_layer*, const float*, float*);
 void decode_gemv_f16(nqb_context*, const nqb_layer*, const __half*, __half*);
 void prefill_gemm_f16(nqb_context*, const nqb_layer*, const __half*, uint32_t, __half*);
+void prefill_gemm_tc(nqb_context*, const nqb_layer*, const __half*, uint32_t, __half*);
 
 thread_local std::string g_last_error;
 
@@ -531,7 +532,7 @@ int nqb_gemm_f16_device(nqb_context* ctx, const nqb_layer* L, const uint16_t* d_
   check_ctx(ctx);
   check_layer(L);
   if (b == 0) return NQB_OK;
-  prefill_gemm_f16(ctx, L, (const __half*)d_x, b, (__half*)d_y);
+  prefill_gemm_tc(ctx, L, (const __half*)d_x, b, (__half*)d_y);
   API_END
 }
 
