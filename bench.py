@@ -57,6 +57,13 @@ def algo_bytes(n, m, r):
     return r * (n + m) / 8.0 + 2 * (n + m) + 2 * m + 2 * n
 
 
+def tensor_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["bf16_tflops"])
+    return 1590.0
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -271,6 +278,18 @@ def shape_roofline(nq, ctx, torch, stream, n, m, r, reps=20):
     return sec / copies, per
 
 
+def prefill_roofline(nq, ctx, torch, stream, n, m, r, b=2048, reps=10):
+    """Prefill GEMM (tcgen05 kind::f16) on one layer, b tokens: seconds per call
+    and TFLOP/s of the algorithmic 2*b*r*(n+m) FLOPs."""
+    rng = np.random.default_rng(n * 3 + m)
+    lay = nq.DeviceLayer.upload_f16(n, m, r, *random_layer_arrays(rng, n, m, r), ctx)
+    x = torch.randn(b, m, device="cuda", dtype=torch.float16)
+    y = torch.empty(b, n, device="cuda", dtype=torch.float16)
+    sec, _, g = graph_time(torch, ctx, stream, lambda: lay.gemm_device(x, y), reps)
+    g.free()
+    return sec, 2.0 * b * r * (n + m) / sec / 1e12
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -392,6 +411,15 @@ def main():
                 shapes[f"{name}_{bpw}"] = {"n": n, "m": m, "r": r, "us": sec * 1e6,
                                            "gbs": per / sec / 1e9, "frac": per / sec / 1e9 / peak}
         extra["per_shape_single_layer"] = shapes
+        if not args.no_shapes:
+            pref = {}
+            tpk = tensor_peak()
+            for name, n, m, bpw in L70_SHAPES:
+                r = rank_for(n, m, bpw)
+                sec, tf = prefill_roofline(nq, ctx, torch, stream, n, m, r)
+                pref[f"{name}_{bpw}_b2048"] = {"n": n, "m": m, "r": r, "ms": sec * 1e3,
+                                               "tflops": tf, "frac_of_bf16_peak": tf / tpk}
+            extra["prefill_tcgen05"] = pref
         achieved = step_bytes * args.steps / secs / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,

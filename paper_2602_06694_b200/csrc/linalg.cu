@@ -17,10 +17,13 @@
 //       blocked right-looking Cholesky (DMMA trailing updates), blocked
 //       triangular solves and one refinement pass against the original A.
 // All reductions use fixed trees, so results are bitwise reproducible.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace nqb {
 
@@ -28,6 +31,10 @@ void dgemm(nqb_context*, bool, bool, uint32_t, uint32_t, uint32_t, double, const
            uint32_t, const double*, uint32_t, double, double*, uint32_t);
 
 constexpr int PI_THREADS = 512;
+static bool getenv_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && *v && *v != '0';
+}
 constexpr uint32_t PI_MAX_COLS = 14336;
 
 // ---------------------------------------------------------------------------
@@ -148,7 +155,16 @@ __global__ void k_colstats_finish(const double* __restrict__ colpart, uint32_t n
                                   double* __restrict__ v0, double* __restrict__ total) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (uint32_t b = 0; b < nparts; ++b) s += colpart[(uint64_t)b * cols + j];
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 independent load chains
+    uint32_t b = 0;
+    for (; b + 3 < nparts; b += 4) {
+      s += colpart[(uint64_t)b * cols + j];
+      s1 += colpart[(uint64_t)(b + 1) * cols + j];
+      s2 += colpart[(uint64_t)(b + 2) * cols + j];
+      s3 += colpart[(uint64_t)(b + 3) * cols + j];
+    }
+    for (; b < nparts; ++b) s += colpart[(uint64_t)b * cols + j];
+    s = (s + s1) + (s2 + s3);
     v0[j] = sqrt(s);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -279,7 +295,16 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
     double wq = 0.0;
     for (uint32_t j = bid * PI_THREADS + tid; j < a.cols; j += G * PI_THREADS) {
       double s = 0.0;
-      for (uint32_t b = 0; b < G; ++b) s += __ldcg(a.wpart + (uint64_t)b * a.cols + j);
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 independent load chains
+      uint32_t b = 0;
+      for (; b + 3 < G; b += 4) {
+        s += __ldcg(a.wpart + (uint64_t)b * a.cols + j);
+        s1 += __ldcg(a.wpart + (uint64_t)(b + 1) * a.cols + j);
+        s2 += __ldcg(a.wpart + (uint64_t)(b + 2) * a.cols + j);
+        s3 += __ldcg(a.wpart + (uint64_t)(b + 3) * a.cols + j);
+      }
+      for (; b < G; ++b) s += __ldcg(a.wpart + (uint64_t)b * a.cols + j);
+      s = (s + s1) + (s2 + s3);
       a.w[j] = s;
       wq += s * s;
     }
@@ -288,11 +313,15 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
     grid_sync(a.bar, G);
 
     // ---- phase C (every block, identical): sigma, normalise, stop rule ------
+    // G partials: one (independent) load per thread, then the fixed block tree
+    // (identical in every block) instead of G dependent L2 round trips.
     double s2 = 0.0, w2 = 0.0;
-    for (uint32_t b = 0; b < G; ++b) {
+    for (uint32_t b = tid; b < G; b += PI_THREADS) {
       s2 += __ldcg(ssp + b);
       w2 += __ldcg(a.wsspart + b);
     }
+    s2 = block_sum(s2, bred);
+    w2 = block_sum(w2, bred);
     sigma = sqrt(s2);
     if (sigma == 0.0) break;  // linalg.cpp:111
     const double wn = sqrt(w2);
@@ -332,7 +361,8 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
   if (tid == 0) ssf[bid] = ss;
   grid_sync(a.bar, G);
   double s2 = 0.0;
-  for (uint32_t b = 0; b < G; ++b) s2 += __ldcg(ssf + b);
+  for (uint32_t b = tid; b < G; b += PI_THREADS) s2 += __ldcg(ssf + b);
+  s2 = block_sum(s2, bred);
   const double fsig = sqrt(s2);
   for (uint32_t i = r0 + tid; i < r1; i += PI_THREADS) {
     a.left[i] = fsig > 0.0 ? a.left[i] / fsig : 0.0;
@@ -345,6 +375,222 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
       a.out[2] = (double)it;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Streaming persistent power iteration (even column counts).  Same algorithm
+// and outputs as k_power; each block's rows stream through a shared-memory
+// ring filled by 1-D TMA bulk copies (HBM-bound phase A with the next rows
+// already in flight), and the cross-block reduction of w is spread over all
+// blocks and warps with independent loads (phase B), fixed order throughout.
+// ---------------------------------------------------------------------------
+constexpr int PS_MAX_SLOTS = 8;
+
+template <int CPT>
+__global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uint32_t nslots,
+                                                               uint32_t row_bytes) {
+  extern __shared__ __align__(128) uint8_t ring[];               // nslots x row_bytes
+  __shared__ uint64_t fullb[PS_MAX_SLOTS];
+  __shared__ double bred[PI_THREADS / 32];
+  __shared__ double cred[PI_THREADS / 32][33];
+  const uint32_t tid = threadIdx.x, G = gridDim.x, bid = blockIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const uint32_t r0 = (uint32_t)((uint64_t)a.rows * bid / G);
+  const uint32_t r1 = (uint32_t)((uint64_t)a.rows * (bid + 1) / G);
+  const uint32_t nrows = r1 - r0;
+  const uint32_t cb0 = (uint32_t)((uint64_t)a.cols * bid / G);
+  const uint32_t cb1 = (uint32_t)((uint64_t)a.cols * (bid + 1) / G);
+  if (tid == 0) {
+    for (uint32_t s = 0; s < nslots; ++s) tc::mbar_init(&fullb[s], 1);
+    tc::fence_mbar_init();
+  }
+  // v lives in registers: thread t owns columns t + c*PI_THREADS
+  double vr[CPT];
+  double sq = 0.0;
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const uint32_t j = tid + c * PI_THREADS;
+    vr[c] = j < a.cols ? a.v[j] : 0.0;
+    sq += vr[c] * vr[c];
+  }
+  const double nrm = sqrt(block_sum(sq, bred));  // normalize (linalg.cpp:70-75)
+  if (nrm > 0.0)
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) vr[c] /= nrm;
+  __syncthreads();
+
+  uint32_t phase = 0;  // bit s: parity of the next completion of slot s
+  auto issue = [&](uint32_t i) {  // row r0+i -> slot i % nslots (thread 0)
+    uint64_t* bar = &fullb[i % nslots];
+    tc::mbar_arrive_expect_tx(bar, row_bytes);
+    tc::bulk_g2s(ring + (size_t)(i % nslots) * row_bytes, a.M + (uint64_t)(r0 + i) * a.cols,
+                 row_bytes, bar);
+  };
+  double sigma = 0.0, sigma_prev = -1.0;
+  int converged = 0, it = 0;
+  for (it = 0; it < a.max_iters; ++it) {
+    // ---- phase A: s_i = M_i . v ; w += s_i M_i, rows streamed through smem --
+    if (tid == 0)
+      for (uint32_t i = 0; i < nrows && i < nslots; ++i) issue(i);
+    double wl[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) wl[c] = 0.0;
+    double ss = 0.0;
+    for (uint32_t i = 0; i < nrows; ++i) {
+      const uint32_t slot = i % nslots;
+      tc::mbar_wait(&fullb[slot], (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+      const double* x = (const double*)(ring + (size_t)slot * row_bytes);
+      double p = 0.0;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const uint32_t j = tid + c * PI_THREADS;
+        if (j < a.cols) {
+          double xx = x[j];
+          if (a.abs_mode) xx = fabs(xx);
+          p += xx * vr[c];
+        }
+      }
+      const double s = block_sum(p, bred);  // identical in every thread
+      ss += s * s;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const uint32_t j = tid + c * PI_THREADS;
+        if (j < a.cols) {
+          double xx = x[j];
+          if (a.abs_mode) xx = fabs(xx);
+          wl[c] += xx * s;
+        }
+      }
+      __syncthreads();  // everyone is done with this slot
+      if (tid == 0 && i + nslots < nrows) issue(i + nslots);
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const uint32_t j = tid + c * PI_THREADS;
+      if (j < a.cols) a.wpart[(uint64_t)bid * a.cols + j] = wl[c];
+    }
+    double* ssp = a.sspart + (size_t)(it & 1) * G;
+    if (tid == 0) ssp[bid] = ss;
+    grid_sync(a.bar, G);
+
+    // ---- phase B: w_j = sum_b wpart[b][j] for this block's columns; warp k
+    // sums partials b = k, k+16, ... (independent loads), then a fixed-order
+    // cross-warp sum.
+    double wq = 0.0;
+    for (uint32_t c0 = cb0; c0 < cb1; c0 += 32) {
+      const uint32_t j = c0 + lane;
+      double acc = 0.0;
+      if (j < cb1) {
+        double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+        uint32_t b = warp;
+        for (; b + 48 < G; b += 64) {
+          q0 += __ldcg(a.wpart + (uint64_t)b * a.cols + j);
+          q1 += __ldcg(a.wpart + (uint64_t)(b + 16) * a.cols + j);
+          q2 += __ldcg(a.wpart + (uint64_t)(b + 32) * a.cols + j);
+          q3 += __ldcg(a.wpart + (uint64_t)(b + 48) * a.cols + j);
+        }
+        for (; b < G; b += 16) q0 += __ldcg(a.wpart + (uint64_t)b * a.cols + j);
+        acc = (q0 + q1) + (q2 + q3);
+      }
+      cred[warp][lane] = acc;
+      __syncthreads();
+      if (warp == 0 && j < cb1) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < PI_THREADS / 32; ++k) s += cred[k][lane];
+        a.w[j] = s;
+        wq += s * s;
+      }
+      __syncthreads();
+    }
+    wq = block_sum(wq, bred);
+    if (tid == 0) a.wsspart[bid] = wq;
+    grid_sync(a.bar, G);
+
+    // ---- phase C (every block, identical): sigma, normalise, stop rule ------
+    // G partials: one (independent) load per thread, then the fixed block tree
+    // (identical in every block) instead of G dependent L2 round trips.
+    double s2 = 0.0, w2 = 0.0;
+    for (uint32_t b = tid; b < G; b += PI_THREADS) {
+      s2 += __ldcg(ssp + b);
+      w2 += __ldcg(a.wsspart + b);
+    }
+    s2 = block_sum(s2, bred);
+    w2 = block_sum(w2, bred);
+    sigma = sqrt(s2);
+    if (sigma == 0.0) break;  // linalg.cpp:111
+    const double wn = sqrt(w2);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const uint32_t j = tid + c * PI_THREADS;
+      if (j < a.cols) {
+        const double x = __ldcg(a.w + j);
+        vr[c] = wn > 0.0 ? x / wn : x;
+      }
+    }
+    if (sigma_prev >= 0.0 && fabs(sigma - sigma_prev) <= a.tol * fmax(sigma, 1e-300)) {
+      converged = 1;
+      ++it;
+      break;
+    }
+    sigma_prev = sigma;
+  }
+
+  // ---- final: mv = M v, sigma = ||mv||, left = mv / sigma (linalg.cpp:124-130)
+  double ss = 0.0;
+  for (uint32_t i = r0; i < r1; ++i) {
+    double p = 0.0;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const uint32_t j = tid + c * PI_THREADS;
+      if (j < a.cols) {
+        double x = __ldg(a.M + (uint64_t)i * a.cols + j);
+        if (a.abs_mode) x = fabs(x);
+        p += x * vr[c];
+      }
+    }
+    const double s = block_sum(p, bred);
+    if (tid == 0) {
+      a.left[i] = s;
+      ss += s * s;
+    }
+  }
+  double* ssf = a.sspart + 2 * (size_t)G;
+  if (tid == 0) ssf[bid] = ss;
+  grid_sync(a.bar, G);
+  double s2 = 0.0;
+  for (uint32_t b = tid; b < G; b += PI_THREADS) s2 += __ldcg(ssf + b);
+  s2 = block_sum(s2, bred);
+  const double fsig = sqrt(s2);
+  for (uint32_t i = r0 + tid; i < r1; i += PI_THREADS) {
+    a.left[i] = fsig > 0.0 ? a.left[i] / fsig : 0.0;
+  }
+  if (bid == 0) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const uint32_t j = tid + c * PI_THREADS;
+      if (j < a.cols) a.v[j] = vr[c];
+    }
+    if (tid == 0) {
+      a.out[0] = fsig;
+      a.out[1] = (fsig > 0.0) ? (double)converged : 0.0;
+      a.out[2] = (double)it;
+    }
+  }
+}
+
+template <int CPT>
+static void launch_power_stream(nqb_context* ctx, PowerArgs& a, uint32_t grid) {
+  const uint32_t row_bytes = a.cols * 8;  // cols even: 16-byte multiple, 16-byte aligned rows
+  uint32_t nslots = (uint32_t)std::min<size_t>(PS_MAX_SLOTS, (200 * 1024) / row_bytes);
+  const size_t smem = (size_t)nslots * row_bytes;
+  auto kern = k_power_stream<CPT>;
+  NQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* args[] = {&a, &nslots, (void*)&row_bytes};
+  NQB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(PI_THREADS), args,
+                                       smem, ctx->stream));
+  NQB_LAUNCHED(ctx);
 }
 
 struct PowerWork {
@@ -392,7 +638,16 @@ void power_iterate_device(nqb_context* ctx, const double* d_m, uint32_t rows, ui
   a.out = a.wsspart + grid;
   a.bar = ctx->barrier;
   const uint32_t cpt = ceil_div(cols, PI_THREADS);
-  if (cpt <= 2) launch_power_t<2, 8, false>(ctx, a, grid);
+  const bool stream = (cols % 2 == 0) && 2 * (size_t)cols * 8 <= 200 * 1024 &&
+                      cpt <= 22 && rows >= 2 * grid && !getenv_flag("NQB_POWER_LEGACY");
+  if (stream) {
+    if (cpt <= 2) launch_power_stream<2>(ctx, a, grid);
+    else if (cpt <= 4) launch_power_stream<4>(ctx, a, grid);
+    else if (cpt <= 8) launch_power_stream<8>(ctx, a, grid);
+    else if (cpt <= 12) launch_power_stream<12>(ctx, a, grid);
+    else if (cpt <= 16) launch_power_stream<16>(ctx, a, grid);
+    else launch_power_stream<22>(ctx, a, grid);
+  } else if (cpt <= 2) launch_power_t<2, 8, false>(ctx, a, grid);
   else if (cpt <= 4) launch_power_t<4, 8, false>(ctx, a, grid);
   else if (cpt <= 8) launch_power_t<8, 4, false>(ctx, a, grid);
   else if (cpt <= 12) launch_power_t<12, 2, false>(ctx, a, grid);

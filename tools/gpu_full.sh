@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/status.txt
+for sz in "1024 1024 1.0" "2048 2048 1.0" "4096 4096 1.0"; do timeout 900 python tools/admm_time.py $sz >> gpurun_out/admm_time.log 2>&1; done
+echo admm=$? >> gpurun_out/status.txt
+timeout 900 python bench.py --steps 20 --warmup 3 --cpu-seconds 10 > gpurun_out/bench.log 2>&1; echo bench=$? >> gpurun_out/status.txt

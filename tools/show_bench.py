@@ -10,3 +10,5 @@ for f in sys.argv[1:]:
           round(ro.get("us_per_launch", 0), 2), "e2e", round((d.get("e2e") or {}).get("value", 0), 1))
     for k, v in sh.items():
         print(f"   {k:16s} {v['us']:8.2f} us  {v['gbs']:8.1f} GB/s  frac {v['frac']:.3f}")
+    for k, v in (d.get("extra") or {}).get("prefill_tcgen05", {}).items():
+        print(f"   prefill {k:22s} {v['ms']:8.3f} ms  {v['tflops']:7.1f} TFLOP/s  frac {v['frac_of_bf16_peak']:.3f}")
