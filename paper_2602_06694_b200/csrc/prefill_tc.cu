@@ -14,6 +14,9 @@
 // TMEM (tcgen05.ld), applies the row scale (s1) and writes token-major
 // binary16.  At N = 256 one 4 KB A operand feeds 128x256x16 MACs, so unlike
 // batch-1 decode the expansion is cheap relative to the math.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -23,12 +26,14 @@ namespace nqb {
 namespace pf {
 
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 3;
-constexpr int A_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_BYTES = BN * BK * 2;  // 32 KB
-constexpr int kProducers = 128;       // 4 warps; warp 4 issues the MMAs
-constexpr uint32_t kTmemCols = 256;   // D: 128 lanes x 256 fp32 columns
+constexpr int MH = 2;                      // M=128 halves per CTA: 256 rows share each B tile
+constexpr int A_BYTES = MH * BM * BK * 2;  // 32 KB
+constexpr int B_BYTES = BN * BK * 2;       // 32 KB
+constexpr int kProducers = MH * BM;        // one thread per A row; the next warp issues MMAs
+constexpr uint32_t kTmemCols = 512;        // D_h: 128 lanes x 256 fp32 columns each
 
-struct Args {
+struct alignas(64) Args {
+  CUtensorMap bmap;       // B (tokens x K binary16) for TMA: box 8 K x 256 tokens
   const uint32_t* bits;   // A sign bits: row-major, words_per_row u32 per row
   uint32_t wpr;           // words per A row
   uint32_t M;             // A rows (r or n)
@@ -50,6 +55,17 @@ __device__ __forceinline__ uint32_t canon(uint32_t row, uint32_t k8, uint32_t R)
   return ((ks * 2 + kh) * (R / 8) + (row >> 3)) * 128 + (row & 7) * 16;
 }
 
+// 2-D TMA: box (8 K-elements, 256 tokens) at (k, token) -> one canonical
+// [row group][row][16 B] column of the B tile; complete_tx on the mbarrier.
+__device__ __forceinline__ void tma_b(void* dst, const CUtensorMap* map, uint32_t k, uint32_t tok,
+                                      uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(map), "r"(k), "r"(tok), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+
 struct __align__(8) Bars {
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
@@ -63,11 +79,11 @@ __global__ void __launch_bounds__(kProducers + 32, 1) k_prefill(const __grid_con
   uint8_t* tiles = smem + 1024;  // STAGES x [A 16 KB | B 32 KB]
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(~0u, tid >> 5, 0);
-  const uint32_t m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const uint32_t m0 = blockIdx.x * (MH * BM), n0 = blockIdx.y * BN;
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      tc::mbar_init(&bars->full[s], kProducers);
+      tc::mbar_init(&bars->full[s], kProducers + 1);  // producers + the TMA issuer
       tc::mbar_init(&bars->empty[s], 1);
     }
     tc::mbar_init(&bars->dready, 1);
@@ -93,53 +109,63 @@ __global__ void __launch_bounds__(kProducers + 32, 1) k_prefill(const __grid_con
         const uint32_t bbase = abase + A_BYTES;
 #pragma unroll
         for (uint32_t ks = 0; ks < BK / 16; ++ks) {
-          const uint64_t ad = tc::smem_desc_kmajor(abase + ks * 2 * (BM / 8) * 128, (BM / 8) * 128, 128);
           const uint64_t bd = tc::smem_desc_kmajor(bbase + ks * 2 * (BN / 8) * 128, (BN / 8) * 128, 128);
-          tc::mma_f16_ss(tmem, ad, bd, idesc, (kt | ks) ? 1u : 0u);
+#pragma unroll
+          for (uint32_t h = 0; h < MH; ++h) {
+            const uint64_t ad = tc::smem_desc_kmajor(abase + h * (A_BYTES / MH) + ks * 2 * (BM / 8) * 128,
+                                                     (BM / 8) * 128, 128);
+            tc::mma_f16_ss(tmem + h * BN, ad, bd, idesc, (kt | ks) ? 1u : 0u);
+          }
         }
         tc::mma_commit(&bars->empty[slot]);
       }
       tc::mma_commit(&bars->dready);
     }
   } else {  // ------------------------------------------------------ producers
+    // thread t expands row t of the A tile: one 64-bit load covers its 64 K of
+    // a K tile; the next tile's bits are prefetched while this one is written.
+    const uint32_t row = tid, grow = m0 + row;
+    const bool rv = grow < a.M;
+    const uint32_t* brow = a.bits + (size_t)(rv ? grow : 0) * a.wpr;
+    auto load_bits = [&](uint32_t kt) -> uint2 {
+      return (rv && kt < a.nk) ? __ldg((const uint2*)(brow + kt * 2)) : make_uint2(0u, 0u);
+    };
+    uint2 cur = load_bits(0);
     for (uint32_t kt = 0; kt < a.nk; ++kt) {
+      const uint2 nxt = load_bits(kt + 1);
       const uint32_t slot = kt % STAGES, use = kt / STAGES;
       if (use > 0) tc::mbar_wait(&bars->empty[slot], (use - 1) & 1);
       uint8_t* As = tiles + slot * (A_BYTES + B_BYTES);
       uint8_t* Bs = As + A_BYTES;
-      // A: 128 rows x 64 K signs -> +-1 binary16 (8 elements per 16-byte chunk)
-#pragma unroll 2
-      for (uint32_t c = tid; c < BM * (BK / 8); c += kProducers) {
-        const uint32_t row = c >> 3, k8 = c & 7, k = kt * BK + k8 * 8;
-        uint32_t byte = 0;
-        if (m0 + row < a.M) byte = (__ldg(a.bits + (size_t)(m0 + row) * a.wpr + (k >> 5)) >> (k & 31)) & 0xFFu;
+      if (tid == 0) {  // B: 8 TMA boxes (one per 8-wide K chunk) of 256 tokens
+        tc::mbar_arrive_expect_tx(&bars->full[slot], B_BYTES);
+#pragma unroll
+        for (uint32_t k8 = 0; k8 < BK / 8; ++k8)
+          tma_b(Bs + canon(0, k8, BN), &a.bmap, kt * BK + k8 * 8, n0, &bars->full[slot]);
+      }
+      // A: 64 signs of this row -> 8 chunks of 8 +-1 binary16 (bit 1 -> +1 0x3C00, 0 -> -1 0xBC00)
+#pragma unroll
+      for (uint32_t k8 = 0; k8 < 8; ++k8) {
+        const uint32_t byte = ((k8 < 4 ? cur.x : cur.y) >> (8 * (k8 & 3))) & 0xFFu;
         uint4 v;
         uint32_t* pv = &v.x;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)  // bit 1 -> +1 (0x3C00), 0 -> -1 (0xBC00)
+        for (int i = 0; i < 4; ++i)
           pv[i] = 0xBC00BC00u ^ (((byte >> (2 * i)) & 1u) << 15) ^ (((byte >> (2 * i + 1)) & 1u) << 31);
-        *(uint4*)(As + canon(row, k8, BM)) = v;
+        *(uint4*)(As + (row / BM) * (A_BYTES / MH) + canon(row % BM, k8, BM)) = v;
       }
-      // B: 256 tokens x 64 K binary16
-#pragma unroll 4
-      for (uint32_t c = tid; c < BN * (BK / 8); c += kProducers) {
-        const uint32_t row = c >> 3, k8 = c & 7;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (n0 + row < a.N) v = __ldg((const uint4*)(a.B + (size_t)(n0 + row) * a.ldb + kt * BK + k8 * 8));
-        *(uint4*)(Bs + canon(row, k8, BN)) = v;
-      }
+      cur = nxt;
       tc::fence_proxy_async_smem();  // generic-proxy writes -> MMA (async proxy) reads
       tc::mbar_arrive(&bars->full[slot]);
     }
     // ------------------------------------------------------------- epilogue
     tc::mbar_wait(&bars->dready, 0);
     tc::fence_after_sync();
-    const uint32_t row = warp * 32 + lane, grow = m0 + row;
     const float sc = (grow < a.Mvalid && a.scale) ? __half2float(a.scale[grow]) : 1.f;
     const bool keep = grow < a.Mvalid;
     for (uint32_t c0 = 0; c0 < BN; c0 += 16) {
       uint32_t v[16];
-      tc::tmem_ld_x16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+      tc::tmem_ld_x16(tmem + (row / BM) * BN + ((uint32_t)((warp & 3) * 32) << 16) + c0, v);
       tc::wait_ld();
       if (grow < a.Mout) {
 #pragma unroll
@@ -173,6 +199,32 @@ __global__ void k_prescale(const __half* __restrict__ x, const __half* __restric
 
 using namespace pf;
 
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    NQB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    NQB_REQUIRE(p && q == cudaDriverEntryPointSuccess, NQB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// B = tokens x ld binary16 (K = kdim valid columns); box 8 K x 256 tokens;
+// out-of-range tokens / K read as zero.
+static void make_bmap(CUtensorMap* map, const __half* B, uint32_t kdim, uint32_t ld, uint32_t tokens) {
+  const cuuint64_t dims[2] = {kdim, tokens};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t box[2] = {8, (cuuint32_t)BN};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)B, dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  NQB_REQUIRE(r == CUDA_SUCCESS, NQB_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
 static void launch_stage(nqb_context* ctx, const Args& a, uint32_t grid_m, uint32_t grid_n) {
   static bool attr = false;
   if (!attr) {
@@ -180,8 +232,8 @@ static void launch_stage(nqb_context* ctx, const Args& a, uint32_t grid_m, uint3
                                   1024 + STAGES * (A_BYTES + B_BYTES)));
     attr = true;
   }
-  k_prefill<<<dim3(grid_m, grid_n), kProducers + 32, 1024 + STAGES * (A_BYTES + B_BYTES),
-              ctx->stream>>>(a);
+  k_prefill<<<dim3((grid_m + MH - 1) / MH, grid_n), kProducers + 32,
+              1024 + STAGES * (A_BYTES + B_BYTES), ctx->stream>>>(a);
   NQB_LAUNCHED(ctx);
 }
 
@@ -198,10 +250,12 @@ void prefill_gemm_tc(nqb_context* ctx, const nqb_layer* L, const __half* d_x, ui
       d_x, L->s2h, L->m, b, mpad, xs);
   NQB_LAUNCHED(ctx);
   // stage 1: T^T[token][k] = sum_j sign(V[j][k]) * xs[token][j]   (rows k < r, padded rows 0)
-  Args a1{L->vt, L->vt_words, L->r, L->r, rpad, mpad / BK, xs, mpad, b, nullptr, tt, rpad};
+  Args a1{{}, L->vt, L->vt_words, L->r, L->r, rpad, mpad / BK, xs, mpad, b, nullptr, tt, rpad};
+  make_bmap(&a1.bmap, xs, mpad, mpad, b);
   launch_stage(ctx, a1, (rpad + BM - 1) / BM, (b + BN - 1) / BN);
   // stage 2: Y[token][i] = s1_i * sum_k sign(U[i][k]) * T^T[token][k]
-  Args a2{L->u, L->u_words, L->n, L->n, L->n, rpad / BK, tt, rpad, b, L->s1h, d_y, L->n};
+  Args a2{{}, L->u, L->u_words, L->n, L->n, L->n, rpad / BK, tt, rpad, b, L->s1h, d_y, L->n};
+  make_bmap(&a2.bmap, tt, rpad, rpad, b);
   launch_stage(ctx, a2, (L->n + BM - 1) / BM, (b + BN - 1) / BN);
 }
 
