@@ -421,8 +421,16 @@ def main():
                                                "tflops": tf, "frac_of_bf16_peak": tf / tpk}
             extra["prefill_tcgen05"] = pref
         achieved = step_bytes * args.steps / secs / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "r01_decode_imma", "traffic.json")
+        if os.path.exists(tp):  # ncu dram__bytes_read+write per launch of this same step
+            traffic = json.load(open(tp))["step"]["dram_bytes_per_launch"]
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_note": "ncu dram bytes per launch (profiles/r01_decode_imma/traffic.json); "
+                                "algorithmic bytes per launch = algorithmic_bytes_per_step / "
+                                "launches_per_step",
+                "peak_source": peak_kind,
                 "kernel": "nqb::dec::k_decode (fused two-stage decode GEMV; every launch of the "
                           "step is this kernel, PDL-overlapped, so duration = step time / launches)",
                 "algorithmic_bytes_per_step": step_bytes, "launches_per_step": launches_per_step,
