@@ -113,6 +113,28 @@ __device__ __forceinline__ long long cta_sum_i64(long long v, long long* red8) {
   return s;
 }
 
+__device__ __forceinline__ void cta_sum2_i64(long long& a, long long& b, long long* red8) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(~0u, a, o);
+    b += __shfl_xor_sync(~0u, b, o);
+  }
+  consumers_sync();
+  if (lane == 0) {
+    red8[warp] = a;
+    red8[kConsumerWarps + warp] = b;
+  }
+  consumers_sync();
+  a = 0;
+  b = 0;
+#pragma unroll
+  for (int w = 0; w < kConsumerWarps; ++w) {
+    a += red8[w];
+    b += red8[kConsumerWarps + w];
+  }
+}
+
 __device__ __forceinline__ unsigned long long cta_max_u64(unsigned long long v,
                                                           unsigned long long* red8) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -516,8 +538,8 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
       cur = nxt;
       qd = nx;
     }
-    const long long A = cta_sum_i64(asum, red8);  // also orders the bfrag stores
-    const long long Aabs = cta_sum_i64(aabs, red8);
+    cta_sum2_i64(asum, aabs, red8);  // also orders the bfrag stores
+    const long long A = asum, Aabs = aabs;
     // one CTA per slab range publishes sum|a_int| (bounds every |t_k| of the segment)
     if (tid == 0 && C.s1_rt0 == 0)
       atomicAdd((unsigned long long*)&p.st->abs_a[(ep & 1)][C.s1_seg], (unsigned long long)Aabs);
