@@ -83,6 +83,10 @@ int nqb_destroy(nqb_context* ctx);
 int nqb_set_stream(nqb_context* ctx, void* cuda_stream);
 void* nqb_get_stream(nqb_context* ctx);
 int nqb_synchronize(nqb_context* ctx);
+/* Limit the persistent ADMM kernels of this context to `sms` SMs (<= 0: all),
+ * so several contexts can factorize matrices concurrently on one device.
+ * Decode plans built afterwards use the same budget. */
+int nqb_set_sm_budget(nqb_context* ctx, int sms);
 /* Device kernels launched by this context since creation (instrumentation). */
 uint64_t nqb_kernel_launches(const nqb_context* ctx);
 

@@ -93,6 +93,7 @@ PROTOTYPES = {
     "nqb_group_gemv_f16_device": (C.c_int, [P, P, P, PP]),
     "nqb_group_gemv_f32_device": (C.c_int, [P, P, P, PP]),
     "nqb_set_pdl": (C.c_int, [P, C.c_int]),
+    "nqb_set_sm_budget": (C.c_int, [P, C.c_int]),
     "nqb_debug_decode_trace": (C.c_int, [P, P, P, P, P, PU32]),
     "nqb_graph_begin": (C.c_int, [P]),
     "nqb_graph_end": (C.c_int, [P, PP]),

@@ -200,6 +200,15 @@ int nqb_synchronize(nqb_context* ctx) {
 
 uint64_t nqb_kernel_launches(const nqb_context* ctx) { return ctx ? ctx->launches : 0; }
 
+int nqb_set_sm_budget(nqb_context* ctx, int sms) {
+  API_BEGIN
+  check_ctx(ctx);
+  cudaDeviceProp prop;
+  NQB_CUDA(cudaGetDeviceProperties(&prop, ctx->device));
+  ctx->num_sms = (sms <= 0 || sms > prop.multiProcessorCount) ? prop.multiProcessorCount : sms;
+  API_END
+}
+
 // storage.cpp:124-141 (host arithmetic; no device work).
 int nqb_rank_for_target_bpw(uint64_t n, uint64_t m, double t, uint32_t* rank) {
   API_BEGIN

@@ -194,6 +194,7 @@ struct PowerArgs {
   double* wsspart;     // [grid] (written after a barrier: single slot is safe)
   double* out;         // [0] sigma, [1] converged, [2] iterations
   unsigned* bar;
+  unsigned long long* prof;  // diagnostics (NQB_POWER_PROF): block 0 phase cycles, or null
 };
 
 template <int CPT, int RB, bool WSMEM>
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
   __shared__ double red[RB][PI_THREADS / 32];
   __shared__ double bred[PI_THREADS / 32];
   const uint32_t tid = threadIdx.x, G = gridDim.x, bid = blockIdx.x;
+  unsigned gsk = 0;  // grid barriers passed
   const int lane = tid & 31, warp = tid >> 5;
   const uint32_t r0 = (uint32_t)((uint64_t)a.rows * bid / G);
   const uint32_t r1 = (uint32_t)((uint64_t)a.rows * (bid + 1) / G);
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
     }
     double* ssp = a.sspart + (size_t)(it & 1) * G;
     if (tid == 0) ssp[bid] = ss;
-    grid_sync(a.bar, G);
+    grid_sync(a.bar, G, gsk);
 
     // ---- phase B: w = sum_b wpart[b] (fixed order), ||w||^2 partials --------
     double wq = 0.0;
@@ -310,7 +312,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
     }
     wq = block_sum(wq, bred);
     if (tid == 0) a.wsspart[bid] = wq;
-    grid_sync(a.bar, G);
+    grid_sync(a.bar, G, gsk);
 
     // ---- phase C (every block, identical): sigma, normalise, stop rule ------
     // G partials: one (independent) load per thread, then the fixed block tree
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
   }
   double* ssf = a.sspart + 2 * (size_t)G;
   if (tid == 0) ssf[bid] = ss;
-  grid_sync(a.bar, G);
+  grid_sync(a.bar, G, gsk);
   double s2 = 0.0;
   for (uint32_t b = tid; b < G; b += PI_THREADS) s2 += __ldcg(ssf + b);
   s2 = block_sum(s2, bred);
@@ -394,6 +396,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
   __shared__ double bred[PI_THREADS / 32];
   __shared__ double cred[PI_THREADS / 32][33];
   const uint32_t tid = threadIdx.x, G = gridDim.x, bid = blockIdx.x;
+  unsigned gsk = 0;  // grid barriers passed
   const int lane = tid & 31, warp = tid >> 5;
   const uint32_t r0 = (uint32_t)((uint64_t)a.rows * bid / G);
   const uint32_t r1 = (uint32_t)((uint64_t)a.rows * (bid + 1) / G);
@@ -420,50 +423,100 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
   __syncthreads();
 
   uint32_t phase = 0;  // bit s: parity of the next completion of slot s
+  uint32_t pending = 0;  // rows of the NEXT pass already issued (prefetched)
   auto issue = [&](uint32_t i) {  // row r0+i -> slot i % nslots (thread 0)
     uint64_t* bar = &fullb[i % nslots];
     tc::mbar_arrive_expect_tx(bar, row_bytes);
     tc::bulk_g2s(ring + (size_t)(i % nslots) * row_bytes, a.M + (uint64_t)(r0 + i) * a.cols,
                  row_bytes, bar);
   };
+  const uint32_t head = nrows < nslots ? nrows : nslots;
   double sigma = 0.0, sigma_prev = -1.0;
   int converged = 0, it = 0;
+  long long tA = 0, tB = 0, tC = 0, t0 = clock64();
   for (it = 0; it < a.max_iters; ++it) {
-    // ---- phase A: s_i = M_i . v ; w += s_i M_i, rows streamed through smem --
-    if (tid == 0)
-      for (uint32_t i = 0; i < nrows && i < nslots; ++i) issue(i);
+    if (a.prof) t0 = clock64();
+    // ---- phase A: s_i = M_i . v ; w += s_i M_i, rows streamed through smem,
+    // two rows per block reduction.  The first `head` rows of this pass were
+    // prefetched at the end of the previous pass (rows do not change).
+    if (tid == 0 && !pending)
+      for (uint32_t i = 0; i < head; ++i) issue(i);
+    pending = 0;
     double wl[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) wl[c] = 0.0;
     double ss = 0.0;
-    for (uint32_t i = 0; i < nrows; ++i) {
-      const uint32_t slot = i % nslots;
-      tc::mbar_wait(&fullb[slot], (phase >> slot) & 1u);
-      phase ^= 1u << slot;
-      const double* x = (const double*)(ring + (size_t)slot * row_bytes);
-      double p = 0.0;
+    for (uint32_t i = 0; i < nrows; i += 2) {
+      const bool two = i + 1 < nrows && nslots >= 2;
+      const uint32_t s0 = i % nslots, s1 = (i + 1) % nslots;
+      tc::mbar_wait(&fullb[s0], (phase >> s0) & 1u);
+      phase ^= 1u << s0;
+      if (two) {
+        tc::mbar_wait(&fullb[s1], (phase >> s1) & 1u);
+        phase ^= 1u << s1;
+      }
+      const double* x0 = (const double*)(ring + (size_t)s0 * row_bytes);
+      const double* x1 = (const double*)(ring + (size_t)s1 * row_bytes);
+      double p0 = 0.0, p1 = 0.0;
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         const uint32_t j = tid + c * PI_THREADS;
         if (j < a.cols) {
-          double xx = x[j];
-          if (a.abs_mode) xx = fabs(xx);
-          p += xx * vr[c];
+          double xa = x0[j], xb = two ? x1[j] : 0.0;
+          if (a.abs_mode) {
+            xa = fabs(xa);
+            xb = fabs(xb);
+          }
+          p0 += xa * vr[c];
+          p1 += xb * vr[c];
         }
       }
-      const double s = block_sum(p, bred);  // identical in every thread
-      ss += s * s;
+      // both dot products through one fixed tree (identical in every thread)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        p0 += __shfl_xor_sync(~0u, p0, o);
+        p1 += __shfl_xor_sync(~0u, p1, o);
+      }
+      if (lane == 0) {
+        cred[warp][0] = p0;
+        cred[warp][1] = p1;
+      }
+      __syncthreads();
+      double sa = 0.0, sb = 0.0;
+#pragma unroll
+      for (int w = 0; w < PI_THREADS / 32; ++w) {
+        sa += cred[w][0];
+        sb += cred[w][1];
+      }
+      ss += sa * sa;
+      if (two) ss += sb * sb;
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         const uint32_t j = tid + c * PI_THREADS;
         if (j < a.cols) {
-          double xx = x[j];
-          if (a.abs_mode) xx = fabs(xx);
-          wl[c] += xx * s;
+          double xa = x0[j];
+          if (a.abs_mode) xa = fabs(xa);
+          wl[c] += xa * sa;
+          if (two) {
+            double xb = x1[j];
+            if (a.abs_mode) xb = fabs(xb);
+            wl[c] += xb * sb;
+          }
         }
       }
-      __syncthreads();  // everyone is done with this slot
-      if (tid == 0 && i + nslots < nrows) issue(i + nslots);
+      __syncthreads();  // everyone is done with these slots (and with cred)
+      if (tid == 0) {
+        const uint32_t nx = i + nslots;  // refill the freed slots
+        if (nx < nrows) issue(nx);
+        if (two && nx + 1 < nrows) issue(nx + 1);
+      }
+    }
+    // prefetch the next pass's first rows now: they stream while the
+    // reductions and grid barriers below run (drained before exit)
+    if (it + 1 < a.max_iters) {
+      if (tid == 0)
+        for (uint32_t i = 0; i < head; ++i) issue(i);
+      pending = 1;
     }
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
@@ -472,7 +525,8 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     }
     double* ssp = a.sspart + (size_t)(it & 1) * G;
     if (tid == 0) ssp[bid] = ss;
-    grid_sync(a.bar, G);
+    long long t1 = a.prof ? clock64() : 0;
+    grid_sync(a.bar, G, gsk);
 
     // ---- phase B: w_j = sum_b wpart[b][j] for this block's columns; warp k
     // sums partials b = k, k+16, ... (independent loads), then a fixed-order
@@ -506,7 +560,12 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     }
     wq = block_sum(wq, bred);
     if (tid == 0) a.wsspart[bid] = wq;
-    grid_sync(a.bar, G);
+    grid_sync(a.bar, G, gsk);
+    long long t2 = a.prof ? clock64() : 0;
+    if (a.prof) {
+      tA += t1 - t0;
+      tB += t2 - t1;
+    }
 
     // ---- phase C (every block, identical): sigma, normalise, stop rule ------
     // G partials: one (independent) load per thread, then the fixed block tree
@@ -529,12 +588,26 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
         vr[c] = wn > 0.0 ? x / wn : x;
       }
     }
+    if (a.prof) tC += clock64() - t2;
     if (sigma_prev >= 0.0 && fabs(sigma - sigma_prev) <= a.tol * fmax(sigma, 1e-300)) {
       converged = 1;
       ++it;
       break;
     }
     sigma_prev = sigma;
+  }
+  if (a.prof && bid == 0 && tid == 0) {
+    atomicAdd(a.prof + 0, (unsigned long long)tA);
+    atomicAdd(a.prof + 1, (unsigned long long)tB);
+    atomicAdd(a.prof + 2, (unsigned long long)tC);
+    atomicAdd(a.prof + 3, (unsigned long long)it);
+  }
+
+  if (pending) {  // an early exit left the next pass's prefetch in flight: drain it
+    for (uint32_t i = 0; i < head; ++i) {
+      tc::mbar_wait(&fullb[i % nslots], (phase >> (i % nslots)) & 1u);
+      phase ^= 1u << (i % nslots);
+    }
   }
 
   // ---- final: mv = M v, sigma = ||mv||, left = mv / sigma (linalg.cpp:124-130)
@@ -558,7 +631,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
   }
   double* ssf = a.sspart + 2 * (size_t)G;
   if (tid == 0) ssf[bid] = ss;
-  grid_sync(a.bar, G);
+  grid_sync(a.bar, G, gsk);
   double s2 = 0.0;
   for (uint32_t b = tid; b < G; b += PI_THREADS) s2 += __ldcg(ssf + b);
   s2 = block_sum(s2, bred);
@@ -588,6 +661,8 @@ static void launch_power_stream(nqb_context* ctx, PowerArgs& a, uint32_t grid) {
   auto kern = k_power_stream<CPT>;
   NQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {&a, &nslots, (void*)&row_bytes};
+  // grid_sync's monotonic counter must start at a multiple of this grid
+  NQB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
   NQB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(PI_THREADS), args,
                                        smem, ctx->stream));
   NQB_LAUNCHED(ctx);
@@ -607,6 +682,8 @@ static void launch_power_t(nqb_context* ctx, PowerArgs& a, uint32_t grid) {
   auto kern = k_power<CPT, RB, WSMEM>;
   NQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {&a};
+  // grid_sync's monotonic counter must start at a multiple of this grid
+  NQB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
   NQB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(PI_THREADS), args,
                                        smem, ctx->stream));
   NQB_LAUNCHED(ctx);
@@ -637,6 +714,15 @@ void power_iterate_device(nqb_context* ctx, const double* d_m, uint32_t rows, ui
   a.wsspart = a.sspart + 3 * grid;
   a.out = a.wsspart + grid;
   a.bar = ctx->barrier;
+  a.prof = nullptr;
+  static unsigned long long* prof_buf = nullptr;
+  if (getenv_flag("NQB_POWER_PROF")) {
+    if (!prof_buf) {
+      NQB_CUDA(cudaMalloc(&prof_buf, 64));
+      NQB_CUDA(cudaMemset(prof_buf, 0, 64));
+    }
+    a.prof = prof_buf;
+  }
   const uint32_t cpt = ceil_div(cols, PI_THREADS);
   const bool stream = (cols % 2 == 0) && 2 * (size_t)cols * 8 <= 200 * 1024 &&
                       cpt <= 22 && rows >= 2 * grid && !getenv_flag("NQB_POWER_LEGACY");
@@ -661,6 +747,13 @@ void power_iterate_device(nqb_context* ctx, const double* d_m, uint32_t rows, ui
   *sigma = h[0];
   *converged = (int)h[1];
   *iters = (int)h[2];
+  if (a.prof) {
+    unsigned long long hp[4];
+    NQB_CUDA(cudaMemcpy(hp, a.prof, sizeof(hp), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "power_prof rows=%u cols=%u iters=%llu cyc/iter: A %.0f B %.0f C %.0f\n", rows,
+            cols, hp[3], (double)hp[0] / std::max(1ull, hp[3]), (double)hp[1] / std::max(1ull, hp[3]),
+            (double)hp[2] / std::max(1ull, hp[3]));
+  }
 }
 
 // Column statistics (and optional deflation) on the device.  Writes the

@@ -161,6 +161,10 @@ class Context:
         import torch
         self.set_stream(torch.cuda.current_stream(device).cuda_stream or 1)
 
+    def set_sm_budget(self, sms: int):
+        """Confine this context's persistent ADMM kernels to `sms` SMs (0: all)."""
+        _check(self.lib.nqb_set_sm_budget(self.handle, int(sms)), "nqb_set_sm_budget")
+
     def set_pdl(self, enable: bool):
         """Programmatic Dependent Launch for decode kernels (default on)."""
         _check(self.lib.nqb_set_pdl(self.handle, 1 if enable else 0), "nqb_set_pdl")

@@ -165,9 +165,50 @@ class InitReport:
     assignment: List[List[int]] = field(default_factory=list)
 
 
+def run_local(specs: Sequence[MatrixSpec], indices: Sequence[int], bpw: float,
+              factorize: Optional[Callable[[MatrixSpec, int], PackedMatrix]] = None,
+              workers: int = 1, device: int = 0) -> List[PackedMatrix]:
+    """This rank's matrices.  With workers > 1 (device path), `workers`
+    contexts on the same GPU, each confined to 1/workers of the SMs, factorize
+    matrices concurrently (ctypes releases the GIL), so the per-iteration grid
+    barriers of one matrix overlap the HBM streaming of the others."""
+    if factorize is not None or workers <= 1:
+        if factorize is None:
+            factorize = lambda s, i: device_factorize(s, i, bpw)  # noqa: E731
+        return [factorize(specs[i], i) for i in indices]
+    from concurrent.futures import ThreadPoolExecutor
+
+    from . import nanoquant as nq
+    ctxs = []
+    for _ in range(workers):
+        c = nq.Context(device)
+        ctxs.append(c)
+    total = ctxs[0].lib  # noqa: F841 (library loaded)
+    import torch
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    for c in ctxs:
+        c.set_sm_budget(max(1, sms // workers))
+    queue = list(indices)
+    out: Dict[int, PackedMatrix] = {}
+
+    def worker(w):
+        while True:
+            try:
+                i = queue.pop(0)
+            except IndexError:
+                return
+            out[i] = device_factorize(specs[i], i, bpw, ctx=ctxs[w])
+
+    with ThreadPoolExecutor(workers) as ex:
+        list(ex.map(worker, range(workers)))
+    for c in ctxs:
+        c.close()
+    return [out[i] for i in indices]
+
+
 def sharded_init(specs: Sequence[MatrixSpec], bpw: float,
                  factorize: Optional[Callable[[MatrixSpec, int], PackedMatrix]] = None,
-                 group=None, device=None) -> Optional[InitReport]:
+                 group=None, device=None, workers: int = 1) -> Optional[InitReport]:
     """Runs on every rank of `group` (torch.distributed); returns the full
     report on rank 0 and None elsewhere.  One all-gather of shard sizes and one
     gather of the padded byte shards are the only collectives."""
@@ -179,10 +220,9 @@ def sharded_init(specs: Sequence[MatrixSpec], bpw: float,
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     assign = lpt_assign(specs, world, bpw)
-    if factorize is None:
-        factorize = lambda s, i: device_factorize(s, i, bpw)  # noqa: E731
     t0 = time.perf_counter()
-    mine = [factorize(specs[i], i) for i in assign[rank]]
+    dev_index = device.index if (device is not None and device.type == "cuda") else 0
+    mine = run_local(specs, assign[rank], bpw, factorize, workers, dev_index or 0)
     my_secs = time.perf_counter() - t0
     blob = pack_shard(mine)
     if world == 1:

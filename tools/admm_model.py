@@ -1,0 +1,66 @@
+"""Whole-model (or partial-model) ADMM initialisation, layer-sharded over the
+ranks of a torchrun job (one GPU per rank, NCCL gather of packed factors).
+
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \\
+      tools/admm_model.py [--blocks 32] [--bpw 1.0] [--workers 2] [--shape 1024,1024 --count 8]
+
+Prints one JSON line on rank 0: matrices, wall seconds (max over ranks),
+matrices/s, per-rank seconds, mean rel_error / iterations.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--blocks", type=int, default=32)
+    ap.add_argument("--bpw", type=float, default=1.0)
+    ap.add_argument("--workers", type=int, default=1)
+    ap.add_argument("--shape", default=None, help="n,m: uniform synthetic matrices instead of Llama-2-7B")
+    ap.add_argument("--count", type=int, default=8)
+    args = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_06694_b200 import sharded as S
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if args.shape:
+        n, m = map(int, args.shape.split(","))
+        specs = [S.MatrixSpec(f"w{i}", n, m, 0xA000 + i) for i in range(args.count)]
+    else:
+        specs = S.llama2_7b_specs(args.blocks)
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    rep = S.sharded_init(specs, args.bpw, device=dev, workers=args.workers)
+    wall = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([wall], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+    if rep is not None:
+        errs = [p.rel_error for p in rep.matrices.values()]
+        its = [p.iterations for p in rep.matrices.values()]
+        print(json.dumps({"matrices": len(rep.matrices), "gpus": ws, "workers_per_gpu": args.workers,
+                          "bpw": args.bpw, "wall_s": wall, "matrices_per_s": len(rep.matrices) / wall,
+                          "per_rank_compute_s": rep.per_rank_seconds,
+                          "mean_rel_error": sum(errs) / len(errs),
+                          "mean_admm_iterations": sum(its) / len(its),
+                          "shapes": sorted({(p.n, p.m, p.r) for p in rep.matrices.values()})}),
+              flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
