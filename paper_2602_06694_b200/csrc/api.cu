@@ -331,8 +331,12 @@ nqb_layer* layer_from_device_words(nqb_context* ctx, uint32_t n, uint32_t m, uin
   try {
     NQB_CUDA(cudaMalloc(&L->u, (size_t)n * L->u_words * 4));
     NQB_CUDA(cudaMalloc(&L->vt, (size_t)r * L->vt_words * 4));
-    NQB_CUDA(cudaMalloc(&L->s1h, (size_t)n * 2));
-    NQB_CUDA(cudaMalloc(&L->s2h, (size_t)m * 2));
+    // scales zero-padded to whole 64-element blocks: the decode kernel stages
+    // slab-aligned slices of them with TMA bulk copies
+    NQB_CUDA(cudaMalloc(&L->s1h, (size_t)round_up(n, 64) * 2));
+    NQB_CUDA(cudaMalloc(&L->s2h, (size_t)round_up(m, 64) * 2));
+    NQB_CUDA(cudaMemsetAsync(L->s1h, 0, (size_t)round_up(n, 64) * 2, ctx->stream));
+    NQB_CUDA(cudaMemsetAsync(L->s2h, 0, (size_t)round_up(m, 64) * 2, ctx->stream));
     NQB_CUDA(cudaMemsetAsync(L->u, 0, (size_t)n * L->u_words * 4, ctx->stream));
     NQB_CUDA(cudaMemsetAsync(L->vt, 0, (size_t)r * L->vt_words * 4, ctx->stream));
     NQB_CUDA(cudaMemcpy2DAsync(L->u, L->u_words * 4, d_u, wpr * 4, wpr * 4, n,

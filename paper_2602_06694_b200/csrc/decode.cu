@@ -2,6 +2,7 @@
 // as one fused two-stage sm_100a kernel.  Design: decode.cuh, DESIGN.md §4.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "decode.cuh"
 #include "tc_common.cuh"
@@ -44,6 +45,18 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     }                                                                             \
   } while (0)
 
+__device__ __forceinline__ void red_add_u64(long long* p, long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+// Grid-barrier arrival: the release half publishes this CTA's t reds (ordered
+// before it by the CTA barrier), the acquire half orders the last arriver's
+// state updates after everyone's arrival.
+__device__ __forceinline__ uint32_t arrive_acq_rel(uint32_t* p) {
+  uint32_t v;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -77,16 +90,28 @@ __device__ __forceinline__ uint32_t q_of(uint32_t k, uint32_t K) {
   return (k - k0) >> 5;
 }
 
-// Signed base-256 digits of v (|v| <= 2^37) into byte e of the kLimbs limb words.
-__device__ __forceinline__ void put_limbs(long long v, uint32_t e, uint32_t (&w)[kLimbs]) {
-  const uint32_t s = 8 * e;
+// Signed base-256 digits (each in [-128, 127]) of the four values v[e]
+// (|v| < 2^46): byte e of limb word w[l] is digit l of v[e].  Adding
+// B = 0x808080808080 makes every digit d_l = byte_l(v + B) - 128, i.e. the
+// byte XOR 0x80, so the digits are byte transposes (PRMT) of v + B.
+static_assert(kLimbs == 6, "limb transpose assumes six limbs");
+__device__ __forceinline__ void limbs4(const long long (&v)[4], uint32_t (&w)[kLimbs]) {
+  uint32_t lo[4], hi[4];
 #pragma unroll
-  for (int l = 0; l < kLimbs - 1; ++l) {
-    const int d = (int)(int8_t)(v & 0xFF);
-    w[l] |= (uint32_t)(d & 0xFF) << s;
-    v = (v - d) >> 8;
+  for (int e = 0; e < 4; ++e) {
+    const unsigned long long u = (unsigned long long)v[e] + 0x808080808080ull;
+    lo[e] = (uint32_t)u ^ 0x80808080u;
+    hi[e] = (uint32_t)(u >> 32) ^ 0x8080u;
   }
-  w[kLimbs - 1] |= (uint32_t)(v & 0xFF) << s;
+  const uint32_t a0 = __byte_perm(lo[0], lo[1], 0x5140), a1 = __byte_perm(lo[0], lo[1], 0x7362);
+  const uint32_t b0 = __byte_perm(lo[2], lo[3], 0x5140), b1 = __byte_perm(lo[2], lo[3], 0x7362);
+  const uint32_t h0 = __byte_perm(hi[0], hi[1], 0x5140), h1 = __byte_perm(hi[2], hi[3], 0x5140);
+  w[0] = __byte_perm(a0, b0, 0x5410);
+  w[1] = __byte_perm(a0, b0, 0x7632);
+  w[2] = __byte_perm(a1, b1, 0x5410);
+  w[3] = __byte_perm(a1, b1, 0x7632);
+  w[4] = __byte_perm(h0, h1, 0x5410);
+  w[5] = __byte_perm(h0, h1, 0x7632);
 }
 
 // B-fragment words for the quad of inputs k0..k0+3 (values already << (7-q)):
@@ -345,9 +370,10 @@ __device__ __forceinline__ float scale_pow2(float a, int k) {
 // Limbs of the quad v[0..3] (tile-in-slab q) into the B-fragment buffer.
 __device__ __forceinline__ void emit_quad(uint8_t* bfrag, uint32_t klo, uint32_t k0, uint32_t q,
                                           const long long (&v)[4]) {
-  uint32_t w[kLimbs] = {};
-#pragma unroll
-  for (int e = 0; e < 4; ++e) put_limbs(v[e] * (1 << (7 - q)), e, w);
+  uint32_t w[kLimbs];
+  const long long sv[4] = {v[0] * (1 << (7 - q)), v[1] * (1 << (7 - q)), v[2] * (1 << (7 - q)),
+                           v[3] * (1 << (7 - q))};
+  limbs4(sv, w);
   store_quad(bfrag, klo, k0, w);
 }
 
@@ -355,11 +381,12 @@ struct XQuad {
   float s[4], x[4];
 };
 
-__device__ __forceinline__ XQuad load_xquad(const Params& p, const __half* s2h, uint32_t k0,
+// s2s: the CTA's staged s2 slice, indexed by k (zero beyond m)
+__device__ __forceinline__ XQuad load_xquad(const Params& p, const __half* s2s, uint32_t k0,
                                             uint32_t m) {
   XQuad r;
   if (k0 + 3 < m && p.x_vec) {
-    const uint2 sh2 = *(const uint2*)(s2h + k0);
+    const uint2 sh2 = *(const uint2*)(s2s + k0);
     const float2 s01 = __half22float2(*(const __half2*)&sh2.x);
     const float2 s23 = __half22float2(*(const __half2*)&sh2.y);
     r.s[0] = s01.x; r.s[1] = s01.y; r.s[2] = s23.x; r.s[3] = s23.y;
@@ -378,7 +405,7 @@ __device__ __forceinline__ XQuad load_xquad(const Params& p, const __half* s2h, 
       const uint32_t j = k0 + e;
       r.s[e] = r.x[e] = 0.f;
       if (j < m) {
-        r.s[e] = __half2float(s2h[j]);
+        r.s[e] = __half2float(s2s[j]);
         r.x[e] = p.x_f32 ? __ldcg((const float*)p.x + j)
                          : __half2float(__ushort_as_half(__ldcg((const unsigned short*)p.x + j)));
       }
@@ -404,10 +431,12 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   const uint32_t NB = p.nbar;
   uint64_t* full = (uint64_t*)smem;
   uint64_t* empty = full + NB;
-  long long* red8 = (long long*)(smem + 16 * NB);
-  int* red = (int*)(smem + 16 * NB + 256);
-  const uint32_t head = ((16 * NB + 256 + kMaxRt * 16 * kRedStride * 4) + 127) / 128 * 128;
-  uint8_t* bfrag = smem + head;
+  uint64_t* scb = empty + NB;  // the two scale slices landed
+  long long* red8 = (long long*)(smem + 16 * NB + 16);
+  int* red = (int*)(smem + 16 * NB + 16 + 256);
+  __half* sc2 = (__half*)(smem + 16 * NB + 16 + 256 + kRedBytes);
+  __half* sc1 = sc2 + kSc2Elems;
+  uint8_t* bfrag = smem + head_bytes(NB);
   uint8_t* buf = bfrag + p.bfrag_bytes;
 
   const int tid = threadIdx.x, lane = tid & 31;
@@ -427,6 +456,13 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   }
   const uint32_t n1 = C.s1_rtn ? C.s1_sln : 0;
   const uint32_t m = p.m;
+  // stage-1 input range [klo1, klo1 + nk1) of this CTA (slab-aligned)
+  uint32_t klo1 = 0, nk1 = 0;
+  if (n1) {
+    klo1 = slab_of(m, C.s1_sl0).k0;
+    const Slab last = slab_of(m, C.s1_sl0 + C.s1_sln - 1);
+    nk1 = last.k0 + 32 * last.nq - klo1;
+  }
   const bool ring_mode = C.ring != 0;
   const uint32_t NS = ring_mode ? p.buf_bytes / p.slot_bytes : 0;  // ring slots
   auto sec_bytes = [&](uint32_t sec) -> uint32_t {
@@ -439,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], kConsumerWarps);
     }
+    tc::mbar_init(scb, 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
@@ -447,6 +484,14 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   // ------------------------------------------------------------------ producer
   if (warp == kConsumerWarps) {
     if (lane == 0) {
+      // scale slices first: weights, so independent of the previous kernel
+      // (layer scales are zero-padded to whole slabs / row tiles, api.cu)
+      const uint32_t sb2 = 2 * nk1, sb1 = 32u * C.s2_rtn;
+      if (sb1 + sb2) {
+        tc::mbar_arrive_expect_tx(scb, sb1 + sb2);
+        if (sb2) tc::bulk_g2s(sc2, p.seg[C.s1_seg].s2h + klo1, sb2, scb);
+        if (sb1) tc::bulk_g2s(sc1, p.seg[C.s2_seg].s1h + (size_t)C.s2_rt0 * 16, sb1, scb);
+      }
       const uint8_t* src = p.bits + C.stream_off;
       uint32_t off = 0;
       for (uint32_t sec = 0; sec < C.nsec; ++sec) {
@@ -478,14 +523,21 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   }
 
   // ----------------------------------------------------------------- consumers
-  for (int i = tid; i < kMaxRt * 16 * kRedStride; i += kConsumerThreads) red[i] = 0;
+  for (int i = tid; i < kMaxRt * 16 * kRedStride / 4; i += kConsumerThreads)
+    ((int4*)red)[i] = make_int4(0, 0, 0, 0);
   TRACE(1);
   pdl_wait();  // x (and the t accumulator) may be written by the previous kernel
   TRACE(2);
   State* st = p.st;
-  const uint32_t ep = __ldcg(&st->epoch);
-  const uint32_t dirty_next = __ldcg(&st->dirty[(ep & 1) ^ 1]);
+  // epoch and both dirty counts in one load, issued here (volatile: not sunk
+  // to the first use) so nothing waits on it before the t publish
+  uint32_t ep, dirty0, dirty1;
+  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0,%1}, [%3];\n\t"
+               "ld.relaxed.gpu.global.u32 %2, [%3+8];\n"
+               : "=r"(ep), "=r"(dirty0), "=r"(dirty1)
+               : "l"(st) : "memory");
   const uint32_t b = ep & 1;
+  const uint32_t dirty_next = b ? dirty0 : dirty1;
 
   // ---- activation exponent: a = s2*x with |a| <= max|s2| * X, X = 65504 for
   // binary16 x (no pass over x), max|x| over all m for fp32 x.
@@ -516,15 +568,16 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   if (n1) {
     const Seg& S = p.seg[C.s1_seg];
     const int ea = exponent_of(S.s2max * xmax);
-    const uint32_t klo = slab_of(m, C.s1_sl0).k0;
-    const Slab last = slab_of(m, C.s1_sl0 + C.s1_sln - 1);
-    const uint32_t nquad = (last.k0 + 32 * last.nq - klo) / 4;
+    const uint32_t klo = klo1;
+    const uint32_t nquad = nk1 / 4;
+    const __half* s2s = sc2 - klo;
     long long asum = 0, aabs = 0;
     uint32_t qd = tid;
-    XQuad cur = load_xquad(p, S.s2h, klo + 4 * min(qd, nquad - 1), m);
+    mbar_wait_wd(scb, 0);
+    XQuad cur = load_xquad(p, s2s, klo + 4 * min(qd, nquad - 1), m);
     while (qd < nquad) {  // one quad in flight ahead of the one being quantised
       const uint32_t nx = qd + kConsumerThreads;
-      const XQuad nxt = load_xquad(p, S.s2h, klo + 4 * min(nx, nquad - 1), m);
+      const XQuad nxt = load_xquad(p, s2s, klo + 4 * min(nx, nquad - 1), m);
       const uint32_t k0 = klo + 4 * qd;
       long long v[4];
 #pragma unroll
@@ -541,8 +594,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
     cta_sum2_i64(asum, aabs, red8);  // also orders the bfrag stores
     const long long A = asum, Aabs = aabs;
     // one CTA per slab range publishes sum|a_int| (bounds every |t_k| of the segment)
-    if (tid == 0 && C.s1_rt0 == 0)
-      atomicAdd((unsigned long long*)&p.st->abs_a[(ep & 1)][C.s1_seg], (unsigned long long)Aabs);
+    if (tid == 0 && C.s1_rt0 == 0) red_add_u64(&p.st->abs_a[b][C.s1_seg], Aabs);
     TRACE(4);
     StageArgs sa{C.s1_rtn, n1, 0, m, C.s1_sl0, klo, 0};  // linear: barrier full[0]
     run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
@@ -551,28 +603,28 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
     consumers_sync();
     TRACE(5);
     long long* Tseg = p.T + (size_t)b * p.r_cap + S.t_off + (size_t)C.s1_rt0 * 16;
-    for (uint32_t i = tid; i < (uint32_t)C.s1_rtn * 16; i += kConsumerThreads)
-      atomicAdd((unsigned long long*)&Tseg[i],
-                (unsigned long long)(2 * row_value(red + i * kRedStride) - A));
+    if (!(p.dbg & 1))
+      for (uint32_t i = tid; i < (uint32_t)C.s1_rtn * 16; i += kConsumerThreads)
+        red_add_u64(&Tseg[i], 2 * row_value(red + i * kRedStride) - A);
   }
   {  // clear this CTA's share of the other t buffer for the next launch
     long long* Tn = p.T + (size_t)(b ^ 1) * p.r_cap;
-    const uint32_t lo = (uint32_t)((uint64_t)dirty_next * blockIdx.x / gridDim.x);
-    const uint32_t hi = (uint32_t)((uint64_t)dirty_next * (blockIdx.x + 1) / gridDim.x);
-    for (uint32_t i = lo + tid; i < hi; i += kConsumerThreads) Tn[i] = 0;
+    const uint32_t per = (dirty_next + gridDim.x - 1) / gridDim.x;  // 32-bit: no 64-bit divide
+    const uint32_t lo = min(dirty_next, per * blockIdx.x), hi = min(dirty_next, lo + per);
+    if (!(p.dbg & 2))
+      for (uint32_t i = lo + tid; i < hi; i += kConsumerThreads) Tn[i] = 0;
   }
 
   // --------------------------------------------------------------- grid barrier
   consumers_sync();  // the CTA's reds to t happen-before thread 0's fence (cumulativity)
   TRACE(6);
   if (tid == 0) {
-    __threadfence();
-    const uint32_t arrived = atomicAdd(&st->done[b], 1u);
+    const uint32_t arrived = arrive_acq_rel(&st->done[b].v);
     if (arrived == gridDim.x - 1) {  // every CTA has read epoch and dirty: advance them
       st->epoch = ep + 1;
       st->dirty[b] = p.R1;
       st->dirty[b ^ 1] = 0;
-      st->done[b ^ 1] = 0;
+      st->done[b ^ 1].v = 0;
 #pragma unroll
       for (int sg = 0; sg < kMaxSeg; ++sg) st->abs_a[b ^ 1][sg] = 0;
     }
@@ -581,14 +633,15 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   TRACE(7);
   if (tid == 0) {
     uint32_t it = 0;
-    while (ld_acquire(&st->done[b]) < gridDim.x) {
+    while (ld_acquire(&st->done[b].v) < gridDim.x) {
       __nanosleep(20);
       if (++it > (1u << 26)) __trap();
     }
   }
   consumers_sync();
   TRACE(8);
-  for (int i = tid; i < kMaxRt * 16 * kRedStride; i += kConsumerThreads) red[i] = 0;
+  for (int i = tid; i < kMaxRt * 16 * kRedStride / 4; i += kConsumerThreads)
+    ((int4*)red)[i] = make_int4(0, 0, 0, 0);
 
   // ------------------------------------------------------------------ stage 2
   const Seg& S = p.seg[C.s2_seg];
@@ -631,11 +684,12 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   consumers_sync();
   TRACE(10);
   const int E = sh + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
+  if (!n1) mbar_wait_wd(scb, 0);
   for (uint32_t i = tid; i < (uint32_t)C.s2_rtn * 16; i += kConsumerThreads) {
     const uint32_t row = C.s2_rt0 * 16 + i;
     if (row >= S.n) continue;
     const long long Y = 2 * row_value(red + i * kRedStride) - Tsum;
-    const double y = (double)__half2float(S.s1h[row]) * ldexp((double)Y, E);  // packed.cpp:189
+    const double y = (double)__half2float(sc1[i]) * ldexp((double)Y, E);  // packed.cpp:189
     if (p.y_f32) ((float*)p.y[C.s2_seg])[row] = (float)y;
     else ((__half*)p.y[C.s2_seg])[row] = __float2half_rn((float)y);
   }
@@ -686,6 +740,11 @@ void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32
   p.x_vec = ((uintptr_t)d_x % 16 == 0) ? 1u : 0u;
   p.x = d_x;
   p.trace = (unsigned long long*)ctx->dec_trace;
+  {
+    static const uint32_t dbg = [] { const char* v = std::getenv("NQB_DEC_DBG");
+                                     return v ? (uint32_t)std::strtoul(v, nullptr, 0) : 0u; }();
+    p.dbg = dbg;
+  }
   if (!ctx->dec_attr_set) {
     NQB_CUDA(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   227 * 1024));

@@ -41,6 +41,16 @@ constexpr int kMaxGrid = 160;      // CTA table lives in the kernel parameters
 constexpr int kTileB = kLimbs * 32;    // B-fragment bytes per 32-wide K tile
 constexpr int kBytesPerK = kLimbs;     // B-fragment bytes per input
 constexpr int kRedStride = 8;          // ints per row of the per-limb row sums
+constexpr int kSc2Elems = kMaxSlabs1 * 256;  // stage-1 input scales (s2) staged per CTA
+constexpr int kSc1Elems = kMaxRt * 16;       // stage-2 output scales (s1) staged per CTA
+
+// Shared-memory head: [full nbar][empty nbar][scale mbarrier, 16 B][red8 256 B]
+// [red kMaxRt*16*kRedStride ints][s2 slice][s1 slice], then B fragments and the
+// stream buffer.  The scale slices arrive by TMA ahead of griddepcontrol.wait.
+constexpr uint32_t kRedBytes = kMaxRt * 16 * kRedStride * 4;
+__host__ __device__ __forceinline__ uint32_t head_bytes(uint32_t nbar) {
+  return (16 * nbar + 16 + 256 + kRedBytes + 2 * kSc2Elems + 2 * kSc1Elems + 127) / 128 * 128;
+}
 
 // ---- K slabs: 256-wide (8 tiles of 32), then a 128 tail, then a 64 tail ----
 struct Slab {
@@ -99,13 +109,21 @@ struct Seg {
   float pad2;
 };
 
-struct State {               // per-context decode state (device memory)
+// Per-context decode state (device memory).  The arrival counters, which
+// every CTA hits with atomics and polls, live in their own 128-byte lines so
+// the epoch/dirty loads and the abs_a reads do not queue behind them at L2.
+struct alignas(128) State {
   uint32_t epoch;            // selects the t buffer (epoch & 1)
-  uint32_t done[2];          // grid-barrier arrival counters
   uint32_t dirty[2];         // rows of t[b] that may be non-zero
-  uint32_t pad[3];
+  uint32_t pad0[29];
   long long abs_a[2][kMaxSeg];  // sum_j |a_int_j| per segment (bounds |t_k|)
+  uint32_t pad1[16];
+  struct alignas(128) Counter {
+    uint32_t v;
+    uint32_t pad[31];
+  } done[2];                 // grid-barrier arrival counters
 };
+static_assert(sizeof(State) == 512, "State layout");
 
 struct Params {
   const uint8_t* bits;
@@ -123,6 +141,7 @@ struct Params {
   const void* x;
   void* y[kMaxSeg];
   unsigned long long* trace;  // diagnostics (nqb_debug_decode_trace), or null
+  uint32_t dbg;              // diagnostics: NQB_DEC_DBG bits (timing experiments only)
   Cta ctas[kMaxGrid];
 };
 

@@ -179,6 +179,7 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
                                                                          min_cta_bytes));
   G = std::max(G, count);
 
+  const double quant_bytes = env_u32("NQB_DEC_QUANT_X100", (uint32_t)(kQuantBytes * 100)) / 100.0;
   std::vector<Cta> ctas;
   for (;; ++G) {
     NQB_REQUIRE(G <= Gmax, NQB_E_DIMENSION_MISMATCH,
@@ -223,7 +224,7 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
           heavy = std::max(heavy, b);
         }
         // bytes streamed + the CTA's quantisation work (kQuantBytes per input)
-        const double cost = ((double)rt_max * heavy + kQuantBytes * 256.0 * sl_max) *
+        const double cost = ((double)rt_max * heavy + quant_bytes * 256.0 * sl_max) *
                             (1.0 + 1e-3 * Gj);
         if (cost < best) {
           best = cost;
@@ -259,7 +260,7 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
       C.s1_sln = (uint16_t)b.sln;
       uint64_t bytes = 0;
       for (uint32_t q = b.sl0; q < b.sl0 + b.sln; ++q) bytes += u1[q];
-      st1[c] = bytes * b.rtn + (uint64_t)(kQuantBytes * 256.0 * b.sln);
+      st1[c] = bytes * b.rtn + (uint64_t)(quant_bytes * 256.0 * b.sln);
     }
     // ---- stage-2 row tiles: every CTA's total cost close to the mean --------
     // CTA ranges per segment proportional to stage-2 bytes, then largest-
@@ -391,8 +392,7 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   g->slot_bytes = slot;
   g->nbar = nbar;
   g->bfrag_bytes = (bfrag + 127) / 128 * 128;
-  // [mbarriers 2*nbar*8][misc 256][red kMaxRt*16*8][bfrag][stream buffer]
-  const uint32_t head = ((16 * nbar + 256 + kMaxRt * 16 * kRedStride * 4) + 127) / 128 * 128;
+  const uint32_t head = head_bytes(nbar);  // decode.cuh
   g->smem_bytes = head + g->bfrag_bytes + buf;
   NQB_REQUIRE(g->smem_bytes <= 227 * 1024, NQB_E_DIMENSION_MISMATCH,
               "decode plan exceeds shared memory (" + std::to_string(g->smem_bytes) + " B)");
