@@ -33,9 +33,11 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 // Diagnostics: slot 0 = %globaltimer at CTA start, slots 1.. = SM clock64
 // cycles since the CTA started (exact, per CTA; the base stays in a register).
+// Compiled only into the kTrace instance of the kernel: the production kernel
+// carries no trace code (each check would re-read the parameter bank).
 #define TRACE(i)                                                                  \
   do {                                                                            \
-    if (p.trace && threadIdx.x == 0) {                                            \
+    if (kTrace && threadIdx.x == 0) {                                             \
       if ((i) == 0) {                                                             \
         trace_t0 = clock64();                                                     \
         p.trace[blockIdx.x * 32] = globaltimer();                                 \
@@ -48,13 +50,10 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 __device__ __forceinline__ void red_add_u64(long long* p, long long v) {
   asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
 }
-// Grid-barrier arrival: the release half publishes this CTA's t reds (ordered
-// before it by the CTA barrier), the acquire half orders the last arriver's
-// state updates after everyone's arrival.
-__device__ __forceinline__ uint32_t arrive_acq_rel(uint32_t* p) {
-  uint32_t v;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
+// Grid-barrier arrival: the release publishes this CTA's t reds (ordered
+// before it by the CTA barrier, cumulativity).
+__device__ __forceinline__ void red_release_add_u32(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
@@ -284,7 +283,7 @@ __device__ __forceinline__ void tiles_mma(const uint8_t* unit0, uint32_t ub, uin
 // work items (pair of row tiles, run of sections) go round-robin to the
 // consumer warps, each B-fragment load serving both tiles.  Ring mode: the
 // stream is longer than the buffer; every warp walks every section in order
-// and releases it (slot reuse), handling tiles t = w mod warps.
+// and releases it (slot reuse), handling tiles t = w mod warp.
 __device__ __forceinline__ void run_stage(const StageArgs& A, uint32_t NS, bool ring_mode,
                                           uint32_t slot_bytes, uint64_t* full, uint64_t* empty,
                                           const uint8_t* buf, const uint8_t* bfrag,
@@ -426,10 +425,11 @@ __device__ __forceinline__ void load_tquad(const long long* Tseg, uint32_t k0, u
   }
 }
 
+template <bool kTrace>
 __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_decode(const __grid_constant__ Params p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t NB = p.nbar;
-  uint64_t* full = (uint64_t*)smem;
+  uint64_t* full = (uint64_t*)(smem);
   uint64_t* empty = full + NB;
   uint64_t* scb = empty + NB;  // the two scale slices landed
   long long* red8 = (long long*)(smem + 16 * NB + 16);
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   long long trace_t0 = 0;
   TRACE(0);
   const Cta C = p.ctas[blockIdx.x];
-  if (p.trace && tid == 0) {
+  if (kTrace && tid == 0) {
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     p.trace[blockIdx.x * 32 + 16] = smid;
@@ -512,8 +512,8 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
         }
         off += bytes;
       }
-      if (p.trace) p.trace[blockIdx.x * 32 + 14] = clock64() - trace_t0;
-      if (p.trace && !ring_mode && C.nsec) {  // diagnostics: the whole stream landed
+      if (kTrace) p.trace[blockIdx.x * 32 + 14] = clock64() - trace_t0;
+      if (kTrace && !ring_mode && C.nsec) {  // diagnostics: the whole stream landed
         if (n1) mbar_wait_wd(&full[0], 0);
         if (C.nsec > n1) mbar_wait_wd(&full[1], 0);
         p.trace[blockIdx.x * 32 + 15] = clock64() - trace_t0;
@@ -598,29 +598,37 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
     TRACE(4);
     StageArgs sa{C.s1_rtn, n1, 0, m, C.s1_sl0, klo, 0};  // linear: barrier full[0]
     run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
-              (p.trace && warp == 0) ? p.trace + blockIdx.x * 32 + 22 : nullptr);
+              (kTrace && warp == 0) ? p.trace + blockIdx.x * 32 + 22 : nullptr);
     TRACE(12);
     consumers_sync();
     TRACE(5);
-    long long* Tseg = p.T + (size_t)b * p.r_cap + S.t_off + (size_t)C.s1_rt0 * 16;
-    if (!(p.dbg & 1))
-      for (uint32_t i = tid; i < (uint32_t)C.s1_rtn * 16; i += kConsumerThreads)
-        red_add_u64(&Tseg[i], 2 * row_value(red + i * kRedStride) - A);
+    long long* Tseg = p.T + (size_t)b * p.r_cap + p.seg[C.s1_seg].t_off + (size_t)C.s1_rt0 * 16;
+    for (uint32_t i = tid; i < (uint32_t)C.s1_rtn * 16; i += kConsumerThreads)
+      red_add_u64(&Tseg[i], 2 * row_value(red + i * kRedStride) - A);
   }
   {  // clear this CTA's share of the other t buffer for the next launch
     long long* Tn = p.T + (size_t)(b ^ 1) * p.r_cap;
     const uint32_t per = (dirty_next + gridDim.x - 1) / gridDim.x;  // 32-bit: no 64-bit divide
     const uint32_t lo = min(dirty_next, per * blockIdx.x), hi = min(dirty_next, lo + per);
-    if (!(p.dbg & 2))
-      for (uint32_t i = lo + tid; i < hi; i += kConsumerThreads) Tn[i] = 0;
+    for (uint32_t i = lo + tid; i < hi; i += kConsumerThreads) Tn[i] = 0;
   }
 
   // --------------------------------------------------------------- grid barrier
   consumers_sync();  // the CTA's reds to t happen-before thread 0's fence (cumulativity)
   TRACE(6);
+  // Arrival is a fire-and-forget release reduction (no round trip on the
+  // critical path); CTA 0 advances the state once everyone has arrived (every
+  // CTA read epoch and dirty before arriving).
+  if (tid == 0) red_release_add_u32(&st->done[b].v, 1u);
+  if (!C.s2_rtn && blockIdx.x != 0) return;
+  TRACE(7);
   if (tid == 0) {
-    const uint32_t arrived = arrive_acq_rel(&st->done[b].v);
-    if (arrived == gridDim.x - 1) {  // every CTA has read epoch and dirty: advance them
+    uint32_t it = 0;
+    while (ld_acquire(&st->done[b].v) < gridDim.x) {
+      __nanosleep(20);
+      if (++it > (1u << 26)) __trap();
+    }
+    if (blockIdx.x == 0) {
       st->epoch = ep + 1;
       st->dirty[b] = p.R1;
       st->dirty[b ^ 1] = 0;
@@ -630,14 +638,6 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
     }
   }
   if (!C.s2_rtn) return;
-  TRACE(7);
-  if (tid == 0) {
-    uint32_t it = 0;
-    while (ld_acquire(&st->done[b].v) < gridDim.x) {
-      __nanosleep(20);
-      if (++it > (1u << 26)) __trap();
-    }
-  }
   consumers_sync();
   TRACE(8);
   for (int i = tid; i < kMaxRt * 16 * kRedStride / 4; i += kConsumerThreads)
@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   StageArgs sa{C.s2_rtn, C.nsec - n1, n1, S.r, 0, 0, s1_bytes};
   if (!ring_mode) sa.sec_base = 1;  // linear: barrier full[1]
   run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
-            (p.trace && warp == 0) ? p.trace + blockIdx.x * 32 + 27 : nullptr);
+            (kTrace && warp == 0) ? p.trace + blockIdx.x * 32 + 27 : nullptr);
   TRACE(13);
   consumers_sync();
   TRACE(10);
@@ -740,13 +740,11 @@ void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32
   p.x_vec = ((uintptr_t)d_x % 16 == 0) ? 1u : 0u;
   p.x = d_x;
   p.trace = (unsigned long long*)ctx->dec_trace;
-  {
-    static const uint32_t dbg = [] { const char* v = std::getenv("NQB_DEC_DBG");
-                                     return v ? (uint32_t)std::strtoul(v, nullptr, 0) : 0u; }();
-    p.dbg = dbg;
-  }
+
   if (!ctx->dec_attr_set) {
-    NQB_CUDA(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    NQB_CUDA(cudaFuncSetAttribute(k_decode<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    NQB_CUDA(cudaFuncSetAttribute(k_decode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   227 * 1024));
     ctx->dec_attr_set = true;
   }
@@ -760,7 +758,8 @@ void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32
   attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  NQB_CUDA(cudaLaunchKernelEx(&cfg, k_decode, p));
+  if (p.trace) NQB_CUDA(cudaLaunchKernelEx(&cfg, k_decode<true>, p));
+  else NQB_CUDA(cudaLaunchKernelEx(&cfg, k_decode<false>, p));
   NQB_LAUNCHED(ctx);
 }
 

@@ -21,6 +21,8 @@
 // partial sums are int64 red.add'ed into a global t accumulator; a grid
 // barrier (all CTAs co-resident: grid <= #SMs) separates the stages.
 #pragma once
+#include <cstddef>
+
 #include "common.cuh"
 
 namespace nqb {
@@ -49,7 +51,8 @@ constexpr int kSc1Elems = kMaxRt * 16;       // stage-2 output scales (s1) stage
 // stream buffer.  The scale slices arrive by TMA ahead of griddepcontrol.wait.
 constexpr uint32_t kRedBytes = kMaxRt * 16 * kRedStride * 4;
 __host__ __device__ __forceinline__ uint32_t head_bytes(uint32_t nbar) {
-  return (16 * nbar + 16 + 256 + kRedBytes + 2 * kSc2Elems + 2 * kSc1Elems + 127) / 128 * 128;
+  return (16 * nbar + 16 + 256 + kRedBytes + 2 * kSc2Elems + 2 * kSc1Elems + 127) / 128 *
+         128;
 }
 
 // ---- K slabs: 256-wide (8 tiles of 32), then a 128 tail, then a 64 tail ----
@@ -141,9 +144,9 @@ struct Params {
   const void* x;
   void* y[kMaxSeg];
   unsigned long long* trace;  // diagnostics (nqb_debug_decode_trace), or null
-  uint32_t dbg;              // diagnostics: NQB_DEC_DBG bits (timing experiments only)
   Cta ctas[kMaxGrid];
 };
+
 
 }  // namespace dec
 }  // namespace nqb

@@ -1,6 +1,10 @@
+# A/B two builds of the library on the bench: libnqb_a.so vs libnqb_b.so (copied over libnqb.so in turn)
 mkdir -p gpurun_out
-for d in 0 1 2 3; do
-  echo "=== NQB_DEC_DBG=$d" >> gpurun_out/trace_dbg.log
-  NQB_DEC_DBG=$d timeout 300 python tools/trace_decode.py l7_q >> gpurun_out/trace_dbg.log 2>&1
+cp paper_2602_06694_b200/libnqb.so /tmp/libnqb_keep.so
+for v in a b a b; do
+  cp paper_2602_06694_b200/libnqb_$v.so paper_2602_06694_b200/libnqb.so
+  timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$v.log 2>&1
+  python tools/show_bench.py gpurun_out/bench_$v.log 2>/dev/null | head -7 >> gpurun_out/ab.txt
 done
+cp /tmp/libnqb_keep.so paper_2602_06694_b200/libnqb.so
 echo done >> gpurun_out/status.txt
