@@ -137,6 +137,28 @@ __device__ __forceinline__ long long cta_sum_i64(long long v, long long* red8) {
   return s;
 }
 
+// Warp sums of (a, b) into red8[warp] and red8[kConsumerWarps + warp]; the
+// next consumers_sync publishes them and sum_partials() finishes the CTA sum
+// later, off the critical path.
+__device__ __forceinline__ void warp_partials2(long long a, long long b, long long* red8) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(~0u, a, o);
+    b += __shfl_xor_sync(~0u, b, o);
+  }
+  if (lane == 0) {
+    red8[warp] = a;
+    red8[kConsumerWarps + warp] = b;
+  }
+}
+__device__ __forceinline__ long long sum_partials(const long long* red8) {
+  long long s = 0;
+#pragma unroll
+  for (int w = 0; w < kConsumerWarps; ++w) s += red8[w];
+  return s;
+}
+
 __device__ __forceinline__ void cta_sum2_i64(long long& a, long long& b, long long* red8) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -433,8 +455,9 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   uint64_t* empty = full + NB;
   uint64_t* scb = empty + NB;  // the two scale slices landed
   long long* red8 = (long long*)(smem + 16 * NB + 16);
-  int* red = (int*)(smem + 16 * NB + 16 + 256);
-  __half* sc2 = (__half*)(smem + 16 * NB + 16 + 256 + kRedBytes);
+  float* xred = (float*)(smem + 16 * NB + 16 + 256);  // per-warp max|x| (fp32 x)
+  int* red = (int*)(smem + 16 * NB + 16 + 256 + 64);
+  __half* sc2 = (__half*)(smem + 16 * NB + 16 + 256 + 64 + kRedBytes);
   __half* sc1 = sc2 + kSc2Elems;
   uint8_t* bfrag = smem + head_bytes(NB);
   uint8_t* buf = bfrag + p.bfrag_bytes;
@@ -554,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
     for (uint32_t i = 4 * nv + tid; i < m; i += kConsumerThreads) mx = fmaxf(mx, fabsf(__ldcg(xf + i)));
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(~0u, mx, o));
-    float* rf = (float*)red8;
+    float* rf = xred;
     if (lane == 0) rf[warp] = mx;
     consumers_sync();
     mx = 0.f;
@@ -591,10 +614,8 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
       cur = nxt;
       qd = nx;
     }
-    cta_sum2_i64(asum, aabs, red8);  // also orders the bfrag stores
-    const long long A = asum, Aabs = aabs;
-    // one CTA per slab range publishes sum|a_int| (bounds every |t_k| of the segment)
-    if (tid == 0 && C.s1_rt0 == 0) red_add_u64(&p.st->abs_a[b][C.s1_seg], Aabs);
+    warp_partials2(asum, aabs, red8);
+    consumers_sync();  // B fragments and the partial sums are visible
     TRACE(4);
     StageArgs sa{C.s1_rtn, n1, 0, m, C.s1_sl0, klo, 0};  // linear: barrier full[0]
     run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
@@ -602,9 +623,18 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
     TRACE(12);
     consumers_sync();
     TRACE(5);
+    const long long A = sum_partials(red8);
+    // one CTA per slab range publishes sum|a_int| (bounds every |t_k| of the segment)
+    if (tid == 0 && C.s1_rt0 == 0)
+      red_add_u64(&p.st->abs_a[b][C.s1_seg], sum_partials(red8 + kConsumerWarps));
     long long* Tseg = p.T + (size_t)b * p.r_cap + p.seg[C.s1_seg].t_off + (size_t)C.s1_rt0 * 16;
-    for (uint32_t i = tid; i < (uint32_t)C.s1_rtn * 16; i += kConsumerThreads)
-      red_add_u64(&Tseg[i], 2 * row_value(red + i * kRedStride) - A);
+    for (uint32_t i = tid; i < (uint32_t)C.s1_rtn * 16; i += kConsumerThreads) {
+      const long long v = 2 * row_value(red + i * kRedStride) - A;
+      int4* rr = (int4*)(red + i * kRedStride);  // leave the row zeroed for stage 2
+      rr[0] = make_int4(0, 0, 0, 0);
+      rr[1] = make_int4(0, 0, 0, 0);
+      red_add_u64(&Tseg[i], v);
+    }
   }
   {  // clear this CTA's share of the other t buffer for the next launch
     long long* Tn = p.T + (size_t)(b ^ 1) * p.r_cap;
@@ -640,8 +670,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   if (!C.s2_rtn) return;
   consumers_sync();
   TRACE(8);
-  for (int i = tid; i < kMaxRt * 16 * kRedStride / 4; i += kConsumerThreads)
-    ((int4*)red)[i] = make_int4(0, 0, 0, 0);
+  // (red is all zero here: stage 1 cleared the rows it used while publishing)
 
   // ------------------------------------------------------------------ stage 2
   const Seg& S = p.seg[C.s2_seg];
@@ -672,7 +701,8 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
       qd = nx;
     }
   }
-  const long long Tsum = cta_sum_i64(tsum, red8);
+  warp_partials2(tsum, 0, red8);
+  consumers_sync();  // B fragments and the partial sums are visible
   TRACE(9);
   uint32_t s1_bytes = 0;  // linear offset of the first stage-2 section
   for (uint32_t s = 0; s < n1; ++s) s1_bytes += sec_bytes(s);
@@ -683,6 +713,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   TRACE(13);
   consumers_sync();
   TRACE(10);
+  const long long Tsum = sum_partials(red8);
   const int E = sh + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
   if (!n1) mbar_wait_wd(scb, 0);
   for (uint32_t i = tid; i < (uint32_t)C.s2_rtn * 16; i += kConsumerThreads) {

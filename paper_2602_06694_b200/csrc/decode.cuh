@@ -46,12 +46,12 @@ constexpr int kRedStride = 8;          // ints per row of the per-limb row sums
 constexpr int kSc2Elems = kMaxSlabs1 * 256;  // stage-1 input scales (s2) staged per CTA
 constexpr int kSc1Elems = kMaxRt * 16;       // stage-2 output scales (s1) staged per CTA
 
-// Shared-memory head: [full nbar][empty nbar][scale mbarrier, 16 B][red8 256 B]
+// Shared-memory head: [full nbar][empty nbar][scale mbarrier, 16 B][red8 256 B][xmax 64 B]
 // [red kMaxRt*16*kRedStride ints][s2 slice][s1 slice], then B fragments and the
 // stream buffer.  The scale slices arrive by TMA ahead of griddepcontrol.wait.
 constexpr uint32_t kRedBytes = kMaxRt * 16 * kRedStride * 4;
 __host__ __device__ __forceinline__ uint32_t head_bytes(uint32_t nbar) {
-  return (16 * nbar + 16 + 256 + kRedBytes + 2 * kSc2Elems + 2 * kSc1Elems + 127) / 128 *
+  return (16 * nbar + 16 + 256 + 64 + kRedBytes + 2 * kSc2Elems + 2 * kSc1Elems + 127) / 128 *
          128;
 }
 
