@@ -382,7 +382,7 @@ def main():
 
     def e2e_step():
         for l, x, y in zip(all_layers, hx, hy):
-            y[:] = l.gemv_f32(x)
+            l.gemv_f32(x, out=y)
     e2e_step()
     e2e_steps = max(1, min(args.steps, 5))
     t0 = time.perf_counter()

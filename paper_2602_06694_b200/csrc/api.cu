@@ -421,6 +421,7 @@ int nqb_layer_free(nqb_layer* L) {
   if (!L) return NQB_OK;
   cudaSetDevice(L->device);
   group_free(L->dec);
+  cudaFree(L->hp_buf);
   cudaFree(L->u);
   cudaFree(L->vt);
   cudaFree(L->s1h);
@@ -498,9 +499,13 @@ int nqb_gemv_f32_host(nqb_context* ctx, const nqb_layer* L, const float* x, floa
   API_BEGIN
   check_ctx(ctx);
   check_layer(L);
-  DevBuf buf(ctx, 4 * ((size_t)L->m + L->n));
-  float* dx = buf.as<float>();
-  float* dy = dx + L->m;
+  NQB_REQUIRE(x != nullptr && y != nullptr, NQB_E_VALIDATION, "null buffer");
+  // per-layer device staging for x and y (no allocation on the per-token path)
+  nqb_layer* ML = const_cast<nqb_layer*>(L);
+  if (!ML->hp_buf)
+    NQB_CUDA(cudaMalloc(&ML->hp_buf, 4 * ((size_t)round_up(L->m, 4) + L->n)));
+  float* dx = ML->hp_buf;
+  float* dy = dx + round_up(L->m, 4);
   NQB_CUDA(cudaMemcpyAsync(dx, x, 4 * (size_t)L->m, cudaMemcpyHostToDevice, ctx->stream));
   decode_gemv_f32(ctx, L, dx, dy);
   NQB_CUDA(cudaMemcpyAsync(y, dy, 4 * (size_t)L->n, cudaMemcpyDeviceToHost, ctx->stream));

@@ -97,6 +97,7 @@ struct nqb_layer {
   __half* s2h = nullptr;
   int device = 0;
   nqb_group* dec = nullptr;  // decode plan of this layer alone (decode.cuh)
+  float* hp_buf = nullptr;  // host drop-in path (nqb_gemv_f32_host): device x, y staging
 };
 
 namespace nqb {

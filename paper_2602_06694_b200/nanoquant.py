@@ -382,11 +382,18 @@ class DeviceLayer:
         return FactorizedLayer(self.n, self.m, self.r, u, v, s1, s2)
 
     # -- forward on host buffers (drop-in) --------------------------------
-    def gemv_f32(self, x) -> np.ndarray:
+    def gemv_f32(self, x, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """gemv_packed_f32 (packed.cpp:201-204).  `out` (contiguous float32, n) is
+        written in place when given, e.g. a pinned buffer."""
         x = np.ascontiguousarray(x, dtype=np.float32)
         if x.size != self.m:
             raise DimensionMismatch("gemv_packed: |x| != m")
-        y = np.empty(self.n, np.float32)
+        if out is None:
+            y = np.empty(self.n, np.float32)
+        else:
+            if out.dtype != np.float32 or out.size != self.n or not out.flags.c_contiguous:
+                raise DimensionMismatch("gemv_packed: out must be contiguous float32 of size n")
+            y = out
         _check(self.ctx.lib.nqb_gemv_f32_host(self.ctx.handle, self.handle, _ptr(x), _ptr(y)),
                "gemv_packed_f32")
         return y
