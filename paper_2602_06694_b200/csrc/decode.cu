@@ -300,12 +300,57 @@ __device__ __forceinline__ void tiles_mma(const uint8_t* unit0, uint32_t ub, uin
   }
 }
 
+// A run of cnt full (256-wide) slabs for NT row tiles starting at unit u (the
+// next slab's unit is ustep bytes on) against B fragments at bp (next slab
+// kBytesPerK*256 on).  Software-pipelined: the next slab's A words and B
+// fragments are loaded before this slab's 8*NT MMAs issue.
+template <int NT>
+__device__ __forceinline__ void full_run(const uint8_t* u, uint32_t ustep, const uint8_t* bp,
+                                         uint32_t cnt, int lane, bool limb_lane,
+                                         int (&acc)[2][4][4]) {
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  uint4 w[NT], bq[4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) w[j] = *(const uint4*)(u + j * 512 + lane * 16);
+#pragma unroll
+  for (int h = 0; h < 4; ++h) bq[h] = limb_lane ? *(const uint4*)(bp + 2 * h * kTileB) : z;
+  for (uint32_t i = 0; i < cnt; ++i) {
+    const bool more = i + 1 < cnt;
+    const uint8_t* un = more ? u + ustep : u;
+    const uint8_t* bn = more ? bp + kBytesPerK * 256 : bp;
+    uint4 nw[NT], nb[4];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) nw[j] = *(const uint4*)(un + j * 512 + lane * 16);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) nb[h] = limb_lane ? *(const uint4*)(bn + 2 * h * kTileB) : z;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t mask = 0x01010101u << q;
+      const uint32_t b0 = (q & 1) ? bq[q >> 1].z : bq[q >> 1].x;
+      const uint32_t b1 = (q & 1) ? bq[q >> 1].w : bq[q >> 1].y;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+        mma_u8s8(acc[j][q & 3], w[j].x & mask, w[j].y & mask, w[j].z & mask, w[j].w & mask, b0, b1);
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) w[j] = nw[j];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) bq[h] = nb[h];
+    u = un;
+    bp = bn;
+  }
+}
+
 // All sections of one stage; leaves sum_K bit*value per row in red[] (exact).
 // Linear mode: the stage's sections are resident (one mbarrier per stage);
 // work items (pair of row tiles, run of sections) go round-robin to the
 // consumer warps, each B-fragment load serving both tiles.  Ring mode: the
 // stream is longer than the buffer; every warp walks every section in order
 // and releases it (slot reuse), handling tiles t = w mod warp.
+// kBig (plans with long per-CTA streams): a warp's consecutive full slabs of
+// one tile pair run software-pipelined (full_run); the small-layer instance
+// keeps the plain loop (smaller code, lower latency for 1-2 steps per warp).
+template <bool kBig>
 __device__ __forceinline__ void run_stage(const StageArgs& A, uint32_t NS, bool ring_mode,
                                           uint32_t slot_bytes, uint64_t* full, uint64_t* empty,
                                           const uint8_t* buf, const uint8_t* bfrag,
@@ -333,6 +378,42 @@ __device__ __forceinline__ void run_stage(const StageArgs& A, uint32_t NS, bool 
     }
     uint32_t cur = f0 < f1 ? f0 / A.nsec : 0;
     long long c1 = prof ? clock64() : 0, tf = 0;
+    if constexpr (kBig) {
+      uint32_t F, rem;
+      slab_split(A.K, F, rem);
+      const uint32_t nfull = F > A.slab_base ? F - A.slab_base : 0;  // full slabs come first
+      for (uint32_t f = f0; f < f1;) {
+        // one run: the warp's consecutive sections of tile pair pr
+        const uint32_t pr = f / A.nsec;
+        uint32_t s = f - pr * A.nsec;
+        const uint32_t send = min(A.nsec, s + (f1 - f));
+        f = pr * A.nsec + send;
+        if (pr != cur) {
+          flush_rows(acc[0], red + 2 * cur * 16 * kRedStride, lane);
+          if (2 * cur + 1 < A.rtn) flush_rows(acc[1], red + (2 * cur + 1) * 16 * kRedStride, lane);
+          cur = pr;
+        }
+        const uint32_t t0 = 2 * pr;
+        const bool two = t0 + 1 < A.rtn;
+        const uint32_t sf = min(send, nfull);
+        if (s < sf) {
+          const uint32_t k0 = 256 * (A.slab_base + s);
+          const uint8_t* unit = buf + A.lin_off + 2u * A.rtn * (k0 - A.klo) + t0 * 512;
+          const uint8_t* bp = bfrag + kBytesPerK * (k0 - A.klo) + (g * 4 + c) * 16;
+          if (two) full_run<2>(unit, 512u * A.rtn, bp, sf - s, lane, g < (uint32_t)kLimbs, acc);
+          else full_run<1>(unit, 512u * A.rtn, bp, sf - s, lane, g < (uint32_t)kLimbs, acc);
+          s = sf;
+        }
+        for (; s < send; ++s) {  // the 128 / 64 tails
+          const Slab sl = slab_of(A.K, A.slab_base + s);
+          const uint32_t ub = unit_bytes(sl.nq);
+          const uint8_t* unit = buf + A.lin_off + 2u * A.rtn * (sl.k0 - A.klo) + t0 * ub;
+          load_b(bfrag, A.klo, sl, g, c, b);
+          if (two) tiles_mma<2>(unit, ub, sl.nq, lane, b, acc);
+          else tiles_mma<1>(unit, ub, sl.nq, lane, b, acc);
+        }
+      }
+    } else
     for (uint32_t f = f0; f < f1; ++f) {
       const uint32_t pr = f / A.nsec, s = f % A.nsec;
       if (pr != cur) {
@@ -447,7 +528,7 @@ __device__ __forceinline__ void load_tquad(const long long* Tseg, uint32_t k0, u
   }
 }
 
-template <bool kTrace>
+template <bool kTrace, bool kBig>
 __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_decode(const __grid_constant__ Params p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t NB = p.nbar;
@@ -620,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
     consumers_sync();  // B fragments and the partial sums are visible
     TRACE(4);
     StageArgs sa{C.s1_rtn, n1, 0, m, C.s1_sl0, klo, 0};  // linear: barrier full[0]
-    run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
+    run_stage<kBig>(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
               (kTrace && warp == 0) ? p.trace + blockIdx.x * 32 + 22 : nullptr);
     TRACE(12);
     consumers_sync();
@@ -720,7 +801,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   for (uint32_t s = 0; s < n1; ++s) s1_bytes += sec_bytes(s);
   StageArgs sa{C.s2_rtn, C.nsec - n1, n1, S.r, 0, 0, s1_bytes};
   if (!ring_mode) sa.sec_base = 1;  // linear: barrier full[1]
-  run_stage(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
+  run_stage<kBig>(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
             (kTrace && warp == 0) ? p.trace + blockIdx.x * 32 + 27 : nullptr);
   TRACE(13);
   consumers_sync();
@@ -787,10 +868,9 @@ void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32
   p.trace = (unsigned long long*)ctx->dec_trace;
 
   if (!ctx->dec_attr_set) {
-    NQB_CUDA(cudaFuncSetAttribute(k_decode<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024));
-    NQB_CUDA(cudaFuncSetAttribute(k_decode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024));
+    for (auto fn : {k_decode<false, false>, k_decode<false, true>, k_decode<true, false>,
+                    k_decode<true, true>})
+      NQB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     ctx->dec_attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -803,8 +883,9 @@ void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32
   attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (p.trace) NQB_CUDA(cudaLaunchKernelEx(&cfg, k_decode<true>, p));
-  else NQB_CUDA(cudaLaunchKernelEx(&cfg, k_decode<false>, p));
+  const bool big = g->big;
+  if (p.trace) NQB_CUDA(cudaLaunchKernelEx(&cfg, big ? k_decode<true, true> : k_decode<true, false>, p));
+  else NQB_CUDA(cudaLaunchKernelEx(&cfg, big ? k_decode<false, true> : k_decode<false, false>, p));
   NQB_LAUNCHED(ctx);
 }
 

@@ -158,6 +158,7 @@ struct nqb_group {
   uint32_t nseg = 0, m = 0, R1 = 0, grid = 0;
   uint32_t buf_bytes = 0, slot_bytes = 0, nbar = 0, bfrag_bytes = 0, smem_bytes = 0;
   uint64_t stream_bytes = 0;
+  bool big = false;                    // long per-CTA streams: pipelined MMA instance
   uint8_t* bits = nullptr;             // device, stream_bytes
   nqb::dec::Cta* ctas = nullptr;       // host copy of the CTA table (grid entries)
   nqb::dec::Seg seg[nqb::dec::kMaxSeg];
