@@ -611,6 +611,9 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
           tc::bulk_g2s(buf + (size_t)slot * p.slot_bytes, src + off, bytes, &full[slot]);
         } else {  // linear: the section lives at its stream offset; one barrier per stage
           uint64_t* bar = &full[sec < n1 ? 0 : 1];
+          // stage-1 bits first: HBM serves them before the (larger, later
+          // needed) stage-2 stream, so stage 1 is not starved by stage 2
+          if (p.seq && sec == n1 && n1) mbar_wait_wd(&full[0], 0);
           if (sec == 0 || sec == n1) {
             uint32_t total = 0;
             for (uint32_t q = sec; q < (sec < n1 ? n1 : C.nsec); ++q) total += sec_bytes(q);
@@ -864,6 +867,11 @@ void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32
   p.x_f32 = x_f32 ? 1u : 0u;
   p.y_f32 = y_f32 ? 1u : 0u;
   p.x_vec = ((uintptr_t)d_x % 16 == 0) ? 1u : 0u;
+  {
+    static const uint32_t seq = [] { const char* v = std::getenv("NQB_DEC_SEQ");
+                                     return v ? (uint32_t)std::strtoul(v, nullptr, 10) : 1u; }();
+    p.seq = seq;
+  }
   p.x = d_x;
   p.trace = (unsigned long long*)ctx->dec_trace;
 

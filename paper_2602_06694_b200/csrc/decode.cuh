@@ -141,6 +141,7 @@ struct Params {
   uint32_t nbar;             // mbarrier pairs (max sections of a linear CTA, or slots)
   uint32_t bfrag_bytes;
   uint32_t x_f32, y_f32, x_vec;
+  uint32_t seq;              // linear mode: issue stage-2 copies once stage 1 has landed
   const void* x;
   void* y[kMaxSeg];
   unsigned long long* trace;  // diagnostics (nqb_debug_decode_trace), or null
