@@ -290,6 +290,32 @@ def prefill_roofline(nq, ctx, torch, stream, n, m, r, b=2048, reps=10):
     return sec, 2.0 * b * r * (n + m) / sec / 1e12
 
 
+def admm_leg(nq, torch, ws, rank, local):
+    """Whole-model-init throughput sample: `ws` Llama-2-7B q matrices (4096x4096, synthetic
+    N(0, 0.02^2) weights, 1.0 bpw -> r = 2032), one per rank by the LPT plan, each factorised
+    by nqb_factorize_layer (fp64 SVD init + ADMM, reference defaults), packed factors
+    gathered to rank 0 (NCCL).  Returns rank 0's summary (None elsewhere)."""
+    from paper_2602_06694_b200 import sharded as S
+    specs = [S.MatrixSpec(f"b{i}.q", 4096, 4096, 0x7B000000 + 7 * i) for i in range(ws)]
+    if ws > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    rep = S.sharded_init(specs, 1.0, device=torch.device("cuda", local))
+    wall = time.perf_counter() - t0
+    if rank != 0:
+        return None
+    secs = max(rep.per_rank_seconds)
+    errs = [rep.matrices[i].rel_error for i in sorted(rep.matrices)]
+    its = [rep.matrices[i].iterations for i in sorted(rep.matrices)]
+    return {"matrices": len(specs), "shape": "4096x4096", "bpw": 1.0,
+            "rank": rep.matrices[0].r, "seconds_max_rank": secs, "seconds_wall_incl_gather": wall,
+            "matrices_per_s": len(specs) / wall, "scaling": "weak (one matrix per rank)",
+            "rel_error": errs, "admm_iterations": its,
+            "converged": [rep.matrices[i].converged for i in sorted(rep.matrices)],
+            "note": "fp64 on device (SVD-init power iterations + ADMM); CPU reference ~36 h "
+                    "per 4096^2 matrix (SURVEY.md section 6)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -299,6 +325,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-shapes", action="store_true", help="skip the per-shape roofline sweep")
+    ap.add_argument("--no-admm", action="store_true",
+                    help="skip the ADMM-init leg (one 4096x4096 matrix per rank, ~80 s)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     ws, rank, local = dist_env()
@@ -398,8 +426,16 @@ def main():
            "api": "nqb_gemv_f32_host per layer (gemv_packed_f32 drop-in, pinned host buffers)",
            "steps": e2e_steps}
 
+    # ---- ADMM init (north_star part 2): the layer-sharded driver, one Llama-2-7B
+    #      4096x4096 matrix per rank at 1 bit/param, gathered to rank 0 -> matrices/s ----
+    admm = None
+    if not args.no_admm:
+        admm = admm_leg(nq, torch, ws, rank, local)
+
     peak, peak_kind = measured_peaks()
     extra = {}
+    if admm is not None and rank == 0:
+        extra["admm_init"] = admm
     roof = None
     if rank == 0:
         shapes = {}

@@ -173,8 +173,10 @@ def run_local(specs: Sequence[MatrixSpec], indices: Sequence[int], bpw: float,
     matrices concurrently (ctypes releases the GIL), so the per-iteration grid
     barriers of one matrix overlap the HBM streaming of the others."""
     if factorize is not None or workers <= 1:
-        if factorize is None:
-            factorize = lambda s, i: device_factorize(s, i, bpw)  # noqa: E731
+        if factorize is None:  # this rank's GPU (one process per GPU)
+            from . import nanoquant as nq
+            ctx = nq.context(device)
+            factorize = lambda s, i: device_factorize(s, i, bpw, ctx=ctx)  # noqa: E731
         return [factorize(specs[i], i) for i in indices]
     from concurrent.futures import ThreadPoolExecutor
 
