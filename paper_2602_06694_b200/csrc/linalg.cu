@@ -195,6 +195,10 @@ struct PowerArgs {
   double* out;         // [0] sigma, [1] converged, [2] iterations
   unsigned* bar;
   unsigned long long* prof;  // diagnostics (NQB_POWER_PROF): block 0 phase cycles, or null
+  // k_power_stream: the first keep_num/keep_den of each block's rows are read
+  // with an L2 evict_last hint so they stay L2-resident across iterations (the
+  // matrix is re-read up to 1000 times per singular vector); the rest stream.
+  uint32_t keep_num, keep_den;
 };
 
 template <int CPT, int RB, bool WSMEM>
@@ -395,6 +399,8 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
   __shared__ uint64_t fullb[PS_MAX_SLOTS];
   __shared__ double bred[PI_THREADS / 32];
   __shared__ double cred[PI_THREADS / 32][33];
+  __shared__ double cred2[2][PI_THREADS / 32][2];  // phase A: per-warp dot partials, by step parity
+  constexpr bool kKeep = CPT <= 12;  // phase A keeps each row pair in registers
   const uint32_t tid = threadIdx.x, G = gridDim.x, bid = blockIdx.x;
   unsigned gsk = 0;  // grid barriers passed
   const int lane = tid & 31, warp = tid >> 5;
@@ -424,16 +430,18 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
 
   uint32_t phase = 0;  // bit s: parity of the next completion of slot s
   uint32_t pending = 0;  // rows of the NEXT pass already issued (prefetched)
+  const uint32_t keep = a.keep_den ? (uint32_t)((uint64_t)nrows * a.keep_num / a.keep_den) : 0;
+  const uint64_t pol_keep = tc::policy_evict_last(), pol_stream = tc::policy_evict_first();
   auto issue = [&](uint32_t i) {  // row r0+i -> slot i % nslots (thread 0)
     uint64_t* bar = &fullb[i % nslots];
     tc::mbar_arrive_expect_tx(bar, row_bytes);
-    tc::bulk_g2s(ring + (size_t)(i % nslots) * row_bytes, a.M + (uint64_t)(r0 + i) * a.cols,
-                 row_bytes, bar);
+    tc::bulk_g2s_hint(ring + (size_t)(i % nslots) * row_bytes, a.M + (uint64_t)(r0 + i) * a.cols,
+                      row_bytes, bar, i < keep ? pol_keep : pol_stream);
   };
   const uint32_t head = nrows < nslots ? nrows : nslots;
   double sigma = 0.0, sigma_prev = -1.0;
   int converged = 0, it = 0;
-  long long tA = 0, tB = 0, tC = 0, t0 = clock64();
+  long long tA = 0, tB = 0, tC = 0, tW = 0, tD = 0, tX = 0, tY = 0, tZ = 0, t0 = clock64();
   for (it = 0; it < a.max_iters; ++it) {
     if (a.prof) t0 = clock64();
     // ---- phase A: s_i = M_i . v ; w += s_i M_i, rows streamed through smem,
@@ -446,71 +454,125 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
 #pragma unroll
     for (int c = 0; c < CPT; ++c) wl[c] = 0.0;
     double ss = 0.0;
+    uint32_t par = 0;  // cred2 buffer of this step
     for (uint32_t i = 0; i < nrows; i += 2) {
       const bool two = i + 1 < nrows && nslots >= 2;
       const uint32_t s0 = i % nslots, s1 = (i + 1) % nslots;
+      long long pw0 = a.prof ? clock64() : 0;
       tc::mbar_wait(&fullb[s0], (phase >> s0) & 1u);
       phase ^= 1u << s0;
       if (two) {
         tc::mbar_wait(&fullb[s1], (phase >> s1) & 1u);
         phase ^= 1u << s1;
       }
+      long long pw1 = a.prof ? clock64() : 0;
+      if (a.prof) tW += pw1 - pw0;
       const double* x0 = (const double*)(ring + (size_t)s0 * row_bytes);
       const double* x1 = (const double*)(ring + (size_t)s1 * row_bytes);
-      double p0 = 0.0, p1 = 0.0;
+      // The two rows' elements are read from shared memory once and kept in
+      // registers for the axpy after the block reduction (shared-memory
+      // bandwidth, not HBM, bounds this loop otherwise).  Wide rows (CPT > 12)
+      // re-read them to stay within the register budget.
+      double xa_r[kKeep ? CPT : 1], xb_r[kKeep ? CPT : 1];
+      // four independent partial sums per row (fp64 latency, not throughput,
+      // bounds a single dependent chain), combined in a fixed tree below
+      double pa[4] = {0.0, 0.0, 0.0, 0.0}, pb[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         const uint32_t j = tid + c * PI_THREADS;
+        double xa = 0.0, xb = 0.0;
         if (j < a.cols) {
-          double xa = x0[j], xb = two ? x1[j] : 0.0;
+          xa = x0[j];
+          xb = two ? x1[j] : 0.0;
           if (a.abs_mode) {
             xa = fabs(xa);
             xb = fabs(xb);
           }
-          p0 += xa * vr[c];
-          p1 += xb * vr[c];
+          pa[c & 3] += xa * vr[c];
+          pb[c & 3] += xb * vr[c];
+        }
+        if constexpr (kKeep) {
+          xa_r[c] = xa;
+          xb_r[c] = xb;
         }
       }
+      double p0 = (pa[0] + pa[1]) + (pa[2] + pa[3]);
+      double p1 = (pb[0] + pb[1]) + (pb[2] + pb[3]);
       // both dot products through one fixed tree (identical in every thread)
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
         p0 += __shfl_xor_sync(~0u, p0, o);
         p1 += __shfl_xor_sync(~0u, p1, o);
       }
+      double* cr = &cred2[par][0][0];
       if (lane == 0) {
-        cred[warp][0] = p0;
-        cred[warp][1] = p1;
+        cr[2 * warp] = p0;
+        cr[2 * warp + 1] = p1;
       }
       __syncthreads();
-      double sa = 0.0, sb = 0.0;
-#pragma unroll
-      for (int w = 0; w < PI_THREADS / 32; ++w) {
-        sa += cred[w][0];
-        sb += cred[w][1];
+      if (a.prof) tD += clock64() - pw1;
+      if constexpr (kKeep) {
+        // the rows are in registers now: refill their slots right away (the
+        // copies overlap the axpy; one barrier per step, cred double-buffered)
+        if (tid == 0) {
+          const uint32_t nx = i + nslots;
+          if (nx < nrows) issue(nx);
+          if (two && nx + 1 < nrows) issue(nx + 1);
+        }
       }
+      // cross-warp sums: lane w < warps holds warp w's partial, one xor tree
+      // per warp (fixed order, identical everywhere) instead of every thread
+      // adding all partials (the fp64 pipe is shared by 16 warps)
+      static_assert(PI_THREADS / 32 <= 32, "warps per block");
+      double ta = lane < PI_THREADS / 32 ? cr[2 * lane] : 0.0;
+      double tb = lane < PI_THREADS / 32 ? cr[2 * lane + 1] : 0.0;
+#pragma unroll
+      for (int o = PI_THREADS / 64; o; o >>= 1) {
+        ta += __shfl_xor_sync(~0u, ta, o);
+        tb += __shfl_xor_sync(~0u, tb, o);
+      }
+      const double sa = __shfl_sync(~0u, ta, 0), sb = __shfl_sync(~0u, tb, 0);
       ss += sa * sa;
       if (two) ss += sb * sb;
+      long long px = a.prof ? clock64() : 0;
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         const uint32_t j = tid + c * PI_THREADS;
         if (j < a.cols) {
-          double xa = x0[j];
-          if (a.abs_mode) xa = fabs(xa);
-          wl[c] += xa * sa;
-          if (two) {
-            double xb = x1[j];
-            if (a.abs_mode) xb = fabs(xb);
-            wl[c] += xb * sb;
+          double xa, xb;
+          if constexpr (kKeep) {
+            xa = xa_r[c];
+            xb = xb_r[c];
+          } else {
+            xa = x0[j];
+            xb = two ? x1[j] : 0.0;
+            if (a.abs_mode) {
+              xa = fabs(xa);
+              xb = fabs(xb);
+            }
           }
+          wl[c] += xa * sa;
+          if (two) wl[c] += xb * sb;
         }
       }
-      __syncthreads();  // everyone is done with these slots (and with cred)
-      if (tid == 0) {
-        const uint32_t nx = i + nslots;  // refill the freed slots
-        if (nx < nrows) issue(nx);
-        if (two && nx + 1 < nrows) issue(nx + 1);
+      long long py = a.prof ? clock64() : 0;
+      if constexpr (!kKeep) {
+        __syncthreads();  // everyone is done with these slots
+        if (tid == 0) {
+          const uint32_t nx = i + nslots;  // refill the freed slots
+          if (nx < nrows) issue(nx);
+          if (two && nx + 1 < nrows) issue(nx + 1);
+        }
       }
+      if (a.prof) {
+        const long long pz = clock64();
+        tX += px - pw1;
+        tY += py - px;
+        tZ += pz - py;
+      }
+      par ^= 1;
     }
+    __syncthreads();  // (kKeep) the last step's cred reads are done
     // prefetch the next pass's first rows now: they stream while the
     // reductions and grid barriers below run (drained before exit)
     if (it + 1 < a.max_iters) {
@@ -601,6 +663,11 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     atomicAdd(a.prof + 1, (unsigned long long)tB);
     atomicAdd(a.prof + 2, (unsigned long long)tC);
     atomicAdd(a.prof + 3, (unsigned long long)it);
+    atomicAdd(a.prof + 4, (unsigned long long)tW);
+    atomicAdd(a.prof + 5, (unsigned long long)tD);
+    atomicAdd(a.prof + 6, (unsigned long long)tX);
+    atomicAdd(a.prof + 7, (unsigned long long)tY);
+    atomicAdd(a.prof + 8, (unsigned long long)tZ);
   }
 
   if (pending) {  // an early exit left the next pass's prefetch in flight: drain it
@@ -715,11 +782,29 @@ void power_iterate_device(nqb_context* ctx, const double* d_m, uint32_t rows, ui
   a.out = a.wsspart + grid;
   a.bar = ctx->barrier;
   a.prof = nullptr;
+  {  // L2-resident share of the matrix (NQB_POWER_L2_MB, default 80 of the 126 MB L2)
+    static const uint64_t budget = [] {
+      const char* e = std::getenv("NQB_POWER_L2_MB");
+      return (uint64_t)(e ? std::strtoul(e, nullptr, 10) : 80ul) << 20;
+    }();
+    const uint64_t total = (uint64_t)rows * cols * 8;
+    static bool limit_set = false;  // evict_last lines live in the persisting L2 set-aside
+    if (!limit_set && budget) {
+      cudaDeviceProp pr;
+      NQB_CUDA(cudaGetDeviceProperties(&pr, ctx->device));
+      const size_t want = std::min<size_t>(budget, (size_t)pr.persistingL2CacheMaxSize);
+      if (want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+      cudaGetLastError();
+      limit_set = true;
+    }
+    a.keep_den = 1u << 20;
+    a.keep_num = total ? (uint32_t)std::min<uint64_t>(a.keep_den, budget * a.keep_den / total) : 0;
+  }
   static unsigned long long* prof_buf = nullptr;
   if (getenv_flag("NQB_POWER_PROF")) {
     if (!prof_buf) {
-      NQB_CUDA(cudaMalloc(&prof_buf, 64));
-      NQB_CUDA(cudaMemset(prof_buf, 0, 64));
+      NQB_CUDA(cudaMalloc(&prof_buf, 128));
+      NQB_CUDA(cudaMemset(prof_buf, 0, 128));
     }
     a.prof = prof_buf;
   }
@@ -748,11 +833,14 @@ void power_iterate_device(nqb_context* ctx, const double* d_m, uint32_t rows, ui
   *converged = (int)h[1];
   *iters = (int)h[2];
   if (a.prof) {
-    unsigned long long hp[4];
+    unsigned long long hp[9];
     NQB_CUDA(cudaMemcpy(hp, a.prof, sizeof(hp), cudaMemcpyDeviceToHost));
-    fprintf(stderr, "power_prof rows=%u cols=%u iters=%llu cyc/iter: A %.0f B %.0f C %.0f\n", rows,
-            cols, hp[3], (double)hp[0] / std::max(1ull, hp[3]), (double)hp[1] / std::max(1ull, hp[3]),
-            (double)hp[2] / std::max(1ull, hp[3]));
+    const double it = (double)std::max(1ull, hp[3]);
+    fprintf(stderr,
+            "power_prof rows=%u cols=%u iters=%llu cyc/iter: A %.0f B %.0f C %.0f (A: row waits %.0f, "
+            "dot+reduce %.0f, +sums %.0f, axpy %.0f, sync %.0f)\n",
+            rows, cols, hp[3], hp[0] / it, hp[1] / it, hp[2] / it, hp[4] / it, hp[5] / it,
+            hp[6] / it, hp[7] / it, hp[8] / it);
   }
 }
 
