@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "tc_common.cuh"
@@ -183,6 +184,138 @@ __global__ void __launch_bounds__(kProducers + 32, 1) k_prefill(const __grid_con
   if (warp == 0) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// TS variant: the expanded +-1 A tile never touches shared memory.  Producer
+// thread t expands its row's 64 signs of a K tile in registers and writes them
+// straight into TMEM (tcgen05.st.32x32b.x32: its lane, 32 columns of two
+// binary16); the MMA reads A from TMEM and only the token tile (B) from shared
+// memory, cutting shared-memory traffic per MAC by ~40% (the SS kernel is
+// L1/shared-bandwidth bound: l1tex throughput 85% in ncu); N = 128 tokens per
+// CTA keeps D (2 x 128 columns) plus four A stages (4 x 64 columns) in the 512
+// TMEM columns, and 256 rows still share every B tile.
+namespace ts {
+constexpr int BN = 128, STAGES = 4;
+constexpr int B_BYTES = BN * BK * 2;       // 16 KB
+constexpr uint32_t kDCols = MH * BN;       // 256: D_h at columns h * BN
+constexpr uint32_t kACols = MH * BK / 2;   // 64 per stage: half h at + h * 32
+
+struct __align__(8) Bars {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t dready;
+  uint32_t tmem;
+};
+}  // namespace ts
+
+__global__ void __launch_bounds__(kProducers + 32, 1) k_prefill_ts(const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  ts::Bars* bars = (ts::Bars*)smem;
+  uint8_t* tiles = smem + 1024;  // ts::STAGES x B 16 KB
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(~0u, tid >> 5, 0);
+  const uint32_t m0 = blockIdx.x * (MH * BM), n0 = blockIdx.y * ts::BN;
+
+  if (tid == 0) {
+    for (int s = 0; s < ts::STAGES; ++s) {
+      tc::mbar_init(&bars->full[s], kProducers + 1);  // producers + the TMA issuer
+      tc::mbar_init(&bars->empty[s], 1);
+    }
+    tc::mbar_init(&bars->dready, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) {
+    tc::tmem_alloc(&bars->tmem, kTmemCols);
+    tc::tmem_relinquish();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = bars->tmem;
+
+  if (warp == kProducers / 32) {  // ------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_f16(BM, ts::BN);
+      for (uint32_t kt = 0; kt < a.nk; ++kt) {
+        const uint32_t slot = kt % ts::STAGES;
+        tc::mbar_wait(&bars->full[slot], (kt / ts::STAGES) & 1);
+        tc::fence_after_sync();
+        const uint32_t bbase = tc::smem_u32(tiles + slot * ts::B_BYTES);
+        const uint32_t abase = tmem + ts::kDCols + slot * ts::kACols;
+#pragma unroll
+        for (uint32_t ks = 0; ks < BK / 16; ++ks) {
+          const uint64_t bd = tc::smem_desc_kmajor(bbase + ks * 2 * (ts::BN / 8) * 128, (ts::BN / 8) * 128, 128);
+#pragma unroll
+          for (uint32_t h = 0; h < MH; ++h)
+            tc::mma_f16_ts(tmem + h * ts::BN, abase + h * (BK / 2) + ks * 8, bd, idesc,
+                           (kt | ks) ? 1u : 0u);
+        }
+        tc::mma_commit(&bars->empty[slot]);
+      }
+      tc::mma_commit(&bars->dready);
+    }
+  } else {  // ------------------------------------------------------ producers
+    const uint32_t row = tid, grow = m0 + row;
+    const bool rv = grow < a.M;
+    const uint32_t* brow = a.bits + (size_t)(rv ? grow : 0) * a.wpr;
+    auto load_bits = [&](uint32_t kt) -> uint2 {
+      return (rv && kt < a.nk) ? __ldg((const uint2*)(brow + kt * 2)) : make_uint2(0u, 0u);
+    };
+    // this warp's TMEM lane quadrant (warp w: lanes 32*(w%4).., half w/4)
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t hcol = (uint32_t)(warp >> 2) * (BK / 2);
+    uint2 cur = load_bits(0);
+    for (uint32_t kt = 0; kt < a.nk; ++kt) {
+      const uint2 nxt = load_bits(kt + 1);
+      const uint32_t slot = kt % ts::STAGES, use = kt / ts::STAGES;
+      if (use > 0) {
+        tc::mbar_wait(&bars->empty[slot], (use - 1) & 1);
+        tc::fence_after_sync();
+      }
+      if (tid == 0) {  // B: 8 TMA boxes (one per 8-wide K chunk) of 128 tokens
+        uint8_t* Bs = tiles + slot * ts::B_BYTES;
+        tc::mbar_arrive_expect_tx(&bars->full[slot], ts::B_BYTES);
+#pragma unroll
+        for (uint32_t k8 = 0; k8 < BK / 8; ++k8)
+          tma_b(Bs + canon(0, k8, ts::BN), &a.bmap, kt * BK + k8 * 8, n0, &bars->full[slot]);
+      }
+      // 64 signs -> 32 columns of two +-1 binary16 (bit 1 -> +1 0x3C00, 0 -> -1 0xBC00)
+      uint32_t v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t w = i < 16 ? cur.x : cur.y, b = 2 * (i & 15);
+        v[i] = 0xBC00BC00u ^ (((w >> b) & 1u) << 15) ^ (((w >> (b + 1)) & 1u) << 31);
+      }
+      tc::tmem_st_x32(tmem + lane_base + ts::kDCols + slot * ts::kACols + hcol, v);
+      tc::wait_st();
+      tc::fence_before_sync();  // TMEM stores -> the MMA issuer's barrier wait
+      tc::mbar_arrive(&bars->full[slot]);
+      cur = nxt;
+    }
+    // ------------------------------------------------------------- epilogue
+    tc::mbar_wait(&bars->dready, 0);
+    tc::fence_after_sync();
+    const float sc = (grow < a.Mvalid && a.scale) ? __half2float(a.scale[grow]) : 1.f;
+    const bool keep = grow < a.Mvalid;
+    for (uint32_t c0 = 0; c0 < ts::BN; c0 += 16) {
+      uint32_t d[16];
+      tc::tmem_ld_x16(tmem + lane_base + (uint32_t)(warp >> 2) * ts::BN + c0, d);
+      tc::wait_ld();
+      if (grow < a.Mout) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t tok = n0 + c0 + j;
+          if (tok < a.N)
+            a.out[(size_t)tok * a.ldo + grow] =
+                __float2half_rn(keep ? sc * __uint_as_float(d[j]) : 0.f);
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, kTmemCols);
+}
+
 // X (b x m, binary16, token-major) -> s2 .* X with K padded to kpad (zeros).
 __global__ void k_prescale(const __half* __restrict__ x, const __half* __restrict__ s2h,
                            uint32_t m, uint32_t b, uint32_t kpad, __half* __restrict__ out) {
@@ -213,10 +346,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // B = tokens x ld binary16 (K = kdim valid columns); box 8 K x 256 tokens;
 // out-of-range tokens / K read as zero.
-static void make_bmap(CUtensorMap* map, const __half* B, uint32_t kdim, uint32_t ld, uint32_t tokens) {
+static void make_bmap(CUtensorMap* map, const __half* B, uint32_t kdim, uint32_t ld, uint32_t tokens,
+                      uint32_t box_tokens) {
   const cuuint64_t dims[2] = {kdim, tokens};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  const cuuint32_t box[2] = {8, (cuuint32_t)BN};
+  const cuuint32_t box[2] = {8, box_tokens};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)B, dims, strides, box,
                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -225,15 +359,32 @@ static void make_bmap(CUtensorMap* map, const __half* B, uint32_t kdim, uint32_t
   NQB_REQUIRE(r == CUDA_SUCCESS, NQB_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
 
-static void launch_stage(nqb_context* ctx, const Args& a, uint32_t grid_m, uint32_t grid_n) {
+// The SS kernel is the default.  NQB_PREFILL_TS=1 selects the TS variant:
+// parity-green, faster on 70B q (574 vs 488 TFLOP/s) but slower on gate/down
+// (675 vs 733, 559 vs 639).  ncu shows l1tex still at 84% with A in TMEM, so the
+// TMEM stores and A reads load the same datapath that the shared-memory A
+// traffic did.
+static bool use_ts() {
+  static const bool ts = [] { const char* e = std::getenv("NQB_PREFILL_TS");
+                              return e && e[0] == '1'; }();
+  return ts;
+}
+
+static void launch_stage(nqb_context* ctx, const Args& a, uint32_t grid_m, uint32_t tokens) {
   static bool attr = false;
   if (!attr) {
     NQB_CUDA(cudaFuncSetAttribute(k_prefill, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   1024 + STAGES * (A_BYTES + B_BYTES)));
+    NQB_CUDA(cudaFuncSetAttribute(k_prefill_ts, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  1024 + ts::STAGES * ts::B_BYTES));
     attr = true;
   }
-  k_prefill<<<dim3((grid_m + MH - 1) / MH, grid_n), kProducers + 32,
-              1024 + STAGES * (A_BYTES + B_BYTES), ctx->stream>>>(a);
+  if (use_ts())
+    k_prefill_ts<<<dim3((grid_m + MH - 1) / MH, (tokens + ts::BN - 1) / ts::BN), kProducers + 32,
+                   1024 + ts::STAGES * ts::B_BYTES, ctx->stream>>>(a);
+  else
+    k_prefill<<<dim3((grid_m + MH - 1) / MH, (tokens + BN - 1) / BN), kProducers + 32,
+                1024 + STAGES * (A_BYTES + B_BYTES), ctx->stream>>>(a);
   NQB_LAUNCHED(ctx);
 }
 
@@ -251,12 +402,13 @@ void prefill_gemm_tc(nqb_context* ctx, const nqb_layer* L, const __half* d_x, ui
   NQB_LAUNCHED(ctx);
   // stage 1: T^T[token][k] = sum_j sign(V[j][k]) * xs[token][j]   (rows k < r, padded rows 0)
   Args a1{{}, L->vt, L->vt_words, L->r, L->r, rpad, mpad / BK, xs, mpad, b, nullptr, tt, rpad};
-  make_bmap(&a1.bmap, xs, mpad, mpad, b);
-  launch_stage(ctx, a1, (rpad + BM - 1) / BM, (b + BN - 1) / BN);
+  const uint32_t box = use_ts() ? (uint32_t)ts::BN : (uint32_t)BN;
+  make_bmap(&a1.bmap, xs, mpad, mpad, b, box);
+  launch_stage(ctx, a1, (rpad + BM - 1) / BM, b);
   // stage 2: Y[token][i] = s1_i * sum_k sign(U[i][k]) * T^T[token][k]
   Args a2{{}, L->u, L->u_words, L->n, L->n, L->n, rpad / BK, tt, rpad, b, L->s1h, d_y, L->n};
-  make_bmap(&a2.bmap, tt, rpad, rpad, b);
-  launch_stage(ctx, a2, (L->n + BM - 1) / BM, (b + BN - 1) / BN);
+  make_bmap(&a2.bmap, tt, rpad, rpad, b, box);
+  launch_stage(ctx, a2, (L->n + BM - 1) / BM, b);
 }
 
 }  // namespace nqb
