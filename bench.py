@@ -448,6 +448,20 @@ def main():
                                            "gbs": per / sec / 1e9, "frac": per / sec / 1e9 / peak}
         extra["per_shape_single_layer"] = shapes
         if not args.no_shapes:
+            # BASELINE config 5: bitrate sweep on Llama-2-13B shapes (decode GB/s; the ADMM
+            # reconstruction error vs the CPU reference at these bitrates is pinned by the
+            # l13s16_* fixtures in tests/test_gpu_admm.py)
+            sweep = {}
+            for name, n, m in [("l13_q", 5120, 5120), ("l13_gate", 13824, 5120),
+                               ("l13_down", 5120, 13824)]:
+                for bpw in (0.55, 0.8, 1.0):
+                    r = rank_for(n, m, bpw)
+                    sec, per = shape_roofline(nq, ctx, torch, stream, n, m, r, reps=10)
+                    sweep[f"{name}_{bpw}"] = {"n": n, "m": m, "r": r, "us": sec * 1e6,
+                                              "gbs": per / sec / 1e9,
+                                              "frac": per / sec / 1e9 / peak}
+            extra["bitrate_sweep_l13_decode"] = sweep
+        if not args.no_shapes:
             pref = {}
             tpk = tensor_peak()
             for name, n, m, bpw in L70_SHAPES:
