@@ -316,6 +316,201 @@ __global__ void __launch_bounds__(kProducers + 32, 1) k_prefill_ts(const __grid_
   if (warp == 0) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2).  A cluster of two CTAs on one TPC
+// runs M = 256 MMAs: each CTA holds 256 rows of A (two 128-row halves, expanded
+// by its producers as in k_prefill) and HALF of the 256-token B tile (128
+// tokens, by TMA).  The leader (rank 0) issues `tcgen05.mma.cta_group::2`; the
+// tensor cores of the pair read each B half once for both SMs, so shared-memory
+// traffic per MAC drops by ~30% against k_prefill (which is l1tex-bound) and
+// L2 traffic for B halves.  Each CTA's TMEM holds D for its own rows.
+//   full[s] (leader): one arrival per producer warp of both CTAs (after the
+//     warp's A rows are written) + the transaction bytes of both B halves;
+//   empty[s], dready (both CTAs): one multicast commit from the leader.
+namespace p2 {
+constexpr int BNP = 256;                 // tokens per pair
+constexpr int BNH = BNP / 2;             // tokens per CTA (B half)
+constexpr int STAGES = 4;
+constexpr int B_BYTES = BNH * BK * 2;    // 16 KB
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the rank-0 CTA
+
+struct __align__(8) Bars {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t dready;
+  uint32_t tmem;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+// arrive on the leader's barrier (a shared::cluster address), release at cluster scope
+__device__ __forceinline__ void arrive_leader(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster)
+               : "memory");
+}
+__device__ __forceinline__ void arrive_leader_expect_tx(uint32_t bar_cluster, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(
+                   bar_cluster),
+               "r"(bytes)
+               : "memory");
+}
+// 2-D TMA of this CTA's B box; complete_tx lands on the leader's barrier
+__device__ __forceinline__ void tma_b_2sm(void* dst, const CUtensorMap* map, uint32_t k, uint32_t tok,
+                                          uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(map), "r"(k), "r"(tok), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_ss_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit: arrive on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          tc::smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+}  // namespace p2
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kProducers + 32, 1)
+    k_prefill2(const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  p2::Bars* bars = (p2::Bars*)smem;
+  uint8_t* tiles = smem + 1024;  // p2::STAGES x [A 32 KB | B half 16 KB]
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(~0u, tid >> 5, 0);
+  const uint32_t rank = p2::cluster_rank();
+  const bool leader = rank == 0;
+  const uint32_t m0 = blockIdx.x * (MH * BM);
+  const uint32_t np = blockIdx.y * p2::BNP;      // the pair's first token
+  const uint32_t n0 = np + rank * p2::BNH;       // this CTA's B half
+
+  if (tid == 0) {
+    for (int s = 0; s < p2::STAGES; ++s) {
+      // leader: one arrival per producer warp of both CTAs (+ tx of both B halves)
+      tc::mbar_init(&bars->full[s], 2 * (kProducers / 32));
+      tc::mbar_init(&bars->empty[s], 1);
+    }
+    tc::mbar_init(&bars->dready, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     tc::smem_u32(&bars->tmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
+  }
+  tc::fence_before_sync();
+  p2::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+  tc::fence_after_sync();
+  const uint32_t tmem = bars->tmem;
+  const uint32_t full_leader0 = tc::smem_u32(&bars->full[0]) & p2::kPeerMask;
+
+  if (warp == kProducers / 32) {  // ------------------- MMA issuer (leader CTA only)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_f16(2 * BM, p2::BNP);
+      for (uint32_t kt = 0; kt < a.nk; ++kt) {
+        const uint32_t slot = kt % p2::STAGES;
+        tc::mbar_wait(&bars->full[slot], (kt / p2::STAGES) & 1);
+        tc::fence_after_sync();
+        const uint32_t abase = tc::smem_u32(tiles + slot * (A_BYTES + p2::B_BYTES));
+        const uint32_t bbase = abase + A_BYTES;
+#pragma unroll
+        for (uint32_t ks = 0; ks < BK / 16; ++ks) {
+          const uint64_t bd =
+              tc::smem_desc_kmajor(bbase + ks * 2 * (p2::BNH / 8) * 128, (p2::BNH / 8) * 128, 128);
+#pragma unroll
+          for (uint32_t h = 0; h < MH; ++h) {
+            const uint64_t ad = tc::smem_desc_kmajor(abase + h * (A_BYTES / MH) + ks * 2 * (BM / 8) * 128,
+                                                     (BM / 8) * 128, 128);
+            p2::mma_f16_ss_2sm(tmem + h * p2::BNP, ad, bd, idesc, (kt | ks) ? 1u : 0u);
+          }
+        }
+        p2::commit_pair(&bars->empty[slot]);
+      }
+      p2::commit_pair(&bars->dready);
+    }
+  } else {  // ------------------------------------------------------ producers
+    const uint32_t row = tid, grow = m0 + row;
+    const bool rv = grow < a.M;
+    const uint32_t* brow = a.bits + (size_t)(rv ? grow : 0) * a.wpr;
+    auto load_bits = [&](uint32_t kt) -> uint2 {
+      return (rv && kt < a.nk) ? __ldg((const uint2*)(brow + kt * 2)) : make_uint2(0u, 0u);
+    };
+    uint2 cur = load_bits(0);
+    for (uint32_t kt = 0; kt < a.nk; ++kt) {
+      const uint2 nxt = load_bits(kt + 1);
+      const uint32_t slot = kt % p2::STAGES, use = kt / p2::STAGES;
+      if (use > 0) tc::mbar_wait(&bars->empty[slot], (use - 1) & 1);
+      uint8_t* As = tiles + slot * (A_BYTES + p2::B_BYTES);
+      uint8_t* Bs = As + A_BYTES;
+      const uint32_t fullL = full_leader0 + slot * 8;
+      if (tid == 0) {  // this CTA's B half: 8 TMA boxes of 128 tokens, bytes counted at the leader
+#pragma unroll
+        for (uint32_t k8 = 0; k8 < BK / 8; ++k8)
+          p2::tma_b_2sm(Bs + canon(0, k8, p2::BNH), &a.bmap, kt * BK + k8 * 8, n0, fullL);
+      }
+#pragma unroll
+      for (uint32_t k8 = 0; k8 < 8; ++k8) {
+        const uint32_t byte = ((k8 < 4 ? cur.x : cur.y) >> (8 * (k8 & 3))) & 0xFFu;
+        uint4 v;
+        uint32_t* pv = &v.x;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          pv[i] = 0xBC00BC00u ^ (((byte >> (2 * i)) & 1u) << 15) ^ (((byte >> (2 * i + 1)) & 1u) << 31);
+        *(uint4*)(As + (row / BM) * (A_BYTES / MH) + canon(row % BM, k8, BM)) = v;
+      }
+      cur = nxt;
+      tc::fence_proxy_async_smem();  // generic-proxy writes -> the pair's MMA (async proxy)
+      __syncwarp();                  // the warp's rows are written; lane 0 arrives (release)
+      if (lane == 0) {
+        if (leader && tid == 0) p2::arrive_leader_expect_tx(fullL, 2 * p2::B_BYTES);
+        else p2::arrive_leader(fullL);
+      }
+    }
+    // ------------------------------------------------------------- epilogue
+    tc::mbar_wait(&bars->dready, 0);
+    tc::fence_after_sync();
+    const float sc = (grow < a.Mvalid && a.scale) ? __half2float(a.scale[grow]) : 1.f;
+    const bool keep = grow < a.Mvalid;
+    for (uint32_t c0 = 0; c0 < p2::BNP; c0 += 16) {
+      uint32_t v[16];
+      tc::tmem_ld_x16(tmem + (row / BM) * p2::BNP + ((uint32_t)((warp & 3) * 32) << 16) + c0, v);
+      tc::wait_ld();
+      if (grow < a.Mout) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t tok = np + c0 + j;
+          if (tok < a.N)
+            a.out[(size_t)tok * a.ldo + grow] =
+                __float2half_rn(keep ? sc * __uint_as_float(v[j]) : 0.f);
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  p2::cluster_sync();  // both CTAs are done with the pair's TMEM
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+}
+
 // X (b x m, binary16, token-major) -> s2 .* X with K padded to kpad (zeros).
 __global__ void k_prescale(const __half* __restrict__ x, const __half* __restrict__ s2h,
                            uint32_t m, uint32_t b, uint32_t kpad, __half* __restrict__ out) {
@@ -364,6 +559,16 @@ static void make_bmap(CUtensorMap* map, const __half* B, uint32_t kdim, uint32_t
 // (675 vs 733, 559 vs 639).  ncu shows l1tex still at 84% with A in TMEM, so the
 // TMEM stores and A reads load the same datapath that the shared-memory A
 // traffic did.
+// NQB_PREFILL_2SM=1 selects the CTA-pair kernel.  It is parity-green, and ncu
+// shows it moves the bottleneck: l1tex drops from 85% to 41%.  But the tensor
+// pipe does not rise (35% vs 39% active), and it measures ~10% slower than the
+// SS kernel at b = 2048 on the 70B shapes, so it is opt-in.
+static bool use_2sm() {
+  static const bool v = [] { const char* e = std::getenv("NQB_PREFILL_2SM");
+                             return e && e[0] == '1'; }();
+  return v;
+}
+
 static bool use_ts() {
   static const bool ts = [] { const char* e = std::getenv("NQB_PREFILL_TS");
                               return e && e[0] == '1'; }();
@@ -379,7 +584,17 @@ static void launch_stage(nqb_context* ctx, const Args& a, uint32_t grid_m, uint3
                                   1024 + ts::STAGES * ts::B_BYTES));
     attr = true;
   }
-  if (use_ts())
+  static bool attr2 = false;
+  if (use_2sm() && !use_ts()) {
+    if (!attr2) {
+      NQB_CUDA(cudaFuncSetAttribute(k_prefill2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    1024 + p2::STAGES * (A_BYTES + p2::B_BYTES)));
+      attr2 = true;
+    }
+    const uint32_t gx = ((grid_m + MH - 1) / MH + 1) / 2 * 2;  // whole CTA pairs
+    k_prefill2<<<dim3(gx, (tokens + p2::BNP - 1) / p2::BNP), kProducers + 32,
+                 1024 + p2::STAGES * (A_BYTES + p2::B_BYTES), ctx->stream>>>(a);
+  } else if (use_ts())
     k_prefill_ts<<<dim3((grid_m + MH - 1) / MH, (tokens + ts::BN - 1) / ts::BN), kProducers + 32,
                    1024 + ts::STAGES * ts::B_BYTES, ctx->stream>>>(a);
   else
@@ -402,7 +617,7 @@ void prefill_gemm_tc(nqb_context* ctx, const nqb_layer* L, const __half* d_x, ui
   NQB_LAUNCHED(ctx);
   // stage 1: T^T[token][k] = sum_j sign(V[j][k]) * xs[token][j]   (rows k < r, padded rows 0)
   Args a1{{}, L->vt, L->vt_words, L->r, L->r, rpad, mpad / BK, xs, mpad, b, nullptr, tt, rpad};
-  const uint32_t box = use_ts() ? (uint32_t)ts::BN : (uint32_t)BN;
+  const uint32_t box = use_ts() ? (uint32_t)ts::BN : use_2sm() ? (uint32_t)p2::BNH : (uint32_t)BN;
   make_bmap(&a1.bmap, xs, mpad, mpad, b, box);
   launch_stage(ctx, a1, (rpad + BM - 1) / BM, b);
   // stage 2: Y[token][i] = s1_i * sum_k sign(U[i][k]) * T^T[token][k]
