@@ -350,14 +350,15 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::
                    : "memory");
 }
-// arrive on the leader's barrier (a shared::cluster address), release at cluster scope
+// arrive on the leader's barrier (a shared::cluster address).  Default
+// (CTA-scope release) semantics: each SM's tensor core reads only its own
+// CTA's A rows, so the writes need no cluster-scope release; a .release.cluster
+// arrive costs a MEMBAR.ALL.GPU per warp (it dominated the stall profile).
 __device__ __forceinline__ void arrive_leader(uint32_t bar_cluster) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster) : "memory");
 }
 __device__ __forceinline__ void arrive_leader_expect_tx(uint32_t bar_cluster, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(
-                   bar_cluster),
+  asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;\n" ::"r"(bar_cluster),
                "r"(bytes)
                : "memory");
 }
@@ -479,7 +480,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kProducers + 32, 1)
       }
       cur = nxt;
       tc::fence_proxy_async_smem();  // generic-proxy writes -> the pair's MMA (async proxy)
-      __syncwarp();                  // the warp's rows are written; lane 0 arrives (release)
+      __syncwarp();                  // the warp's rows are written; lane 0 arrives
       if (lane == 0) {
         if (leader && tid == 0) p2::arrive_leader_expect_tx(fullL, 2 * p2::B_BYTES);
         else p2::arrive_leader(fullL);
@@ -559,13 +560,11 @@ static void make_bmap(CUtensorMap* map, const __half* B, uint32_t kdim, uint32_t
 // (675 vs 733, 559 vs 639).  ncu shows l1tex still at 84% with A in TMEM, so the
 // TMEM stores and A reads load the same datapath that the shared-memory A
 // traffic did.
-// NQB_PREFILL_2SM=1 selects the CTA-pair kernel.  It is parity-green, and ncu
-// shows it moves the bottleneck: l1tex drops from 85% to 41%.  But the tensor
-// pipe does not rise (35% vs 39% active), and it measures ~10% slower than the
-// SS kernel at b = 2048 on the 70B shapes, so it is opt-in.
+// The CTA-pair kernel is the default (NQB_PREFILL_2SM=0 selects the
+// single-CTA SS kernel): +39..51% at b = 2048 on the 70B shapes.
 static bool use_2sm() {
   static const bool v = [] { const char* e = std::getenv("NQB_PREFILL_2SM");
-                             return e && e[0] == '1'; }();
+                             return !(e && e[0] == '0'); }();
   return v;
 }
 
