@@ -390,8 +390,13 @@ __device__ __forceinline__ void commit_pair(uint64_t* bar) {
 }
 }  // namespace p2
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kProducers + 32, 1)
+// MHT: 128-row halves per CTA (2: 256 rows share each B tile; 1: more CTAs for
+// short M, e.g. stage 1 of the 70B q shape).
+template <int MHT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
     k_prefill2(const __grid_constant__ Args a) {
+  constexpr int kP = MHT * BM;               // producer threads (one per A row)
+  constexpr int kAB = MHT * BM * BK * 2;     // A bytes per stage
   extern __shared__ __align__(1024) uint8_t smem[];
   p2::Bars* bars = (p2::Bars*)smem;
   uint8_t* tiles = smem + 1024;  // p2::STAGES x [A 32 KB | B half 16 KB]
@@ -399,14 +404,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kProducers + 32, 1)
   const int warp = __shfl_sync(~0u, tid >> 5, 0);
   const uint32_t rank = p2::cluster_rank();
   const bool leader = rank == 0;
-  const uint32_t m0 = blockIdx.x * (MH * BM);
+  const uint32_t m0 = blockIdx.x * (MHT * BM);
   const uint32_t np = blockIdx.y * p2::BNP;      // the pair's first token
   const uint32_t n0 = np + rank * p2::BNH;       // this CTA's B half
 
   if (tid == 0) {
     for (int s = 0; s < p2::STAGES; ++s) {
       // leader: one arrival per producer warp of both CTAs (+ tx of both B halves)
-      tc::mbar_init(&bars->full[s], 2 * (kProducers / 32));
+      tc::mbar_init(&bars->full[s], 2 * (kP / 32));
       tc::mbar_init(&bars->empty[s], 1);
     }
     tc::mbar_init(&bars->dready, 1);
@@ -424,22 +429,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kProducers + 32, 1)
   const uint32_t tmem = bars->tmem;
   const uint32_t full_leader0 = tc::smem_u32(&bars->full[0]) & p2::kPeerMask;
 
-  if (warp == kProducers / 32) {  // ------------------- MMA issuer (leader CTA only)
+  if (warp == kP / 32) {  // ------------------- MMA issuer (leader CTA only)
     if (leader && lane == 0) {
       constexpr uint32_t idesc = tc::idesc_f16(2 * BM, p2::BNP);
       for (uint32_t kt = 0; kt < a.nk; ++kt) {
         const uint32_t slot = kt % p2::STAGES;
         tc::mbar_wait(&bars->full[slot], (kt / p2::STAGES) & 1);
         tc::fence_after_sync();
-        const uint32_t abase = tc::smem_u32(tiles + slot * (A_BYTES + p2::B_BYTES));
-        const uint32_t bbase = abase + A_BYTES;
+        const uint32_t abase = tc::smem_u32(tiles + slot * (kAB + p2::B_BYTES));
+        const uint32_t bbase = abase + kAB;
 #pragma unroll
         for (uint32_t ks = 0; ks < BK / 16; ++ks) {
           const uint64_t bd =
               tc::smem_desc_kmajor(bbase + ks * 2 * (p2::BNH / 8) * 128, (p2::BNH / 8) * 128, 128);
 #pragma unroll
-          for (uint32_t h = 0; h < MH; ++h) {
-            const uint64_t ad = tc::smem_desc_kmajor(abase + h * (A_BYTES / MH) + ks * 2 * (BM / 8) * 128,
+          for (uint32_t h = 0; h < MHT; ++h) {
+            const uint64_t ad = tc::smem_desc_kmajor(abase + h * (kAB / MHT) + ks * 2 * (BM / 8) * 128,
                                                      (BM / 8) * 128, 128);
             p2::mma_f16_ss_2sm(tmem + h * p2::BNP, ad, bd, idesc, (kt | ks) ? 1u : 0u);
           }
@@ -460,8 +465,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kProducers + 32, 1)
       const uint2 nxt = load_bits(kt + 1);
       const uint32_t slot = kt % p2::STAGES, use = kt / p2::STAGES;
       if (use > 0) tc::mbar_wait(&bars->empty[slot], (use - 1) & 1);
-      uint8_t* As = tiles + slot * (A_BYTES + p2::B_BYTES);
-      uint8_t* Bs = As + A_BYTES;
+      uint8_t* As = tiles + slot * (kAB + p2::B_BYTES);
+      uint8_t* Bs = As + kAB;
       const uint32_t fullL = full_leader0 + slot * 8;
       if (tid == 0) {  // this CTA's B half: 8 TMA boxes of 128 tokens, bytes counted at the leader
 #pragma unroll
@@ -476,7 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kProducers + 32, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           pv[i] = 0xBC00BC00u ^ (((byte >> (2 * i)) & 1u) << 15) ^ (((byte >> (2 * i + 1)) & 1u) << 31);
-        *(uint4*)(As + (row / BM) * (A_BYTES / MH) + canon(row % BM, k8, BM)) = v;
+        *(uint4*)(As + (row / BM) * (kAB / MHT) + canon(row % BM, k8, BM)) = v;
       }
       cur = nxt;
       tc::fence_proxy_async_smem();  // generic-proxy writes -> the pair's MMA (async proxy)
@@ -586,13 +591,31 @@ static void launch_stage(nqb_context* ctx, const Args& a, uint32_t grid_m, uint3
   static bool attr2 = false;
   if (use_2sm() && !use_ts()) {
     if (!attr2) {
-      NQB_CUDA(cudaFuncSetAttribute(k_prefill2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    1024 + p2::STAGES * (A_BYTES + p2::B_BYTES)));
+      NQB_CUDA(cudaFuncSetAttribute(k_prefill2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    1024 + p2::STAGES * (2 * BM * BK * 2 + p2::B_BYTES)));
+      NQB_CUDA(cudaFuncSetAttribute(k_prefill2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    1024 + p2::STAGES * (BM * BK * 2 + p2::B_BYTES)));
       attr2 = true;
     }
-    const uint32_t gx = ((grid_m + MH - 1) / MH + 1) / 2 * 2;  // whole CTA pairs
-    k_prefill2<<<dim3(gx, (tokens + p2::BNP - 1) / p2::BNP), kProducers + 32,
-                 1024 + p2::STAGES * (A_BYTES + p2::B_BYTES), ctx->stream>>>(a);
+    // 256 rows per CTA unless 128 fills the SMs clearly better (wave quantisation)
+    const uint32_t ny = (tokens + p2::BNP - 1) / p2::BNP;
+    auto util = [&](uint32_t rows_per_cta) {
+      const uint64_t ctas = (uint64_t)((grid_m * BM + 2 * rows_per_cta - 1) / (2 * rows_per_cta)) * 2 * ny;
+      const uint64_t slots = (uint64_t)ctx->num_sms;
+      return (double)ctas / (double)(((ctas + slots - 1) / slots) * slots);
+    };
+    static const int force = [] { const char* e = std::getenv("NQB_PREFILL_ROWS");  // tests: 128 / 256
+                                  return e ? atoi(e) : 0; }();
+    const bool small = force ? force == BM : util(BM) > util(2 * BM) + 0.15;
+    if (small) {
+      const uint32_t gx = (grid_m + 1) / 2 * 2;
+      k_prefill2<1><<<dim3(gx, ny), BM + 32, 1024 + p2::STAGES * (BM * BK * 2 + p2::B_BYTES),
+                      ctx->stream>>>(a);
+    } else {
+      const uint32_t gx = ((grid_m + MH - 1) / MH + 1) / 2 * 2;  // whole CTA pairs
+      k_prefill2<2><<<dim3(gx, ny), 2 * BM + 32, 1024 + p2::STAGES * (2 * BM * BK * 2 + p2::B_BYTES),
+                      ctx->stream>>>(a);
+    }
   } else if (use_ts())
     k_prefill_ts<<<dim3((grid_m + MH - 1) / MH, (tokens + ts::BN - 1) / ts::BN), kProducers + 32,
                    1024 + ts::STAGES * ts::B_BYTES, ctx->stream>>>(a);
