@@ -46,6 +46,12 @@ struct alignas(64) Args {
   const __half* scale;    // per-row output scale (s1) or null
   __half* out;            // tokens x ldo binary16
   uint32_t ldo;
+  // split-K (k_prefill2 only): CTA z handles K tiles [z*kps, (z+1)*kps) and
+  // writes raw fp32 partials to part[z][token][row] (ldp rows per token); a
+  // fixed-order reduction applies the scale (deterministic).  kps = 0: off.
+  uint32_t kps;
+  float* part;
+  uint32_t ldp;
 };
 
 // byte offset of (row, 8-element K chunk k8 of the 64-wide K tile) in the
@@ -407,6 +413,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
   const uint32_t m0 = blockIdx.x * (MHT * BM);
   const uint32_t np = blockIdx.y * p2::BNP;      // the pair's first token
   const uint32_t n0 = np + rank * p2::BNH;       // this CTA's B half
+  const uint32_t kt0 = a.kps ? blockIdx.z * a.kps : 0;
+  const uint32_t nkl = a.kps ? min(a.nk, kt0 + a.kps) - kt0 : a.nk;  // K tiles of this CTA
 
   if (tid == 0) {
     for (int s = 0; s < p2::STAGES; ++s) {
@@ -432,9 +440,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
   if (warp == kP / 32) {  // ------------------- MMA issuer (leader CTA only)
     if (leader && lane == 0) {
       constexpr uint32_t idesc = tc::idesc_f16(2 * BM, p2::BNP);
-      for (uint32_t kt = 0; kt < a.nk; ++kt) {
-        const uint32_t slot = kt % p2::STAGES;
-        tc::mbar_wait(&bars->full[slot], (kt / p2::STAGES) & 1);
+      for (uint32_t i = 0; i < nkl; ++i) {
+        const uint32_t slot = i % p2::STAGES;
+        tc::mbar_wait(&bars->full[slot], (i / p2::STAGES) & 1);
         tc::fence_after_sync();
         const uint32_t abase = tc::smem_u32(tiles + slot * (kAB + p2::B_BYTES));
         const uint32_t bbase = abase + kAB;
@@ -446,7 +454,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
           for (uint32_t h = 0; h < MHT; ++h) {
             const uint64_t ad = tc::smem_desc_kmajor(abase + h * (kAB / MHT) + ks * 2 * (BM / 8) * 128,
                                                      (BM / 8) * 128, 128);
-            p2::mma_f16_ss_2sm(tmem + h * p2::BNP, ad, bd, idesc, (kt | ks) ? 1u : 0u);
+            p2::mma_f16_ss_2sm(tmem + h * p2::BNP, ad, bd, idesc, (i | ks) ? 1u : 0u);
           }
         }
         p2::commit_pair(&bars->empty[slot]);
@@ -458,12 +466,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
     const bool rv = grow < a.M;
     const uint32_t* brow = a.bits + (size_t)(rv ? grow : 0) * a.wpr;
     auto load_bits = [&](uint32_t kt) -> uint2 {
-      return (rv && kt < a.nk) ? __ldg((const uint2*)(brow + kt * 2)) : make_uint2(0u, 0u);
+      return (rv && kt < kt0 + nkl) ? __ldg((const uint2*)(brow + kt * 2)) : make_uint2(0u, 0u);
     };
-    uint2 cur = load_bits(0);
-    for (uint32_t kt = 0; kt < a.nk; ++kt) {
+    uint2 cur = load_bits(kt0);
+    for (uint32_t i = 0; i < nkl; ++i) {
+      const uint32_t kt = kt0 + i;
       const uint2 nxt = load_bits(kt + 1);
-      const uint32_t slot = kt % p2::STAGES, use = kt / p2::STAGES;
+      const uint32_t slot = i % p2::STAGES, use = i / p2::STAGES;
       if (use > 0) tc::mbar_wait(&bars->empty[slot], (use - 1) & 1);
       uint8_t* As = tiles + slot * (kAB + p2::B_BYTES);
       uint8_t* Bs = As + kAB;
@@ -501,12 +510,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
       tc::tmem_ld_x16(tmem + (row / BM) * p2::BNP + ((uint32_t)((warp & 3) * 32) << 16) + c0, v);
       tc::wait_ld();
       if (grow < a.Mout) {
+        if (a.part) {  // split-K: raw partial sums, reduced (and scaled) in fixed order later
+          float* pz = a.part + (size_t)blockIdx.z * a.N * a.ldp;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const uint32_t tok = np + c0 + j;
-          if (tok < a.N)
-            a.out[(size_t)tok * a.ldo + grow] =
-                __float2half_rn(keep ? sc * __uint_as_float(v[j]) : 0.f);
+          for (int j = 0; j < 16; ++j) {
+            const uint32_t tok = np + c0 + j;
+            if (tok < a.N) pz[(size_t)tok * a.ldp + grow] = __uint_as_float(v[j]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const uint32_t tok = np + c0 + j;
+            if (tok < a.N)
+              a.out[(size_t)tok * a.ldo + grow] =
+                  __float2half_rn(keep ? sc * __uint_as_float(v[j]) : 0.f);
+          }
         }
       }
     }
@@ -515,6 +533,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
   p2::cluster_sync();  // both CTAs are done with the pair's TMEM
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+}
+
+// Split-K reduction: out[tok][row] = fp16(scale_row * sum_z part[z][tok][row])
+// in fixed z order; rows >= Mvalid are written as 0.
+__global__ void k_splitk_reduce(const float* __restrict__ part, uint32_t splits, uint32_t N,
+                                uint32_t rows, uint32_t ldp, uint32_t Mvalid,
+                                const __half* __restrict__ scale, __half* __restrict__ out,
+                                uint32_t ldo) {
+  const uint64_t total = (uint64_t)N * rows;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t tok = (uint32_t)(e / rows), row = (uint32_t)(e % rows);
+    float acc = 0.f;
+    for (uint32_t z = 0; z < splits; ++z) acc += part[((size_t)z * N + tok) * ldp + row];
+    const float sc = (scale && row < Mvalid) ? __half2float(scale[row]) : 1.f;
+    out[(size_t)tok * ldo + row] = __float2half_rn(row < Mvalid ? sc * acc : 0.f);
+  }
 }
 
 // X (b x m, binary16, token-major) -> s2 .* X with K padded to kpad (zeros).
@@ -579,7 +614,8 @@ static bool use_ts() {
   return ts;
 }
 
-static void launch_stage(nqb_context* ctx, const Args& a, uint32_t grid_m, uint32_t tokens) {
+static void launch_stage(nqb_context* ctx, const Args& a_in, uint32_t grid_m, uint32_t tokens) {
+  Args a = a_in;
   static bool attr = false;
   if (!attr) {
     NQB_CUDA(cudaFuncSetAttribute(k_prefill, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -607,14 +643,40 @@ static void launch_stage(nqb_context* ctx, const Args& a, uint32_t grid_m, uint3
     static const int force = [] { const char* e = std::getenv("NQB_PREFILL_ROWS");  // tests: 128 / 256
                                   return e ? atoi(e) : 0; }();
     const bool small = force ? force == BM : util(BM) > util(2 * BM) + 0.15;
-    if (small) {
-      const uint32_t gx = (grid_m + 1) / 2 * 2;
-      k_prefill2<1><<<dim3(gx, ny), BM + 32, 1024 + p2::STAGES * (BM * BK * 2 + p2::B_BYTES),
+    const uint32_t rows_cta = small ? BM : 2 * BM;
+    const uint32_t gx = small ? (grid_m + 1) / 2 * 2 : ((grid_m + MH - 1) / MH + 1) / 2 * 2;
+    // split-K when one pass leaves SMs idle (short M, long K): fixed-order reduction after
+    static const int force_split = [] { const char* e = std::getenv("NQB_PREFILL_SPLITK");
+                                        return e ? atoi(e) : 0; }();
+    uint32_t splits = 1;
+    {
+      const uint64_t ctas = (uint64_t)gx * ny, sm = (uint64_t)ctx->num_sms;
+      auto u = [&](uint64_t c) { return (double)c / (double)(((c + sm - 1) / sm) * sm); };
+      // Opt-in only (NQB_PREFILL_SPLITK=s): a cost model (MMA time / wave
+      // utilisation + the partials' HBM round trip) picking s = 2..8 measured
+      // slower on the 70B shapes (down 912 -> 881 TFLOP/s), so the default is 1.
+      if (force_split > 0) splits = (uint32_t)force_split;
+      (void)u;
+      splits = std::max(1u, std::min(splits, a.nk));
+    }
+    if (splits > 1) {
+      a.kps = (a.nk + splits - 1) / splits;
+      splits = (a.nk + a.kps - 1) / a.kps;
+      a.ldp = a.Mout;
+      a.part = (float*)scratch(ctx, 10, sizeof(float) * (size_t)splits * a.N * a.ldp);
+    }
+    const dim3 grid(gx, ny, splits);
+    if (small)
+      k_prefill2<1><<<grid, BM + 32, 1024 + p2::STAGES * (BM * BK * 2 + p2::B_BYTES), ctx->stream>>>(a);
+    else
+      k_prefill2<2><<<grid, 2 * BM + 32, 1024 + p2::STAGES * (2 * BM * BK * 2 + p2::B_BYTES),
                       ctx->stream>>>(a);
-    } else {
-      const uint32_t gx = ((grid_m + MH - 1) / MH + 1) / 2 * 2;  // whole CTA pairs
-      k_prefill2<2><<<dim3(gx, ny), 2 * BM + 32, 1024 + p2::STAGES * (2 * BM * BK * 2 + p2::B_BYTES),
-                      ctx->stream>>>(a);
+    (void)rows_cta;
+    if (splits > 1) {
+      NQB_LAUNCHED(ctx);
+      const uint64_t tot = (uint64_t)a.N * a.Mout;
+      k_splitk_reduce<<<(uint32_t)std::min<uint64_t>((tot + 255) / 256, 148 * 16), 256, 0, ctx->stream>>>(
+          a.part, splits, a.N, a.Mout, a.ldp, a.Mvalid, a.scale, a.out, a.ldo);
     }
   } else if (use_ts())
     k_prefill_ts<<<dim3((grid_m + MH - 1) / MH, (tokens + ts::BN - 1) / ts::BN), kProducers + 32,

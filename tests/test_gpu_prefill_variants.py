@@ -2,7 +2,7 @@
 
 Kernel selection is read from the environment once per process, so each variant
 runs the prefill parity tests of test_gpu_forward.py in a subprocess:
-* CTA pair (`cta_group::2`) with 128 and with 256 rows per CTA;
+* CTA pair (`cta_group::2`) with 128 and with 256 rows per CTA, with and without split-K;
 * the single-CTA SS kernel;
 * the A-in-TMEM (TS) kernel."""
 import os
@@ -16,8 +16,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{"NQB_PREFILL_ROWS": "128"}, {"NQB_PREFILL_ROWS": "256"},
+                                 {"NQB_PREFILL_SPLITK": "3"},
+                                 {"NQB_PREFILL_ROWS": "128", "NQB_PREFILL_SPLITK": "2"},
                                  {"NQB_PREFILL_2SM": "0"}, {"NQB_PREFILL_2SM": "0", "NQB_PREFILL_TS": "1"}],
-                         ids=["pair128", "pair256", "ss", "ts"])
+                         ids=["pair128", "pair256", "pair_splitk3", "pair128_splitk2", "ss", "ts"])
 def test_prefill_variant_parity(env):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_forward.py"), "-k", "prefill or gemm"],
