@@ -645,20 +645,14 @@ static void launch_stage(nqb_context* ctx, const Args& a_in, uint32_t grid_m, ui
     const bool small = force ? force == BM : util(BM) > util(2 * BM) + 0.15;
     const uint32_t rows_cta = small ? BM : 2 * BM;
     const uint32_t gx = small ? (grid_m + 1) / 2 * 2 : ((grid_m + MH - 1) / MH + 1) / 2 * 2;
-    // split-K when one pass leaves SMs idle (short M, long K): fixed-order reduction after
+    // Split-K (fixed-order reduction after) is opt-in, NQB_PREFILL_SPLITK=s: a
+    // cost model (MMA time / wave utilisation + the partials' HBM round trip)
+    // picking s = 2..8 measured slower on the 70B shapes (down 912 -> 881
+    // TFLOP/s), so the default is one pass.
     static const int force_split = [] { const char* e = std::getenv("NQB_PREFILL_SPLITK");
                                         return e ? atoi(e) : 0; }();
-    uint32_t splits = 1;
-    {
-      const uint64_t ctas = (uint64_t)gx * ny, sm = (uint64_t)ctx->num_sms;
-      auto u = [&](uint64_t c) { return (double)c / (double)(((c + sm - 1) / sm) * sm); };
-      // Opt-in only (NQB_PREFILL_SPLITK=s): a cost model (MMA time / wave
-      // utilisation + the partials' HBM round trip) picking s = 2..8 measured
-      // slower on the 70B shapes (down 912 -> 881 TFLOP/s), so the default is 1.
-      if (force_split > 0) splits = (uint32_t)force_split;
-      (void)u;
-      splits = std::max(1u, std::min(splits, a.nk));
-    }
+    const uint32_t splits0 = force_split > 0 ? std::min<uint32_t>((uint32_t)force_split, a.nk) : 1u;
+    uint32_t splits = std::max(1u, splits0);
     if (splits > 1) {
       a.kps = (a.nk + splits - 1) / splits;
       splits = (a.nk + a.kps - 1) / a.kps;
