@@ -4,8 +4,9 @@ Every matrix's initialisation depends only on its own weight when the
 preconditioner is the identity (pipeline.cpp:95-110), so a model is sharded by
 matrix: one process per GPU, matrices assigned by LPT (longest processing time
 first) on the cost model below, each rank runs `nqb_factorize_layer` on its own
-matrices, and ONE gather moves the packed factors (u32 sign words + binary16
-scales + per-matrix metrics) to rank 0.  There is no other collective on the
+matrices, and ONE collective moves the packed factors (u32 sign words +
+binary16 scales + per-matrix metrics) to rank 0 (an all-gather, which every
+backend supports; rank 0 keeps the result).  There is no other collective on the
 data path.  With `torch.distributed` over NCCL the gather crosses NVLink; the
 same code runs over gloo for the CPU tests.
 
@@ -213,7 +214,7 @@ def sharded_init(specs: Sequence[MatrixSpec], bpw: float,
                  group=None, device=None, workers: int = 1) -> Optional[InitReport]:
     """Runs on every rank of `group` (torch.distributed); returns the full
     report on rank 0 and None elsewhere.  One all-gather of shard sizes and one
-    gather of the padded byte shards are the only collectives."""
+    all-gather of the padded byte shards are the only collectives."""
     import time
 
     import torch
@@ -236,9 +237,10 @@ def sharded_init(specs: Sequence[MatrixSpec], bpw: float,
     maxlen = int(max(s[0].item() for s in sizes))
     buf = torch.zeros(maxlen, dtype=torch.uint8, device=dev)
     buf[:blob.size] = torch.from_numpy(blob).to(dev)
-    gathered = [torch.zeros(maxlen, dtype=torch.uint8, device=dev) for _ in range(world)] \
-        if rank == 0 else None
-    dist.gather(buf, gathered, dst=0, group=group)
+    # all_gather rather than gather: supported by every backend (NCCL and gloo);
+    # the shards are a few MB of packed factors per matrix
+    gathered = [torch.zeros(maxlen, dtype=torch.uint8, device=dev) for _ in range(world)]
+    dist.all_gather(gathered, buf, group=group)
     if rank != 0:
         return None
     rep = InitReport(assignment=assign)
