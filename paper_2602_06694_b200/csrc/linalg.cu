@@ -632,13 +632,36 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     // ---- phase C (every block, identical): sigma, normalise, stop rule ------
     // G partials: one (independent) load per thread, then the fixed block tree
     // (identical in every block) instead of G dependent L2 round trips.
+    // w is loaded before the two norms are reduced (its L2 latency overlaps the
+    // reductions); both norms share one pair of barriers (same summation order
+    // as block_sum).
+    double wx[kKeep ? CPT : 1];
+    if constexpr (kKeep) {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const uint32_t j = tid + c * PI_THREADS;
+        wx[c] = j < a.cols ? __ldcg(a.w + j) : 0.0;
+      }
+    }
     double s2 = 0.0, w2 = 0.0;
     for (uint32_t b = tid; b < G; b += PI_THREADS) {
       s2 += __ldcg(ssp + b);
       w2 += __ldcg(a.wsspart + b);
     }
-    s2 = block_sum(s2, bred);
-    w2 = block_sum(w2, bred);
+    s2 = warp_sum(s2);
+    w2 = warp_sum(w2);
+    __syncthreads();
+    if (lane == 0) {  // cred: phase B is done with it, the next use is after a barrier
+      cred[warp][0] = s2;
+      cred[warp][1] = w2;
+    }
+    __syncthreads();
+    s2 = 0.0;
+    w2 = 0.0;
+    for (int w = 0; w < PI_THREADS / 32; ++w) {
+      s2 += cred[w][0];
+      w2 += cred[w][1];
+    }
     sigma = sqrt(s2);
     if (sigma == 0.0) break;  // linalg.cpp:111
     const double wn = sqrt(w2);
@@ -646,7 +669,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     for (int c = 0; c < CPT; ++c) {
       const uint32_t j = tid + c * PI_THREADS;
       if (j < a.cols) {
-        const double x = __ldcg(a.w + j);
+        const double x = kKeep ? wx[c] : __ldcg(a.w + j);
         vr[c] = wn > 0.0 ? x / wn : x;
       }
     }
