@@ -620,8 +620,12 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
       }
       __syncthreads();
     }
-    wq = block_sum(wq, bred);
-    if (tid == 0) a.wsspart[bid] = wq;
+    // only warp 0 holds column sums: its warp tree equals block_sum here
+    // (the other warps would add exact zeros), without two block barriers
+    if (warp == 0) {
+      wq = warp_sum(wq);
+      if (lane == 0) a.wsspart[bid] = wq;
+    }
     grid_sync(a.bar, G, gsk);
     long long t2 = a.prof ? clock64() : 0;
     if (a.prof) {
