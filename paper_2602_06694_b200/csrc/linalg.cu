@@ -432,11 +432,15 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
   uint32_t pending = 0;  // rows of the NEXT pass already issued (prefetched)
   const uint32_t keep = a.keep_den ? (uint32_t)((uint64_t)nrows * a.keep_num / a.keep_den) : 0;
   const uint64_t pol_keep = tc::policy_evict_last(), pol_stream = tc::policy_evict_first();
-  auto issue = [&](uint32_t i) {  // row r0+i -> slot i % nslots (thread 0)
+  // rows r0+i and r0+i+1 (i even) -> slots i % nslots and the next one (nslots
+  // is even, so they are adjacent) in ONE bulk copy signalling fullb[i % nslots]:
+  // half the copy issues on thread 0, which every step waits for
+  auto issue = [&](uint32_t i) {
     uint64_t* bar = &fullb[i % nslots];
-    tc::mbar_arrive_expect_tx(bar, row_bytes);
+    const uint32_t bytes = (i + 1 < nrows ? 2u : 1u) * row_bytes;
+    tc::mbar_arrive_expect_tx(bar, bytes);
     tc::bulk_g2s_hint(ring + (size_t)(i % nslots) * row_bytes, a.M + (uint64_t)(r0 + i) * a.cols,
-                      row_bytes, bar, i < keep ? pol_keep : pol_stream);
+                      bytes, bar, i < keep ? pol_keep : pol_stream);
   };
   const uint32_t head = nrows < nslots ? nrows : nslots;
   double sigma = 0.0, sigma_prev = -1.0;
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     // two rows per block reduction.  The first `head` rows of this pass were
     // prefetched at the end of the previous pass (rows do not change).
     if (tid == 0 && !pending)
-      for (uint32_t i = 0; i < head; ++i) issue(i);
+      for (uint32_t i = 0; i < head; i += 2) issue(i);
     pending = 0;
     double wl[CPT];
 #pragma unroll
@@ -457,14 +461,10 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     uint32_t par = 0;  // cred2 buffer of this step
     for (uint32_t i = 0; i < nrows; i += 2) {
       const bool two = i + 1 < nrows && nslots >= 2;
-      const uint32_t s0 = i % nslots, s1 = (i + 1) % nslots;
+      const uint32_t s0 = i % nslots, s1 = s0 + 1;  // adjacent slots (nslots even)
       long long pw0 = a.prof ? clock64() : 0;
-      tc::mbar_wait(&fullb[s0], (phase >> s0) & 1u);
+      tc::mbar_wait(&fullb[s0], (phase >> s0) & 1u);  // both rows of the step
       phase ^= 1u << s0;
-      if (two) {
-        tc::mbar_wait(&fullb[s1], (phase >> s1) & 1u);
-        phase ^= 1u << s1;
-      }
       long long pw1 = a.prof ? clock64() : 0;
       if (a.prof) tW += pw1 - pw0;
       const double* x0 = (const double*)(ring + (size_t)s0 * row_bytes);
@@ -517,7 +517,6 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
         if (tid == 0) {
           const uint32_t nx = i + nslots;
           if (nx < nrows) issue(nx);
-          if (two && nx + 1 < nrows) issue(nx + 1);
         }
       }
       // cross-warp sums: lane w < warps holds warp w's partial, one xor tree
@@ -561,7 +560,6 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
         if (tid == 0) {
           const uint32_t nx = i + nslots;  // refill the freed slots
           if (nx < nrows) issue(nx);
-          if (two && nx + 1 < nrows) issue(nx + 1);
         }
       }
       if (a.prof) {
@@ -577,7 +575,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     // reductions and grid barriers below run (drained before exit)
     if (it + 1 < a.max_iters) {
       if (tid == 0)
-        for (uint32_t i = 0; i < head; ++i) issue(i);
+        for (uint32_t i = 0; i < head; i += 2) issue(i);
       pending = 1;
     }
 #pragma unroll
@@ -698,7 +696,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
   }
 
   if (pending) {  // an early exit left the next pass's prefetch in flight: drain it
-    for (uint32_t i = 0; i < head; ++i) {
+    for (uint32_t i = 0; i < head; i += 2) {
       tc::mbar_wait(&fullb[i % nslots], (phase >> (i % nslots)) & 1u);
       phase ^= 1u << (i % nslots);
     }
@@ -751,6 +749,7 @@ template <int CPT>
 static void launch_power_stream(nqb_context* ctx, PowerArgs& a, uint32_t grid) {
   const uint32_t row_bytes = a.cols * 8;  // cols even: 16-byte multiple, 16-byte aligned rows
   uint32_t nslots = (uint32_t)std::min<size_t>(PS_MAX_SLOTS, (200 * 1024) / row_bytes);
+  nslots &= ~1u;  // row pairs share one copy and one barrier (>= 2: dispatch condition)
   const size_t smem = (size_t)nslots * row_bytes;
   auto kern = k_power_stream<CPT>;
   NQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
