@@ -514,7 +514,9 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
       if constexpr (kKeep) {
         // the rows are in registers now: refill their slots right away (the
         // copies overlap the axpy; one barrier per step, cred double-buffered)
-        if (tid == 0) {
+        // the issuing lane rotates over the warps: a bulk-copy issue costs its
+        // warp several hundred cycles, and the next barrier waits for that warp
+        if (tid == (uint32_t)(32 * ((i >> 1) % (PI_THREADS / 32)))) {
           const uint32_t nx = i + nslots;
           if (nx < nrows) issue(nx);
         }
