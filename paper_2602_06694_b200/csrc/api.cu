@@ -506,9 +506,24 @@ int nqb_gemv_f32_host(nqb_context* ctx, const nqb_layer* L, const float* x, floa
     NQB_CUDA(cudaMalloc(&ML->hp_buf, 4 * ((size_t)round_up(L->m, 4) + L->n)));
   float* dx = ML->hp_buf;
   float* dy = dx + round_up(L->m, 4);
+  // A pinned (page-locked, mapped) y is written by the kernel directly over the
+  // host link: no separate device-to-host copy.  Pageable y goes through dy.
+  if (ML->hp_y_host != y) {
+    cudaPointerAttributes at{};
+    ML->hp_y_dev = nullptr;
+    if (cudaPointerGetAttributes(&at, y) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+        at.devicePointer)
+      ML->hp_y_dev = (float*)at.devicePointer;
+    cudaGetLastError();
+    ML->hp_y_host = y;
+  }
   NQB_CUDA(cudaMemcpyAsync(dx, x, 4 * (size_t)L->m, cudaMemcpyHostToDevice, ctx->stream));
-  decode_gemv_f32(ctx, L, dx, dy);
-  NQB_CUDA(cudaMemcpyAsync(y, dy, 4 * (size_t)L->n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (ML->hp_y_dev) {
+    decode_gemv_f32(ctx, L, dx, ML->hp_y_dev);
+  } else {
+    decode_gemv_f32(ctx, L, dx, dy);
+    NQB_CUDA(cudaMemcpyAsync(y, dy, 4 * (size_t)L->n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
   NQB_CUDA(cudaStreamSynchronize(ctx->stream));
   API_END
 }

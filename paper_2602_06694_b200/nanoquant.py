@@ -385,7 +385,9 @@ class DeviceLayer:
     def gemv_f32(self, x, out: Optional[np.ndarray] = None) -> np.ndarray:
         """gemv_packed_f32 (packed.cpp:201-204).  `out` (contiguous float32, n) is
         written in place when given, e.g. a pinned buffer."""
-        x = np.ascontiguousarray(x, dtype=np.float32)
+        # per-token path: keep the Python side thin (raw addresses, cached entry point)
+        if type(x) is not np.ndarray or x.dtype != np.float32 or not x.flags.c_contiguous:
+            x = np.ascontiguousarray(x, dtype=np.float32)
         if x.size != self.m:
             raise DimensionMismatch("gemv_packed: |x| != m")
         if out is None:
@@ -394,8 +396,9 @@ class DeviceLayer:
             if out.dtype != np.float32 or out.size != self.n or not out.flags.c_contiguous:
                 raise DimensionMismatch("gemv_packed: out must be contiguous float32 of size n")
             y = out
-        _check(self.ctx.lib.nqb_gemv_f32_host(self.ctx.handle, self.handle, _ptr(x), _ptr(y)),
-               "gemv_packed_f32")
+        st = self.ctx.lib.nqb_gemv_f32_host(self.ctx.handle, self.handle, x.ctypes.data, y.ctypes.data)
+        if st:
+            _check(st, "gemv_packed_f32")
         return y
 
     def gemv_f64(self, x) -> np.ndarray:
