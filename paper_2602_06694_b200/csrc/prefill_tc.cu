@@ -334,10 +334,7 @@ __global__ void __launch_bounds__(kProducers + 32, 1) k_prefill_ts(const __grid_
 //     warp's A rows are written) + the transaction bytes of both B halves;
 //   empty[s], dready (both CTAs): one multicast commit from the leader.
 namespace p2 {
-constexpr int BNP = 256;                 // tokens per pair
-constexpr int BNH = BNP / 2;             // tokens per CTA (B half)
-constexpr int STAGES = 4;
-constexpr int B_BYTES = BNH * BK * 2;    // 16 KB
+constexpr int STAGES = 4;               // (tile sizes: template parameters of k_prefill2)
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the rank-0 CTA
 
 struct __align__(8) Bars {
@@ -398,11 +395,16 @@ __device__ __forceinline__ void commit_pair(uint64_t* bar) {
 
 // MHT: 128-row halves per CTA (2: 256 rows share each B tile; 1: more CTAs for
 // short M, e.g. stage 1 of the 70B q shape).
-template <int MHT>
+// BNPT: tokens per pair (256, or 208 = 13 x 16 when that fills the SMs
+// better; each CTA holds BNPT/2 of them).
+template <int MHT, int BNPT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
     k_prefill2(const __grid_constant__ Args a) {
   constexpr int kP = MHT * BM;               // producer threads (one per A row)
   constexpr int kAB = MHT * BM * BK * 2;     // A bytes per stage
+  constexpr int kBNH = BNPT / 2;             // tokens of this CTA's B half
+  constexpr int kBB = kBNH * BK * 2;         // B-half bytes per stage
+  static_assert(BNPT % 16 == 0 && BNPT <= 256 && kBNH % 8 == 0, "pair N tile");
   extern __shared__ __align__(1024) uint8_t smem[];
   p2::Bars* bars = (p2::Bars*)smem;
   uint8_t* tiles = smem + 1024;  // p2::STAGES x [A 32 KB | B half 16 KB]
@@ -411,8 +413,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
   const uint32_t rank = p2::cluster_rank();
   const bool leader = rank == 0;
   const uint32_t m0 = blockIdx.x * (MHT * BM);
-  const uint32_t np = blockIdx.y * p2::BNP;      // the pair's first token
-  const uint32_t n0 = np + rank * p2::BNH;       // this CTA's B half
+  const uint32_t np = blockIdx.y * BNPT;      // the pair's first token
+  const uint32_t n0 = np + rank * kBNH;       // this CTA's B half
   const uint32_t kt0 = a.kps ? blockIdx.z * a.kps : 0;
   const uint32_t nkl = a.kps ? min(a.nk, kt0 + a.kps) - kt0 : a.nk;  // K tiles of this CTA
 
@@ -439,22 +441,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
 
   if (warp == kP / 32) {  // ------------------- MMA issuer (leader CTA only)
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_f16(2 * BM, p2::BNP);
+      constexpr uint32_t idesc = tc::idesc_f16(2 * BM, BNPT);
       for (uint32_t i = 0; i < nkl; ++i) {
         const uint32_t slot = i % p2::STAGES;
         tc::mbar_wait(&bars->full[slot], (i / p2::STAGES) & 1);
         tc::fence_after_sync();
-        const uint32_t abase = tc::smem_u32(tiles + slot * (kAB + p2::B_BYTES));
+        const uint32_t abase = tc::smem_u32(tiles + slot * (kAB + kBB));
         const uint32_t bbase = abase + kAB;
 #pragma unroll
         for (uint32_t ks = 0; ks < BK / 16; ++ks) {
           const uint64_t bd =
-              tc::smem_desc_kmajor(bbase + ks * 2 * (p2::BNH / 8) * 128, (p2::BNH / 8) * 128, 128);
+              tc::smem_desc_kmajor(bbase + ks * 2 * (kBNH / 8) * 128, (kBNH / 8) * 128, 128);
 #pragma unroll
           for (uint32_t h = 0; h < MHT; ++h) {
             const uint64_t ad = tc::smem_desc_kmajor(abase + h * (kAB / MHT) + ks * 2 * (BM / 8) * 128,
                                                      (BM / 8) * 128, 128);
-            p2::mma_f16_ss_2sm(tmem + h * p2::BNP, ad, bd, idesc, (i | ks) ? 1u : 0u);
+            p2::mma_f16_ss_2sm(tmem + h * BNPT, ad, bd, idesc, (i | ks) ? 1u : 0u);
           }
         }
         p2::commit_pair(&bars->empty[slot]);
@@ -474,13 +476,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
       const uint2 nxt = load_bits(kt + 1);
       const uint32_t slot = i % p2::STAGES, use = i / p2::STAGES;
       if (use > 0) tc::mbar_wait(&bars->empty[slot], (use - 1) & 1);
-      uint8_t* As = tiles + slot * (kAB + p2::B_BYTES);
+      uint8_t* As = tiles + slot * (kAB + kBB);
       uint8_t* Bs = As + kAB;
       const uint32_t fullL = full_leader0 + slot * 8;
       if (tid == 0) {  // this CTA's B half: 8 TMA boxes of 128 tokens, bytes counted at the leader
 #pragma unroll
         for (uint32_t k8 = 0; k8 < BK / 8; ++k8)
-          p2::tma_b_2sm(Bs + canon(0, k8, p2::BNH), &a.bmap, kt * BK + k8 * 8, n0, fullL);
+          p2::tma_b_2sm(Bs + canon(0, k8, kBNH), &a.bmap, kt * BK + k8 * 8, n0, fullL);
       }
 #pragma unroll
       for (uint32_t k8 = 0; k8 < 8; ++k8) {
@@ -496,7 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
       tc::fence_proxy_async_smem();  // generic-proxy writes -> the pair's MMA (async proxy)
       __syncwarp();                  // the warp's rows are written; lane 0 arrives
       if (lane == 0) {
-        if (leader && tid == 0) p2::arrive_leader_expect_tx(fullL, 2 * p2::B_BYTES);
+        if (leader && tid == 0) p2::arrive_leader_expect_tx(fullL, 2 * kBB);
         else p2::arrive_leader(fullL);
       }
     }
@@ -505,9 +507,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
     tc::fence_after_sync();
     const float sc = (grow < a.Mvalid && a.scale) ? __half2float(a.scale[grow]) : 1.f;
     const bool keep = grow < a.Mvalid;
-    for (uint32_t c0 = 0; c0 < p2::BNP; c0 += 16) {
+    for (uint32_t c0 = 0; c0 < BNPT; c0 += 16) {
       uint32_t v[16];
-      tc::tmem_ld_x16(tmem + (row / BM) * p2::BNP + ((uint32_t)((warp & 3) * 32) << 16) + c0, v);
+      tc::tmem_ld_x16(tmem + (row / BM) * BNPT + ((uint32_t)((warp & 3) * 32) << 16) + c0, v);
       tc::wait_ld();
       if (grow < a.Mout) {
         if (a.part) {  // split-K: raw partial sums, reduced (and scaled) in fixed order later
@@ -614,7 +616,58 @@ static bool use_ts() {
   return ts;
 }
 
-static void launch_stage(nqb_context* ctx, const Args& a_in, uint32_t grid_m, uint32_t tokens) {
+struct PairCfg {
+  uint32_t mht, bnp;
+};
+
+// CTA-pair tiling: rows per CTA (128 x mht) and tokens per pair (bnp).  The
+// large tile (256 rows, 256 tokens) has the most operand reuse; a smaller one
+// is used only when the large grid is under two waves and leaves clearly more
+// SMs idle (measured: on multi-wave grids the large tile wins regardless).
+static PairCfg choose_pair(nqb_context* ctx, uint32_t rows, uint32_t tokens) {
+  static const int force_rows = [] { const char* e = std::getenv("NQB_PREFILL_ROWS");  // 128 / 256
+                                     return e ? atoi(e) : 0; }();
+  static const int force_n = [] { const char* e = std::getenv("NQB_PREFILL_N");  // 256 / 208
+                                  return e ? atoi(e) : 0; }();
+  const PairCfg cands[4] = {{2, 256}, {2, 208}, {1, 256}, {1, 208}};
+  const uint64_t sm = (uint64_t)ctx->num_sms;
+  auto ctas_of = [&](const PairCfg& c) {
+    const uint64_t pairs = (rows + 2 * BM * c.mht - 1) / (2 * BM * c.mht);
+    return pairs * 2 * ((tokens + c.bnp - 1) / c.bnp);
+  };
+  auto util_of = [&](uint64_t ctas) {
+    return (double)ctas / (double)(((ctas + sm - 1) / sm) * sm);
+  };
+  if (force_rows || force_n) {
+    for (const PairCfg& c : cands)
+      if ((!force_rows || (int)(c.mht * BM) == force_rows) && (!force_n || (int)c.bnp == force_n))
+        return c;
+  }
+  PairCfg pick = cands[0];
+  const uint64_t base = ctas_of(pick);
+  if (base >= 2 * sm) return pick;
+  double best = util_of(base) + 0.1;
+  for (const PairCfg& c : cands) {
+    const double u = util_of(ctas_of(c));
+    if (u > best) best = u, pick = c;
+  }
+  return pick;
+}
+
+template <int MHT, int BNPT>
+static void launch_pair(nqb_context* ctx, const Args& a, dim3 grid) {
+  constexpr int smem = 1024 + p2::STAGES * (MHT * BM * BK * 2 + (BNPT / 2) * BK * 2);
+  static bool attr = false;
+  if (!attr) {
+    NQB_CUDA(cudaFuncSetAttribute(k_prefill2<MHT, BNPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem));
+    attr = true;
+  }
+  k_prefill2<MHT, BNPT><<<grid, MHT * BM + 32, smem, ctx->stream>>>(a);
+}
+
+static void launch_stage(nqb_context* ctx, const Args& a_in, uint32_t grid_m, uint32_t tokens,
+                         PairCfg pc) {
   Args a = a_in;
   static bool attr = false;
   if (!attr) {
@@ -624,35 +677,15 @@ static void launch_stage(nqb_context* ctx, const Args& a_in, uint32_t grid_m, ui
                                   1024 + ts::STAGES * ts::B_BYTES));
     attr = true;
   }
-  static bool attr2 = false;
   if (use_2sm() && !use_ts()) {
-    if (!attr2) {
-      NQB_CUDA(cudaFuncSetAttribute(k_prefill2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    1024 + p2::STAGES * (2 * BM * BK * 2 + p2::B_BYTES)));
-      NQB_CUDA(cudaFuncSetAttribute(k_prefill2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    1024 + p2::STAGES * (BM * BK * 2 + p2::B_BYTES)));
-      attr2 = true;
-    }
-    // 256 rows per CTA unless 128 fills the SMs clearly better (wave quantisation)
-    const uint32_t ny = (tokens + p2::BNP - 1) / p2::BNP;
-    auto util = [&](uint32_t rows_per_cta) {
-      const uint64_t ctas = (uint64_t)((grid_m * BM + 2 * rows_per_cta - 1) / (2 * rows_per_cta)) * 2 * ny;
-      const uint64_t slots = (uint64_t)ctx->num_sms;
-      return (double)ctas / (double)(((ctas + slots - 1) / slots) * slots);
-    };
-    static const int force = [] { const char* e = std::getenv("NQB_PREFILL_ROWS");  // tests: 128 / 256
-                                  return e ? atoi(e) : 0; }();
-    const bool small = force ? force == BM : util(BM) > util(2 * BM) + 0.15;
-    const uint32_t rows_cta = small ? BM : 2 * BM;
-    const uint32_t gx = small ? (grid_m + 1) / 2 * 2 : ((grid_m + MH - 1) / MH + 1) / 2 * 2;
+    const uint32_t ny = (tokens + pc.bnp - 1) / pc.bnp;
+    const uint32_t gx = (grid_m + 2 * pc.mht - 1) / (2 * pc.mht) * 2;  // whole CTA pairs
     // Split-K (fixed-order reduction after) is opt-in, NQB_PREFILL_SPLITK=s: a
     // cost model (MMA time / wave utilisation + the partials' HBM round trip)
-    // picking s = 2..8 measured slower on the 70B shapes (down 912 -> 881
-    // TFLOP/s), so the default is one pass.
+    // picking s = 2..8 measured slower on the 70B shapes, so the default is one pass.
     static const int force_split = [] { const char* e = std::getenv("NQB_PREFILL_SPLITK");
                                         return e ? atoi(e) : 0; }();
-    const uint32_t splits0 = force_split > 0 ? std::min<uint32_t>((uint32_t)force_split, a.nk) : 1u;
-    uint32_t splits = std::max(1u, splits0);
+    uint32_t splits = force_split > 0 ? std::min<uint32_t>((uint32_t)force_split, a.nk) : 1u;
     if (splits > 1) {
       a.kps = (a.nk + splits - 1) / splits;
       splits = (a.nk + a.kps - 1) / a.kps;
@@ -660,12 +693,10 @@ static void launch_stage(nqb_context* ctx, const Args& a_in, uint32_t grid_m, ui
       a.part = (float*)scratch(ctx, 10, sizeof(float) * (size_t)splits * a.N * a.ldp);
     }
     const dim3 grid(gx, ny, splits);
-    if (small)
-      k_prefill2<1><<<grid, BM + 32, 1024 + p2::STAGES * (BM * BK * 2 + p2::B_BYTES), ctx->stream>>>(a);
-    else
-      k_prefill2<2><<<grid, 2 * BM + 32, 1024 + p2::STAGES * (2 * BM * BK * 2 + p2::B_BYTES),
-                      ctx->stream>>>(a);
-    (void)rows_cta;
+    if (pc.mht == 2 && pc.bnp == 256) launch_pair<2, 256>(ctx, a, grid);
+    else if (pc.mht == 2) launch_pair<2, 208>(ctx, a, grid);
+    else if (pc.bnp == 256) launch_pair<1, 256>(ctx, a, grid);
+    else launch_pair<1, 208>(ctx, a, grid);
     if (splits > 1) {
       NQB_LAUNCHED(ctx);
       const uint64_t tot = (uint64_t)a.N * a.Mout;
@@ -693,15 +724,19 @@ void prefill_gemm_tc(nqb_context* ctx, const nqb_layer* L, const __half* d_x, ui
   pf::k_prescale<<<(uint32_t)std::min<uint64_t>((tot + 255) / 256, 148 * 16), 256, 0, ctx->stream>>>(
       d_x, L->s2h, L->m, b, mpad, xs);
   NQB_LAUNCHED(ctx);
+  auto box_of = [&](const PairCfg& pc) -> uint32_t {
+    return use_ts() ? (uint32_t)ts::BN : use_2sm() ? pc.bnp / 2 : (uint32_t)BN;
+  };
   // stage 1: T^T[token][k] = sum_j sign(V[j][k]) * xs[token][j]   (rows k < r, padded rows 0)
   Args a1{{}, L->vt, L->vt_words, L->r, L->r, rpad, mpad / BK, xs, mpad, b, nullptr, tt, rpad};
-  const uint32_t box = use_ts() ? (uint32_t)ts::BN : use_2sm() ? (uint32_t)p2::BNH : (uint32_t)BN;
-  make_bmap(&a1.bmap, xs, mpad, mpad, b, box);
-  launch_stage(ctx, a1, (rpad + BM - 1) / BM, b);
+  const PairCfg p1 = choose_pair(ctx, rpad, b);
+  make_bmap(&a1.bmap, xs, mpad, mpad, b, box_of(p1));
+  launch_stage(ctx, a1, (rpad + BM - 1) / BM, b, p1);
   // stage 2: Y[token][i] = s1_i * sum_k sign(U[i][k]) * T^T[token][k]
   Args a2{{}, L->u, L->u_words, L->n, L->n, L->n, rpad / BK, tt, rpad, b, L->s1h, d_y, L->n};
-  make_bmap(&a2.bmap, tt, rpad, rpad, b, box);
-  launch_stage(ctx, a2, (L->n + BM - 1) / BM, b);
+  const PairCfg p2c = choose_pair(ctx, L->n, b);
+  make_bmap(&a2.bmap, tt, rpad, rpad, b, box_of(p2c));
+  launch_stage(ctx, a2, (L->n + BM - 1) / BM, b, p2c);
 }
 
 }  // namespace nqb

@@ -16,10 +16,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{"NQB_PREFILL_ROWS": "128"}, {"NQB_PREFILL_ROWS": "256"},
-                                 {"NQB_PREFILL_SPLITK": "3"},
+                                 {"NQB_PREFILL_SPLITK": "3"}, {"NQB_PREFILL_N": "208"},
+                                 {"NQB_PREFILL_ROWS": "128", "NQB_PREFILL_N": "208"},
                                  {"NQB_PREFILL_ROWS": "128", "NQB_PREFILL_SPLITK": "2"},
                                  {"NQB_PREFILL_2SM": "0"}, {"NQB_PREFILL_2SM": "0", "NQB_PREFILL_TS": "1"}],
-                         ids=["pair128", "pair256", "pair_splitk3", "pair128_splitk2", "ss", "ts"])
+                         ids=["pair128", "pair256", "pair_splitk3", "pair_n208", "pair128_n208", "pair128_splitk2",
+                              "ss", "ts"])
 def test_prefill_variant_parity(env):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_forward.py"), "-k", "prefill or gemm"],
