@@ -288,6 +288,41 @@ int nqb_dgemm_device(nqb_context* ctx, int trans_a, int trans_b, uint32_t m, uin
                      uint32_t k, double alpha, const double* d_a, uint32_t lda,
                      const double* d_b, uint32_t ldb, double beta, double* d_c, uint32_t ldc);
 
+/* ------------------------------------------------------------------------ */
+/* NQPK packed-model files (io.hpp:27-54, io.cpp:139-193) */
+/* ------------------------------------------------------------------------ */
+/* Host-side parse of the reference's on-disk format ("NQPK", version 1, layers
+ * of name / n / m / r / U words / V words / binary16 s1 / binary16 s2, little
+ * endian).  Errors: NQB_E_PARSE (bad magic, version, zero dimension, truncated
+ * or trailing bytes: the ParseError cases of deserialize_packed_model),
+ * NQB_E_IO (file not readable / writable: IoError).  No device needed. */
+typedef struct nqb_nqpk nqb_nqpk;
+/* read_packed_model (io.cpp:191-193) */
+int nqb_nqpk_open(const char* path, nqb_nqpk** out);
+/* deserialize_packed_model (io.cpp:160-185) */
+int nqb_nqpk_parse(const uint8_t* bytes, uint64_t len, nqb_nqpk** out);
+uint32_t nqb_nqpk_count(const nqb_nqpk* file);
+/* name is NUL-terminated, truncated to name_cap - 1 bytes; name_len gets the full length */
+int nqb_nqpk_layer_info(const nqb_nqpk* file, uint32_t index, char* name, uint32_t name_cap,
+                        uint32_t* name_len, uint32_t* n, uint32_t* m, uint32_t* r);
+/* Views of the layer's reference-layout words and binary16 scales (valid until free). */
+int nqb_nqpk_layer_data(const nqb_nqpk* file, uint32_t index, const uint32_t** u_words,
+                        const uint32_t** v_words, const uint16_t** s1_half,
+                        const uint16_t** s2_half);
+/* Straight to the device layout with the file's binary16 scales (nqb_layer_upload_f16). */
+int nqb_nqpk_layer_upload(nqb_context* ctx, const nqb_nqpk* file, uint32_t index,
+                          nqb_layer** out);
+void nqb_nqpk_free(nqb_nqpk* file);
+/* serialize_packed_model (io.cpp:139-158) from host arrays; buf == NULL queries *len. */
+int nqb_nqpk_serialize(uint32_t count, const char* const* names, const uint32_t* n,
+                       const uint32_t* m, const uint32_t* r, const uint32_t* const* u_words,
+                       const uint32_t* const* v_words, const uint16_t* const* s1_half,
+                       const uint16_t* const* s2_half, uint8_t* buf, uint64_t cap,
+                       uint64_t* len);
+/* write_packed_model (io.cpp:187-189) from device layers (bit-exact download). */
+int nqb_nqpk_write_layers(nqb_context* ctx, const char* path, uint32_t count,
+                          const char* const* names, const nqb_layer* const* layers);
+
 #ifdef __cplusplus
 }
 #endif

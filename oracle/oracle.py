@@ -186,6 +186,31 @@ class Checker:
         self._call("gemv_f64", *self._layer_args(L), _ptr(x), _U32(x.size), _ptr(y))
         return y
 
+    def serialize_nqpk(self, named_layers):
+        """serialize_packed_model (io.cpp:139-158) of [(name, Layer)] -- reference only
+        (nqref_serialize_nqpk in ref_harness.cpp); scales snapped by double_to_half."""
+        if self.prefix != "nqref_":
+            raise NotImplementedError("NQPK serialisation is checked against the reference only")
+        cnt = len(named_layers)
+        names = (C.c_char_p * cnt)(*[nm.encode("utf-8") for nm, _ in named_layers])
+        lays = [l for _, l in named_layers]
+        keep = [(_u32(l.u), _u32(l.v), _f64(l.s1), _f64(l.s2)) for l in lays]
+        u32a = lambda vals: (C.c_uint32 * cnt)(*vals)  # noqa: E731
+        ptrs = lambda idx: (C.c_void_p * cnt)(*[k[idx].ctypes.data for k in keep])  # noqa: E731
+        cap = 64 + sum(16 + len(nm.encode()) + 4 * (l.u.size + l.v.size) + 2 * (l.n + l.m)
+                       for nm, l in named_layers)
+        buf = (C.c_uint8 * cap)()
+        ln = C.c_uint64()
+        fn = self._fn("serialize_nqpk")
+        fn.argtypes = [_U32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                       C.POINTER(C.c_uint64)]
+        st = fn(cnt, names, u32a([l.n for l in lays]), u32a([l.m for l in lays]),
+                u32a([l.r for l in lays]), ptrs(0), ptrs(1), ptrs(2), ptrs(3), buf, cap, C.byref(ln))
+        if st != 0:
+            raise OracleError(st, "nqref_serialize_nqpk")
+        return bytes(buf)[: ln.value]
+
     def gemv_packed_f32(self, L: Layer, x):
         x = np.ascontiguousarray(x, dtype=np.float32)
         y = np.empty(L.n, np.float32)

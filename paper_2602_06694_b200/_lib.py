@@ -101,6 +101,16 @@ PROTOTYPES = {
     "nqb_graph_free": (C.c_int, [P]),
     "nqb_dgemm_device": (C.c_int, [P, C.c_int, C.c_int, U32, U32, U32, D, P, U32, P, U32, D,
                                    P, U32]),
+    # NQPK files (io.cpp:139-193)
+    "nqb_nqpk_open": (C.c_int, [C.c_char_p, PP]),
+    "nqb_nqpk_parse": (C.c_int, [P, U64, PP]),
+    "nqb_nqpk_count": (U32, [P]),
+    "nqb_nqpk_layer_info": (C.c_int, [P, U32, C.c_char_p, U32, PU32, PU32, PU32, PU32]),
+    "nqb_nqpk_layer_data": (C.c_int, [P, U32, PP, PP, PP, PP]),
+    "nqb_nqpk_layer_upload": (C.c_int, [P, P, U32, PP]),
+    "nqb_nqpk_free": (None, [P]),
+    "nqb_nqpk_serialize": (C.c_int, [U32, P, P, P, P, P, P, P, P, P, U64, C.POINTER(U64)]),
+    "nqb_nqpk_write_layers": (C.c_int, [P, C.c_char_p, U32, P, P]),
 }
 
 _LIB = None

@@ -22,6 +22,7 @@ libnqb.so and a B200.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -751,3 +752,130 @@ def factorize_layer(w, config: AdmmConfig, scale_floor: float = 1e-12,
     d = res.as_dict()
     state = AdmmState(res.rho, res.iteration, [], res.primal_residual, bool(res.converged), d)
     return DeviceLayer(ctx, h), err.value, state
+
+
+# ---------------------------------------------------------------------------
+# NQPK packed-model files (io.hpp:27-54, io.cpp:139-193); SURVEY.md §8(f) row 1
+# ---------------------------------------------------------------------------
+def _nqpk_layers(handle) -> list:
+    lib = L.load()
+    out = []
+    for i in range(lib.nqb_nqpk_count(handle)):
+        name_len, n, m, r = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _check(lib.nqb_nqpk_layer_info(handle, i, None, 0, C.byref(name_len), C.byref(n),
+                                       C.byref(m), C.byref(r)), "read_packed_model")
+        buf = C.create_string_buffer(name_len.value + 1)
+        _check(lib.nqb_nqpk_layer_info(handle, i, buf, name_len.value + 1, None, None, None, None),
+               "read_packed_model")
+        pu, pv, p1, p2 = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(lib.nqb_nqpk_layer_data(handle, i, C.byref(pu), C.byref(pv), C.byref(p1),
+                                       C.byref(p2)), "read_packed_model")
+        k = (r.value + 31) // 32
+
+        def arr(p, count, ct, dt):
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), shape=(count,)).astype(dt)
+
+        u = arr(pu, n.value * k, C.c_uint32, np.uint32).reshape(n.value, k)
+        v = arr(pv, m.value * k, C.c_uint32, np.uint32).reshape(m.value, k)
+        s1 = arr(p1, n.value, C.c_uint16, np.uint16).view(np.float16).astype(np.float64)
+        s2 = arr(p2, m.value, C.c_uint16, np.uint16).view(np.float16).astype(np.float64)
+        out.append((buf.value.decode("utf-8"), FactorizedLayer(n.value, m.value, r.value, u, v, s1, s2)))
+    return out
+
+
+def read_packed_model(path: str) -> list:
+    """read_packed_model (io.cpp:191-193): [(name, FactorizedLayer)] with the file's
+    binary16 scales widened exactly to float64 (host only; no device needed)."""
+    lib = L.load()
+    h = C.c_void_p()
+    _check(lib.nqb_nqpk_open(os.fsencode(path), C.byref(h)), "read_packed_model")
+    try:
+        return _nqpk_layers(h)
+    finally:
+        lib.nqb_nqpk_free(h)
+
+
+def deserialize_packed_model(data: bytes) -> list:
+    """deserialize_packed_model (io.cpp:160-185)."""
+    lib = L.load()
+    h = C.c_void_p()
+    buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(bytes(data) or b"\0")
+    _check(lib.nqb_nqpk_parse(buf, len(data), C.byref(h)), "deserialize_packed_model")
+    try:
+        return _nqpk_layers(h)
+    finally:
+        lib.nqb_nqpk_free(h)
+
+
+def load_packed_model(path: str, ctx: Context | None = None) -> list:
+    """An NQPK file straight to the device layout: [(name, DeviceLayer)], uploaded
+    with the file's binary16 scales unchanged."""
+    ctx = ctx or context()
+    lib = ctx.lib
+    h = C.c_void_p()
+    _check(lib.nqb_nqpk_open(os.fsencode(path), C.byref(h)), "load_packed_model")
+    try:
+        names = [name for name, _ in _nqpk_layers(h)]
+        out = []
+        for i, name in enumerate(names):
+            d = C.c_void_p()
+            _check(lib.nqb_nqpk_layer_upload(ctx.handle, h, i, C.byref(d)), "load_packed_model")
+            out.append((name, DeviceLayer(ctx, d)))
+        return out
+    finally:
+        lib.nqb_nqpk_free(h)
+
+
+def serialize_packed_model(layers) -> bytes:
+    """serialize_packed_model (io.cpp:139-158) of [(name, FactorizedLayer)]; scales
+    are snapped to binary16 like double_to_half (half.hpp:83-85)."""
+    lib = L.load()
+    cnt = len(layers)
+    names = (C.c_char_p * max(1, cnt))(*[nm.encode("utf-8") for nm, _ in layers])
+    keep = []
+
+    def arrp(arrs, ct):
+        ptrs = (C.c_void_p * max(1, cnt))()
+        for i, a in enumerate(arrs):
+            keep.append(a)
+            ptrs[i] = a.ctypes.data
+        return ptrs
+
+    lays = [lay for _, lay in layers]
+    n = (C.c_uint32 * max(1, cnt))(*[l.n for l in lays])
+    m = (C.c_uint32 * max(1, cnt))(*[l.m for l in lays])
+    r = (C.c_uint32 * max(1, cnt))(*[l.r for l in lays])
+    u = arrp([np.ascontiguousarray(l.u, np.uint32) for l in lays], C.c_uint32)
+    v = arrp([np.ascontiguousarray(l.v, np.uint32) for l in lays], C.c_uint32)
+    h = lambda s: np.ascontiguousarray(  # noqa: E731
+        np.asarray(s, np.float64).astype(np.float32).astype(np.float16).view(np.uint16))
+    s1 = arrp([h(l.s1) for l in lays], C.c_uint16)
+    s2 = arrp([h(l.s2) for l in lays], C.c_uint16)
+    ln = C.c_uint64()
+    _check(lib.nqb_nqpk_serialize(cnt, names, n, m, r, u, v, s1, s2, None, 0, C.byref(ln)),
+           "serialize_packed_model")
+    buf = (C.c_uint8 * max(1, ln.value))()
+    _check(lib.nqb_nqpk_serialize(cnt, names, n, m, r, u, v, s1, s2, buf, ln.value, C.byref(ln)),
+           "serialize_packed_model")
+    return bytes(buf)[: ln.value]
+
+
+def write_packed_model(path: str, layers, ctx: Context | None = None) -> None:
+    """write_packed_model (io.cpp:187-189) of [(name, DeviceLayer | FactorizedLayer)]:
+    device layers are written from the device (bit-exact download)."""
+    if layers and all(isinstance(l, DeviceLayer) for _, l in layers):
+        ctx = ctx or layers[0][1].ctx
+        cnt = len(layers)
+        names = (C.c_char_p * cnt)(*[nm.encode("utf-8") for nm, _ in layers])
+        hs = (C.c_void_p * cnt)(*[l.handle.value if isinstance(l.handle, C.c_void_p) else l.handle
+                                  for _, l in layers])
+        _check(ctx.lib.nqb_nqpk_write_layers(ctx.handle, os.fsencode(path), cnt, names, hs),
+               "write_packed_model")
+        return
+    data = serialize_packed_model([(nm, l.download() if isinstance(l, DeviceLayer) else l)
+                                   for nm, l in layers])
+    try:
+        with open(path, "wb") as f:
+            f.write(data)
+    except OSError as e:
+        raise IoError(f"cannot write {path}: {e}") from e
