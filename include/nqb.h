@@ -149,8 +149,8 @@ int nqb_gemv_f32_device(nqb_context* ctx, const nqb_layer* layer, const float* d
 int nqb_gemv_f16_device(nqb_context* ctx, const nqb_layer* layer, const uint16_t* d_x,
                         uint16_t* d_y);
 /* Batched forward (gemm_packed, packed.cpp:260-287): X is m x b row-major fp64
- * host, Y is n x b row-major fp64 host.  Computes with binary16 activations and
- * fp32 accumulation on tensor cores. */
+ * host, Y is n x b row-major fp64 host.  fp64 accumulation on CUDA cores in the
+ * reference's column order (within 1e-10 of gemm_packed). */
 int nqb_gemm_f64_host(nqb_context* ctx, const nqb_layer* layer, const double* x, uint32_t b,
                       double* y);
 /* Prefill GEMM on device buffers: X is b x m row-major binary16 (token-major),
