@@ -55,6 +55,7 @@ typedef enum nqb_status {
   NQB_E_VALIDATION = 9,           /* plain Error(kValidation, ...) e.g. admm.cpp:134-136 */
   NQB_E_PARSE = 10,               /* ParseError          errors.hpp:109-111 */
   NQB_E_IO = 11,                  /* IoError             errors.hpp:104-106 */
+  NQB_E_EMPTY_STATS = 12,         /* EmptyStats          errors.hpp:63-66 */
   /* ErrorKind::kNumerical (CLI exit 3) */
   NQB_E_ZERO_MATRIX = 32,         /* ZeroMatrix          errors.hpp:53-57 */
   NQB_E_NOT_POSITIVE_DEFINITE = 33, /* NotPositiveDefinite errors.hpp:47-51 */
@@ -287,6 +288,38 @@ int nqb_augmented_lagrangian_host(nqb_context* ctx, const double* u, const doubl
 int nqb_dgemm_device(nqb_context* ctx, int trans_a, int trans_b, uint32_t m, uint32_t n,
                      uint32_t k, double alpha, const double* d_a, uint32_t lda,
                      const double* d_b, uint32_t ldb, double beta, double* d_c, uint32_t ldc);
+
+/* ------------------------------------------------------------------------ */
+/* Preconditioner, phase 1 of the pipeline (precondition.cpp:37-153,          */
+/* pipeline.cpp:63-72), SURVEY §8(f) row 3.  Bitwise equal to the reference.  */
+/* ------------------------------------------------------------------------ */
+/* accumulate_stats (precondition.cpp:37-62): batch is rows(samples) x cols(channels)
+ * row-major fp64; the caller owns the ChannelStats state (sum_squares[cols],
+ * sample_count, tau) and passes it in/out.  rows == 0 is a no-op.  Errors:
+ * NQB_E_VALIDATION (percentile outside (0,1)), NQB_E_NON_FINITE_INPUT. */
+int nqb_accumulate_stats_host(nqb_context* ctx, const double* batch, uint64_t rows, uint32_t cols,
+                              double percentile, double* sum_squares, uint64_t* sample_count,
+                              double* tau);
+int nqb_accumulate_stats_device(nqb_context* ctx, const double* d_batch, uint64_t rows,
+                                uint32_t cols, double percentile, double* sum_squares,
+                                uint64_t* sample_count, double* tau);
+/* build_preconditioner (precondition.cpp:99-121): out_sum_squares == NULL means no
+ * gradient-side stats (diag_out = identity, tau_max = max(in_tau, 1)).  Errors:
+ * NQB_E_EMPTY_STATS, NQB_E_VALIDATION (gamma outside [0,1], eps_floor <= 0). */
+int nqb_build_preconditioner(uint32_t in_channels, const double* in_sum_squares,
+                             uint64_t in_count, double in_tau, uint32_t out_channels,
+                             const double* out_sum_squares, uint64_t out_count, double out_tau,
+                             double gamma, double eps_floor, double* diag_in, double* diag_out,
+                             double* tau_max);
+/* precondition_weight (precondition.cpp:123-138): W <- D_out W D_in in place; a NULL
+ * diagonal is the identity. */
+int nqb_precondition_weight_host(nqb_context* ctx, double* w, uint32_t rows, uint32_t cols,
+                                 const double* diag_out, const double* diag_in);
+int nqb_precondition_weight_device(nqb_context* ctx, double* d_w, uint32_t rows, uint32_t cols,
+                                   const double* d_diag_out, const double* d_diag_in);
+/* unprecondition_rows (precondition.cpp:143-153): factor rows /= diag (NULL: identity). */
+int nqb_unprecondition_rows_host(nqb_context* ctx, double* factor, uint32_t rows, uint32_t cols,
+                                 const double* diag);
 
 /* ------------------------------------------------------------------------ */
 /* NQPK packed-model files (io.hpp:27-54, io.cpp:139-193) */

@@ -186,6 +186,61 @@ class Checker:
         self._call("gemv_f64", *self._layer_args(L), _ptr(x), _U32(x.size), _ptr(y))
         return y
 
+    # -- precondition.cpp (reference only; no C restatement) ------------------
+    def _ref_only(self, what):
+        if self.prefix != "nqref_":
+            raise NotImplementedError(f"{what} is checked against the reference only")
+
+    def accumulate_stats(self, sum_squares, count, tau, batch, percentile):
+        """accumulate_stats (precondition.cpp:37-62) -> (sum_squares, count, tau)."""
+        self._ref_only("accumulate_stats")
+        b = _f64(batch)
+        ss = np.array(sum_squares, np.float64, copy=True)
+        c, t = C.c_uint64(count), C.c_double(tau)
+        fn = self._fn("accumulate_stats")
+        fn.argtypes = [C.c_void_p, _U32, _U32, _D, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(_D)]
+        st = fn(b.ctypes.data, b.shape[0], b.shape[1], percentile, ss.ctypes.data, C.byref(c), C.byref(t))
+        if st != 0:
+            raise OracleError(st, "nqref_accumulate_stats")
+        return ss, c.value, t.value
+
+    def build_preconditioner(self, in_ss, in_count, in_tau, out_ss, out_count, out_tau, gamma,
+                             eps_floor):
+        self._ref_only("build_preconditioner")
+        ins = _f64(in_ss)
+        din = np.empty(ins.size, np.float64)
+        outs = _f64(out_ss) if out_ss is not None else None
+        dout = np.empty(outs.size, np.float64) if outs is not None else None
+        tm = C.c_double()
+        fn = self._fn("build_preconditioner")
+        fn.argtypes = [_U32, C.c_void_p, C.c_uint64, _D, _U32, C.c_void_p, C.c_uint64, _D, _D, _D,
+                       C.c_void_p, C.c_void_p, C.POINTER(_D)]
+        st = fn(ins.size, ins.ctypes.data, in_count, in_tau, 0 if outs is None else outs.size,
+                None if outs is None else outs.ctypes.data, out_count, out_tau, gamma, eps_floor,
+                din.ctypes.data, None if dout is None else dout.ctypes.data, C.byref(tm))
+        if st != 0:
+            raise OracleError(st, "nqref_build_preconditioner")
+        return din, dout, tm.value
+
+    def precondition_weight(self, w, diag_out, diag_in):
+        self._ref_only("precondition_weight")
+        w = _f64(w)
+        out = np.empty_like(w)
+        do = _f64(diag_out) if diag_out is not None else None
+        di = _f64(diag_in) if diag_in is not None else None
+        self._call("precondition_weight", _ptr(w), _U32(w.shape[0]), _U32(w.shape[1]),
+                   _ptr(do) if do is not None else None, _ptr(di) if di is not None else None,
+                   _ptr(out))
+        return out
+
+    def unprecondition_rows(self, factor, diag):
+        self._ref_only("unprecondition_rows")
+        f = np.array(factor, np.float64, copy=True)
+        d = _f64(diag) if diag is not None else None
+        self._call("unprecondition_rows", _ptr(f), _U32(f.shape[0]), _U32(f.shape[1]),
+                   _ptr(d) if d is not None else None)
+        return f
+
     def serialize_nqpk(self, named_layers):
         """serialize_packed_model (io.cpp:139-158) of [(name, Layer)] -- reference only
         (nqref_serialize_nqpk in ref_harness.cpp); scales snapped by double_to_half."""

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <optional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -43,6 +44,7 @@ int code_of(const std::exception& e) {
   if (dynamic_cast<const TargetTooSmall*>(&e)) return NQB_E_TARGET_TOO_SMALL;
   if (dynamic_cast<const ParseError*>(&e)) return NQB_E_PARSE;
   if (dynamic_cast<const IoError*>(&e)) return NQB_E_IO;
+  if (dynamic_cast<const EmptyStats*>(&e)) return NQB_E_EMPTY_STATS;
   if (dynamic_cast<const ZeroMatrix*>(&e)) return NQB_E_ZERO_MATRIX;
   if (dynamic_cast<const NotPositiveDefinite*>(&e)) return NQB_E_NOT_POSITIVE_DEFINITE;
   if (auto* err = dynamic_cast<const Error*>(&e)) {
@@ -372,6 +374,68 @@ int nqref_serialize_nqpk(std::uint32_t count, const char* const* names,
     *len = bytes.size();
     if (bytes.size() > cap) throw Error(ErrorKind::kValidation, "buffer too small");
     std::memcpy(buf, bytes.data(), bytes.size());
+  })
+}
+
+// ---- precondition.cpp: phase 1 (precondition.cpp:37-153) --------------------
+// ChannelStats state passed in/out as (sum_squares[cols], sample_count, tau).
+int nqref_accumulate_stats(const double* batch, std::uint32_t rows, std::uint32_t cols,
+                           double percentile, double* sum_squares, std::uint64_t* count,
+                           double* tau) {
+  GUARD({
+    ChannelStats st(cols);
+    std::memcpy(st.sum_squares.data(), sum_squares, sizeof(double) * cols);
+    st.sample_count = *count;
+    st.tau = *tau;
+    accumulate_stats(st, dm(batch, rows, cols), percentile);
+    std::memcpy(sum_squares, st.sum_squares.data(), sizeof(double) * cols);
+    *count = st.sample_count;
+    *tau = st.tau;
+  })
+}
+
+int nqref_build_preconditioner(std::uint32_t in_c, const double* in_sq, std::uint64_t in_count,
+                               double in_tau, std::uint32_t out_c, const double* out_sq,
+                               std::uint64_t out_count, double out_tau, double gamma,
+                               double eps_floor, double* diag_in, double* diag_out,
+                               double* tau_max) {
+  GUARD({
+    ChannelStats in(in_c);
+    std::memcpy(in.sum_squares.data(), in_sq, sizeof(double) * in_c);
+    in.sample_count = in_count;
+    in.tau = in_tau;
+    std::optional<ChannelStats> out;
+    if (out_sq) {
+      out.emplace(out_c);
+      std::memcpy(out->sum_squares.data(), out_sq, sizeof(double) * out_c);
+      out->sample_count = out_count;
+      out->tau = out_tau;
+    }
+    const Preconditioner p = build_preconditioner(in, out, gamma, eps_floor);
+    std::memcpy(diag_in, p.diag_in.data(), sizeof(double) * p.diag_in.size());
+    if (out_sq) std::memcpy(diag_out, p.diag_out.data(), sizeof(double) * p.diag_out.size());
+    *tau_max = p.tau_max;
+  })
+}
+
+int nqref_precondition_weight(const double* w, std::uint32_t rows, std::uint32_t cols,
+                              const double* diag_out, const double* diag_in, double* out) {
+  GUARD({
+    Preconditioner p;
+    if (diag_out) p.diag_out.assign(diag_out, diag_out + rows);
+    if (diag_in) p.diag_in.assign(diag_in, diag_in + cols);
+    put(precondition_weight(dm(w, rows, cols), p), out);
+  })
+}
+
+int nqref_unprecondition_rows(double* factor, std::uint32_t rows, std::uint32_t cols,
+                              const double* diag) {
+  GUARD({
+    DenseMatrix f = dm(factor, rows, cols);
+    std::vector<double> d;
+    if (diag) d.assign(diag, diag + rows);
+    unprecondition_rows(f, d);
+    put(f, factor);
   })
 }
 

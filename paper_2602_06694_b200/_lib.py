@@ -101,6 +101,13 @@ PROTOTYPES = {
     "nqb_graph_free": (C.c_int, [P]),
     "nqb_dgemm_device": (C.c_int, [P, C.c_int, C.c_int, U32, U32, U32, D, P, U32, P, U32, D,
                                    P, U32]),
+    # preconditioner (precondition.cpp:37-153)
+    "nqb_accumulate_stats_host": (C.c_int, [P, P, U64, U32, D, P, C.POINTER(U64), PD]),
+    "nqb_accumulate_stats_device": (C.c_int, [P, P, U64, U32, D, P, C.POINTER(U64), PD]),
+    "nqb_build_preconditioner": (C.c_int, [U32, P, U64, D, U32, P, U64, D, D, D, P, P, PD]),
+    "nqb_precondition_weight_host": (C.c_int, [P, P, U32, U32, P, P]),
+    "nqb_precondition_weight_device": (C.c_int, [P, P, U32, U32, P, P]),
+    "nqb_unprecondition_rows_host": (C.c_int, [P, P, U32, U32, P]),
     # NQPK files (io.cpp:139-193)
     "nqb_nqpk_open": (C.c_int, [C.c_char_p, PP]),
     "nqb_nqpk_parse": (C.c_int, [P, U64, PP]),

@@ -90,6 +90,10 @@ class IoError(Error):
     code = 11
 
 
+class EmptyStats(Error):
+    code = 12
+
+
 class ZeroMatrix(Error):
     kind = KIND_NUMERICAL
     code = 32
@@ -109,7 +113,7 @@ class DeviceError(Error):
 
 _BY_CODE = {cls.code: cls for cls in (DimensionMismatch, NonFiniteInput, NonBinaryEntry,
                                        CorruptPadding, RankTooLarge, InvalidRank,
-                                       NotSymmetric, TargetTooSmall, ParseError, IoError,
+                                       NotSymmetric, TargetTooSmall, ParseError, IoError, EmptyStats,
                                        ZeroMatrix, NotPositiveDefinite)}
 
 
@@ -879,3 +883,110 @@ def write_packed_model(path: str, layers, ctx: Context | None = None) -> None:
             f.write(data)
     except OSError as e:
         raise IoError(f"cannot write {path}: {e}") from e
+
+
+# ---------------------------------------------------------------------------
+# Preconditioner: phase 1 of the pipeline (precondition.hpp, precondition.cpp:37-153),
+# SURVEY.md §8(f) row 3.  Column statistics and the D_out W D_in scaling run on
+# the device in the reference's operation order (bitwise equal results).
+# ---------------------------------------------------------------------------
+@dataclass
+class ChannelStats:  # precondition.hpp:29-38
+    sum_squares: np.ndarray
+    sample_count: int = 0
+    tau: float = 0.0
+
+    @classmethod
+    def zeros(cls, channel_count: int) -> "ChannelStats":
+        return cls(np.zeros(channel_count, np.float64), 0, 0.0)
+
+    def channel_count(self) -> int:
+        return int(self.sum_squares.size)
+
+
+@dataclass
+class Preconditioner:  # precondition.hpp:50-55
+    diag_in: np.ndarray
+    diag_out: np.ndarray  # empty = identity
+    gamma: float = 0.0
+    tau_max: float = 1.0
+
+
+def accumulate_stats(stats: ChannelStats, batch, percentile: float,
+                     ctx: Context | None = None) -> ChannelStats:
+    """accumulate_stats (precondition.cpp:37-62): batch is samples x channels (host
+    array, or a CUDA torch tensor used in place).  Updates and returns `stats`."""
+    ctx = ctx or context()
+    ss = np.ascontiguousarray(stats.sum_squares, np.float64)
+    cnt, tau = C.c_uint64(stats.sample_count), C.c_double(stats.tau)
+    if hasattr(batch, "data_ptr") and getattr(batch, "is_cuda", False):
+        rows, cols = batch.shape
+        if cols != ss.size:
+            raise DimensionMismatch("accumulate_stats: cols(batch) != channel_count")
+        ctx.bind_torch_stream()
+        st = ctx.lib.nqb_accumulate_stats_device(ctx.handle, batch.data_ptr(), rows, cols,
+                                                 percentile, ss.ctypes.data, C.byref(cnt),
+                                                 C.byref(tau))
+    else:
+        b = _mat(batch)
+        if b.shape[1] != ss.size:
+            raise DimensionMismatch("accumulate_stats: cols(batch) != channel_count")
+        st = ctx.lib.nqb_accumulate_stats_host(ctx.handle, _ptr(b), b.shape[0], b.shape[1],
+                                               percentile, ss.ctypes.data, C.byref(cnt),
+                                               C.byref(tau))
+    _check(st, "accumulate_stats")
+    stats.sum_squares, stats.sample_count, stats.tau = ss, cnt.value, tau.value
+    return stats
+
+
+def build_preconditioner(in_stats: ChannelStats, out_stats: Optional[ChannelStats],
+                         gamma: float, eps_floor: float) -> Preconditioner:
+    """build_preconditioner (precondition.cpp:99-121); host arithmetic, no device."""
+    lib = L.load()
+    ins = np.ascontiguousarray(in_stats.sum_squares, np.float64)
+    din = np.empty(ins.size, np.float64)
+    tau_max = C.c_double()
+    if out_stats is not None:
+        outs = np.ascontiguousarray(out_stats.sum_squares, np.float64)
+        dout = np.empty(outs.size, np.float64)
+        st = lib.nqb_build_preconditioner(ins.size, ins.ctypes.data, in_stats.sample_count,
+                                          in_stats.tau, outs.size, outs.ctypes.data,
+                                          out_stats.sample_count, out_stats.tau, gamma, eps_floor,
+                                          din.ctypes.data, dout.ctypes.data, C.byref(tau_max))
+    else:
+        dout = np.empty(0, np.float64)
+        st = lib.nqb_build_preconditioner(ins.size, ins.ctypes.data, in_stats.sample_count,
+                                          in_stats.tau, 0, None, 0, 0.0, gamma, eps_floor,
+                                          din.ctypes.data, None, C.byref(tau_max))
+    _check(st, "build_preconditioner")
+    return Preconditioner(din, dout, gamma, tau_max.value)
+
+
+def precondition_weight(w, p: Preconditioner, ctx: Context | None = None) -> np.ndarray:
+    """precondition_weight (precondition.cpp:123-138): D_out W D_in (a copy)."""
+    ctx = ctx or context()
+    out = np.array(_mat(w), dtype=np.float64, copy=True)
+    rows, cols = out.shape
+    if p.diag_in.size and cols != p.diag_in.size:
+        raise DimensionMismatch("precondition_weight: cols(W) != |diag_in|")
+    if p.diag_out.size and rows != p.diag_out.size:
+        raise DimensionMismatch("precondition_weight: rows(W) != |diag_out|")
+    dout = _f64(p.diag_out) if p.diag_out.size else None
+    din = _f64(p.diag_in) if p.diag_in.size else None
+    _check(ctx.lib.nqb_precondition_weight_host(ctx.handle, out.ctypes.data, rows, cols,
+                                                _ptr(dout), _ptr(din)), "precondition_weight")
+    return out
+
+
+def unprecondition_rows(factor, diag, ctx: Context | None = None) -> np.ndarray:
+    """unprecondition_rows (precondition.cpp:143-153): rows / diag (a copy; empty diag = identity)."""
+    ctx = ctx or context()
+    out = np.array(_mat(factor), dtype=np.float64, copy=True)
+    d = np.asarray(diag, np.float64)
+    if d.size == 0:
+        return out
+    if out.shape[0] != d.size:
+        raise DimensionMismatch("unprecondition_rows: rows(factor) != |diag|")
+    _check(ctx.lib.nqb_unprecondition_rows_host(ctx.handle, out.ctypes.data, out.shape[0],
+                                                out.shape[1], _ptr(_f64(d))), "unprecondition_rows")
+    return out
