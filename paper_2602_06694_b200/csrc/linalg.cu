@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
   const uint32_t head = nrows < nslots ? nrows : nslots;
   double sigma = 0.0, sigma_prev = -1.0;
   int converged = 0, it = 0;
-  long long tA = 0, tB = 0, tC = 0, tW = 0, tD = 0, tX = 0, tY = 0, tZ = 0, t0 = clock64();
+  long long tA = 0, tB = 0, tC = 0, t0 = clock64();
   for (it = 0; it < a.max_iters; ++it) {
     if (a.prof) t0 = clock64();
     // ---- phase A: s_i = M_i . v ; w += s_i M_i, rows streamed through smem,
@@ -462,11 +462,8 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     for (uint32_t i = 0; i < nrows; i += 2) {
       const bool two = i + 1 < nrows && nslots >= 2;
       const uint32_t s0 = i % nslots, s1 = s0 + 1;  // adjacent slots (nslots even)
-      long long pw0 = a.prof ? clock64() : 0;
       tc::mbar_wait(&fullb[s0], (phase >> s0) & 1u);  // both rows of the step
       phase ^= 1u << s0;
-      long long pw1 = a.prof ? clock64() : 0;
-      if (a.prof) tW += pw1 - pw0;
       const double* x0 = (const double*)(ring + (size_t)s0 * row_bytes);
       const double* x1 = (const double*)(ring + (size_t)s1 * row_bytes);
       // The two rows' elements are read from shared memory once and kept in
@@ -510,7 +507,6 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
         cr[2 * warp + 1] = p1;
       }
       __syncthreads();
-      if (a.prof) tD += clock64() - pw1;
       if constexpr (kKeep) {
         // the rows are in registers now: refill their slots right away (the
         // copies overlap the axpy; one barrier per step, cred double-buffered)
@@ -535,7 +531,6 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
       const double sa = __shfl_sync(~0u, ta, 0), sb = __shfl_sync(~0u, tb, 0);
       ss += sa * sa;
       if (two) ss += sb * sb;
-      long long px = a.prof ? clock64() : 0;
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         const uint32_t j = tid + c * PI_THREADS;
@@ -556,19 +551,12 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
           if (two) wl[c] += xb * sb;
         }
       }
-      long long py = a.prof ? clock64() : 0;
       if constexpr (!kKeep) {
         __syncthreads();  // everyone is done with these slots
         if (tid == 0) {
           const uint32_t nx = i + nslots;  // refill the freed slots
           if (nx < nrows) issue(nx);
         }
-      }
-      if (a.prof) {
-        const long long pz = clock64();
-        tX += px - pw1;
-        tY += py - px;
-        tZ += pz - py;
       }
       par ^= 1;
     }
@@ -690,11 +678,6 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     atomicAdd(a.prof + 1, (unsigned long long)tB);
     atomicAdd(a.prof + 2, (unsigned long long)tC);
     atomicAdd(a.prof + 3, (unsigned long long)it);
-    atomicAdd(a.prof + 4, (unsigned long long)tW);
-    atomicAdd(a.prof + 5, (unsigned long long)tD);
-    atomicAdd(a.prof + 6, (unsigned long long)tX);
-    atomicAdd(a.prof + 7, (unsigned long long)tY);
-    atomicAdd(a.prof + 8, (unsigned long long)tZ);
   }
 
   if (pending) {  // an early exit left the next pass's prefetch in flight: drain it
@@ -864,11 +847,8 @@ void power_iterate_device(nqb_context* ctx, const double* d_m, uint32_t rows, ui
     unsigned long long hp[9];
     NQB_CUDA(cudaMemcpy(hp, a.prof, sizeof(hp), cudaMemcpyDeviceToHost));
     const double it = (double)std::max(1ull, hp[3]);
-    fprintf(stderr,
-            "power_prof rows=%u cols=%u iters=%llu cyc/iter: A %.0f B %.0f C %.0f (A: row waits %.0f, "
-            "dot+reduce %.0f, +sums %.0f, axpy %.0f, sync %.0f)\n",
-            rows, cols, hp[3], hp[0] / it, hp[1] / it, hp[2] / it, hp[4] / it, hp[5] / it,
-            hp[6] / it, hp[7] / it, hp[8] / it);
+    fprintf(stderr, "power_prof rows=%u cols=%u iters=%llu cyc/iter: A %.0f B %.0f C %.0f\n", rows,
+            cols, hp[3], hp[0] / it, hp[1] / it, hp[2] / it);
   }
 }
 
