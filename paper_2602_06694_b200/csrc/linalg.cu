@@ -586,16 +586,17 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
       const uint32_t j = c0 + lane;
       double acc = 0.0;
       if (j < cb1) {
-        double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
-        uint32_t b = warp;
-        for (; b + 48 < G; b += 64) {
-          q0 += __ldcg(a.wpart + (uint64_t)b * a.cols + j);
-          q1 += __ldcg(a.wpart + (uint64_t)(b + 16) * a.cols + j);
-          q2 += __ldcg(a.wpart + (uint64_t)(b + 32) * a.cols + j);
-          q3 += __ldcg(a.wpart + (uint64_t)(b + 48) * a.cols + j);
+        // every partial of this lane in flight at once (one L2 round trip),
+        // then a fixed pairwise tree; grids beyond 10 x 16 blocks fold the rest
+        constexpr int kQ = 10;
+        double q[kQ];
+#pragma unroll
+        for (int t = 0; t < kQ; ++t) {
+          const uint32_t b = warp + 16u * t;
+          q[t] = b < G ? __ldcg(a.wpart + (uint64_t)b * a.cols + j) : 0.0;
         }
-        for (; b < G; b += 16) q0 += __ldcg(a.wpart + (uint64_t)b * a.cols + j);
-        acc = (q0 + q1) + (q2 + q3);
+        for (uint32_t b = warp + 16u * kQ; b < G; b += 16) q[0] += __ldcg(a.wpart + (uint64_t)b * a.cols + j);
+        acc = (((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]))) + (q[8] + q[9]);
       }
       cred[warp][lane] = acc;
       __syncthreads();
