@@ -794,10 +794,11 @@ void power_iterate_device(nqb_context* ctx, const double* d_m, uint32_t rows, ui
   a.out = a.wsspart + grid;
   a.bar = ctx->barrier;
   a.prof = nullptr;
-  {  // L2-resident share of the matrix (NQB_POWER_L2_MB, default 80 of the 126 MB L2)
+  {  // L2-resident share of the matrix (NQB_POWER_L2_MB, default 40 of the 126 MB L2: phase A
+     // is SM-bound either way; 40 MB leaves the most L2 for the partial sums of phase B)
     static const uint64_t budget = [] {
       const char* e = std::getenv("NQB_POWER_L2_MB");
-      return (uint64_t)(e ? std::strtoul(e, nullptr, 10) : 80ul) << 20;
+      return (uint64_t)(e ? std::strtoul(e, nullptr, 10) : 40ul) << 20;
     }();
     const uint64_t total = (uint64_t)rows * cols * 8;
     static bool limit_set = false;  // evict_last lines live in the persisting L2 set-aside
