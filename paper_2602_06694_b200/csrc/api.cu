@@ -508,18 +508,17 @@ int nqb_gemv_f32_host(nqb_context* ctx, const nqb_layer* L, const float* x, floa
   float* dy = dx + round_up(L->m, 4);
   // A pinned (page-locked, mapped) y is written by the kernel directly over the
   // host link: no separate device-to-host copy.  Pageable y goes through dy.
-  if (ML->hp_y_host != y) {
+  // Checked every call (a cached answer could outlive the allocation).
+  float* y_dev = nullptr;
+  {
     cudaPointerAttributes at{};
-    ML->hp_y_dev = nullptr;
-    if (cudaPointerGetAttributes(&at, y) == cudaSuccess && at.type == cudaMemoryTypeHost &&
-        at.devicePointer)
-      ML->hp_y_dev = (float*)at.devicePointer;
+    if (cudaPointerGetAttributes(&at, y) == cudaSuccess && at.type == cudaMemoryTypeHost)
+      y_dev = (float*)at.devicePointer;
     cudaGetLastError();
-    ML->hp_y_host = y;
   }
   NQB_CUDA(cudaMemcpyAsync(dx, x, 4 * (size_t)L->m, cudaMemcpyHostToDevice, ctx->stream));
-  if (ML->hp_y_dev) {
-    decode_gemv_f32(ctx, L, dx, ML->hp_y_dev);
+  if (y_dev) {
+    decode_gemv_f32(ctx, L, dx, y_dev);
   } else {
     decode_gemv_f32(ctx, L, dx, dy);
     NQB_CUDA(cudaMemcpyAsync(y, dy, 4 * (size_t)L->n, cudaMemcpyDeviceToHost, ctx->stream));

@@ -98,8 +98,6 @@ struct nqb_layer {
   int device = 0;
   nqb_group* dec = nullptr;  // decode plan of this layer alone (decode.cuh)
   float* hp_buf = nullptr;  // host drop-in path (nqb_gemv_f32_host): device x, y staging
-  const float* hp_y_host = nullptr;  // last host y seen by the drop-in path, and
-  float* hp_y_dev = nullptr;         // its device alias when it is pinned (else null)
 };
 
 namespace nqb {
