@@ -186,7 +186,7 @@ def test_gemm_identity_probe(nq, chk):  # test_packed.cpp:219-225
 
 
 @pytest.mark.parametrize("shape", [(8192, 8192, 2237, 64), (1024, 8192, 485, 256),
-                                   (300, 200, 77, 33)])
+                                   (300, 200, 77, 33), (130, 70, 5, 1), (513, 260, 100, 257)])
 def test_prefill_gemm_f16_vs_reference(nq, chk, shape):
     import torch
     n, m, r, b = shape
