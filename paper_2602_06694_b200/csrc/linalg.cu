@@ -392,14 +392,17 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power(PowerArgs a) {
 // ---------------------------------------------------------------------------
 constexpr int PS_MAX_SLOTS = 8;
 
-template <int CPT>
+// RS: rows per step (one bulk copy, one block barrier and one reduction tree per
+// step; the per-step latency is the bound of phase A, so more rows per step
+// amortise it).  nslots is a multiple of RS.
+template <int CPT, int RS>
 __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uint32_t nslots,
                                                                uint32_t row_bytes) {
   extern __shared__ __align__(128) uint8_t ring[];               // nslots x row_bytes
   __shared__ uint64_t fullb[PS_MAX_SLOTS];
   __shared__ double bred[PI_THREADS / 32];
   __shared__ double cred[PI_THREADS / 32][33];
-  __shared__ double cred2[2][PI_THREADS / 32][2];  // phase A: per-warp dot partials, by step parity
+  __shared__ double cred2[2][PI_THREADS / 32][RS];  // phase A: per-warp dot partials, by step parity
   constexpr bool kKeep = CPT <= 12;  // phase A keeps each row pair in registers
   const uint32_t tid = threadIdx.x, G = gridDim.x, bid = blockIdx.x;
   unsigned gsk = 0;  // grid barriers passed
@@ -432,12 +435,11 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
   uint32_t pending = 0;  // rows of the NEXT pass already issued (prefetched)
   const uint32_t keep = a.keep_den ? (uint32_t)((uint64_t)nrows * a.keep_num / a.keep_den) : 0;
   const uint64_t pol_keep = tc::policy_evict_last(), pol_stream = tc::policy_evict_first();
-  // rows r0+i and r0+i+1 (i even) -> slots i % nslots and the next one (nslots
-  // is even, so they are adjacent) in ONE bulk copy signalling fullb[i % nslots]:
-  // half the copy issues on thread 0, which every step waits for
+  // rows r0+i .. r0+i+RS-1 (i a multiple of RS) -> consecutive slots from
+  // i % nslots in ONE bulk copy signalling fullb[i % nslots]
   auto issue = [&](uint32_t i) {
     uint64_t* bar = &fullb[i % nslots];
-    const uint32_t bytes = (i + 1 < nrows ? 2u : 1u) * row_bytes;
+    const uint32_t bytes = min((uint32_t)RS, nrows - i) * row_bytes;
     tc::mbar_arrive_expect_tx(bar, bytes);
     tc::bulk_g2s_hint(ring + (size_t)(i % nslots) * row_bytes, a.M + (uint64_t)(r0 + i) * a.cols,
                       bytes, bar, i < keep ? pol_keep : pol_stream);
@@ -452,103 +454,91 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     // two rows per block reduction.  The first `head` rows of this pass were
     // prefetched at the end of the previous pass (rows do not change).
     if (tid == 0 && !pending)
-      for (uint32_t i = 0; i < head; i += 2) issue(i);
+      for (uint32_t i = 0; i < head; i += RS) issue(i);
     pending = 0;
     double wl[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) wl[c] = 0.0;
     double ss = 0.0;
     uint32_t par = 0;  // cred2 buffer of this step
-    for (uint32_t i = 0; i < nrows; i += 2) {
-      const bool two = i + 1 < nrows && nslots >= 2;
-      const uint32_t s0 = i % nslots, s1 = s0 + 1;  // adjacent slots (nslots even)
-      tc::mbar_wait(&fullb[s0], (phase >> s0) & 1u);  // both rows of the step
+    for (uint32_t i = 0; i < nrows; i += RS) {
+      const uint32_t cnt = min((uint32_t)RS, nrows - i);
+      const uint32_t s0 = i % nslots;  // the step's rows sit in slots s0 .. s0+RS-1
+      tc::mbar_wait(&fullb[s0], (phase >> s0) & 1u);
       phase ^= 1u << s0;
-      const double* x0 = (const double*)(ring + (size_t)s0 * row_bytes);
-      const double* x1 = (const double*)(ring + (size_t)s1 * row_bytes);
-      // The two rows' elements are read from shared memory once and kept in
-      // registers for the axpy after the block reduction (shared-memory
-      // bandwidth, not HBM, bounds this loop otherwise).  Wide rows (CPT > 12)
-      // re-read them to stay within the register budget.
-      double xa_r[kKeep ? CPT : 1], xb_r[kKeep ? CPT : 1];
-      // four independent partial sums per row (fp64 latency, not throughput,
-      // bounds a single dependent chain), combined in a fixed tree below
-      double pa[4] = {0.0, 0.0, 0.0, 0.0}, pb[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* xs = (const double*)(ring + (size_t)s0 * row_bytes);
+      const uint32_t rstride = row_bytes / 8;
+      // The step's rows are read from shared memory once and kept in registers
+      // for the axpy after the block reduction (kKeep); wide rows re-read them.
+      double xr[kKeep ? RS : 1][kKeep ? CPT : 1];
+      double pp[RS][2];
+#pragma unroll
+      for (int r = 0; r < RS; ++r) pp[r][0] = pp[r][1] = 0.0;
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         const uint32_t j = tid + c * PI_THREADS;
-        double xa = 0.0, xb = 0.0;
-        if (j < a.cols) {
-          xa = x0[j];
-          xb = two ? x1[j] : 0.0;
-          if (a.abs_mode) {
-            xa = fabs(xa);
-            xb = fabs(xb);
-          }
-          pa[c & 3] += xa * vr[c];
-          pb[c & 3] += xb * vr[c];
-        }
-        if constexpr (kKeep) {
-          xa_r[c] = xa;
-          xb_r[c] = xb;
-        }
-      }
-      double p0 = (pa[0] + pa[1]) + (pa[2] + pa[3]);
-      double p1 = (pb[0] + pb[1]) + (pb[2] + pb[3]);
-      // both dot products through one fixed tree (identical in every thread)
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        p0 += __shfl_xor_sync(~0u, p0, o);
-        p1 += __shfl_xor_sync(~0u, p1, o);
+        for (int r = 0; r < RS; ++r) {
+          double x = 0.0;
+          if (j < a.cols && (uint32_t)r < cnt) {
+            x = xs[(size_t)r * rstride + j];
+            if (a.abs_mode) x = fabs(x);
+            pp[r][c & 1] += x * vr[c];  // two independent chains per row
+          }
+          if constexpr (kKeep) xr[r][c] = x;
+        }
       }
+      double pr[RS];
+#pragma unroll
+      for (int r = 0; r < RS; ++r) pr[r] = pp[r][0] + pp[r][1];
+      // the step's dot products through one fixed tree (identical in every thread)
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < RS; ++r) pr[r] += __shfl_xor_sync(~0u, pr[r], o);
       double* cr = &cred2[par][0][0];
-      if (lane == 0) {
-        cr[2 * warp] = p0;
-        cr[2 * warp + 1] = p1;
-      }
+      if (lane == 0)
+#pragma unroll
+        for (int r = 0; r < RS; ++r) cr[RS * warp + r] = pr[r];
       __syncthreads();
       if constexpr (kKeep) {
         // the rows are in registers now: refill their slots right away (the
-        // copies overlap the axpy; one barrier per step, cred double-buffered)
-        // the issuing lane rotates over the warps: a bulk-copy issue costs its
-        // warp several hundred cycles, and the next barrier waits for that warp
-        if (tid == (uint32_t)(32 * ((i >> 1) % (PI_THREADS / 32)))) {
+        // copies overlap the axpy; one barrier per step, cred double-buffered).
+        // The issuing lane rotates over the warps: a bulk-copy issue costs its
+        // warp several hundred cycles, and the next barrier waits for that warp.
+        if (tid == (uint32_t)(32 * ((i / RS) % (PI_THREADS / 32)))) {
           const uint32_t nx = i + nslots;
           if (nx < nrows) issue(nx);
         }
       }
       // cross-warp sums: lane w < warps holds warp w's partial, one xor tree
-      // per warp (fixed order, identical everywhere) instead of every thread
-      // adding all partials (the fp64 pipe is shared by 16 warps)
+      // per warp (fixed order, identical everywhere)
       static_assert(PI_THREADS / 32 <= 32, "warps per block");
-      double ta = lane < PI_THREADS / 32 ? cr[2 * lane] : 0.0;
-      double tb = lane < PI_THREADS / 32 ? cr[2 * lane + 1] : 0.0;
+      double sr[RS];
 #pragma unroll
-      for (int o = PI_THREADS / 64; o; o >>= 1) {
-        ta += __shfl_xor_sync(~0u, ta, o);
-        tb += __shfl_xor_sync(~0u, tb, o);
+      for (int r = 0; r < RS; ++r) {
+        double t = lane < PI_THREADS / 32 ? cr[RS * lane + r] : 0.0;
+#pragma unroll
+        for (int o = PI_THREADS / 64; o; o >>= 1) t += __shfl_xor_sync(~0u, t, o);
+        sr[r] = __shfl_sync(~0u, t, 0);
+        if ((uint32_t)r < cnt) ss += sr[r] * sr[r];
       }
-      const double sa = __shfl_sync(~0u, ta, 0), sb = __shfl_sync(~0u, tb, 0);
-      ss += sa * sa;
-      if (two) ss += sb * sb;
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         const uint32_t j = tid + c * PI_THREADS;
         if (j < a.cols) {
-          double xa, xb;
-          if constexpr (kKeep) {
-            xa = xa_r[c];
-            xb = xb_r[c];
-          } else {
-            xa = x0[j];
-            xb = two ? x1[j] : 0.0;
-            if (a.abs_mode) {
-              xa = fabs(xa);
-              xb = fabs(xb);
+#pragma unroll
+          for (int r = 0; r < RS; ++r) {
+            if ((uint32_t)r >= cnt) break;
+            double x;
+            if constexpr (kKeep) {
+              x = xr[r][c];
+            } else {
+              x = xs[(size_t)r * rstride + j];
+              if (a.abs_mode) x = fabs(x);
             }
+            wl[c] += x * sr[r];
           }
-          wl[c] += xa * sa;
-          if (two) wl[c] += xb * sb;
         }
       }
       if constexpr (!kKeep) {
@@ -565,7 +555,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
     // reductions and grid barriers below run (drained before exit)
     if (it + 1 < a.max_iters) {
       if (tid == 0)
-        for (uint32_t i = 0; i < head; i += 2) issue(i);
+        for (uint32_t i = 0; i < head; i += RS) issue(i);
       pending = 1;
     }
 #pragma unroll
@@ -682,7 +672,7 @@ __global__ void __launch_bounds__(PI_THREADS, 1) k_power_stream(PowerArgs a, uin
   }
 
   if (pending) {  // an early exit left the next pass's prefetch in flight: drain it
-    for (uint32_t i = 0; i < head; i += 2) {
+    for (uint32_t i = 0; i < head; i += RS) {
       tc::mbar_wait(&fullb[i % nslots], (phase >> (i % nslots)) & 1u);
       phase ^= 1u << (i % nslots);
     }
@@ -735,9 +725,13 @@ template <int CPT>
 static void launch_power_stream(nqb_context* ctx, PowerArgs& a, uint32_t grid) {
   const uint32_t row_bytes = a.cols * 8;  // cols even: 16-byte multiple, 16-byte aligned rows
   uint32_t nslots = (uint32_t)std::min<size_t>(PS_MAX_SLOTS, (200 * 1024) / row_bytes);
-  nslots &= ~1u;  // row pairs share one copy and one barrier (>= 2: dispatch condition)
+  // Row pairs per step (>= 2 slots: dispatch condition).  Three rows per step
+  // (NQB_POWER_RS3=1, six slots) measured slower: 42.4k vs 39.2k cycles per
+  // iteration at 4096^2 (registers: the 24 kept values spill).
+  const bool three = CPT <= 8 && nslots >= 6 && getenv_flag("NQB_POWER_RS3");
+  nslots = three ? nslots / 3 * 3 : (nslots & ~1u);
   const size_t smem = (size_t)nslots * row_bytes;
-  auto kern = k_power_stream<CPT>;
+  auto kern = three ? k_power_stream<CPT, 3> : k_power_stream<CPT, 2>;
   NQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {&a, &nslots, (void*)&row_bytes};
   // grid_sync's monotonic counter must start at a multiple of this grid
