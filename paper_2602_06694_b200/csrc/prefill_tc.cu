@@ -507,6 +507,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
     tc::fence_after_sync();
     const float sc = (grow < a.Mvalid && a.scale) ? __half2float(a.scale[grow]) : 1.f;
     const bool keep = grow < a.Mvalid;
+    // the stage buffers are idle now (every MMA has completed): epilogue tile
+    __half* ep = (__half*)tiles;
+    const bool vec_out = !a.part && (a.ldo % 8 == 0) && (((uintptr_t)a.out) % 16 == 0);
     for (uint32_t c0 = 0; c0 < BNPT; c0 += 16) {
       uint32_t v[16];
       tc::tmem_ld_x16(tmem + (row / BM) * BNPT + ((uint32_t)((warp & 3) * 32) << 16) + c0, v);
@@ -519,7 +522,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
             const uint32_t tok = np + c0 + j;
             if (tok < a.N) pz[(size_t)tok * a.ldp + grow] = __uint_as_float(v[j]);
           }
-        } else {
+        } else if (!vec_out) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const uint32_t tok = np + c0 + j;
@@ -528,6 +531,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MHT * BM + 32, 1)
                   __float2half_rn(keep ? sc * __uint_as_float(v[j]) : 0.f);
           }
         }
+      }
+      if (vec_out) {
+        // token-major output through shared memory: each thread writes its
+        // row's 16 values into a [16 tokens][kP rows] tile, then 16-byte
+        // stores of 8 consecutive rows per token (8x fewer store instructions)
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          ep[j * kP + row] = __float2half_rn(keep ? sc * __uint_as_float(v[j]) : 0.f);
+        asm volatile("bar.sync 1, %0;\n" ::"n"(kP) : "memory");
+        for (uint32_t q = row; q < 16u * (kP / 8); q += kP) {
+          const uint32_t j = q / (kP / 8), g8 = (q % (kP / 8)) * 8;
+          const uint32_t tok = np + c0 + j, r0g = m0 + g8;
+          if (tok < a.N && r0g < a.Mout) {
+            const uint4 val = *(const uint4*)(ep + j * kP + g8);
+            if (r0g + 8 <= a.Mout) {
+              *(uint4*)(a.out + (size_t)tok * a.ldo + r0g) = val;
+            } else {
+              const __half* hv = (const __half*)&val;
+              for (uint32_t t = 0; r0g + t < a.Mout; ++t) a.out[(size_t)tok * a.ldo + r0g + t] = hv[t];
+            }
+          }
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(kP) : "memory");
       }
     }
   }
