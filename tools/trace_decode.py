@@ -60,14 +60,10 @@ for name in sys.argv[1:] or list(SHAPES):
         col = col[~np.isnan(col)]
         if col.size:
             print(f"   {i:2d} {lab:11s} min {col.min():7.2f}  med {np.median(col):7.2f}  max {col.max():7.2f}  (n={col.size})")
-    sel = full[:, 26] > 0
-    if sel.any():
-        u = full[sel, 26].sum()
-        tot = full[sel, 22:26].sum(0) / u
-        print(f"   stage2 warp0 per pair ({u/sel.sum():.1f} pairs/CTA): loads {tot[0]:.0f} afree-wait {tot[1]:.0f} "
-              f"sttm {tot[2]:.0f} waitst+arrive {tot[3]:.0f} cycles")
-    sel = full[:, 30] > 0
-    if sel.any():
-        u = full[sel, 30].sum()
-        tot = full[sel, 28:30].sum(0) / u
-        print(f"   stage2 MMA thread per pair ({u/sel.sum():.1f} pairs/CTA): aready-wait {tot[0]:.0f} issue {tot[1]:.0f} cycles")
+    for st, base in (("stage1", 22), ("stage2", 27)):
+        sel = full[:, base + 4] > 0  # warp 0 of each CTA: [wait, -, mma, flush, units]
+        if sel.any():
+            u = full[sel, base + 4].sum()
+            print(f"   {st} warp0 ({u/sel.sum():.1f} tile units/CTA): wait-landed {full[sel, base].mean():.0f} "
+                  f"mma {full[sel, base + 2].mean():.0f} flush {full[sel, base + 3].mean():.0f} cycles/CTA, "
+                  f"mma {full[sel, base + 2].sum() / u:.0f} cycles/unit")
