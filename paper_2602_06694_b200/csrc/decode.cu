@@ -550,6 +550,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   // every stamp would perturb the timeline it measures)
   unsigned long long* trp = nullptr;
   if (kTrace) asm volatile("mov.b64 %0, %1;" : "=l"(trp) : "l"(p.trace));
+  if (kTrace) trace_t0 = clock64();  // every thread's base (the producer's stamps use it)
   TRACE(0);
   const Cta C = p.ctas[blockIdx.x];
   if (kTrace && tid == 0) {
