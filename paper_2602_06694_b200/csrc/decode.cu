@@ -314,15 +314,7 @@ __device__ __forceinline__ void full_run(const uint8_t* u, uint32_t ustep, const
   for (int j = 0; j < NT; ++j) w[j] = *(const uint4*)(u + j * 512 + lane * 16);
 #pragma unroll
   for (int h = 0; h < 4; ++h) bq[h] = limb_lane ? *(const uint4*)(bp + 2 * h * kTileB) : z;
-  for (uint32_t i = 0; i < cnt; ++i) {
-    const bool more = i + 1 < cnt;
-    const uint8_t* un = more ? u + ustep : u;
-    const uint8_t* bn = more ? bp + kBytesPerK * 256 : bp;
-    uint4 nw[NT], nb[4];
-#pragma unroll
-    for (int j = 0; j < NT; ++j) nw[j] = *(const uint4*)(un + j * 512 + lane * 16);
-#pragma unroll
-    for (int h = 0; h < 4; ++h) nb[h] = limb_lane ? *(const uint4*)(bn + 2 * h * kTileB) : z;
+  auto slab = [&]() {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const uint32_t mask = 0x01010101u << q;
@@ -332,13 +324,24 @@ __device__ __forceinline__ void full_run(const uint8_t* u, uint32_t ustep, const
       for (int j = 0; j < NT; ++j)
         mma_u8s8(acc[j][q & 3], w[j].x & mask, w[j].y & mask, w[j].z & mask, w[j].w & mask, b0, b1);
     }
+  };
+  // the last slab is peeled: no re-read of operands that will not be used
+  // (shared-memory bandwidth is tight when every warp runs only one slab)
+  for (uint32_t i = 0; i + 1 < cnt; ++i) {
+    u += ustep;
+    bp += kBytesPerK * 256;
+    uint4 nw[NT], nb[4];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) nw[j] = *(const uint4*)(u + j * 512 + lane * 16);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) nb[h] = limb_lane ? *(const uint4*)(bp + 2 * h * kTileB) : z;
+    slab();
 #pragma unroll
     for (int j = 0; j < NT; ++j) w[j] = nw[j];
 #pragma unroll
     for (int h = 0; h < 4; ++h) bq[h] = nb[h];
-    u = un;
-    bp = bn;
   }
+  slab();
 }
 
 // All sections of one stage; leaves sum_K bit*value per row in red[] (exact).
