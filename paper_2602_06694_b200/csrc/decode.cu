@@ -710,7 +710,6 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
     StageArgs sa{C.s1_rtn, n1, 0, m, C.s1_sl0, klo, 0};  // linear: barrier full[0]
     run_stage<kBig>(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
               (kTrace && warp == 0) ? p.trace + blockIdx.x * 32 + 22 : nullptr);
-    TRACE(12);
     consumers_sync();
     TRACE(5);
   }
@@ -722,6 +721,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
                : "r"(ep_ld), "r"(dirty0_ld), "r"(dirty1_ld));
   const uint32_t b = ep & 1;
   const uint32_t dirty_next = b ? dirty0 : dirty1;
+  TRACE(12);
   if (n1) {
     const long long A = sum_partials(red8);
     // one CTA per slab range publishes sum|a_int| (bounds every |t_k| of the segment)
@@ -736,6 +736,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
       red_add_u64(&Tseg[i], v);
     }
   }
+  TRACE(13);
   {  // clear this CTA's share of the other t buffer for the next launch
     long long* Tn = p.T + (size_t)(b ^ 1) * p.r_cap;
     const uint32_t per = (dirty_next + gridDim.x - 1) / gridDim.x;  // 32-bit: no 64-bit divide
@@ -810,7 +811,6 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   if (!ring_mode) sa.sec_base = 1;  // linear: barrier full[1]
   run_stage<kBig>(sa, NS, ring_mode, p.slot_bytes, full, empty, buf, bfrag, red,
             (kTrace && warp == 0) ? p.trace + blockIdx.x * 32 + 27 : nullptr);
-  TRACE(13);
   consumers_sync();
   TRACE(10);
   const long long Tsum = sum_partials(red8);

@@ -48,7 +48,7 @@ for name in sys.argv[1:] or list(SHAPES):
     print(f"{name}: n={n} m={m} r={r} grid={G} bytes={lay.device_bytes/1e6:.2f} MB "
           f"(HBM time at 6.4 TB/s: {lay.device_bytes/6.4e12*1e6:.2f} us); times in us since CTA start @1.9GHz")
     labels = ["start_skew", "ready", "pdl_wait", "x_stats", "s1_frag", "s1_mma", "s1_pub", "arrived",
-              "barrier", "s2_frag", "s2_mma", "end", "s1_w0done", "s2_w0done", "prod_issued",
+              "barrier", "s2_frag", "s2_mma", "end", "ep_ready", "t_reds", "prod_issued",
               "all_landed"]
     endt = np.nan_to_num(us[:, 11])
     order = np.argsort(-endt)
