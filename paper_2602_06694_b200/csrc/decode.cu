@@ -644,13 +644,19 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   pdl_wait();  // x (and the t accumulator) may be written by the previous kernel
   TRACE(2);
   State* st = p.st;
-  // epoch and both dirty counts in one load, issued here (volatile: not sunk
-  // to the first use) so nothing waits on it before the t publish
-  uint32_t ep_ld, dirty0_ld, dirty1_ld;
-  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0,%1}, [%3];\n\t"
-               "ld.relaxed.gpu.global.u32 %2, [%3+8];\n"
-               : "=r"(ep_ld), "=r"(dirty0_ld), "=r"(dirty1_ld)
-               : "l"(st) : "memory");
+  // epoch and the dirty count of the next t buffer: one thread of the last
+  // consumer warp loads them right away and parks them in shared memory (the
+  // other warps read them after the stage-1 barrier), so no warp carries the
+  // load's scoreboard through stage 1
+  uint32_t* stw = (uint32_t*)(smem + 16 * NB + 8);  // spare 8 bytes after scb
+  if (warp == kConsumerWarps - 1 && lane == 0) {
+    uint32_t e, d0, d1;
+    asm volatile("ld.relaxed.gpu.global.v2.u32 {%0,%1}, [%3];\n\t"
+                 "ld.relaxed.gpu.global.u32 %2, [%3+8];\n"
+                 : "=r"(e), "=r"(d0), "=r"(d1) : "l"(st) : "memory");
+    stw[0] = e;
+    stw[1] = (e & 1) ? d0 : d1;
+  }
 
   // ---- activation exponent: a = s2*x with |a| <= max|s2| * X, X = 65504 for
   // binary16 x (no pass over x), max|x| over all m for fp32 x.
@@ -713,14 +719,9 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
     consumers_sync();
     TRACE(5);
   }
-  // First use of the state words, pinned here (asm volatile is not hoisted
-  // above the barriers before it): their load latency hides behind stage 1.
-  uint32_t ep, dirty0, dirty1;
-  asm volatile("mov.b32 %0, %3;\n\tmov.b32 %1, %4;\n\tmov.b32 %2, %5;\n"
-               : "=r"(ep), "=r"(dirty0), "=r"(dirty1)
-               : "r"(ep_ld), "r"(dirty0_ld), "r"(dirty1_ld));
+  if (!n1) consumers_sync();  // (CTAs with stage 1 passed a consumer barrier after it)
+  const uint32_t ep = stw[0], dirty_next = stw[1];
   const uint32_t b = ep & 1;
-  const uint32_t dirty_next = b ? dirty0 : dirty1;
   TRACE(12);
   if (n1) {
     const long long A = sum_partials(red8);
