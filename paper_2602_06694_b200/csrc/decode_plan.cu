@@ -362,7 +362,7 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
     max_stream = std::max(max_stream, bytes);
   }
   g->stream_bytes = off;
-  g->big = max_stream >= (uint64_t)env_u32("NQB_DEC_BIG_KB", 80) * 1024;
+  g->big = max_stream >= (uint64_t)env_u32("NQB_DEC_BIG_KB", 0) * 1024;
   // Stream buffer: the whole per-CTA stream when it fits the cap (linear mode:
   // every copy issued up front, one mbarrier per section); otherwise the CTA
   // streams through fixed slots (ring mode).

@@ -170,3 +170,19 @@ def test_host_dropin_pinned_and_pageable_agree(nq, chk):
     dev.gemv_f32(xp, out=pinned2)
     assert np.array_equal(pageable, pinned) and np.array_equal(pageable, pinned2)
     assert rel(pageable, chk.gemv_packed_f32(lay, x)) <= TIGHT_TOL
+
+
+@pytest.mark.parametrize("shape", [(300, 320, 320), (77, 100, 45), (2048, 512, 511), (4096, 4096, 1622),
+                                   (1, 1, 1)], ids=lambda s: "x".join(map(str, s)))
+def test_compact_and_pipelined_instances_bitwise(nq, chk, shape, monkeypatch):
+    """The two kernel instances (compact loop, software-pipelined slab runs;
+    NQB_DEC_BIG_KB picks per plan) do the same integer arithmetic: bitwise equal."""
+    n, m, r = shape
+    lay = O.synthetic_layer(chk, 0xB16 + n + m, n, m, r)
+    x = chk.rng(5 * n + m).gaussian(m).astype(np.float32)
+    out = {}
+    for kb in ("0", "1000000"):
+        monkeypatch.setenv("NQB_DEC_BIG_KB", kb)
+        out[kb] = nq.DeviceLayer.upload(to_nq(nq, lay)).gemv_f32(x)
+    assert np.array_equal(out["0"], out["1000000"])
+    assert rel(out["0"], chk.gemv_packed_f32(lay, x)) <= TIGHT_TOL
