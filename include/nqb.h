@@ -184,6 +184,38 @@ int nqb_set_pdl(nqb_context* ctx, int enable);
 int nqb_debug_decode_trace(nqb_context* ctx, const nqb_layer* layer, const uint16_t* d_x,
                            uint16_t* d_y, uint64_t* stamps, uint32_t* grid);
 
+/* Decode passes: a whole sequence of decode launches (e.g. the 224 linear
+ * layers of a decoder, as q/k/v, o, gate/up, down steps) run by ONE launch of
+ * a persistent kernel.  Each step is a decode group (or one
+ * layer) with its device input and outputs; buffers are fixed at creation.
+ * A step whose input overlaps an earlier step's output waits for that output
+ * inside the kernel (dependencies are found from the buffer ranges), and takes
+ * its activation bound from the producer's published max|y|; independent
+ * steps overlap.  Results equal the per-call kernel's up to that bound (same
+ * arithmetic).  Groups and layers must outlive the pass. */
+typedef struct nqb_pass nqb_pass;
+typedef struct nqb_pass_step {
+  const nqb_group* group;  /* layers sharing the input, or NULL to use `layer` */
+  const nqb_layer* layer;  /* a single layer (its own decode plan) */
+  const void* d_x;         /* device input, m elements */
+  void* d_y[4];            /* device outputs, one per layer of the group */
+  int32_t f32;             /* 0: binary16 in/out, 1: fp32 in/out */
+  int32_t reserved;
+} nqb_pass_step;
+int nqb_pass_create(nqb_context* ctx, uint32_t count, const nqb_pass_step* steps,
+                    nqb_pass** out);
+int nqb_pass_launch(nqb_context* ctx, const nqb_pass* pass);
+int nqb_pass_free(nqb_pass* pass);
+/* Bits streamed per launch, and the algorithmic bytes of the pass: per layer
+ * r(n+m)/8 + 2(n+m) scales + y, plus x once per step. */
+uint64_t nqb_pass_stream_bytes(const nqb_pass* pass);
+uint64_t nqb_pass_algorithmic_bytes(const nqb_pass* pass);
+/* Diagnostics: one launch with per-CTA %globaltimer stamps: stamps holds
+ * grid * (2 * count + 2) words: [start, per step (t barrier passed, stage 2
+ * done), end]. */
+int nqb_debug_pass_trace(nqb_context* ctx, const nqb_pass* pass, uint64_t* stamps,
+                         uint32_t* grid);
+
 /* CUDA graphs of library calls on the context stream (e.g. one decode pass
  * over a layer stack), replayed with a single launch.  Between begin and end
  * only device-buffer entry points may be called. */

@@ -41,6 +41,13 @@ class AdmmResultC(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
 
 
+class PassStep(C.Structure):
+    """nqb_pass_step."""
+
+    _fields_ = [("group", P), ("layer", P), ("d_x", P), ("d_y", P * 4), ("f32", I32),
+                ("reserved", I32)]
+
+
 # name -> (restype, argtypes); mirrors include/nqb.h one-to-one.
 PROTOTYPES = {
     "nqb_status_kind": (C.c_int, [C.c_int]),
@@ -92,6 +99,12 @@ PROTOTYPES = {
     "nqb_group_stream_bytes": (U64, [P]),
     "nqb_group_gemv_f16_device": (C.c_int, [P, P, P, PP]),
     "nqb_group_gemv_f32_device": (C.c_int, [P, P, P, PP]),
+    "nqb_pass_create": (C.c_int, [P, U32, P, PP]),
+    "nqb_pass_launch": (C.c_int, [P, P]),
+    "nqb_pass_free": (C.c_int, [P]),
+    "nqb_pass_stream_bytes": (U64, [P]),
+    "nqb_pass_algorithmic_bytes": (U64, [P]),
+    "nqb_debug_pass_trace": (C.c_int, [P, P, P, PU32]),
     "nqb_set_pdl": (C.c_int, [P, C.c_int]),
     "nqb_set_sm_budget": (C.c_int, [P, C.c_int]),
     "nqb_debug_decode_trace": (C.c_int, [P, P, P, P, P, PU32]),

@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "decode.cuh"
+#include "decode_pass.cuh"
 
 namespace nqb {
 
@@ -24,10 +25,9 @@ uint64_t rel_error_partial_count(const nqb_layer*);
 template <typename Acc, typename In>
 void simt_gemv(nqb_context*, const nqb_layer*, const In*, Acc*);
 void simt_gemm_f64(nqb_context*, const nqb_layer*, const double*, uint32_t, double*);
-// decode.cu / prefill.cu
+// decode.cu / prefill_tc.cu
 void decode_gemv_f32(nqb_context*, const nqb_layer*, const float*, float*);
 void decode_gemv_f16(nqb_context*, const nqb_layer*, const __half*, __half*);
-void prefill_gemm_f16(nqb_context*, const nqb_layer*, const __half*, uint32_t, __half*);
 void prefill_gemm_tc(nqb_context*, const nqb_layer*, const __half*, uint32_t, __half*);
 
 thread_local std::string g_last_error;
@@ -172,6 +172,8 @@ int nqb_destroy(nqb_context* ctx) {
   for (auto& s : ctx->scratch)
     if (s.ptr) cudaFree(s.ptr);
   if (ctx->barrier) cudaFree(ctx->barrier);
+  if (ctx->dec_state) cudaFree(ctx->dec_state);
+  for (void* p : ctx->dec_retired) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -670,6 +672,61 @@ int nqb_debug_decode_trace(nqb_context* ctx, const nqb_layer* L, const uint16_t*
   }
   cudaFree(ctx->dec_trace);
   ctx->dec_trace = nullptr;
+  API_END
+}
+
+int nqb_pass_create(nqb_context* ctx, uint32_t count, const nqb_pass_step* steps,
+                    nqb_pass** out) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_REQUIRE(out != nullptr && steps != nullptr, NQB_E_VALIDATION, "null argument");
+  *out = nullptr;
+  std::vector<PassStepIn> in(count);
+  for (uint32_t k = 0; k < count; ++k) {
+    const nqb_pass_step& s = steps[k];
+    const nqb_group* g = s.group;
+    if (!g) {
+      NQB_REQUIRE(s.layer != nullptr, NQB_E_VALIDATION, "pass step without group or layer");
+      g = s.layer->dec;
+    }
+    in[k].group = g;
+    in[k].x = s.d_x;
+    for (int q = 0; q < dec::kMaxSeg; ++q) in[k].y[q] = s.d_y[q];
+    in[k].f32 = s.f32;
+  }
+  *out = pass_build(ctx, count, in.data());
+  API_END
+}
+
+int nqb_pass_launch(nqb_context* ctx, const nqb_pass* pass) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_REQUIRE(pass != nullptr, NQB_E_VALIDATION, "null pass");
+  pass_launch(ctx, pass, nullptr);
+  API_END
+}
+
+int nqb_pass_free(nqb_pass* pass) {
+  API_BEGIN
+  pass_free(pass);
+  API_END
+}
+
+uint64_t nqb_pass_stream_bytes(const nqb_pass* pass) { return pass ? pass->stream_bytes : 0; }
+uint64_t nqb_pass_algorithmic_bytes(const nqb_pass* pass) { return pass ? pass->algo_bytes : 0; }
+
+int nqb_debug_pass_trace(nqb_context* ctx, const nqb_pass* pass, uint64_t* stamps,
+                         uint32_t* grid) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_REQUIRE(pass != nullptr && stamps != nullptr, NQB_E_VALIDATION, "null argument");
+  if (grid) *grid = pass->G;
+  const size_t words = (size_t)pass->G * (2 * pass->K + 2);
+  DevBuf buf(ctx, words * 8);
+  NQB_CUDA(cudaMemsetAsync(buf.p, 0, words * 8, ctx->stream));
+  pass_launch(ctx, pass, buf.as<unsigned long long>());
+  NQB_CUDA(cudaMemcpyAsync(stamps, buf.p, words * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
   API_END
 }
 

@@ -7,6 +7,7 @@
 
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "nqb.h"
 
@@ -74,6 +75,7 @@ struct nqb_context {
   // decode GEMV state (decode.cu): dec::State followed by 2 x dec_cap int64 rows
   void* dec_state = nullptr;
   uint32_t dec_cap = 0;
+  std::vector<void*> dec_retired;  // outgrown decode states (graphs may still use them)
   bool dec_attr_set = false;
   bool pdl = true;  // launch decode kernels with Programmatic Dependent Launch
   void* dec_trace = nullptr;  // diagnostics (nqb_debug_decode_trace)

@@ -366,8 +366,16 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   // Stream buffer: the whole per-CTA stream when it fits the cap (linear mode:
   // every copy issued up front, one mbarrier per section); otherwise the CTA
   // streams through fixed slots (ring mode).
-  const uint32_t cap = env_u32("NQB_DEC_SMEM_KB", 160) * 1024;
-  const uint32_t buf = (uint32_t)std::min<uint64_t>((max_stream + 127) / 128 * 128, cap);
+  // The buffer takes whatever shared memory the head and the B fragments leave
+  // (NQB_DEC_SMEM_KB caps it lower, e.g. to force ring mode in tests); a ring
+  // slot is one section (<= kMaxRt * 512 B = 16 KB), so at least 10 slots fit
+  // and any layer size streams (no upload is refused for size).
+  constexpr uint32_t kMaxBars = 64;
+  const uint32_t bfrag_pad = (bfrag + 127) / 128 * 128;
+  const uint32_t avail = (227u * 1024u - head_bytes(kMaxBars) - bfrag_pad) / 128 * 128;
+  const uint32_t env_cap = env_u32("NQB_DEC_SMEM_KB", 0) * 1024;
+  const uint32_t cap = env_cap ? std::min(env_cap, avail) : avail;
+  uint32_t buf = (uint32_t)std::min<uint64_t>((max_stream + 127) / 128 * 128, cap);
   uint32_t slot = 0, nbar = 2;  // linear mode: one mbarrier per stage
   for (uint32_t c = 0; c < G; ++c) {
     Cta& C = ctas[c];
@@ -386,7 +394,9 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   }
   if (slot) {
     slot = (slot + 127) / 128 * 128;
-    NQB_REQUIRE(buf / slot >= 2, NQB_E_DIMENSION_MISMATCH, "decode ring needs two slots");
+    buf = std::min(buf / slot, kMaxBars) * slot;
+    NQB_REQUIRE(buf / slot >= 2, NQB_E_DIMENSION_MISMATCH,
+                "decode ring needs two slots (NQB_DEC_SMEM_KB too small)");
     nbar = std::max<uint32_t>(nbar, buf / slot);
   }
   g->buf_bytes = buf;

@@ -445,6 +445,7 @@ class DeviceLayer:
     def gemv_device(self, x, y):
         """x: (m,) fp32/fp16 CUDA tensor, y: (n,) same dtype; async on torch's stream."""
         import torch
+        _check_device_io(x, self.m, y, self.n, "gemv_device")
         self._bind_stream(x)
         if x.dtype == torch.float32:
             fn = self.ctx.lib.nqb_gemv_f32_device
@@ -457,10 +458,30 @@ class DeviceLayer:
 
     def gemm_device(self, x, y):
         """x: (b, m) fp16 token-major CUDA tensor -> y: (b, n) fp16."""
+        import torch
+        if x.dim() != 2 or y.dim() != 2 or x.shape[0] != y.shape[0]:
+            raise DimensionMismatch("gemm_packed: x must be (b, m) and y (b, n)")
+        if x.dtype != torch.float16:
+            raise Error("gemm_device: dtype must be float16")
+        _check_device_io(x, x.shape[0] * self.m, y, y.shape[0] * self.n, "gemm_device")
         self._bind_stream(x)
         _check(self.ctx.lib.nqb_gemm_f16_device(self.ctx.handle, self.handle,
                                                 C.c_void_p(x.data_ptr()), x.shape[0],
                                                 C.c_void_p(y.data_ptr())), "gemm_device")
+
+
+def _check_device_io(x, nx, y, ny, what):
+    """Device-buffer entry points write through raw pointers: check sizes, dtypes,
+    contiguity and device first (the reference throws DimensionMismatch)."""
+    if x.numel() != nx or y.numel() != ny:
+        raise DimensionMismatch(f"{what}: |x| = {x.numel()} (want {nx}), |y| = {y.numel()} "
+                                f"(want {ny})")
+    if x.dtype != y.dtype:
+        raise Error(f"{what}: x and y dtypes differ ({x.dtype} vs {y.dtype})")
+    if not (x.is_contiguous() and y.is_contiguous()):
+        raise Error(f"{what}: x and y must be contiguous")
+    if not (x.is_cuda and y.is_cuda) or x.device != y.device:
+        raise Error(f"{what}: x and y must be CUDA tensors on the same device")
 
 
 class DecodeGroup:
@@ -496,6 +517,10 @@ class DecodeGroup:
     def gemv_device(self, x, ys):
         """x: (m,) fp16/fp32 CUDA tensor; ys: one (n_i,) tensor per layer, same dtype."""
         import torch
+        if len(ys) != len(self.layers):
+            raise DimensionMismatch(f"group gemv: {len(ys)} outputs for {len(self.layers)} layers")
+        for lay, y in zip(self.layers, ys):
+            _check_device_io(x, self.m, y, lay.n, "group gemv")
         self.ctx.bind_torch_stream(x.device)
         arr = (C.c_void_p * len(ys))(*[y.data_ptr() for y in ys])
         if x.dtype == torch.float16:
@@ -505,6 +530,82 @@ class DecodeGroup:
         else:
             raise Error("gemv_device: dtype must be float32 or float16")
         _check(fn(self.ctx.handle, self.handle, C.c_void_p(x.data_ptr()), arr), "group gemv")
+
+
+class DecodePass:
+    """A whole decode pass as ONE launch of the persistent decode-pass kernel
+    (nqb_pass).  `steps` is a list of (group_or_layer, x, ys):
+    a DecodeGroup or DeviceLayer, its input tensor and one output tensor per
+    layer.  All tensors are CUDA tensors of one dtype (fp16 or fp32) that stay
+    allocated while the pass lives; a step whose x overlaps an earlier step's
+    output waits for it inside the kernel."""
+
+    def __init__(self, steps, ctx: Context | None = None):
+        import torch
+        if not steps:
+            raise Error("DecodePass: no steps")
+        ctx = ctx or steps[0][0].ctx
+        self.ctx = ctx
+        self._keep = []
+        arr = (L.PassStep * len(steps))()
+        for i, (unit, x, ys) in enumerate(steps):
+            layers = unit.layers if isinstance(unit, DecodeGroup) else [unit]
+            if len(ys) != len(layers):
+                raise DimensionMismatch(f"pass step {i}: {len(ys)} outputs for {len(layers)} "
+                                        "layers")
+            for lay, y in zip(layers, ys):
+                _check_device_io(x, layers[0].m, y, lay.n, f"pass step {i}")
+            if x.dtype not in (torch.float16, torch.float32):
+                raise Error("DecodePass: dtype must be float16 or float32")
+            st = arr[i]
+            if isinstance(unit, DecodeGroup):
+                st.group = unit.handle
+            else:
+                st.layer = unit.handle
+            st.d_x = x.data_ptr()
+            for q, y in enumerate(ys):
+                st.d_y[q] = y.data_ptr()
+            st.f32 = 1 if x.dtype == torch.float32 else 0
+            self._keep.append((unit, x, list(ys)))
+        h = C.c_void_p()
+        _check(ctx.lib.nqb_pass_create(ctx.handle, len(steps), arr, C.byref(h)),
+               "nqb_pass_create")
+        self.handle = h
+        self.steps = len(steps)
+
+    @property
+    def stream_bytes(self) -> int:
+        return int(self.ctx.lib.nqb_pass_stream_bytes(self.handle))
+
+    @property
+    def algorithmic_bytes(self) -> int:
+        return int(self.ctx.lib.nqb_pass_algorithmic_bytes(self.handle))
+
+    def launch(self):
+        """Enqueues the pass on torch's current stream."""
+        self.ctx.bind_torch_stream(self._keep[0][1].device)
+        _check(self.ctx.lib.nqb_pass_launch(self.ctx.handle, self.handle), "nqb_pass_launch")
+
+    def trace(self):
+        """One launch with per-CTA %globaltimer stamps -> (grid, 2K+2) uint64 array."""
+        self.ctx.bind_torch_stream(self._keep[0][1].device)
+        g = C.c_uint32()
+        n = self.ctx.num_sms if hasattr(self.ctx, "num_sms") else 160
+        out = np.zeros(max(n, 160) * (2 * self.steps + 2), np.uint64)
+        _check(self.ctx.lib.nqb_debug_pass_trace(self.ctx.handle, self.handle, _ptr(out),
+                                                 C.byref(g)), "nqb_debug_pass_trace")
+        return out[: g.value * (2 * self.steps + 2)].reshape(g.value, 2 * self.steps + 2)
+
+    def free(self):
+        if getattr(self, "handle", None):
+            self.ctx.lib.nqb_pass_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def make_factorized_layer(latent_u, latent_v, s1, s2, ctx: Context | None = None):

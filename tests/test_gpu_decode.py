@@ -186,3 +186,139 @@ def test_compact_and_pipelined_instances_bitwise(nq, chk, shape, monkeypatch):
         out[kb] = nq.DeviceLayer.upload(to_nq(nq, lay)).gemv_f32(x)
     assert np.array_equal(out["0"], out["1000000"])
     assert rel(out["0"], chk.gemv_packed_f32(lay, x)) <= TIGHT_TOL
+
+
+# ---- activation range, non-finite inputs, ring mode -------------
+@pytest.mark.parametrize("scale", [1e-4, 1e-2, 1.0, 1e2, "heavy"])
+def test_fp16_decode_across_activation_scales(nq, chk, scale):
+    """The activation exponent comes from the device max|x| for binary16 inputs
+    too, so tiny and large activations keep full relative precision."""
+    import torch
+    lays, devs = [], []
+    for i, (n, r) in enumerate([(4096, 1622), (1024, 300)]):
+        lay, dev = dev_layer(nq, chk, 0x5C00 + i, n, 4096, r)
+        lays.append(lay)
+        devs.append(dev)
+    rng = np.random.default_rng(17)
+    if scale == "heavy":
+        x = rng.standard_t(1.5, 4096) * 0.05
+        x = np.clip(x, -6e4, 6e4)
+    else:
+        x = rng.standard_normal(4096) * scale
+    xh = torch.from_numpy(x.astype(np.float16)).cuda()
+    xs = xh.float().cpu().numpy()
+    y = torch.empty(4096, dtype=torch.float16, device="cuda")
+    devs[0].gemv_device(xh, y)
+    want = chk.gemv_packed_f32(lays[0], xs)
+    ok = np.isfinite(want).all() and np.abs(want).max() < 6e4
+    if ok:
+        assert rel(y.float().cpu().numpy(), want) <= FWD_TOL
+    grp = nq.DecodeGroup(devs)
+    ys = [torch.empty(l.n, dtype=torch.float16, device="cuda") for l in lays]
+    grp.gemv_device(xh, ys)
+    torch.cuda.synchronize()
+    assert torch.equal(ys[0], y)
+    for lay, yy in zip(lays, ys):
+        want = chk.gemv_packed_f32(lay, xs)
+        if np.isfinite(want).all() and np.abs(want).max() < 6e4:
+            assert rel(yy.float().cpu().numpy(), want) <= FWD_TOL
+
+
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), -float("inf")])
+@pytest.mark.parametrize("dtype", ["f32", "f16"])
+def test_non_finite_input_gives_nan_outputs(nq, chk, bad, dtype):
+    """gemv_two_stage propagates a NaN/Inf activation into every output
+    (t_k = +-Inf for all k, then y_i = sum of mixed-sign Infs = NaN); the
+    kernel flags the input in its max|x| pass and writes NaN."""
+    import torch
+    lay, dev = dev_layer(nq, chk, 0xBAD, 300, 400, 96)
+    x = chk.rng(3).gaussian(400).astype(np.float32)
+    x[123] = bad
+    want = chk.gemv_packed_f32(lay, x)
+    assert np.isnan(want).all()
+    if dtype == "f32":
+        got = dev.gemv_f32(x)
+    else:
+        xd = torch.from_numpy(x.astype(np.float16)).cuda()
+        yd = torch.empty(300, dtype=torch.float16, device="cuda")
+        dev.gemv_device(xd, yd)
+        got = yd.float().cpu().numpy()
+    assert np.isnan(got).all()
+
+
+@pytest.mark.parametrize("kb", ["24", "48"])
+def test_forced_ring_mode(nq, chk, kb, monkeypatch):
+    """A small stream buffer forces ring mode (sections streamed through slots)."""
+    import torch
+    monkeypatch.setenv("NQB_DEC_SMEM_KB", kb)
+    lays, devs = [], []
+    for i, (n, m, r) in enumerate([(4096, 4096, 1622), (2048, 4096, 900)]):
+        lay, dev = dev_layer(nq, chk, 0x41A0 + i, n, m, r)
+        lays.append(lay)
+        devs.append(dev)
+    x = chk.rng(8).gaussian(4096).astype(np.float32)
+    for lay, dev in zip(lays, devs):
+        assert rel(dev.gemv_f32(x), chk.gemv_packed_f32(lay, x)) <= TIGHT_TOL
+    grp = nq.DecodeGroup(devs)
+    xd = torch.from_numpy(x).cuda()
+    ys = [torch.empty(l.n, dtype=torch.float32, device="cuda") for l in lays]
+    grp.gemv_device(xd, ys)
+    torch.cuda.synchronize()
+    for lay, y in zip(lays, ys):
+        assert rel(y.cpu().numpy(), chk.gemv_packed_f32(lay, x)) <= TIGHT_TOL
+
+
+def test_70b_gate_up_group_and_high_bitrate_layer(nq, chk):
+    """Streams larger than the buffer (ring mode by default): a 70B gate/up group
+    and a 70B q layer at 1.0 bit (r = 4080)."""
+    import torch
+    rng = np.random.default_rng(99)
+    specs = [(28672, 8192, 3488), (28672, 8192, 3488)]
+    devs, lays = [], []
+    for i, (n, m, r) in enumerate(specs):
+        lay, dev = dev_layer(nq, chk, 0x70A0 + i, n, m, r)
+        lays.append(lay)
+        devs.append(dev)
+    grp = nq.DecodeGroup(devs)
+    x = chk.rng(12).gaussian(8192).astype(np.float32)
+    ys = [torch.empty(n, dtype=torch.float32, device="cuda") for n, _, _ in specs]
+    grp.gemv_device(torch.from_numpy(x).cuda(), ys)
+    torch.cuda.synchronize()
+    for lay, y in zip(lays, ys):
+        assert rel(y.cpu().numpy(), chk.gemv_packed_f32(lay, x)) <= TIGHT_TOL
+    lay, dev = dev_layer(nq, chk, 0x70B0, 8192, 8192, 4080)
+    x = chk.rng(13).gaussian(8192).astype(np.float32)
+    assert rel(dev.gemv_f32(x), chk.gemv_packed_f32(lay, x)) <= TIGHT_TOL
+
+
+def test_graph_then_bigger_upload_keeps_graph_valid(nq, chk):
+    """A graph captured before an upload that grows the decode state keeps
+    replaying correctly (old state retired, not freed)."""
+    import torch
+    ctx = nq.context(0)
+    lay, dev = dev_layer(nq, chk, 0x6A1, 512, 512, 128)
+    x = torch.from_numpy(chk.rng(1).gaussian(512).astype(np.float32)).cuda()
+    y = torch.empty(512, dtype=torch.float32, device="cuda")
+    dev.gemv_device(x, y)
+    torch.cuda.synchronize()
+    want = y.clone()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        ctx.bind_torch_stream()
+        with ctx.capture() as cap:
+            dev.gemv_device(x, y)
+    torch.cuda.synchronize()
+    ctx.bind_torch_stream()
+    # a group far larger than the current state capacity (rows of t)
+    big = [dev_layer(nq, chk, 0x6B0 + i, 64, 512, 16000)[1] for i in range(3)]
+    grp = nq.DecodeGroup(big)
+    with torch.cuda.stream(side):
+        for _ in range(3):
+            y.zero_()
+            cap.graph.launch()
+            torch.cuda.synchronize()
+            assert torch.equal(y, want)
+    torch.cuda.synchronize()
+    ctx.bind_torch_stream()
+    del grp
