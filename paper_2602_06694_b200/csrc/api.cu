@@ -721,7 +721,7 @@ int nqb_debug_pass_trace(nqb_context* ctx, const nqb_pass* pass, uint64_t* stamp
   check_ctx(ctx);
   NQB_REQUIRE(pass != nullptr && stamps != nullptr, NQB_E_VALIDATION, "null argument");
   if (grid) *grid = pass->G;
-  const size_t words = (size_t)pass->G * (2 * pass->K + 2);
+  const size_t words = pass_trace_words(pass);
   DevBuf buf(ctx, words * 8);
   NQB_CUDA(cudaMemsetAsync(buf.p, 0, words * 8, ctx->stream));
   pass_launch(ctx, pass, buf.as<unsigned long long>());

@@ -185,9 +185,6 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   TRACE(12);
   if (n1) {
     const long long A = sum_partials(red8);
-    // one CTA per slab range publishes sum|a_int| (bounds every |t_k| of the segment)
-    if (tid == 0 && C.s1_rt0 == 0)
-      red_add_u64(&p.st->abs_a[b][C.s1_seg], sum_partials(red8 + kConsumerWarps));
     long long* Tseg = p.T + (size_t)b * p.r_cap + p.seg[C.s1_seg].t_off + (size_t)C.s1_rt0 * 16;
     for (uint32_t i = tid; i < (uint32_t)C.s1_rtn * 16; i += kConsumerThreads) {
       const long long v = 2 * row_value(red + i * kRedStride) - A;
@@ -237,10 +234,7 @@ __global__ void __launch_bounds__(kThreads, (kConsumerWarps <= 8 ? 2 : 1)) k_dec
   // ------------------------------------------------------------------ stage 2
   const Seg& S = p.seg[C.s2_seg];
   const int ea = act_exponent(S.s2max, xmax);
-  // |t_k| = |sum_j +-a_int_j| <= sum_j |a_int_j|, published exactly by stage 1
-  const unsigned long long tbound = __ldcg((const unsigned long long*)&st->abs_a[b][C.s2_seg]);
-  const int et = tbound ? 64 - __clzll((long long)tbound) : 0;  // |t_k| < 2^et
-  const int sh = et - kFix;
+  const int sh = t_shift(m);  // |t_k| < 2^(kFix + sh)
   const long long* Tseg = p.T + (size_t)b * p.r_cap + S.t_off;
   const uint32_t nquad2 = kpad(S.r) / 4;
   long long tsum = 0;

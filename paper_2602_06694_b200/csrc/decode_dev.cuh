@@ -64,18 +64,35 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 
 // mbarrier wait with a watchdog: a wait that never completes traps the
 // launch (reported as a CUDA error) instead of hanging the device.
-__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity) {
+// With `suspend` the wait sleeps (suspend-time hint) instead of spinning, so
+// waiting warps leave the issue slots to the warps that have work.
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, bool suspend = false) {
   uint32_t ok = 0, it = 0;
+  unsigned long long t0 = 0;
   for (;;) {
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P;\n\t}\n"
-        : "=r"(ok)
-        : "r"(tc::smem_u32(bar)), "r"(parity)
-        : "memory");
+    if (suspend)
+      asm volatile(
+          "{\n\t.reg .pred P;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+          "selp.u32 %0, 1, 0, P;\n\t}\n"
+          : "=r"(ok)
+          : "r"(tc::smem_u32(bar)), "r"(parity), "r"(0x989680u)
+          : "memory");
+    else
+      asm volatile(
+          "{\n\t.reg .pred P;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, P;\n\t}\n"
+          : "=r"(ok)
+          : "r"(tc::smem_u32(bar)), "r"(parity)
+          : "memory");
     if (ok) return;
-    if (++it > (1u << 24)) __trap();
+    // watchdog (wall clock: a suspended try_wait may sleep): trap after ~10 s
+    if ((++it & 255u) == 0) {
+      const unsigned long long now = globaltimer();
+      if (!t0) t0 = now;
+      else if (now - t0 > 10000000000ull) __trap();
+    }
   }
 }
 
@@ -196,10 +213,10 @@ __device__ __forceinline__ unsigned long long cta_max_u64(unsigned long long v,
 }
 
 __device__ __forceinline__ int exponent_of(float M) {
-  if (!(M > 0.f) || isinf(M)) return 0;
-  int e;
-  frexpf(M, &e);
-  return e;  // M < 2^e
+  const uint32_t b = __float_as_uint(M);
+  if (!(M > 0.f) || b >= 0x7f800000u) return 0;
+  if (b >= 0x00800000u) return (int)(b >> 23) - 126;  // normal: frexp exponent, M < 2^e
+  return -126 - __clz((int)b) + 9;                    // subnormal: M < 2^(-149 + bitlength)
 }
 
 // Exponent of the activation bound: |a| = |s2 x| <= s2max * xmax < 2^(e(s2max) + e(xmax)).
@@ -261,6 +278,14 @@ __device__ __forceinline__ float x_absmax(const void* x, uint32_t m, bool f32, b
 #pragma unroll
   for (int w = 0; w < kConsumerWarps; ++w) mx = fmaxf(mx, xred[w]);
   return mx;
+}
+
+// Right shift that takes t to 38-bit fixed point: |a_int| <= 2^kFix, so
+// |t_k| <= m 2^kFix < 2^(kFix + ceil_log2(m) + 1).  A bound known before stage 1
+// (no published sum|a| on the critical path); t keeps >= 2^-30 relative
+// resolution of its largest possible magnitude, far below the 1e-3 bar.
+__device__ __forceinline__ int t_shift(uint32_t m) {
+  return (m <= 1 ? 0 : 32 - __clz((int)(m - 1))) + 1;
 }
 
 __device__ __forceinline__ bool is_inf(float v) { return __float_as_int(v) == 0x7f800000; }

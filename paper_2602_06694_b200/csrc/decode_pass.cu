@@ -3,10 +3,15 @@
 //
 // Arithmetic is the per-call kernel's (decode.cu, gemv_two_stage of
 // packed.cpp:153-192 in exact integer IMMA form), so a layer's output is the
-// same function of its input in both kernels; only the activation bound of a
-// chained step comes from the producing step's published max|y| instead of a
-// pass over x.
+// same function of its input in both kernels: the activation exponent comes
+// from max|x| (a prepass or the producing step's published max|y|, equal to
+// the per-call kernel's own pass over x) and the t exponent from m.
+//
+// This translation unit runs 12 consumer warps (+4 helper warps = 512 threads,
+// 128 registers per thread at one CTA per SM).
+#define NQB_DEC_WARPS 12
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -17,32 +22,53 @@
 namespace nqb {
 namespace dec {
 
-__device__ __forceinline__ void wait_ctr(const unsigned long long* c, unsigned long long target) {
-  if (threadIdx.x == 0) {
-    unsigned long long cur;
-    const unsigned long long t0 = globaltimer();
-    for (uint32_t it = 0;; ++it) {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(cur) : "l"(c) : "memory");
-      if (cur >= target) break;
-      // watchdog: a barrier that does not complete within seconds means the
-      // grid is not co-resident or diverged; fail the launch instead of hanging
-      if ((it & 255u) == 255u && globaltimer() - t0 > 4000000000ull) __trap();
-    }
-  }
-  consumers_sync();
-}
+constexpr int kPassThreads = kConsumerThreads + 32 * kPassHelpers;
 
+// ---- global-memory handshakes (helper warps only; one lane) -------------------
+__device__ __forceinline__ void poll_ctr(const unsigned long long* c, unsigned long long target) {
+  unsigned long long cur;
+  const unsigned long long t0 = globaltimer();
+  for (uint32_t it = 0;; ++it) {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(cur) : "l"(c) : "memory");
+    if (cur >= target) break;
+    __nanosleep(32);  // leave the issue slots to the consumer warps
+    // watchdog: a barrier that does not complete within seconds means the grid
+    // is not co-resident or diverged; fail the launch instead of hanging
+    if ((it & 255u) == 255u && globaltimer() - t0 > 4000000000ull) __trap();
+  }
+  // the data behind the barrier is read next by TMA (async proxy)
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
 __device__ __forceinline__ void arrive_ctr(unsigned long long* c) {
-  consumers_sync();  // the CTA's prior global writes / reds happen-before the release
-  if (threadIdx.x == 0)
-    asm volatile("red.release.gpu.global.add.u64 [%0], 1;\n" ::"l"(c) : "memory");
+  asm volatile("red.release.gpu.global.add.u64 [%0], 1;\n" ::"l"(c) : "memory");
+}
+// LSU-path async copy (cp.async, not the TMA engine): small staging copies
+// must not queue behind the CTA's weight stream in the TMA unit.
+__device__ __forceinline__ void lsu_copy16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(smem_dst)),
+               "l"(gsrc)
+               : "memory");
+}
+// Copies `bytes` (multiple of 16, both ends 16-byte aligned) with all 32 lanes
+// and hooks completion onto `bar` (each lane's async arrive is pre-counted).
+__device__ __forceinline__ void lsu_copy(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                         uint64_t* bar, int lane) {
+  for (uint32_t i = 16u * lane; i < bytes; i += 512u)
+    lsu_copy16((uint8_t*)smem_dst + i, (const uint8_t*)gsrc + i);
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(tc::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* c) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(c) : "memory");
+  return v;
 }
 
 // Stage geometry of one CTA in one step.
 struct StageGeo {
-  uint32_t rtn, nsec, K, slab0, klo, kfirst;  // kfirst: k0 of section 0
-  uint64_t src_off;                          // byte offset of section 0 in the step's bits
-  uint32_t prefix, suffix;                   // staged scale bytes (stage 1: s2, stage 2: s1)
+  uint32_t rtn, nsec, K, slab0, klo;
+  uint64_t src_off;   // byte offset of section 0 in the step's bits
+  uint32_t prefix, suffix;  // staged scale bytes (stage 1: s2, stage 2: s1)
 };
 
 __device__ __forceinline__ StageGeo stage1_geo(const StepDesc& D, const Cta& C) {
@@ -52,11 +78,10 @@ __device__ __forceinline__ StageGeo stage1_geo(const StepDesc& D, const Cta& C) 
   g.nsec = C.s1_sln;
   g.K = D.m;
   g.slab0 = C.s1_sl0;
-  g.klo = g.kfirst = slab_of(D.m, C.s1_sl0).k0;
+  g.klo = slab_of(D.m, C.s1_sl0).k0;
   const Slab last = slab_of(D.m, C.s1_sl0 + C.s1_sln - 1);
-  const uint32_t nk1 = last.k0 + 32 * last.nq - g.klo;
   g.src_off = C.stream_off;
-  g.prefix = 2 * nk1;
+  g.prefix = 2 * (last.k0 + 32 * last.nq - g.klo);
   return g;
 }
 
@@ -67,8 +92,6 @@ __device__ __forceinline__ StageGeo stage2_geo(const StepDesc& D, const Cta& C) 
   g.rtn = C.s2_rtn;
   g.nsec = nslabs(r);
   g.K = r;
-  g.slab0 = 0;
-  g.klo = g.kfirst = 0;
   uint64_t s1b = 0;
   if (C.s1_rtn && C.s1_sln) {
     const uint32_t k0 = slab_of(D.m, C.s1_sl0).k0;
@@ -106,35 +129,45 @@ __device__ __forceinline__ uint64_t ring_place(uint64_t& pos, uint32_t bytes, ui
   return start;
 }
 
+// Where the producer put a chunk (written before the chunk's copies are issued;
+// the consumers read it after the chunk's full barrier): the consumers never
+// repeat the section / ring arithmetic.
+struct ChunkRec {
+  uint32_t off;     // ring byte offset of the chunk (prefix first)
+  uint16_t s0, s1;  // sections [s0, s1) of the stage
+  uint32_t pre;     // prefix bytes (stage-1 s2 scales) before the sections
+  uint32_t sb;      // section bytes (the stage-2 s1 scales follow them in the last chunk)
+};
+
 // All (tile pair, section) work of one resident chunk, split over the consumer
-// warps (the per-call kernel's linear-mode loop, decode.cu run_stage<true>);
+// warps (the per-call kernel's linear-mode loop, decode_dev.cuh run_stage);
 // leaves the chunk's partial row sums added into red[].
 __device__ __forceinline__ void run_chunk(const uint8_t* base, const StageGeo& g, uint32_t s0,
                                           uint32_t nsec, const uint8_t* bfrag, int* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t gq = lane >> 2, c = lane & 3;
-  int acc[2][4][4];
-#pragma unroll
-  for (int j = 0; j < 2; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[j][q][0] = acc[j][q][1] = acc[j][q][2] = acc[j][q][3] = 0;
   const uint32_t rtn = g.rtn;
   const uint32_t npair = (rtn + 1) / 2, U = npair * nsec;
   const uint32_t f0 = (uint32_t)((uint64_t)U * warp / kConsumerWarps);
   const uint32_t f1 = (uint32_t)((uint64_t)U * (warp + 1) / kConsumerWarps);
   if (f0 >= f1) return;
+  int acc[2][4][4];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[j][q][0] = acc[j][q][1] = acc[j][q][2] = acc[j][q][3] = 0;
   uint32_t F, rem;
   slab_split(g.K, F, rem);
   const uint32_t sl_first = g.slab0 + s0;  // absolute slab of the chunk's first section
   const uint32_t k_first = slab_of(g.K, sl_first).k0;
   const uint32_t nfull = F > sl_first ? F - sl_first : 0;  // full slabs come first
   uint32_t cur = f0 / nsec;
-  uint2 b[8];
-  for (uint32_t f = f0; f < f1;) {
-    const uint32_t pr = f / nsec;
-    uint32_t s = f - pr * nsec;
+  uint32_t snext = f0 - cur * nsec;
+  for (uint32_t f = f0, pr = cur; f < f1; ++pr) {
+    uint32_t s = snext;
     const uint32_t send = min(nsec, s + (f1 - f));
-    f = pr * nsec + send;
+    f += send - s;
+    snext = 0;
     if (pr != cur) {
       flush_rows(acc[0], red + 2 * cur * 16 * kRedStride, lane);
       if (2 * cur + 1 < rtn) flush_rows(acc[1], red + (2 * cur + 1) * 16 * kRedStride, lane);
@@ -152,6 +185,7 @@ __device__ __forceinline__ void run_chunk(const uint8_t* base, const StageGeo& g
       s = sf;
     }
     for (; s < send; ++s) {  // the 128 / 64 tails
+      uint2 b[8];
       const Slab sl = slab_of(g.K, sl_first + s);
       const uint32_t ub = unit_bytes(sl.nq);
       const uint8_t* unit = base + 2u * rtn * (sl.k0 - k_first) + t0 * ub;
@@ -164,44 +198,136 @@ __device__ __forceinline__ void run_chunk(const uint8_t* base, const StageGeo& g
   if (2 * cur + 1 < rtn) flush_rows(acc[1], red + (2 * cur + 1) * 16 * kRedStride, lane);
 }
 
-// Phase order shared by producer and consumers: S1(0), then per step k
-// [S1(k+1) if lookahead] S2(k) [S1(k+1) otherwise].
-template <typename S1, typename S2, typename DescOf>
-__device__ __forceinline__ void for_each_phase(uint32_t K, DescOf desc_of, S1 s1, S2 s2) {
-  s1(0u);
-  uint32_t next1 = 1;
-  for (uint32_t k = 0; k < K; ++k) {
-    const bool la = (desc_of(k).flags & kStepLookahead) != 0;
-    if (k + 1 < K && la && next1 == k + 1) s1(next1++);
-    s2(k);
-    if (k + 1 < K && next1 == k + 1) s1(next1++);
+// Sections [sa, sb) of row-tile pair pr inside a resident chunk whose first
+// section is s0c, accumulated into acc and flushed into red[] (pair's rows).
+__device__ __forceinline__ void run_pair(const uint8_t* base, const StageGeo& g, uint32_t s0c,
+                                         uint32_t pr, uint32_t sa, uint32_t sb,
+                                         const uint8_t* bfrag, int* red, int (&acc)[2][4][4]) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gq = lane >> 2, c = lane & 3;
+  const uint32_t rtn = g.rtn, t0 = 2 * pr;
+  const bool two = t0 + 1 < rtn;
+  uint32_t F, rem;
+  slab_split(g.K, F, rem);
+  const uint32_t sl0 = g.slab0 + s0c;  // absolute slab of the chunk's first section
+  const uint32_t k_first = slab_of(g.K, sl0).k0;
+  const uint32_t nfull = F > sl0 ? F - sl0 : 0;  // chunk-relative sections that are full slabs
+  uint32_t s = sa - s0c;
+  const uint32_t send = sb - s0c, sf = min(send, nfull);
+  if (s < sf) {
+    const uint32_t k0 = 256 * (sl0 + s);
+    const uint8_t* unit = base + 2u * rtn * (k0 - k_first) + t0 * 512;
+    const uint8_t* bp = bfrag + kBytesPerK * (k0 - g.klo) + (gq * 4 + c) * 16;
+    if (two) full_run<2>(unit, 512u * rtn, bp, sf - s, lane, gq < (uint32_t)kLimbs, acc);
+    else full_run<1>(unit, 512u * rtn, bp, sf - s, lane, gq < (uint32_t)kLimbs, acc);
+    s = sf;
   }
+  for (; s < send; ++s) {  // the 128 / 64 tails
+    uint2 b[8];
+    const Slab sl = slab_of(g.K, sl0 + s);
+    const uint32_t ub = unit_bytes(sl.nq);
+    const uint8_t* unit = base + 2u * rtn * (sl.k0 - k_first) + t0 * ub;
+    load_b(bfrag, g.klo, sl, gq, c, b);
+    if (two) tiles_mma<2>(unit, ub, sl.nq, lane, b, acc);
+    else tiles_mma<1>(unit, ub, sl.nq, lane, b, acc);
+  }
+  flush_rows(acc[0], red + t0 * 16 * kRedStride, lane);
+  if (two) flush_rows(acc[1], red + (t0 + 1) * 16 * kRedStride, lane);
 }
 
+// max|x| bits over x[lo, hi): binary16 magnitude bits (>= 0x7C00: non-finite)
+// or |fp32| bits (non-finite -> +Inf bits), so every bound is an ordered uint.
+__device__ __forceinline__ uint32_t absmax_bits(const void* x, uint32_t lo, uint32_t hi, bool f32,
+                                                bool vec, uint32_t t, uint32_t nt) {
+  uint32_t mb = 0;
+  if (f32) {
+    const uint32_t* xf = (const uint32_t*)x;
+    uint32_t i = lo + t * 4;
+    if (vec)
+      for (; i + 3 < hi; i += 4 * nt) {
+        const uint4 v = __ldcg((const uint4*)(xf + i));
+        mb = max(mb, max(max(v.x & 0x7FFFFFFFu, v.y & 0x7FFFFFFFu),
+                         max(v.z & 0x7FFFFFFFu, v.w & 0x7FFFFFFFu)));
+      }
+    for (uint32_t j = i; j < min(hi, i + 4); ++j) mb = max(mb, __ldcg(xf + j) & 0x7FFFFFFFu);
+    if (!vec)
+      for (uint32_t j = lo + t; j < hi; j += nt) mb = max(mb, __ldcg(xf + j) & 0x7FFFFFFFu);
+    return mb >= 0x7F800000u ? 0x7F800000u : mb;
+  }
+  const unsigned short* xh = (const unsigned short*)x;
+  uint32_t i = lo + t * 8;
+  if (vec)
+    for (; i + 7 < hi; i += 8 * nt) {
+      const uint4 v = __ldcg((const uint4*)(xh + i));
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) mb = max(mb, max(w[e] & 0x7FFFu, (w[e] >> 16) & 0x7FFFu));
+    }
+  if (vec) {
+    for (uint32_t j = i; j < min(hi, i + 8); ++j) mb = max(mb, (uint32_t)(__ldcg(xh + j) & 0x7FFFu));
+  } else {
+    for (uint32_t j = lo + t; j < hi; j += nt) mb = max(mb, (uint32_t)(__ldcg(xh + j) & 0x7FFFu));
+  }
+  return mb;
+}
+// Bound bits -> float max|x| (+Inf for a non-finite input).
+__device__ __forceinline__ float bound_value(uint32_t bits, bool f32) {
+  if (f32) return __uint_as_float(bits);
+  return bits >= 0x7C00u ? __int_as_float(0x7f800000)
+                         : __half2float(__ushort_as_half((unsigned short)bits));
+}
+// Share [lo, hi) of m inputs for CTA b of G (8-aligned boundaries).
+__device__ __forceinline__ void share_of(uint32_t m, uint32_t b, uint32_t G, uint32_t& lo,
+                                         uint32_t& hi) {
+  const uint32_t units = (m + 7) / 8, per = (units + G - 1) / G;
+  lo = min(m, 8 * per * b);
+  hi = min(m, lo + 8 * per);
+}
+
+#define PSTAMP(k, i)                                                           \
+  do {                                                                         \
+    if (kTrace) trp[1 + kPassStamps * (k) + (i)] = globaltimer();              \
+  } while (0)
+
 template <bool kTrace>
-__global__ void __launch_bounds__(kThreads, 1) k_decode_pass(const __grid_constant__ PassParams p) {
+__global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_constant__ PassParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = (uint64_t*)smem;
   uint64_t* empty = full + kPassSlots;
   uint64_t* dfull = empty + kPassSlots;
   uint64_t* dempty = dfull + kDescSlots;
-  uint8_t* dslots = (uint8_t*)(dempty + kDescSlots);
+  uint64_t* xfull = dempty + kDescSlots;
+  uint64_t* xempty = xfull + kXSlots;
+  uint64_t* tfull = xempty + kXSlots;
+  uint64_t* tempty = tfull + kMaxTSlots;
+  uint64_t* cdone = tempty + kMaxTSlots;
+  uint32_t* misc = (uint32_t*)(cdone + kDoneRing);  // [0] parity, [2..3] target
+  uint8_t* dslots = (uint8_t*)misc + 64;
   long long* red8 = (long long*)(dslots + kDescSlots * kDescSlotBytes);
   float* xred = (float*)((uint8_t*)red8 + 256);
-  unsigned long long* misc = (unsigned long long*)((uint8_t*)xred + 64);  // [0] launch target
-  int* red = (int*)((uint8_t*)misc + 64);
-  uint8_t* bfrag = smem + pass_head_bytes();
-  uint8_t* ring = bfrag + p.bfrag_bytes;
+  float* xmaxs = xred + 16;  // max|x| of steps in flight (ring of 16)
+  ChunkRec* recs = (ChunkRec*)((uint8_t*)xred + 128);
+  int* red1 = (int*)(recs + kPassSlots);       // stage-1 row sums
+  // stage-2 row sums and B fragments: own buffers only when a phase runs both stages
+  int* red2 = p.fused ? red1 + kMaxRt * 16 * kRedStride : red1;
+  uint8_t* bfrag1 = smem + p.head_bytes;                          // stage-1 (x limbs)
+  uint8_t* bfrag2 = p.fused ? bfrag1 + p.bfrag_bytes : bfrag1;    // stage-2 (t limbs)
+  uint8_t* xslots = bfrag2 + p.bfrag_bytes;
+  uint8_t* tslots = xslots + kXSlots * p.xslot_bytes;
+  const uint32_t TS = p.tslots;
+  uint8_t* ring = tslots + TS * p.tslot_bytes;
 
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(~0u, tid >> 5, 0);
-  const uint32_t K = p.K, RB = p.ring_bytes, cap = p.chunk_cap;
+  const uint32_t K = p.K, G = p.G, RB = p.ring_bytes, cap = p.chunk_cap;
+  const bool sus = (p.debug & 4u) != 0;
   auto desc_of = [&](uint32_t k) -> const StepDesc& {
     return *(const StepDesc*)(dslots + (k % kDescSlots) * kDescSlotBytes);
   };
   auto cta_of = [&](uint32_t k) -> const Cta& {
     return *(const Cta*)(dslots + (k % kDescSlots) * kDescSlotBytes + 480);
   };
+  auto wait_desc = [&](uint32_t k) { mbar_wait_wd(&dfull[k % kDescSlots], (k / kDescSlots) & 1, sus); };
 
   if (tid == 0) {
     for (int s = 0; s < kPassSlots; ++s) {
@@ -210,316 +336,480 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode_pass(const __grid_consta
     }
     for (int s = 0; s < kDescSlots; ++s) {
       tc::mbar_init(&dfull[s], 1);
-      tc::mbar_init(&dempty[s], kConsumerWarps);
+      tc::mbar_init(&dempty[s], 4);  // consumers, producer, x stager, t loader
     }
+    for (int s = 0; s < kXSlots; ++s) {
+      tc::mbar_init(&xfull[s], 1);
+      tc::mbar_init(&xempty[s], 1);
+    }
+    for (int s = 0; s < kMaxTSlots; ++s) {
+      tc::mbar_init(&tfull[s], 1);
+      tc::mbar_init(&tempty[s], 1);
+    }
+    for (int s = 0; s < kDoneRing; ++s) tc::mbar_init(&cdone[s], 1);
     tc::fence_mbar_init();
+    const unsigned long long gen = ld_relaxed_u64(p.ctr);
+    misc[0] = (uint32_t)(gen & 1);
+    *(unsigned long long*)(misc + 2) = (gen + 1) * G;
   }
   __syncthreads();
+  const uint32_t par = misc[0];
+  const unsigned long long target = *(const unsigned long long*)(misc + 2);
+  unsigned long long* xinit = p.ctr + kCtrStride;
+  unsigned long long* tbar = p.ctr + 2 * kCtrStride;
+  unsigned long long* ybar = tbar + (size_t)K * kCtrStride;
+  unsigned* amax = p.amax + (size_t)par * p.amax_words * 4;
+  long long* arena = p.arena + (size_t)par * p.arena_len;
+  unsigned long long* trp = nullptr;
+  if (kTrace) {
+    trp = p.trace + (size_t)blockIdx.x * (kPassStamps * K + 2);
+    if (tid == 0) trp[0] = globaltimer();
+  }
 
-  // ------------------------------------------------------------------ producer
-  if (warp == kConsumerWarps) {
-    uint64_t pos = 0;
-    uint32_t chunk = 0, rel = 0;
-    uint64_t ends[kPassSlots];
-    auto load_desc = [&](uint32_t k) {
-      const uint32_t slot = k % kDescSlots;
-      if (k >= (uint32_t)kDescSlots) mbar_wait_wd(&dempty[slot], ((k / kDescSlots) - 1) & 1);
-      uint8_t* dst = dslots + slot * kDescSlotBytes;
-      const uint4* src = (const uint4*)(p.desc + k);
-      if (lane < (int)(kDescBytes / 16)) ((uint4*)dst)[lane] = __ldg(src + lane);
-      const StepDesc* Dg = p.desc + k;
-      if (lane == 30 || lane == 31) {
-        const uint4* cs = (const uint4*)(Dg->ctas + blockIdx.x);
-        ((uint4*)(dst + 480))[lane - 30] = __ldg(cs + (lane - 30));
-      }
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&dfull[slot]);
-    };
-    auto issue_stage = [&](uint32_t k, int stage) {
-      const StepDesc& D = desc_of(k);
-      const Cta& C = cta_of(k);
-      const StageGeo g = stage == 1 ? stage1_geo(D, C) : stage2_geo(D, C);
-      if (!g.nsec) return;
-      uint32_t s0 = 0;
-      uint64_t src = g.src_off;
-      while (s0 < g.nsec) {
-        uint32_t s1;
-        const uint32_t sb = chunk_span(g, s0, cap, &s1);
-        const uint32_t pre = s0 == 0 ? g.prefix : 0;
-        const uint32_t suf = s1 == g.nsec ? g.suffix : 0;
-        const uint32_t bytes = pre + sb + (suf + 127) / 128 * 128;
-        const uint64_t start = ring_place(pos, bytes, RB);
-        // wait for the slot and for every older chunk overlapping this range
-        while (rel < chunk && (chunk - rel >= (uint32_t)kPassSlots || ends[rel % kPassSlots] + RB > pos)) {
-          mbar_wait_wd(&empty[rel % kPassSlots], (rel / kPassSlots) & 1);
-          ++rel;
-        }
-        ends[chunk % kPassSlots] = pos;
-        if (lane == 0) {
-          uint64_t* bar = &full[chunk % kPassSlots];
-          uint8_t* dst = ring + (uint32_t)(start % RB);
-          tc::mbar_arrive_expect_tx(bar, pre + sb + suf);
-          if (pre) {
-            const Seg& S = D.seg[C.s1_seg];
-            tc::bulk_g2s(dst, S.s2h + g.klo, pre, bar);
+  // ============================================================= helper warps
+  if (warp >= kConsumerWarps) {
+    const int role = warp - kConsumerWarps;
+    if (role == 0) {
+      // ------------------------------------------------------------ producer
+      if (lane != 0) return;
+      uint64_t pos = 0;
+      uint32_t chunk = 0, rel = 0;
+      uint64_t starts[kPassSlots];
+      auto issue_stage = [&](uint32_t k, int stage) {
+        const StepDesc& D = desc_of(k);
+        const Cta& C = cta_of(k);
+        const StageGeo g = stage == 1 ? stage1_geo(D, C) : stage2_geo(D, C);
+        uint32_t s0 = 0;
+        uint64_t src = g.src_off;
+        while (s0 < g.nsec) {
+          uint32_t s1;
+          const uint32_t sb = chunk_span(g, s0, cap, &s1);
+          const uint64_t start = ring_place(pos, sb, RB);
+          // wait for the slot and for every older chunk this range overwrites: chunks
+          // are placed monotonically, so [start, pos) reaches older chunk c's bytes
+          // in the ring exactly when pos > start_c + RB
+          while (rel < chunk &&
+                 (chunk - rel >= (uint32_t)kPassSlots || starts[rel % kPassSlots] + RB < pos)) {
+            mbar_wait_wd(&empty[rel % kPassSlots], (rel / kPassSlots) & 1, sus);
+            ++rel;
           }
-          tc::bulk_g2s(dst + pre, D.bits + src, sb, bar);
-          if (suf) {
-            const Seg& S = D.seg[C.s2_seg];
-            tc::bulk_g2s(dst + pre + sb, S.s1h + (size_t)C.s2_rt0 * 16, suf, bar);
+          starts[chunk % kPassSlots] = start;
+          uint64_t* bar = &full[chunk % kPassSlots];
+          const uint32_t roff = (uint32_t)(start % RB);
+          uint8_t* dst = ring + roff;
+          recs[chunk % kPassSlots] = ChunkRec{roff, (uint16_t)s0, (uint16_t)s1, 0u, sb};
+          tc::mbar_arrive_expect_tx(bar, sb);
+          tc::bulk_g2s(dst, D.bits + src, sb, bar);
+          src += sb;
+          s0 = s1;
+          ++chunk;
+        }
+      };
+      uint32_t n1 = 0;
+      for (uint32_t k = 0; k < K; ++k) {
+        wait_desc(k);
+        const uint32_t ahead = desc_of(k).s1_ahead;
+        while (n1 < ahead) {
+          wait_desc(n1);
+          if (kTrace) PSTAMP(n1, 11);
+          issue_stage(n1, 1);
+          if (kTrace) PSTAMP(n1, 6);
+          ++n1;
+        }
+        if (kTrace) PSTAMP(k, 14);
+        issue_stage(k, 2);
+        if (kTrace) PSTAMP(k, 15);
+        tc::mbar_arrive(&dempty[k % kDescSlots]);
+      }
+      return;
+    }
+    if (role == 1) {
+      // ----------------------------------------------------------- x stager
+      // clear this CTA's share of the other parity's bound words (used by the
+      // previous launch, which has completed)
+      {
+        unsigned* other = p.amax + (size_t)(par ^ 1) * p.amax_words * 4;
+        const uint32_t per = (p.amax_words + G - 1) / G;
+        const uint32_t lo = min(p.amax_words, per * blockIdx.x), hi = min(p.amax_words, lo + per);
+        for (uint32_t i = lo + lane; i < hi; i += 32) other[4 * i] = 0u;
+      }
+      bool pre_done = p.has_pre == 0;
+      int32_t ywaited = -1;
+      for (uint32_t j = 0; j < K; ++j) {
+        const uint32_t slot = j % kXSlots;
+        if (j >= (uint32_t)kXSlots) mbar_wait_wd(&xempty[slot], ((j / kXSlots) - 1) & 1, sus);
+        wait_desc(j);
+        const StepDesc& D = desc_of(j);
+        const Cta& C = cta_of(j);
+        const StageGeo g = stage1_geo(D, C);
+        uint8_t* xs = xslots + slot * p.xslot_bytes;
+        uint64_t* bar = &xfull[slot];
+        // every CTA needs the bound (stage 2 uses it), the slice only with stage-1 work
+        if (lane == 0) {
+          if (D.x_src >= 0 && D.x_src > ywaited) {
+            poll_ctr(ybar + (size_t)D.x_src * kCtrStride, target);
+            ywaited = D.x_src;
+          }
+          if ((D.flags & kStepXPre) && !pre_done) {
+            poll_ctr(xinit, target);
+            pre_done = true;
           }
         }
         __syncwarp();
-        src += sb;
-        s0 = s1;
-        ++chunk;
+        const bool f32 = D.flags & kStepXF32;
+        const uint32_t esz = f32 ? 4 : 2;
+        if (D.flags & kStepXSelf) {  // whole-input bound, read after the dependency
+          uint32_t mb = absmax_bits(D.x, 0, D.m, f32, (D.flags & kStepXVec) != 0, lane, 32);
+#pragma unroll
+          for (int o = 16; o; o >>= 1) mb = max(mb, __shfl_xor_sync(~0u, mb, o));
+          if (lane == 0) *(uint32_t*)xs = mb;
+        }
+        uint32_t bulk = 0, s2b = 0;
+        const uint8_t* src = nullptr;
+        if (g.nsec) {
+          s2b = g.prefix;  // the segment's s2 slice (padded allocation, 128-byte aligned start)
+          const uint32_t hi = min(D.m, g.klo + g.prefix / 2);
+          const uint32_t nb = (hi - g.klo) * esz;
+          src = (const uint8_t*)D.x + (size_t)g.klo * esz;
+          if (D.flags & kStepXVec) bulk = nb / 16 * 16;
+          for (uint32_t b = bulk + lane; b < nb; b += 32) xs[16 + b] = __ldcg(src + b);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          const bool by_copy = !(D.flags & kStepXSelf);
+          tc::mbar_arrive_expect_tx(bar, bulk + s2b + (by_copy ? 16 : 0));
+          if (by_copy) tc::bulk_g2s(xs, amax + 4 * (size_t)D.amax_idx, 16, bar);
+          if (bulk) tc::bulk_g2s(xs + 16, src, bulk, bar);
+          if (s2b) tc::bulk_g2s(xs + p.xs2_off, D.seg[C.s1_seg].s2h + g.klo, s2b, bar);
+        }
+        if (kTrace && lane == 0) PSTAMP(j, 5);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&dempty[j % kDescSlots]);
       }
+      return;
+    }
+    if (role == 2) {
+      // ------------------------------------------------------------ t loader
+      for (uint32_t k = 0; k < K; ++k) {
+        const uint32_t slot = k % TS;
+        if (k >= TS) mbar_wait_wd(&tempty[slot], ((k / TS) - 1) & 1, sus);
+        if (kTrace && lane == 0) PSTAMP(k, 12);
+        wait_desc(k);
+        const StepDesc& D = desc_of(k);
+        const Cta& C = cta_of(k);
+        if (lane == 0) {
+          if (C.s2_rtn || (k == 0 && blockIdx.x == 0)) poll_ctr(tbar + (size_t)k * kCtrStride, target);
+          // every CTA read the generation before its first arrival: advance it
+          if (k == 0 && blockIdx.x == 0) p.ctr[0] = target / G;
+          if (kTrace) PSTAMP(k, 4);
+        }
+        __syncwarp();
+        uint64_t* bar = &tfull[slot];
+        if (C.s2_rtn && !(p.debug & 16u)) {
+          const Seg& S = D.seg[C.s2_seg];
+          const uint32_t lo = S.t_off & ~1u, cnt = ((S.t_off & 1u) + S.r + 1) & ~1u;
+          uint8_t* ts = tslots + slot * p.tslot_bytes;
+          lsu_copy(ts, arena + D.t_off + lo, cnt * 8, bar, lane);
+          lsu_copy(ts + p.ts1_off, S.s1h + (size_t)C.s2_rt0 * 16, 32u * C.s2_rtn, bar, lane);
+          if (kTrace && lane == 0) PSTAMP(k, 13);
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(bar);
+        {  // clear this CTA's share of the step's region in the other parity
+          long long* Z = p.arena + (size_t)(par ^ 1) * p.arena_len + D.t_off;
+          const uint32_t pairs = D.t_len / 2, per = (pairs + G - 1) / G;
+          const uint32_t lo = min(pairs, per * blockIdx.x), hi = min(pairs, lo + per);
+          for (uint32_t i = lo + lane; i < hi; i += 32) ((longlong2*)Z)[i] = make_longlong2(0, 0);
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&dempty[k % kDescSlots]);
+      }
+      return;
+    }
+    // -------------------------------------------------------------- sequencer
+    if (lane != 0) return;
+    auto issue_desc = [&](uint32_t k) {
+      const uint32_t slot = k % kDescSlots;
+      uint8_t* dst = dslots + slot * kDescSlotBytes;
+      tc::mbar_arrive_expect_tx(&dfull[slot], (uint32_t)sizeof(StepDesc) + 32);
+      tc::bulk_g2s(dst, p.desc + k, (uint32_t)sizeof(StepDesc), &dfull[slot]);
+      tc::bulk_g2s(dst + 480, p.ctas + (size_t)k * G + blockIdx.x, 32, &dfull[slot]);
     };
-    for_each_phase(
-        K, desc_of,
-        [&](uint32_t k) {
-          load_desc(k);
-          issue_stage(k, 1);
-        },
-        [&](uint32_t k) { issue_stage(k, 2); });
+    for (uint32_t k = 0; k < min(K, (uint32_t)kDescSlots); ++k) issue_desc(k);
+    uint32_t n1 = 0, ph = 0;
+    auto wait_phase = [&]() {
+      mbar_wait_wd(&cdone[ph % kDoneRing], (ph / kDoneRing) & 1, sus);
+      ++ph;
+    };
+    for (uint32_t k = 0; k < K; ++k) {
+      wait_desc(k);
+      const uint32_t ahead = desc_of(k).s1_ahead;
+      const bool publish = desc_of(k).flags & kStepPublish;
+      while (n1 < ahead) {
+        wait_phase();  // stage 1 of n1 done: its t reds are ordered before the release
+        arrive_ctr(tbar + (size_t)n1 * kCtrStride);
+        ++n1;
+      }
+      wait_phase();  // stage 2 of k done
+      if (publish) arrive_ctr(ybar + (size_t)k * kCtrStride);
+      if (k + kDescSlots < K) {
+        mbar_wait_wd(&dempty[k % kDescSlots], (k / kDescSlots) & 1, sus);
+        issue_desc(k + kDescSlots);
+      }
+    }
     return;
   }
 
-  // ----------------------------------------------------------------- consumers
-  for (int i = tid; i < kMaxRt * 16 * kRedStride / 4; i += kConsumerThreads)
-    ((int4*)red)[i] = make_int4(0, 0, 0, 0);
-  if (tid == 0) {
-    unsigned long long gen;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(gen) : "l"(p.ctr) : "memory");
-    misc[0] = (gen + 1) * p.G;
+  // ================================================================ consumers
+  for (int i = tid; i < (p.fused ? 2 : 1) * kMaxRt * 16 * kRedStride / 4; i += kConsumerThreads)
+    ((int4*)red1)[i] = make_int4(0, 0, 0, 0);
+  // ---- |x| prepass: this CTA's share of every independent input, one grid barrier
+  if (p.has_pre) {
+    for (uint32_t k = tid; k < K; k += kConsumerThreads) {
+      const StepDesc* Dg = p.desc + k;
+      const uint32_t fl = __ldg(&Dg->flags);
+      if (!(fl & kStepXPre)) continue;
+      const uint32_t m = __ldg(&Dg->m);
+      const void* x = (const void*)__ldg((const unsigned long long*)&Dg->x);
+      uint32_t lo, hi;
+      share_of(m, blockIdx.x, G, lo, hi);
+      if (lo < hi) {
+        const uint32_t mb = absmax_bits(x, lo, hi, fl & kStepXF32, (fl & kStepXVec) != 0, 0, 1);
+        atomicMax(amax + 4 * (size_t)__ldg(&Dg->amax_idx), mb);
+      }
+    }
+    consumers_sync();
+    if (tid == 0) arrive_ctr(xinit);
   }
-  unsigned long long* trp = nullptr;
-  if (kTrace) {
-    trp = p.trace + (size_t)blockIdx.x * (2 * K + 2);
-    if (tid == 0) trp[0] = globaltimer();
-  }
-  consumers_sync();
-  const unsigned long long target = misc[0];
-  unsigned long long* tbar = p.ctr + 2 * kCtrStride;
-  unsigned long long* ybar = tbar + (size_t)K * kCtrStride;
-
-  uint64_t pos = 0;
-  uint32_t chunk = 0;
-  int32_t ywaited = -1;
-
-  auto wait_chunk = [&](uint32_t bytes) -> const uint8_t* {
-    const uint64_t start = ring_place(pos, bytes, RB);
-    mbar_wait_wd(&full[chunk % kPassSlots], (chunk / kPassSlots) & 1);
-    return ring + (uint32_t)(start % RB);
+  uint32_t n1 = 0, ph = 0, chunk = 0;
+  auto wait_chunk = [&]() -> ChunkRec {
+    mbar_wait_wd(&full[chunk % kPassSlots], (chunk / kPassSlots) & 1, sus);
+    return recs[chunk % kPassSlots];
   };
   auto release_chunk = [&]() {
     __syncwarp();
     if (lane == 0) tc::mbar_arrive(&empty[chunk % kPassSlots]);
     ++chunk;
   };
-
-  auto stage1 = [&](uint32_t k) {
-    mbar_wait_wd(&dfull[k % kDescSlots], (k / kDescSlots) & 1);
-    const StepDesc& D = desc_of(k);
-    const Cta& C = cta_of(k);
-    if (D.x_src >= 0 && D.x_src > ywaited) {
-      wait_ctr(ybar + (size_t)D.x_src * kCtrStride, target);
-      ywaited = D.x_src;
-    }
-    const StageGeo g = stage1_geo(D, C);
-    if (g.nsec) {
-      const bool xf32 = D.flags & kStepXF32, xvec = D.flags & kStepXVec;
-      float xmax;
-      if (D.xmax_src >= 0) xmax = __uint_as_float(__ldcg(p.ymax + D.xmax_src));
-      else xmax = x_absmax(D.x, D.m, xf32, xvec, xred);
-      const bool nonfinite = is_inf(xmax);
-      const Seg& S = D.seg[C.s1_seg];
-      const int ea = act_exponent(S.s2max, xmax);
-      long long asum = 0, aabs = 0;
-      uint32_t s0 = 0;
-      while (s0 < g.nsec) {
-        uint32_t s1;
-        const uint32_t sb = chunk_span(g, s0, cap, &s1);
-        const uint32_t pre = s0 == 0 ? g.prefix : 0;
-        const uint8_t* base = wait_chunk(pre + sb);
-        if (s0 == 0) {  // quantise this CTA's input slice (packed.cpp:160) into B fragments
-          const uint32_t klo = g.klo, nquad = g.prefix / 8;
-          const __half* s2s = (const __half*)base - klo;
-          uint32_t qd = tid;
-          XQuad cur = load_xquad(D.x, xf32, xvec, s2s, klo + 4 * min(qd, nquad - 1), D.m);
-          while (qd < nquad) {
-            const uint32_t nx = qd + kConsumerThreads;
-            const XQuad nxt = load_xquad(D.x, xf32, xvec, s2s, klo + 4 * min(nx, nquad - 1), D.m);
-            const uint32_t k0 = klo + 4 * qd;
-            long long v[4];
+  // The stage's (pair, section) items are split over the warps once for the
+  // whole stage (pair-major, contiguous per warp), not per chunk: each warp walks
+  // the chunks as they land and runs its items in each.
+  auto mma_stage = [&](const StageGeo& g, const uint8_t* bf, int* rd) {
+    if (!g.nsec) return;
+    const uint32_t npair = (g.rtn + 1) / 2, U = npair * g.nsec;
+    const uint32_t f0 = (uint32_t)((uint64_t)U * warp / kConsumerWarps);
+    const uint32_t f1 = (uint32_t)((uint64_t)U * (warp + 1) / kConsumerWarps);
+    const uint32_t p0 = f0 / g.nsec, p1 = f1 ? (f1 - 1) / g.nsec : 0;
+    int acc[2][4][4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float a = nonfinite ? 0.f : cur.s[e] * cur.x[e];
-              v[e] = __float2ll_rn(scale_pow2(a, kFix - ea));
-              asum += v[e];
-              aabs += v[e] < 0 ? -v[e] : v[e];
-            }
-            emit_quad(bfrag, klo, k0, q_of(k0, D.m), v);
-            cur = nxt;
-            qd = nx;
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[j][q][0] = acc[j][q][1] = acc[j][q][2] = acc[j][q][3] = 0;
+    for (uint32_t s0 = 0; s0 < g.nsec;) {
+      const ChunkRec cr = wait_chunk();
+      if (f0 < f1 && !(p.debug & 1u)) {
+        for (uint32_t pr = p0; pr <= p1; ++pr) {
+          const uint32_t sa = max(s0, pr == p0 ? f0 - p0 * g.nsec : 0u);
+          const uint32_t sb = min((uint32_t)cr.s1, pr == p1 ? f1 - p1 * g.nsec : g.nsec);
+          if (sa < sb) run_pair(ring + cr.off, g, s0, pr, sa, sb, bf, rd, acc);
+        }
+      }
+      release_chunk();
+      s0 = cr.s1;
+    }
+  };
+
+  // One phase: stage 2 of step k2 and stage 1 of step j1 (either may be absent,
+  // -1), with one quantise / MMA / publish sequence and three CTA barriers.
+  auto run_phase = [&](int32_t k2, int32_t j1) {
+    StageGeo g2{}, g1{};
+    uint32_t ts_slot = 0, xs_slot = 0;
+    const StepDesc* D2 = nullptr;
+    const Cta* C2 = nullptr;
+    const StepDesc* D1 = nullptr;
+    const Cta* C1 = nullptr;
+    float xmax1 = 0.f;
+    if (k2 >= 0) {
+      D2 = &desc_of(k2);
+      C2 = &cta_of(k2);
+      g2 = stage2_geo(*D2, *C2);
+      ts_slot = k2 % TS;
+      mbar_wait_wd(&tfull[ts_slot], (k2 / TS) & 1, sus);
+      if (kTrace && tid == 0) PSTAMP(k2, 2);
+    }
+    if (j1 >= 0) {
+      wait_desc(j1);
+      D1 = &desc_of(j1);
+      C1 = &cta_of(j1);
+      g1 = stage1_geo(*D1, *C1);
+      xs_slot = j1 % kXSlots;
+      mbar_wait_wd(&xfull[xs_slot], (j1 / kXSlots) & 1, sus);
+      xmax1 = bound_value(*(const uint32_t*)(xslots + xs_slot * p.xslot_bytes),
+                          (D1->flags & kStepXF32) != 0);
+      if (kTrace && tid == 0) PSTAMP(j1, 0);
+    }
+    // ---- quantise t (stage 2) and x (stage 1) into their B fragments
+    long long asum = 0, tsum = 0;
+    if (g2.nsec && !(p.debug & 2u)) {
+      const Seg& S = D2->seg[C2->s2_seg];
+      const int sh = t_shift(D2->m);
+      const long long* T = (const long long*)(tslots + ts_slot * p.tslot_bytes) + (S.t_off & 1u);
+      const uint32_t nquad2 = kpad(S.r) / 4;
+      for (uint32_t qd = tid; qd < nquad2; qd += kConsumerThreads) {
+        long long v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t kk = 4 * qd + e;
+          const long long t = kk < S.r ? T[kk] : 0;
+          v[e] = (t + (1ll << (sh - 1))) >> sh;
+          tsum += v[e];
+        }
+        emit_quad(bfrag2, 0, 4 * qd, q_of(4 * qd, S.r), v);
+      }
+    }
+    if (g1.nsec && !(p.debug & 2u)) {
+      const uint8_t* xs = xslots + xs_slot * p.xslot_bytes;
+      const bool xf32 = D1->flags & kStepXF32;
+      const bool nonfinite = is_inf(xmax1);
+      const int ea = act_exponent(D1->seg[C1->s1_seg].s2max, xmax1);
+      const uint32_t klo = g1.klo, nquad = g1.prefix / 8, m = D1->m;
+      const __half* s2s = (const __half*)(xs + p.xs2_off) - klo;
+      for (uint32_t qd = tid; qd < nquad; qd += kConsumerThreads) {
+        const uint32_t k0 = klo + 4 * qd;
+        float xv[4], sv[4];
+        if (k0 + 3 < m) {
+          const uint2 sh2 = *(const uint2*)(s2s + k0);
+          const float2 s01 = __half22float2(*(const __half2*)&sh2.x);
+          const float2 s23 = __half22float2(*(const __half2*)&sh2.y);
+          sv[0] = s01.x; sv[1] = s01.y; sv[2] = s23.x; sv[3] = s23.y;
+          if (xf32) {
+            const float4 v = *(const float4*)(xs + 16 + 16 * qd);
+            xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+          } else {
+            const uint2 v = *(const uint2*)(xs + 16 + 8 * qd);
+            const float2 x01 = __half22float2(*(const __half2*)&v.x);
+            const float2 x23 = __half22float2(*(const __half2*)&v.y);
+            xv[0] = x01.x; xv[1] = x01.y; xv[2] = x23.x; xv[3] = x23.y;
           }
-          warp_partials2(asum, aabs, red8);
-          consumers_sync();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t kk = k0 + e;
+            sv[e] = xv[e] = 0.f;
+            if (kk < m) {
+              sv[e] = __half2float(s2s[kk]);
+              xv[e] = xf32 ? ((const float*)(xs + 16))[4 * qd + e]
+                           : __half2float(((const __half*)(xs + 16))[4 * qd + e]);
+            }
+          }
         }
-        run_chunk(base + pre, g, s0, s1 - s0, bfrag, red);
-        release_chunk();
-        s0 = s1;
+        long long v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float a = nonfinite ? 0.f : sv[e] * xv[e];  // packed.cpp:160
+          v[e] = __float2ll_rn(scale_pow2(a, kFix - ea));
+          asum += v[e];
+        }
+        emit_quad(bfrag1, klo, k0, q_of(k0, m), v);
       }
-      consumers_sync();
-      // publish: t rows (exact int64 reds), sum|a| and the exponent of this segment
+    }
+    warp_partials2(asum, tsum, red8);
+    consumers_sync();  // fragments and partial sums visible; the x slot is consumed
+    if (j1 >= 0 && tid == 0) {
+      xmaxs[j1 % 16] = xmax1;
+      tc::mbar_arrive(&xempty[xs_slot]);
+    }
+    if (kTrace && tid == 0) {
+      if (k2 >= 0) PSTAMP(k2, 9);
+      if (j1 >= 0) PSTAMP(j1, 7);
+    }
+    // ---- MMA: stage-2 chunks, then stage-1 chunks (the producer's order)
+    mma_stage(g2, bfrag2, red2);
+    mma_stage(g1, bfrag1, red1);
+    consumers_sync();
+    if (kTrace && tid == 0) {
+      if (k2 >= 0) PSTAMP(k2, 10);
+      if (j1 >= 0) PSTAMP(j1, 8);
+    }
+    // ---- publish: stage-1 t rows (exact int64 reds), stage-2 outputs
+    if (g1.nsec && !(p.debug & 8u)) {
       const long long A = sum_partials(red8);
-      long long* R = p.arena + D.t_off;
-      if (tid == 0 && C.s1_rt0 == 0) {
-        red_add_u64(&R[D.R1 + C.s1_seg], sum_partials(red8 + kConsumerWarps));
-        if (C.s1_sl0 == 0) {
-          R[D.R1 + kMaxSeg + C.s1_seg] = ea;
-          if (nonfinite) R[D.R1 + 2 * kMaxSeg] = 1;
-        }
-      }
-      long long* Tseg = R + S.t_off + (size_t)C.s1_rt0 * 16;
-      for (uint32_t i = tid; i < (uint32_t)C.s1_rtn * 16; i += kConsumerThreads) {
-        const long long v = 2 * row_value(red + i * kRedStride) - A;
-        int4* rr = (int4*)(red + i * kRedStride);
+      const Seg& S = D1->seg[C1->s1_seg];
+      long long* Tseg = arena + D1->t_off + S.t_off + (size_t)C1->s1_rt0 * 16;
+      for (uint32_t i = tid; i < (uint32_t)C1->s1_rtn * 16; i += kConsumerThreads) {
+        const long long v = 2 * row_value(red1 + i * kRedStride) - A;
+        int4* rr = (int4*)(red1 + i * kRedStride);
         rr[0] = make_int4(0, 0, 0, 0);
         rr[1] = make_int4(0, 0, 0, 0);
         red_add_u64(&Tseg[i], v);
       }
     }
-    arrive_ctr(tbar + (size_t)k * kCtrStride);
-  };
-
-  auto stage2 = [&](uint32_t k) {
-    const StepDesc& D = desc_of(k);
-    const Cta& C = cta_of(k);
-    wait_ctr(tbar + (size_t)k * kCtrStride, target);
-    if (kTrace && tid == 0) trp[1 + 2 * k] = globaltimer();
-    if (D.zero_len) {  // step k-2's region: every CTA finished its stage 2 before arriving here
-      long long* Z = p.arena + D.zero_off;
-      const uint32_t per = (D.zero_len + p.G - 1) / p.G;
-      const uint32_t lo = min(D.zero_len, per * blockIdx.x), hi = min(D.zero_len, lo + per);
-      for (uint32_t i = lo + tid; i < hi; i += kConsumerThreads) Z[i] = 0;
-    }
-    const StageGeo g = stage2_geo(D, C);
-    const bool publish = D.flags & kStepPublish;
-    float ymx = 0.f;
-    if (g.nsec) {
-      const Seg& S = D.seg[C.s2_seg];
-      const long long* R = p.arena + D.t_off;
-      const int ea = (int)__ldcg(&R[D.R1 + kMaxSeg + C.s2_seg]);
-      const bool nonfinite = __ldcg(&R[D.R1 + 2 * kMaxSeg]) != 0;
-      // |t_k| = |sum_j +-a_int_j| <= sum_j |a_int_j|, published exactly by stage 1
-      const unsigned long long tbound = (unsigned long long)__ldcg(&R[D.R1 + C.s2_seg]);
-      const int et = tbound ? 64 - __clzll((long long)tbound) : 0;
-      const int sh = et - kFix;
-      const long long* Tseg = R + S.t_off;
-      const uint32_t nquad2 = kpad(S.r) / 4;
-      long long tsum = 0;
-      {
-        uint32_t qd = tid;
-        long long cur[4], nxt[4];
-        load_tquad(Tseg, 4 * min(qd, nquad2 - 1), S.r, D.t_off + S.t_off, cur);
-        while (qd < nquad2) {
-          const uint32_t nx = qd + kConsumerThreads;
-          load_tquad(Tseg, 4 * min(nx, nquad2 - 1), S.r, D.t_off + S.t_off, nxt);
-          long long v[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            v[e] = sh > 0 ? (cur[e] + (1ll << (sh - 1))) >> sh : cur[e] * (1ll << (-sh));
-            tsum += v[e];
-          }
-          emit_quad(bfrag, 0, 4 * qd, q_of(4 * qd, S.r), v);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) cur[e] = nxt[e];
-          qd = nx;
-        }
-      }
-      warp_partials2(tsum, 0, red8);
-      consumers_sync();
-      uint32_t s0 = 0;
-      const __half* sc1 = nullptr;
-      while (s0 < g.nsec) {
-        uint32_t s1;
-        const uint32_t sb = chunk_span(g, s0, cap, &s1);
-        const bool last = s1 == g.nsec;
-        const uint32_t suf = last ? (g.suffix + 127) / 128 * 128 : 0;
-        const uint8_t* base = wait_chunk(sb + suf);
-        run_chunk(base, g, s0, s1 - s0, bfrag, red);
-        if (last) sc1 = (const __half*)(base + sb);  // released after the outputs
-        else release_chunk();
-        s0 = s1;
-      }
-      consumers_sync();
-      const long long Tsum = sum_partials(red8);
-      const int E = sh + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
-      const bool yf32 = D.flags & kStepYF32;
-      void* Y = D.y[C.s2_seg];
-      for (uint32_t i = tid; i < (uint32_t)C.s2_rtn * 16; i += kConsumerThreads) {
-        const uint32_t row = C.s2_rt0 * 16 + i;
-        int4* rr = (int4*)(red + i * kRedStride);
+    if (g2.nsec && !(p.debug & 8u)) {
+      const Seg& S = D2->seg[C2->s2_seg];
+      const float xmax = xmaxs[k2 % 16];
+      const int ea = act_exponent(S.s2max, xmax);
+      const bool nonfinite = is_inf(xmax);
+      const long long Tsum = sum_partials(red8 + kConsumerWarps);
+      const int E = t_shift(D2->m) + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
+      const bool yf32 = D2->flags & kStepYF32;
+      const __half* sc1 = (const __half*)(tslots + ts_slot * p.tslot_bytes + p.ts1_off);
+      void* Y = D2->y[C2->s2_seg];
+      uint32_t ymb = 0;
+      for (uint32_t i = tid; i < (uint32_t)C2->s2_rtn * 16; i += kConsumerThreads) {
+        const uint32_t row = C2->s2_rt0 * 16 + i;
+        int4* rr = (int4*)(red2 + i * kRedStride);
         if (row < S.n) {
-          const long long Yi = 2 * row_value(red + i * kRedStride) - Tsum;
+          const long long Yi = 2 * row_value(red2 + i * kRedStride) - Tsum;
           double y = (double)__half2float(sc1[i]) *
                      ((double)Yi * __longlong_as_double((long long)(1023 + E) << 52));  // packed.cpp:189
           if (nonfinite) y = __longlong_as_double(0x7ff8000000000000ll);
-          float yo;
           if (yf32) {
-            yo = (float)y;
+            const float yo = (float)y;
             ((float*)Y)[row] = yo;
+            const uint32_t b = __float_as_uint(yo) & 0x7FFFFFFFu;
+            ymb = max(ymb, b >= 0x7F800000u ? 0x7F800000u : b);
           } else {
             const __half h = __float2half_rn((float)y);
             ((__half*)Y)[row] = h;
-            yo = __half2float(h);
+            ymb = max(ymb, (uint32_t)(__half_as_ushort(h) & 0x7FFFu));
           }
-          const float a = fabsf(yo);
-          ymx = fmaxf(ymx, (a <= FLT_MAX) ? a : __int_as_float(0x7f800000));
         }
         rr[0] = make_int4(0, 0, 0, 0);
         rr[1] = make_int4(0, 0, 0, 0);
       }
-      release_chunk();
-      if (publish) {
+      if (D2->flags & kStepPublish) {
 #pragma unroll
-        for (int o = 16; o; o >>= 1) ymx = fmaxf(ymx, __shfl_xor_sync(~0u, ymx, o));
-        consumers_sync();
-        if (lane == 0) xred[warp] = ymx;
-        consumers_sync();
-        if (tid == 0) {
-          float mx = 0.f;
-          for (int w = 0; w < kConsumerWarps; ++w) mx = fmaxf(mx, xred[w]);
-          atomicMax(p.ymax + (size_t)k * kMaxSeg + C.s2_seg, __float_as_uint(mx));
-        }
+        for (int o = 16; o; o >>= 1) ymb = max(ymb, __shfl_xor_sync(~0u, ymb, o));
+        if (lane == 0 && ymb)
+          atomicMax(amax + 4 * ((size_t)K + (size_t)k2 * kMaxSeg + C2->s2_seg), ymb);
       }
     }
-    if (kTrace && tid == 0) trp[2 + 2 * k] = globaltimer();
-    if (publish) arrive_ctr(ybar + (size_t)k * kCtrStride);
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(&dempty[k % kDescSlots]);
+    consumers_sync();  // this phase's reds / stores happen-before the sequencer's releases
+    if (tid == 0) {
+      if (k2 >= 0) {
+        if (kTrace) PSTAMP(k2, 3);
+        tc::mbar_arrive(&tempty[ts_slot]);
+        tc::mbar_arrive(&cdone[ph % kDoneRing]);
+        ++ph;
+        tc::mbar_arrive(&dempty[k2 % kDescSlots]);
+      }
+      if (j1 >= 0) {
+        if (kTrace) PSTAMP(j1, 1);
+        tc::mbar_arrive(&cdone[ph % kDoneRing]);
+        ++ph;
+      }
+    }
   };
 
-  for_each_phase(K, desc_of, stage1, stage2);
-
-  // -------------------------------------------------------------- exit barrier
-  arrive_ctr(p.ctr + kCtrStride);
-  wait_ctr(p.ctr + kCtrStride, target);
-  // every CTA is past every use: clear the last steps' regions and max|y| words
-  for (uint32_t t = 0; t < p.ntail; ++t) {
-    long long* Z = p.arena + p.tail_off[t];
-    const uint32_t len = p.tail_len[t], per = (len + p.G - 1) / p.G;
-    const uint32_t lo = min(len, per * blockIdx.x), hi = min(len, lo + per);
-    for (uint32_t i = lo + tid; i < hi; i += kConsumerThreads) Z[i] = 0;
+  for (uint32_t k = 0; k < K; ++k) {
+    wait_desc(k);
+    const uint32_t ahead = desc_of(k).s1_ahead;
+    const bool fuse = desc_of(k).flags & kStepFuse;
+    while (n1 < ahead) run_phase(-1, (int32_t)n1++);
+    if (fuse && n1 < K) run_phase((int32_t)k, (int32_t)n1++);
+    else run_phase((int32_t)k, -1);
   }
-  {
-    const uint32_t len = K * kMaxSeg, per = (len + p.G - 1) / p.G;
-    const uint32_t lo = min(len, per * blockIdx.x), hi = min(len, lo + per);
-    for (uint32_t i = lo + tid; i < hi; i += kConsumerThreads) p.ymax[i] = 0u;
-  }
-  if (blockIdx.x == 0 && tid == 0) p.ctr[0] = target / p.G;  // next launch's generation
-  if (kTrace && tid == 0) trp[2 * K + 1] = globaltimer();
+  if (kTrace && tid == 0) trp[kPassStamps * K + 1] = globaltimer();
 }
 
 }  // namespace dec
@@ -540,14 +830,14 @@ bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
 }  // namespace
 
 nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
-  NQB_REQUIRE(K >= 1 && K <= 8192, NQB_E_VALIDATION, "a decode pass holds 1..8192 steps");
+  NQB_REQUIRE(K >= 1 && K <= 65536, NQB_E_VALIDATION, "a decode pass holds 1..65536 steps");
   NQB_REQUIRE(steps != nullptr, NQB_E_VALIDATION, "null steps");
   const uint32_t G = (uint32_t)ctx->num_sms;
   std::vector<StepDesc> desc(K);
-  uint32_t bfrag = 0;
+  uint32_t bfrag = 0, xbytes = 16, s2bytes = 16, tbytes = 16, s1bytes = 16;
   uint64_t arena = 0, stream_bytes = 0;
   double algo = 0;
-  std::vector<uint64_t> t_off(K), t_len(K);
+  bool has_pre = false;
   for (uint32_t k = 0; k < K; ++k) {
     const PassStepIn& s = steps[k];
     const nqb_group* g = s.group;
@@ -557,6 +847,7 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
                 "decode group planned for more SMs than the context's budget");
     NQB_REQUIRE(s.x != nullptr, NQB_E_VALIDATION, "null pass input");
     StepDesc& D = desc[k];
+    std::memset(&D, 0, sizeof(D));
     D.bits = g->bits;
     D.x = s.x;
     D.nseg = g->nseg;
@@ -572,17 +863,27 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       NQB_REQUIRE(!overlaps(s.y[q], (size_t)g->n[q] * esz, s.x, (size_t)g->m * esz),
                   NQB_E_VALIDATION, "a pass step's output overlaps its own input");
       algo += (double)g->r[q] * (g->n[q] + g->m) / 8.0 + 2.0 * (g->n[q] + g->m) + esz * g->n[q];
+      tbytes = std::max(tbytes, (((g->seg[q].t_off & 1u) + g->r[q] + 1) & ~1u) * 8u);
     }
     algo += (double)esz * g->m;
     bfrag = std::max(bfrag, g->bfrag_bytes);
+    for (uint32_t c = 0; c < g->grid; ++c) {  // the CTA's stage-1 input slice
+      const Cta& C = g->ctas[c];
+      if (!C.s1_rtn || !C.s1_sln) continue;
+      const Slab last = slab_of(g->m, C.s1_sl0 + C.s1_sln - 1);
+      const uint32_t nk1 = last.k0 + 32 * last.nq - slab_of(g->m, C.s1_sl0).k0;
+      xbytes = std::max(xbytes, esz * nk1);
+      s2bytes = std::max(s2bytes, 2 * nk1);
+    }
+    for (uint32_t c = 0; c < g->grid; ++c) s1bytes = std::max<uint32_t>(s1bytes, 32u * g->ctas[c].s2_rtn);
     stream_bytes += g->stream_bytes;
-    t_off[k] = arena;
-    t_len[k] = (uint64_t)g->R1 + kStepTail;
-    arena += (t_len[k] + 1) / 2 * 2;  // 16-byte aligned regions (vector t loads)
+    D.t_off = arena;
+    D.t_len = (g->R1 + 3) & ~1u;  // even, plus the odd-start overhang of a segment copy
+    arena += D.t_len;
     // dependencies from buffer ranges: the latest earlier step whose output
     // overlaps this input must have finished (output barrier) before stage 1
     D.x_src = -1;
-    D.xmax_src = -1;
+    int32_t exact = -1;
     for (int j = (int)k - 1; j >= 0 && D.x_src < 0; --j) {
       const uint32_t ej = (desc[j].flags & kStepYF32) ? 4 : 2;
       for (uint32_t q = 0; q < desc[j].nseg; ++q) {
@@ -590,88 +891,150 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
           continue;
         D.x_src = j;
         if (desc[j].y[q] == s.x && desc[j].seg[q].n == g->m && ej == esz)
-          D.xmax_src = (int32_t)(j * kMaxSeg + q);
+          exact = (int32_t)(K + j * kMaxSeg + q);
       }
     }
-    if (D.x_src >= 0) desc[D.x_src].flags |= kStepPublish;
+    if (D.x_src < 0) {
+      D.flags |= kStepXPre;
+      D.amax_idx = k;
+      has_pre = true;
+    } else {
+      desc[D.x_src].flags |= kStepPublish;
+      if (exact >= 0) D.amax_idx = (uint32_t)exact;
+      else D.flags |= kStepXSelf;
+    }
   }
-  // one-step lookahead (stage 1 of k+1 before stage 2 of k) when k+1 neither
-  // reads nor overwrites k's outputs
-  for (uint32_t k = 0; k + 1 < K; ++k) {
-    bool dep = desc[k + 1].x_src == (int32_t)k;
-    const uint32_t ek = (desc[k].flags & kStepYF32) ? 4 : 2;
-    const uint32_t e1 = (desc[k + 1].flags & kStepYF32) ? 4 : 2;
-    for (uint32_t a = 0; a < desc[k].nseg && !dep; ++a)
-      for (uint32_t b = 0; b < desc[k + 1].nseg && !dep; ++b)
-        dep = overlaps(desc[k].y[a], (size_t)desc[k].seg[a].n * ek, desc[k + 1].y[b],
-                       (size_t)desc[k + 1].seg[b].n * e1);
-    if (!dep && env_u32p("NQB_PASS_LOOKAHEAD", 1)) desc[k].flags |= kStepLookahead;
+  // phase order: stage 1 of step j may run before stage 2 of step i < j only if
+  // j reads or writes nothing that steps >= i write (RAW on x, WAW on y);
+  // s1_ahead[k] = stage-1 phases issued before stage 2 of k (non-decreasing)
+  // shared memory: head | 2 B-fragment buffers | x slots | t slots | weight ring.
+  // As many t slots as leave the ring >= NQB_PASS_RING_KB (default 64 KB: 4 x 16 KB
+  // bulk copies in flight already stream at the full per-SM HBM share).
+  const uint32_t bfrag_b = (bfrag + 127) / 128 * 128;
+  const uint32_t xs2_off = (16 + xbytes + 127) / 128 * 128;
+  const uint32_t xslot_b = (xs2_off + s2bytes + 127) / 128 * 128;
+  const uint32_t ts1_off = (tbytes + 127) / 128 * 128;
+  const uint32_t tslot_b = (ts1_off + s1bytes + 127) / 128 * 128;
+  const bool fuse_mode = env_u32p("NQB_PASS_FUSE", 0) != 0;
+  const uint32_t head = pass_head_bytes(fuse_mode);
+  const uint32_t ring_min = env_u32p("NQB_PASS_RING_KB", 128) * 1024;
+  const uint32_t base_b = head + (fuse_mode ? 2 : 1) * bfrag_b + kXSlots * xslot_b;
+  NQB_REQUIRE(base_b + 2 * tslot_b + ring_min / 2 <= 227u * 1024u, NQB_E_DIMENSION_MISMATCH,
+              "decode pass: staging buffers leave no room for the weight ring");
+  uint32_t TS = base_b + ring_min + 2 * tslot_b <= 227u * 1024u
+                    ? (227u * 1024u - base_b - ring_min) / tslot_b : 2u;
+  TS = std::max<uint32_t>(2, std::min<uint32_t>({TS, (uint32_t)kMaxTSlots,
+                                                 env_u32p("NQB_PASS_TSLOTS", 2)}));
+  const uint32_t L = std::min<uint32_t>(env_u32p("NQB_PASS_LOOKAHEAD", 2), kMaxLookahead);
+  std::vector<int32_t> dep(K, -1);
+  for (uint32_t j = 0; j < K; ++j) {
+    const uint32_t ej = (desc[j].flags & kStepYF32) ? 4 : 2;
+    for (int i = (int)j - 1; i >= 0 && dep[j] < 0; --i) {
+      const uint32_t ei = (desc[i].flags & kStepYF32) ? 4 : 2;
+      bool d = desc[j].x_src == i;
+      for (uint32_t a = 0; a < desc[i].nseg && !d; ++a) {
+        d = overlaps(desc[i].y[a], (size_t)desc[i].seg[a].n * ei, desc[j].x,
+                     (size_t)desc[j].m * ((desc[j].flags & kStepXF32) ? 4 : 2));
+        for (uint32_t b = 0; b < desc[j].nseg && !d; ++b)
+          d = overlaps(desc[i].y[a], (size_t)desc[i].seg[a].n * ei, desc[j].y[b],
+                       (size_t)desc[j].seg[b].n * ej);
+      }
+      if (d) dep[j] = i;
+    }
   }
-  for (uint32_t k = 0; k < K; ++k) {
-    desc[k].t_off = t_off[k];
-    desc[k].zero_off = k >= 2 ? t_off[k - 2] : 0;
-    desc[k].zero_len = k >= 2 ? (uint32_t)t_len[k - 2] : 0;
+  {
+    uint32_t n1 = 0;
+    for (uint32_t k = 0; k < K; ++k) {
+      while (n1 < K && n1 <= k + L && dep[n1] < (int32_t)k) ++n1;
+      if (n1 < k + 1) n1 = k + 1;  // (dep[k] < k always holds)
+      desc[k].s1_ahead = n1;
+    }
+    // stage 2 of k shares a phase with the stage 1 that follows it in the order
+    // when that step does not depend on k (its x and y are independent of y_k)
+    if (fuse_mode)
+      for (uint32_t k = 0; k + 1 < K; ++k) {
+        const uint32_t j = desc[k].s1_ahead;  // the next stage-1 event after stage 2 of k
+        if (j < K && desc[k + 1].s1_ahead > j && dep[j] < (int32_t)k) desc[k].flags |= kStepFuse;
+      }
   }
+  NQB_REQUIRE(L + 4 < (uint32_t)kDescSlots && 2 * L + 6 <= (uint32_t)kDoneRing, NQB_E_INTERNAL,
+              "pass lookahead exceeds the descriptor / phase rings");
 
-  // ---- device memory: descriptors | CTA tables | counters | ymax | arena ----
+  // ---- device memory: descriptors | CTA tables | counters | bounds | arena ----
+  const uint32_t amax_words = K * (1 + kMaxSeg);
   const size_t desc_b = sizeof(StepDesc) * K;
   const size_t cta_b = sizeof(Cta) * (size_t)K * G;
   const size_t ctr_b = sizeof(unsigned long long) * kCtrStride * (2 + 2 * (size_t)K);
-  const size_t ymax_b = ((size_t)K * kMaxSeg * 4 + 15) / 16 * 16;
-  const size_t arena_b = arena * 8;
+  const size_t amax_b = 2ull * amax_words * 16;
+  const size_t arena_b = 2ull * arena * 8;
   auto* P = new nqb_pass();
   P->device = ctx->device;
   P->K = K;
   P->G = G;
   try {
-    NQB_CUDA(cudaMalloc(&P->dmem, desc_b + cta_b + ctr_b + ymax_b + arena_b));
+    NQB_CUDA(cudaMalloc(&P->dmem, desc_b + cta_b + ctr_b + amax_b + arena_b));
     char* base = (char*)P->dmem;
     StepDesc* d_desc = (StepDesc*)base;
     Cta* d_ctas = (Cta*)(base + desc_b);
     auto* d_ctr = (unsigned long long*)(base + desc_b + cta_b);
-    auto* d_ymax = (unsigned*)(base + desc_b + cta_b + ctr_b);
-    auto* d_arena = (long long*)(base + desc_b + cta_b + ctr_b + ymax_b);
+    auto* d_amax = (unsigned*)(base + desc_b + cta_b + ctr_b);
+    auto* d_arena = (long long*)(base + desc_b + cta_b + ctr_b + amax_b);
     std::vector<Cta> ctas((size_t)K * G, Cta{});
     for (uint32_t k = 0; k < K; ++k) {
       const nqb_group* g = steps[k].group;
       std::copy(g->ctas, g->ctas + g->grid, ctas.begin() + (size_t)k * G);
       desc[k].ctas = d_ctas + (size_t)k * G;
     }
-    NQB_CUDA(cudaMemsetAsync(d_ctr, 0, ctr_b + ymax_b + arena_b, ctx->stream));
+    NQB_CUDA(cudaMemsetAsync(d_ctr, 0, ctr_b + amax_b + arena_b, ctx->stream));
     NQB_CUDA(cudaMemcpyAsync(d_desc, desc.data(), desc_b, cudaMemcpyHostToDevice, ctx->stream));
     NQB_CUDA(cudaMemcpyAsync(d_ctas, ctas.data(), cta_b, cudaMemcpyHostToDevice, ctx->stream));
     NQB_CUDA(cudaStreamSynchronize(ctx->stream));
 
     PassParams& pp = P->params;
     pp.desc = d_desc;
+    pp.ctas = d_ctas;
     pp.K = K;
     pp.G = G;
     pp.ctr = d_ctr;
-    pp.ymax = d_ymax;
+    pp.amax = d_amax;
+    pp.amax_words = amax_words;
     pp.arena = d_arena;
-    pp.bfrag_bytes = (bfrag + 127) / 128 * 128;
-    const uint32_t head = pass_head_bytes();
-    pp.ring_bytes = (227u * 1024u - head - pp.bfrag_bytes) / 128 * 128;
+    pp.arena_len = arena;
+    pp.has_pre = has_pre ? 1 : 0;
+    pp.debug = env_u32p("NQB_PASS_DEBUG", 0);
+    pp.bfrag_bytes = bfrag_b;
+    pp.xs2_off = xs2_off;
+    pp.xslot_bytes = xslot_b;
+    pp.ts1_off = ts1_off;
+    pp.tslot_bytes = tslot_b;
+    pp.tslots = TS;
+    pp.fused = fuse_mode ? 1 : 0;
+    pp.head_bytes = head;
+    const uint32_t fixed = base_b + TS * tslot_b;
+    pp.ring_bytes = (227u * 1024u - fixed) / 128 * 128;
     const uint32_t cap_kb = env_u32p("NQB_PASS_CHUNK_KB", 0);
-    pp.chunk_cap = cap_kb ? cap_kb * 1024 : pp.ring_bytes / 4 / 128 * 128;
-    // a chunk is at most cap + the largest section + prefix + suffix: keep two in the ring
-    NQB_REQUIRE(pp.chunk_cap + 16384 + 8192 + 1024 <= pp.ring_bytes / 2, NQB_E_VALIDATION,
+    pp.chunk_cap = cap_kb ? cap_kb * 1024 : std::min<uint32_t>(32768, pp.ring_bytes / 3 / 128 * 128);
+    // a chunk is at most cap + the largest section (16 KB); the consumers hold one
+    // chunk at a time, so the ring must fit one
+    NQB_REQUIRE(pp.chunk_cap + 16384 <= pp.ring_bytes, NQB_E_VALIDATION,
                 "NQB_PASS_CHUNK_KB too large for the shared-memory ring");
-    pp.ntail = std::min<uint32_t>(K, 2);
-    for (uint32_t t = 0; t < pp.ntail; ++t) {
-      const uint32_t k = K - pp.ntail + t;
-      pp.tail_off[t] = t_off[k];
-      pp.tail_len[t] = (uint32_t)t_len[k];
-    }
-    P->smem_bytes = head + pp.bfrag_bytes + pp.ring_bytes;
+    P->smem_bytes = fixed + pp.ring_bytes;
+    if (env_u32p("NQB_PASS_VERBOSE", 0))
+      std::fprintf(stderr,
+                   "nqb pass: K=%u G=%u smem=%u head=%u bfrag=%u xslot=%u tslot=%u ring=%u "
+                   "chunk_cap=%u lookahead=%u tslots=%u fused=%u\n",
+                   K, G, P->smem_bytes, head, pp.bfrag_bytes * (fuse_mode ? 2 : 1), pp.xslot_bytes, pp.tslot_bytes,
+                   pp.ring_bytes, pp.chunk_cap, L, TS,
+                   (unsigned)std::count_if(desc.begin(), desc.end(),
+                                           [](const StepDesc& d) { return (d.flags & kStepFuse) != 0; }));
     P->stream_bytes = stream_bytes;
     P->algo_bytes = (uint64_t)algo;
     for (auto fn : {k_decode_pass<false>, k_decode_pass<true>})
       NQB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)P->smem_bytes));
     int per_sm = 0;
-    NQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_pass<false>, kThreads,
-                                                           P->smem_bytes));
+    NQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_pass<false>,
+                                                           kPassThreads, P->smem_bytes));
     NQB_REQUIRE(per_sm >= 1, NQB_E_INTERNAL, "decode pass kernel does not fit an SM");
   } catch (...) {
     pass_free(P);
@@ -686,7 +1049,7 @@ void pass_launch(nqb_context* ctx, const nqb_pass* P, unsigned long long* trace)
   pp.trace = trace;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P->G);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kPassThreads);
   cfg.dynamicSmemBytes = P->smem_bytes;
   cfg.stream = ctx->stream;
   // cooperative launch: the runtime guarantees every CTA is co-resident (the
@@ -700,6 +1063,8 @@ void pass_launch(nqb_context* ctx, const nqb_pass* P, unsigned long long* trace)
   else NQB_CUDA(cudaLaunchKernelEx(&cfg, k_decode_pass<false>, pp));
   NQB_LAUNCHED(ctx);
 }
+
+uint32_t pass_trace_words(const nqb_pass* P) { return P->G * (kPassStamps * P->K + 2); }
 
 void pass_free(nqb_pass* P) {
   if (!P) return;

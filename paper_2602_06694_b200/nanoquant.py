@@ -587,14 +587,19 @@ class DecodePass:
         _check(self.ctx.lib.nqb_pass_launch(self.ctx.handle, self.handle), "nqb_pass_launch")
 
     def trace(self):
-        """One launch with per-CTA %globaltimer stamps -> (grid, 2K+2) uint64 array."""
+        """One launch with per-CTA %globaltimer stamps -> (grid, 16K+2) uint64 array:
+        [CTA start, per step (stage-1 start, stage-1 end, t ready, stage-2 end,
+        t barrier seen by the t loader, x staged by the x stager, stage-1 first
+        chunk landed, x quantised, stage-1 MMA done, t quantised, stage-2 MMA
+        done, producer issued stage 1, t loader got its slot, t copy issued, producer started / finished stage 2),
+        end]; stamp 6 = producer finished stage 1."""
         self.ctx.bind_torch_stream(self._keep[0][1].device)
         g = C.c_uint32()
-        n = self.ctx.num_sms if hasattr(self.ctx, "num_sms") else 160
-        out = np.zeros(max(n, 160) * (2 * self.steps + 2), np.uint64)
+        per = 16 * self.steps + 2
+        out = np.zeros(160 * per, np.uint64)
         _check(self.ctx.lib.nqb_debug_pass_trace(self.ctx.handle, self.handle, _ptr(out),
                                                  C.byref(g)), "nqb_debug_pass_trace")
-        return out[: g.value * (2 * self.steps + 2)].reshape(g.value, 2 * self.steps + 2)
+        return out[: g.value * per].reshape(g.value, per)
 
     def free(self):
         if getattr(self, "handle", None):
