@@ -64,36 +64,40 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 
 // mbarrier wait with a watchdog: a wait that never completes traps the
 // launch (reported as a CUDA error) instead of hanging the device.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity, bool suspend) {
+  uint32_t ok;
+  if (suspend)
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(ok)
+        : "r"(tc::smem_u32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(ok)
+        : "r"(tc::smem_u32(bar)), "r"(parity)
+        : "memory");
+  return ok != 0;
+}
+// Slow path of mbar_wait_wd (one out-of-line copy): keeps waiting, with a
+// wall-clock watchdog (a suspended try_wait may sleep) that traps after ~10 s so
+// a wait that never completes is a reported launch error, not a hung device.
+static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, bool suspend) {
+  const unsigned long long t0 = globaltimer();
+  for (uint32_t it = 1;; ++it) {
+    if (mbar_try(bar, parity, suspend)) return;
+    if ((it & 255u) == 0 && globaltimer() - t0 > 10000000000ull) __trap();
+  }
+}
 // With `suspend` the wait sleeps (suspend-time hint) instead of spinning, so
 // waiting warps leave the issue slots to the warps that have work.
 __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, bool suspend = false) {
-  uint32_t ok = 0, it = 0;
-  unsigned long long t0 = 0;
-  for (;;) {
-    if (suspend)
-      asm volatile(
-          "{\n\t.reg .pred P;\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
-          "selp.u32 %0, 1, 0, P;\n\t}\n"
-          : "=r"(ok)
-          : "r"(tc::smem_u32(bar)), "r"(parity), "r"(0x989680u)
-          : "memory");
-    else
-      asm volatile(
-          "{\n\t.reg .pred P;\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
-          "selp.u32 %0, 1, 0, P;\n\t}\n"
-          : "=r"(ok)
-          : "r"(tc::smem_u32(bar)), "r"(parity)
-          : "memory");
-    if (ok) return;
-    // watchdog (wall clock: a suspended try_wait may sleep): trap after ~10 s
-    if ((++it & 255u) == 0) {
-      const unsigned long long now = globaltimer();
-      if (!t0) t0 = now;
-      else if (now - t0 > 10000000000ull) __trap();
-    }
-  }
+  if (!mbar_try(bar, parity, suspend)) mbar_wait_slow(bar, parity, suspend);
 }
 
 // Tile index q (0..7) of input K inside its slab of a K-long dimension.

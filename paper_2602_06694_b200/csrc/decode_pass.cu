@@ -7,8 +7,8 @@
 // from max|x| (a prepass or the producing step's published max|y|, equal to
 // the per-call kernel's own pass over x) and the t exponent from m.
 //
-// This translation unit runs 12 consumer warps (+4 helper warps = 512 threads,
-// 128 registers per thread at one CTA per SM).
+// This translation unit runs 12 consumer warps in two stage groups (+5 helper
+// warps = 544 threads, 120 registers per thread at one CTA per SM).
 #define NQB_DEC_WARPS 12
 #include <algorithm>
 #include <cstdio>
@@ -139,71 +139,17 @@ struct ChunkRec {
   uint32_t sb;      // section bytes (the stage-2 s1 scales follow them in the last chunk)
 };
 
-// All (tile pair, section) work of one resident chunk, split over the consumer
-// warps (the per-call kernel's linear-mode loop, decode_dev.cuh run_stage);
-// leaves the chunk's partial row sums added into red[].
-__device__ __forceinline__ void run_chunk(const uint8_t* base, const StageGeo& g, uint32_t s0,
-                                          uint32_t nsec, const uint8_t* bfrag, int* red) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t gq = lane >> 2, c = lane & 3;
-  const uint32_t rtn = g.rtn;
-  const uint32_t npair = (rtn + 1) / 2, U = npair * nsec;
-  const uint32_t f0 = (uint32_t)((uint64_t)U * warp / kConsumerWarps);
-  const uint32_t f1 = (uint32_t)((uint64_t)U * (warp + 1) / kConsumerWarps);
-  if (f0 >= f1) return;
+// Sections [sa, sb) of row-tile pair pr inside a resident chunk whose first
+// section is s0c, accumulated and flushed into red[] (the pair's rows).
+__device__ __forceinline__ void run_pair(const uint8_t* base, const StageGeo& g, uint32_t s0c,
+                                         uint32_t pr, uint32_t sa, uint32_t sb,
+                                         const uint8_t* bfrag, int* red) {
+  const int lane = threadIdx.x & 31;
   int acc[2][4][4];
 #pragma unroll
   for (int j = 0; j < 2; ++j)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[j][q][0] = acc[j][q][1] = acc[j][q][2] = acc[j][q][3] = 0;
-  uint32_t F, rem;
-  slab_split(g.K, F, rem);
-  const uint32_t sl_first = g.slab0 + s0;  // absolute slab of the chunk's first section
-  const uint32_t k_first = slab_of(g.K, sl_first).k0;
-  const uint32_t nfull = F > sl_first ? F - sl_first : 0;  // full slabs come first
-  uint32_t cur = f0 / nsec;
-  uint32_t snext = f0 - cur * nsec;
-  for (uint32_t f = f0, pr = cur; f < f1; ++pr) {
-    uint32_t s = snext;
-    const uint32_t send = min(nsec, s + (f1 - f));
-    f += send - s;
-    snext = 0;
-    if (pr != cur) {
-      flush_rows(acc[0], red + 2 * cur * 16 * kRedStride, lane);
-      if (2 * cur + 1 < rtn) flush_rows(acc[1], red + (2 * cur + 1) * 16 * kRedStride, lane);
-      cur = pr;
-    }
-    const uint32_t t0 = 2 * pr;
-    const bool two = t0 + 1 < rtn;
-    const uint32_t sf = min(send, nfull);
-    if (s < sf) {
-      const uint32_t k0 = 256 * (sl_first + s);
-      const uint8_t* unit = base + 2u * rtn * (k0 - k_first) + t0 * 512;
-      const uint8_t* bp = bfrag + kBytesPerK * (k0 - g.klo) + (gq * 4 + c) * 16;
-      if (two) full_run<2>(unit, 512u * rtn, bp, sf - s, lane, gq < (uint32_t)kLimbs, acc);
-      else full_run<1>(unit, 512u * rtn, bp, sf - s, lane, gq < (uint32_t)kLimbs, acc);
-      s = sf;
-    }
-    for (; s < send; ++s) {  // the 128 / 64 tails
-      uint2 b[8];
-      const Slab sl = slab_of(g.K, sl_first + s);
-      const uint32_t ub = unit_bytes(sl.nq);
-      const uint8_t* unit = base + 2u * rtn * (sl.k0 - k_first) + t0 * ub;
-      load_b(bfrag, g.klo, sl, gq, c, b);
-      if (two) tiles_mma<2>(unit, ub, sl.nq, lane, b, acc);
-      else tiles_mma<1>(unit, ub, sl.nq, lane, b, acc);
-    }
-  }
-  flush_rows(acc[0], red + 2 * cur * 16 * kRedStride, lane);
-  if (2 * cur + 1 < rtn) flush_rows(acc[1], red + (2 * cur + 1) * 16 * kRedStride, lane);
-}
-
-// Sections [sa, sb) of row-tile pair pr inside a resident chunk whose first
-// section is s0c, accumulated into acc and flushed into red[] (pair's rows).
-__device__ __forceinline__ void run_pair(const uint8_t* base, const StageGeo& g, uint32_t s0c,
-                                         uint32_t pr, uint32_t sa, uint32_t sb,
-                                         const uint8_t* bfrag, int* red, int (&acc)[2][4][4]) {
-  const int lane = threadIdx.x & 31;
   const uint32_t gq = lane >> 2, c = lane & 3;
   const uint32_t rtn = g.rtn, t0 = 2 * pr;
   const bool two = t0 + 1 < rtn;
@@ -237,8 +183,8 @@ __device__ __forceinline__ void run_pair(const uint8_t* base, const StageGeo& g,
 
 // max|x| bits over x[lo, hi): binary16 magnitude bits (>= 0x7C00: non-finite)
 // or |fp32| bits (non-finite -> +Inf bits), so every bound is an ordered uint.
-__device__ __forceinline__ uint32_t absmax_bits(const void* x, uint32_t lo, uint32_t hi, bool f32,
-                                                bool vec, uint32_t t, uint32_t nt) {
+__device__ __noinline__ uint32_t absmax_bits(const void* x, uint32_t lo, uint32_t hi, bool f32,
+                                             bool vec, uint32_t t, uint32_t nt) {
   uint32_t mb = 0;
   if (f32) {
     const uint32_t* xf = (const uint32_t*)x;
@@ -289,37 +235,59 @@ __device__ __forceinline__ void share_of(uint32_t m, uint32_t b, uint32_t G, uin
     if (kTrace) trp[1 + kPassStamps * (k) + (i)] = globaltimer();              \
   } while (0)
 
+// Named barriers of the two consumer groups (ids 1, 2) and of all consumers (3).
+__device__ __forceinline__ void group_sync(int gid) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(1 + gid), "n"(kGroupThreads) : "memory");
+}
+__device__ __forceinline__ void all_consumers_sync() {
+  asm volatile("bar.sync 3, %0;\n" ::"n"(kConsumerThreads) : "memory");
+}
+__device__ __forceinline__ void gpartial(long long a, long long* red8g, int gw, int lane) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(~0u, a, o);
+  if (lane == 0) red8g[gw] = a;
+}
+__device__ __forceinline__ long long gsum(const long long* red8g) {
+  long long s = 0;
+#pragma unroll
+  for (int w = 0; w < kGroupWarps; ++w) s += red8g[w];
+  return s;
+}
+
 template <bool kTrace>
 __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_constant__ PassParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* full = (uint64_t*)smem;
-  uint64_t* empty = full + kPassSlots;
-  uint64_t* dfull = empty + kPassSlots;
+  uint64_t* full1 = (uint64_t*)smem;  // stage-1 ring
+  uint64_t* empty1 = full1 + kPassSlots;
+  uint64_t* full2 = empty1 + kPassSlots;  // stage-2 ring
+  uint64_t* empty2 = full2 + kPassSlots;
+  uint64_t* dfull = empty2 + kPassSlots;
   uint64_t* dempty = dfull + kDescSlots;
   uint64_t* xfull = dempty + kDescSlots;
   uint64_t* xempty = xfull + kXSlots;
   uint64_t* tfull = xempty + kXSlots;
   uint64_t* tempty = tfull + kMaxTSlots;
-  uint64_t* cdone = tempty + kMaxTSlots;
-  uint32_t* misc = (uint32_t*)(cdone + kDoneRing);  // [0] parity, [2..3] target
+  uint64_t* cdone1 = tempty + kMaxTSlots;
+  uint64_t* cdone2 = cdone1 + kDoneRing;
+  uint32_t* misc = (uint32_t*)(cdone2 + kDoneRing);  // [0] parity, [2..3] target
   uint8_t* dslots = (uint8_t*)misc + 64;
-  long long* red8 = (long long*)(dslots + kDescSlots * kDescSlotBytes);
-  float* xred = (float*)((uint8_t*)red8 + 256);
-  float* xmaxs = xred + 16;  // max|x| of steps in flight (ring of 16)
-  ChunkRec* recs = (ChunkRec*)((uint8_t*)xred + 128);
-  int* red1 = (int*)(recs + kPassSlots);       // stage-1 row sums
-  // stage-2 row sums and B fragments: own buffers only when a phase runs both stages
-  int* red2 = p.fused ? red1 + kMaxRt * 16 * kRedStride : red1;
-  uint8_t* bfrag1 = smem + p.head_bytes;                          // stage-1 (x limbs)
-  uint8_t* bfrag2 = p.fused ? bfrag1 + p.bfrag_bytes : bfrag1;    // stage-2 (t limbs)
-  uint8_t* xslots = bfrag2 + p.bfrag_bytes;
+  long long* red8 = (long long*)(dslots + kDescSlots * kDescSlotBytes);  // 2 x 16 partials
+  float* xmaxs = (float*)((uint8_t*)red8 + 256);  // max|x| of steps in flight (ring of 16)
+  ChunkRec* recs1 = (ChunkRec*)((uint8_t*)xmaxs + 64);
+  ChunkRec* recs2 = recs1 + kPassSlots;
+  int* red1 = (int*)(smem + pass_head_bytes());       // stage-1 row sums
+  int* red2 = (int*)((uint8_t*)red1 + p.red1_bytes);  // stage-2 row sums
+  uint8_t* bfrag1 = (uint8_t*)red2 + p.red2_bytes;    // stage-1 B fragments (x limbs)
+  uint8_t* bfrag2 = bfrag1 + p.bfrag1_bytes;  // stage-2 B fragments (t limbs)
+  uint8_t* xslots = bfrag2 + p.bfrag2_bytes;
   uint8_t* tslots = xslots + kXSlots * p.xslot_bytes;
   const uint32_t TS = p.tslots;
-  uint8_t* ring = tslots + TS * p.tslot_bytes;
+  uint8_t* ring1 = tslots + TS * p.tslot_bytes;
+  uint8_t* ring2 = ring1 + p.ring1_bytes;
 
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(~0u, tid >> 5, 0);
-  const uint32_t K = p.K, G = p.G, RB = p.ring_bytes, cap = p.chunk_cap;
+  const uint32_t K = p.K, G = p.G;
   const bool sus = (p.debug & 4u) != 0;
   auto desc_of = [&](uint32_t k) -> const StepDesc& {
     return *(const StepDesc*)(dslots + (k % kDescSlots) * kDescSlotBytes);
@@ -331,12 +299,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
 
   if (tid == 0) {
     for (int s = 0; s < kPassSlots; ++s) {
-      tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], kConsumerWarps);
+      tc::mbar_init(&full1[s], 1);
+      tc::mbar_init(&empty1[s], kGroupWarps);
+      tc::mbar_init(&full2[s], 1);
+      tc::mbar_init(&empty2[s], kGroupWarps);
     }
     for (int s = 0; s < kDescSlots; ++s) {
       tc::mbar_init(&dfull[s], 1);
-      tc::mbar_init(&dempty[s], 4);  // consumers, producer, x stager, t loader
+      tc::mbar_init(&dempty[s], 4);  // stage-2 group, producer, x stager, t loader
     }
     for (int s = 0; s < kXSlots; ++s) {
       tc::mbar_init(&xfull[s], 1);
@@ -346,7 +316,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       tc::mbar_init(&tfull[s], 1);
       tc::mbar_init(&tempty[s], 1);
     }
-    for (int s = 0; s < kDoneRing; ++s) tc::mbar_init(&cdone[s], 1);
+    for (int s = 0; s < kDoneRing; ++s) {
+      tc::mbar_init(&cdone1[s], 1);
+      tc::mbar_init(&cdone2[s], 1);
+    }
     tc::fence_mbar_init();
     const unsigned long long gen = ld_relaxed_u64(p.ctr);
     misc[0] = (uint32_t)(gen & 1);
@@ -372,37 +345,42 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     if (role == 0) {
       // ------------------------------------------------------------ producer
       if (lane != 0) return;
-      uint64_t pos = 0;
-      uint32_t chunk = 0, rel = 0;
-      uint64_t starts[kPassSlots];
+      uint64_t pos[2] = {0, 0}, starts[2][kPassSlots];
+      uint32_t chunk[2] = {0, 0}, rel[2] = {0, 0};
       auto issue_stage = [&](uint32_t k, int stage) {
         const StepDesc& D = desc_of(k);
         const Cta& C = cta_of(k);
         const StageGeo g = stage == 1 ? stage1_geo(D, C) : stage2_geo(D, C);
+        const int r = stage - 1;
+        const uint32_t RB = r ? p.ring2_bytes : p.ring1_bytes;
+        const uint32_t cap = r ? p.chunk2_cap : p.chunk1_cap;
+        uint64_t* fullr = r ? full2 : full1;
+        uint64_t* emptyr = r ? empty2 : empty1;
+        ChunkRec* recs = r ? recs2 : recs1;
+        uint8_t* ring = r ? ring2 : ring1;
         uint32_t s0 = 0;
         uint64_t src = g.src_off;
         while (s0 < g.nsec) {
           uint32_t s1;
           const uint32_t sb = chunk_span(g, s0, cap, &s1);
-          const uint64_t start = ring_place(pos, sb, RB);
+          const uint64_t start = ring_place(pos[r], sb, RB);
           // wait for the slot and for every older chunk this range overwrites: chunks
           // are placed monotonically, so [start, pos) reaches older chunk c's bytes
           // in the ring exactly when pos > start_c + RB
-          while (rel < chunk &&
-                 (chunk - rel >= (uint32_t)kPassSlots || starts[rel % kPassSlots] + RB < pos)) {
-            mbar_wait_wd(&empty[rel % kPassSlots], (rel / kPassSlots) & 1, sus);
-            ++rel;
+          while (rel[r] < chunk[r] && (chunk[r] - rel[r] >= (uint32_t)kPassSlots ||
+                                       starts[r][rel[r] % kPassSlots] + RB < pos[r])) {
+            mbar_wait_wd(&emptyr[rel[r] % kPassSlots], (rel[r] / kPassSlots) & 1, sus);
+            ++rel[r];
           }
-          starts[chunk % kPassSlots] = start;
-          uint64_t* bar = &full[chunk % kPassSlots];
+          const uint32_t slot = chunk[r] % kPassSlots;
+          starts[r][slot] = start;
           const uint32_t roff = (uint32_t)(start % RB);
-          uint8_t* dst = ring + roff;
-          recs[chunk % kPassSlots] = ChunkRec{roff, (uint16_t)s0, (uint16_t)s1, 0u, sb};
-          tc::mbar_arrive_expect_tx(bar, sb);
-          tc::bulk_g2s(dst, D.bits + src, sb, bar);
+          recs[slot] = ChunkRec{roff, (uint16_t)s0, (uint16_t)s1, 0u, sb};
+          tc::mbar_arrive_expect_tx(&fullr[slot], sb);
+          tc::bulk_g2s(ring + roff, D.bits + src, sb, &fullr[slot]);
           src += sb;
           s0 = s1;
-          ++chunk;
+          ++chunk[r];
         }
       };
       uint32_t n1 = 0;
@@ -490,6 +468,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     }
     if (role == 2) {
       // ------------------------------------------------------------ t loader
+      int32_t ywaited = -1;
       for (uint32_t k = 0; k < K; ++k) {
         const uint32_t slot = k % TS;
         if (k >= TS) mbar_wait_wd(&tempty[slot], ((k / TS) - 1) & 1, sus);
@@ -499,6 +478,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         const Cta& C = cta_of(k);
         if (lane == 0) {
           if (C.s2_rtn || (k == 0 && blockIdx.x == 0)) poll_ctr(tbar + (size_t)k * kCtrStride, target);
+          // an earlier step writing an overlapping output must be done everywhere
+          if (D.y_src >= 0 && D.y_src > ywaited) {
+            poll_ctr(ybar + (size_t)D.y_src * kCtrStride, target);
+            ywaited = D.y_src;
+          }
           // every CTA read the generation before its first arrival: advance it
           if (k == 0 && blockIdx.x == 0) p.ctr[0] = target / G;
           if (kTrace) PSTAMP(k, 4);
@@ -526,8 +510,16 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       }
       return;
     }
-    // -------------------------------------------------------------- sequencer
     if (lane != 0) return;
+    if (role == 3) {
+      // ------------------------------------------- sequencer 1: t barriers
+      for (uint32_t j = 0; j < K; ++j) {
+        mbar_wait_wd(&cdone1[j % kDoneRing], (j / kDoneRing) & 1, sus);
+        arrive_ctr(tbar + (size_t)j * kCtrStride);  // stage-1 t reds ordered before it
+      }
+      return;
+    }
+    // --------------------- sequencer 2: output barriers, descriptor prefetch
     auto issue_desc = [&](uint32_t k) {
       const uint32_t slot = k % kDescSlots;
       uint8_t* dst = dslots + slot * kDescSlotBytes;
@@ -536,21 +528,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       tc::bulk_g2s(dst + 480, p.ctas + (size_t)k * G + blockIdx.x, 32, &dfull[slot]);
     };
     for (uint32_t k = 0; k < min(K, (uint32_t)kDescSlots); ++k) issue_desc(k);
-    uint32_t n1 = 0, ph = 0;
-    auto wait_phase = [&]() {
-      mbar_wait_wd(&cdone[ph % kDoneRing], (ph / kDoneRing) & 1, sus);
-      ++ph;
-    };
     for (uint32_t k = 0; k < K; ++k) {
       wait_desc(k);
-      const uint32_t ahead = desc_of(k).s1_ahead;
       const bool publish = desc_of(k).flags & kStepPublish;
-      while (n1 < ahead) {
-        wait_phase();  // stage 1 of n1 done: its t reds are ordered before the release
-        arrive_ctr(tbar + (size_t)n1 * kCtrStride);
-        ++n1;
-      }
-      wait_phase();  // stage 2 of k done
+      mbar_wait_wd(&cdone2[k % kDoneRing], (k / kDoneRing) & 1, sus);
       if (publish) arrive_ctr(ybar + (size_t)k * kCtrStride);
       if (k + kDescSlots < K) {
         mbar_wait_wd(&dempty[k % kDescSlots], (k / kDescSlots) & 1, sus);
@@ -561,8 +542,13 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   }
 
   // ================================================================ consumers
-  for (int i = tid; i < (p.fused ? 2 : 1) * kMaxRt * 16 * kRedStride / 4; i += kConsumerThreads)
-    ((int4*)red1)[i] = make_int4(0, 0, 0, 0);
+  const int gid = warp / kGroupWarps;  // 0: stage-1 group, 1: stage-2 group
+  const int gw = warp - gid * kGroupWarps;
+  const int gt = tid - gid * kGroupThreads;
+  int* const red = gid ? red2 : red1;
+  long long* const red8g = red8 + 16 * gid;
+  for (uint32_t i = gt; i < (gid ? p.red2_bytes : p.red1_bytes) / 16; i += kGroupThreads)
+    ((int4*)red)[i] = make_int4(0, 0, 0, 0);
   // ---- |x| prepass: this CTA's share of every independent input, one grid barrier
   if (p.has_pre) {
     for (uint32_t k = tid; k < K; k += kConsumerThreads) {
@@ -578,236 +564,185 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         atomicMax(amax + 4 * (size_t)__ldg(&Dg->amax_idx), mb);
       }
     }
-    consumers_sync();
+    all_consumers_sync();
     if (tid == 0) arrive_ctr(xinit);
   }
-  uint32_t n1 = 0, ph = 0, chunk = 0;
-  auto wait_chunk = [&]() -> ChunkRec {
-    mbar_wait_wd(&full[chunk % kPassSlots], (chunk / kPassSlots) & 1, sus);
-    return recs[chunk % kPassSlots];
-  };
-  auto release_chunk = [&]() {
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(&empty[chunk % kPassSlots]);
-    ++chunk;
-  };
-  // The stage's (pair, section) items are split over the warps once for the
-  // whole stage (pair-major, contiguous per warp), not per chunk: each warp walks
-  // the chunks as they land and runs its items in each.
-  auto mma_stage = [&](const StageGeo& g, const uint8_t* bf, int* rd) {
+  uint32_t chunk = 0;
+  uint64_t* const fullr = gid ? full2 : full1;
+  uint64_t* const emptyr = gid ? empty2 : empty1;
+  const ChunkRec* const recs = gid ? recs2 : recs1;
+  const uint8_t* const ring = gid ? ring2 : ring1;
+  // The stage's (pair, section) items are split over the group's warps once for
+  // the whole stage (pair-major, contiguous per warp); each warp walks the
+  // chunks as they land and runs its items in each.
+  auto mma_stage = [&](const StageGeo& g, const uint8_t* bf) {
     if (!g.nsec) return;
     const uint32_t npair = (g.rtn + 1) / 2, U = npair * g.nsec;
-    const uint32_t f0 = (uint32_t)((uint64_t)U * warp / kConsumerWarps);
-    const uint32_t f1 = (uint32_t)((uint64_t)U * (warp + 1) / kConsumerWarps);
+    const uint32_t f0 = U * gw / kGroupWarps, f1 = U * (gw + 1) / kGroupWarps;
     const uint32_t p0 = f0 / g.nsec, p1 = f1 ? (f1 - 1) / g.nsec : 0;
-    int acc[2][4][4];
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[j][q][0] = acc[j][q][1] = acc[j][q][2] = acc[j][q][3] = 0;
     for (uint32_t s0 = 0; s0 < g.nsec;) {
-      const ChunkRec cr = wait_chunk();
+      const uint32_t slot = chunk % kPassSlots;
+      mbar_wait_wd(&fullr[slot], (chunk / kPassSlots) & 1, sus);
+      const ChunkRec cr = recs[slot];
       if (f0 < f1 && !(p.debug & 1u)) {
         for (uint32_t pr = p0; pr <= p1; ++pr) {
           const uint32_t sa = max(s0, pr == p0 ? f0 - p0 * g.nsec : 0u);
           const uint32_t sb = min((uint32_t)cr.s1, pr == p1 ? f1 - p1 * g.nsec : g.nsec);
-          if (sa < sb) run_pair(ring + cr.off, g, s0, pr, sa, sb, bf, rd, acc);
+          if (sa < sb) run_pair(ring + cr.off, g, s0, pr, sa, sb, bf, red);
         }
       }
-      release_chunk();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&emptyr[slot]);
+      ++chunk;
       s0 = cr.s1;
     }
   };
 
-  // One phase: stage 2 of step k2 and stage 1 of step j1 (either may be absent,
-  // -1), with one quantise / MMA / publish sequence and three CTA barriers.
-  auto run_phase = [&](int32_t k2, int32_t j1) {
-    StageGeo g2{}, g1{};
-    uint32_t ts_slot = 0, xs_slot = 0;
-    const StepDesc* D2 = nullptr;
-    const Cta* C2 = nullptr;
-    const StepDesc* D1 = nullptr;
-    const Cta* C1 = nullptr;
-    float xmax1 = 0.f;
-    if (k2 >= 0) {
-      D2 = &desc_of(k2);
-      C2 = &cta_of(k2);
-      g2 = stage2_geo(*D2, *C2);
-      ts_slot = k2 % TS;
-      mbar_wait_wd(&tfull[ts_slot], (k2 / TS) & 1, sus);
-      if (kTrace && tid == 0) PSTAMP(k2, 2);
-    }
-    if (j1 >= 0) {
-      wait_desc(j1);
-      D1 = &desc_of(j1);
-      C1 = &cta_of(j1);
-      g1 = stage1_geo(*D1, *C1);
-      xs_slot = j1 % kXSlots;
-      mbar_wait_wd(&xfull[xs_slot], (j1 / kXSlots) & 1, sus);
-      xmax1 = bound_value(*(const uint32_t*)(xslots + xs_slot * p.xslot_bytes),
-                          (D1->flags & kStepXF32) != 0);
-      if (kTrace && tid == 0) PSTAMP(j1, 0);
-    }
-    // ---- quantise t (stage 2) and x (stage 1) into their B fragments
-    long long asum = 0, tsum = 0;
-    if (g2.nsec && !(p.debug & 2u)) {
-      const Seg& S = D2->seg[C2->s2_seg];
-      const int sh = t_shift(D2->m);
-      const long long* T = (const long long*)(tslots + ts_slot * p.tslot_bytes) + (S.t_off & 1u);
-      const uint32_t nquad2 = kpad(S.r) / 4;
-      for (uint32_t qd = tid; qd < nquad2; qd += kConsumerThreads) {
-        long long v[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t kk = 4 * qd + e;
-          const long long t = kk < S.r ? T[kk] : 0;
-          v[e] = (t + (1ll << (sh - 1))) >> sh;
-          tsum += v[e];
-        }
-        emit_quad(bfrag2, 0, 4 * qd, q_of(4 * qd, S.r), v);
-      }
-    }
-    if (g1.nsec && !(p.debug & 2u)) {
-      const uint8_t* xs = xslots + xs_slot * p.xslot_bytes;
-      const bool xf32 = D1->flags & kStepXF32;
-      const bool nonfinite = is_inf(xmax1);
-      const int ea = act_exponent(D1->seg[C1->s1_seg].s2max, xmax1);
-      const uint32_t klo = g1.klo, nquad = g1.prefix / 8, m = D1->m;
-      const __half* s2s = (const __half*)(xs + p.xs2_off) - klo;
-      for (uint32_t qd = tid; qd < nquad; qd += kConsumerThreads) {
-        const uint32_t k0 = klo + 4 * qd;
-        float xv[4], sv[4];
-        if (k0 + 3 < m) {
-          const uint2 sh2 = *(const uint2*)(s2s + k0);
-          const float2 s01 = __half22float2(*(const __half2*)&sh2.x);
-          const float2 s23 = __half22float2(*(const __half2*)&sh2.y);
-          sv[0] = s01.x; sv[1] = s01.y; sv[2] = s23.x; sv[3] = s23.y;
-          if (xf32) {
-            const float4 v = *(const float4*)(xs + 16 + 16 * qd);
-            xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
-          } else {
-            const uint2 v = *(const uint2*)(xs + 16 + 8 * qd);
-            const float2 x01 = __half22float2(*(const __half2*)&v.x);
-            const float2 x23 = __half22float2(*(const __half2*)&v.y);
-            xv[0] = x01.x; xv[1] = x01.y; xv[2] = x23.x; xv[3] = x23.y;
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t kk = k0 + e;
-            sv[e] = xv[e] = 0.f;
-            if (kk < m) {
-              sv[e] = __half2float(s2s[kk]);
-              xv[e] = xf32 ? ((const float*)(xs + 16))[4 * qd + e]
-                           : __half2float(((const __half*)(xs + 16))[4 * qd + e]);
-            }
-          }
-        }
-        long long v[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float a = nonfinite ? 0.f : sv[e] * xv[e];  // packed.cpp:160
-          v[e] = __float2ll_rn(scale_pow2(a, kFix - ea));
-          asum += v[e];
-        }
-        emit_quad(bfrag1, klo, k0, q_of(k0, m), v);
-      }
-    }
-    warp_partials2(asum, tsum, red8);
-    consumers_sync();  // fragments and partial sums visible; the x slot is consumed
-    if (j1 >= 0 && tid == 0) {
-      xmaxs[j1 % 16] = xmax1;
-      tc::mbar_arrive(&xempty[xs_slot]);
-    }
-    if (kTrace && tid == 0) {
-      if (k2 >= 0) PSTAMP(k2, 9);
-      if (j1 >= 0) PSTAMP(j1, 7);
-    }
-    // ---- MMA: stage-2 chunks, then stage-1 chunks (the producer's order)
-    mma_stage(g2, bfrag2, red2);
-    mma_stage(g1, bfrag1, red1);
-    consumers_sync();
-    if (kTrace && tid == 0) {
-      if (k2 >= 0) PSTAMP(k2, 10);
-      if (j1 >= 0) PSTAMP(j1, 8);
-    }
-    // ---- publish: stage-1 t rows (exact int64 reds), stage-2 outputs
-    if (g1.nsec && !(p.debug & 8u)) {
-      const long long A = sum_partials(red8);
-      const Seg& S = D1->seg[C1->s1_seg];
-      long long* Tseg = arena + D1->t_off + S.t_off + (size_t)C1->s1_rt0 * 16;
-      for (uint32_t i = tid; i < (uint32_t)C1->s1_rtn * 16; i += kConsumerThreads) {
-        const long long v = 2 * row_value(red1 + i * kRedStride) - A;
-        int4* rr = (int4*)(red1 + i * kRedStride);
-        rr[0] = make_int4(0, 0, 0, 0);
-        rr[1] = make_int4(0, 0, 0, 0);
-        red_add_u64(&Tseg[i], v);
-      }
-    }
-    if (g2.nsec && !(p.debug & 8u)) {
-      const Seg& S = D2->seg[C2->s2_seg];
-      const float xmax = xmaxs[k2 % 16];
-      const int ea = act_exponent(S.s2max, xmax);
-      const bool nonfinite = is_inf(xmax);
-      const long long Tsum = sum_partials(red8 + kConsumerWarps);
-      const int E = t_shift(D2->m) + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
-      const bool yf32 = D2->flags & kStepYF32;
-      const __half* sc1 = (const __half*)(tslots + ts_slot * p.tslot_bytes + p.ts1_off);
-      void* Y = D2->y[C2->s2_seg];
-      uint32_t ymb = 0;
-      for (uint32_t i = tid; i < (uint32_t)C2->s2_rtn * 16; i += kConsumerThreads) {
-        const uint32_t row = C2->s2_rt0 * 16 + i;
-        int4* rr = (int4*)(red2 + i * kRedStride);
-        if (row < S.n) {
-          const long long Yi = 2 * row_value(red2 + i * kRedStride) - Tsum;
-          double y = (double)__half2float(sc1[i]) *
-                     ((double)Yi * __longlong_as_double((long long)(1023 + E) << 52));  // packed.cpp:189
-          if (nonfinite) y = __longlong_as_double(0x7ff8000000000000ll);
-          if (yf32) {
-            const float yo = (float)y;
-            ((float*)Y)[row] = yo;
-            const uint32_t b = __float_as_uint(yo) & 0x7FFFFFFFu;
-            ymb = max(ymb, b >= 0x7F800000u ? 0x7F800000u : b);
-          } else {
-            const __half h = __float2half_rn((float)y);
-            ((__half*)Y)[row] = h;
-            ymb = max(ymb, (uint32_t)(__half_as_ushort(h) & 0x7FFFu));
-          }
-        }
-        rr[0] = make_int4(0, 0, 0, 0);
-        rr[1] = make_int4(0, 0, 0, 0);
-      }
-      if (D2->flags & kStepPublish) {
-#pragma unroll
-        for (int o = 16; o; o >>= 1) ymb = max(ymb, __shfl_xor_sync(~0u, ymb, o));
-        if (lane == 0 && ymb)
-          atomicMax(amax + 4 * ((size_t)K + (size_t)k2 * kMaxSeg + C2->s2_seg), ymb);
-      }
-    }
-    consumers_sync();  // this phase's reds / stores happen-before the sequencer's releases
-    if (tid == 0) {
-      if (k2 >= 0) {
-        if (kTrace) PSTAMP(k2, 3);
-        tc::mbar_arrive(&tempty[ts_slot]);
-        tc::mbar_arrive(&cdone[ph % kDoneRing]);
-        ++ph;
-        tc::mbar_arrive(&dempty[k2 % kDescSlots]);
-      }
-      if (j1 >= 0) {
-        if (kTrace) PSTAMP(j1, 1);
-        tc::mbar_arrive(&cdone[ph % kDoneRing]);
-        ++ph;
-      }
-    }
-  };
-
+  // Both groups run the same loop (one copy of the MMA code in the kernel):
+  // group 0 does stage 1 of step k (x -> t), group 1 stage 2 (t -> y).
   for (uint32_t k = 0; k < K; ++k) {
     wait_desc(k);
-    const uint32_t ahead = desc_of(k).s1_ahead;
-    const bool fuse = desc_of(k).flags & kStepFuse;
-    while (n1 < ahead) run_phase(-1, (int32_t)n1++);
-    if (fuse && n1 < K) run_phase((int32_t)k, (int32_t)n1++);
-    else run_phase((int32_t)k, -1);
+    const StepDesc& D = desc_of(k);
+    const Cta& C = cta_of(k);
+    const uint32_t slot = gid ? k % TS : k % kXSlots;
+    const uint8_t* st = gid ? tslots + slot * p.tslot_bytes : xslots + slot * p.xslot_bytes;
+    if (gid) mbar_wait_wd(&tfull[slot], (k / TS) & 1, sus);
+    else mbar_wait_wd(&xfull[slot], (k / kXSlots) & 1, sus);
+    if (kTrace && gt == 0) PSTAMP(k, gid ? 2 : 0);
+    const StageGeo g = gid ? stage2_geo(D, C) : stage1_geo(D, C);
+    const float xmax = gid ? xmaxs[k % 16] : bound_value(*(const uint32_t*)st, (D.flags & kStepXF32) != 0);
+    const Seg& S = D.seg[gid ? C.s2_seg : C.s1_seg];
+    const int ea = act_exponent(S.s2max, xmax);
+    const bool nonfinite = is_inf(xmax);
+    const int sh = t_shift(D.m);
+    long long vsum = 0;  // sum of the quantised inputs (2 sum bit*v - sum v)
+    if (g.nsec && !(p.debug & 2u)) {
+      if (gid) {  // t (exact int64 sums) -> 38-bit fixed point
+        const long long* T = (const long long*)st + (S.t_off & 1u);
+        const uint32_t nquad2 = kpad(S.r) / 4;
+        for (uint32_t qd = gt; qd < nquad2; qd += kGroupThreads) {
+          long long v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t kk = 4 * qd + e;
+            const long long t = kk < S.r ? T[kk] : 0;
+            v[e] = (t + (1ll << (sh - 1))) >> sh;
+            vsum += v[e];
+          }
+          emit_quad(bfrag2, 0, 4 * qd, q_of(4 * qd, S.r), v);
+        }
+      } else {  // a = s2 * x (packed.cpp:160) -> 38-bit fixed point
+        const bool xf32 = D.flags & kStepXF32;
+        const uint32_t klo = g.klo, nquad = g.prefix / 8, m = D.m;
+        const __half* s2s = (const __half*)(st + p.xs2_off) - klo;
+        for (uint32_t qd = gt; qd < nquad; qd += kGroupThreads) {
+          const uint32_t k0 = klo + 4 * qd;
+          float xv[4], sv[4];
+          if (k0 + 3 < m) {
+            const uint2 sh2 = *(const uint2*)(s2s + k0);
+            const float2 s01 = __half22float2(*(const __half2*)&sh2.x);
+            const float2 s23 = __half22float2(*(const __half2*)&sh2.y);
+            sv[0] = s01.x; sv[1] = s01.y; sv[2] = s23.x; sv[3] = s23.y;
+            if (xf32) {
+              const float4 v = *(const float4*)(st + 16 + 16 * qd);
+              xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+            } else {
+              const uint2 v = *(const uint2*)(st + 16 + 8 * qd);
+              const float2 x01 = __half22float2(*(const __half2*)&v.x);
+              const float2 x23 = __half22float2(*(const __half2*)&v.y);
+              xv[0] = x01.x; xv[1] = x01.y; xv[2] = x23.x; xv[3] = x23.y;
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t kk = k0 + e;
+              sv[e] = xv[e] = 0.f;
+              if (kk < m) {
+                sv[e] = __half2float(s2s[kk]);
+                xv[e] = xf32 ? ((const float*)(st + 16))[4 * qd + e]
+                             : __half2float(((const __half*)(st + 16))[4 * qd + e]);
+              }
+            }
+          }
+          long long v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float a = nonfinite ? 0.f : sv[e] * xv[e];
+            v[e] = __float2ll_rn(scale_pow2(a, kFix - ea));
+            vsum += v[e];
+          }
+          emit_quad(bfrag1, klo, k0, q_of(k0, m), v);
+        }
+      }
+    }
+    gpartial(vsum, red8g, gw, lane);
+    group_sync(gid);  // fragments and partials visible; an x slot is consumed
+    if (gt == 0 && !gid) {
+      xmaxs[k % 16] = xmax;
+      tc::mbar_arrive(&xempty[slot]);
+    }
+    if (kTrace && gt == 0) PSTAMP(k, gid ? 9 : 7);
+    mma_stage(g, gid ? bfrag2 : bfrag1);
+    group_sync(gid);
+    if (kTrace && gt == 0) PSTAMP(k, gid ? 10 : 8);
+    if (g.nsec && !(p.debug & 8u)) {
+      const long long A = gsum(red8g);
+      if (!gid) {  // stage-1 publish: t rows (exact int64 reds)
+        long long* Tseg = arena + D.t_off + S.t_off + (size_t)C.s1_rt0 * 16;
+        for (uint32_t i = gt; i < (uint32_t)C.s1_rtn * 16; i += kGroupThreads) {
+          const long long v = 2 * row_value(red + i * kRedStride) - A;
+          int4* rr = (int4*)(red + i * kRedStride);
+          rr[0] = make_int4(0, 0, 0, 0);
+          rr[1] = make_int4(0, 0, 0, 0);
+          red_add_u64(&Tseg[i], v);
+        }
+      } else {  // stage-2 outputs (packed.cpp:174-190)
+        const int E = sh + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
+        const bool yf32 = D.flags & kStepYF32;
+        const __half* sc1 = (const __half*)(st + p.ts1_off);
+        void* Y = D.y[C.s2_seg];
+        uint32_t ymb = 0;
+        for (uint32_t i = gt; i < (uint32_t)C.s2_rtn * 16; i += kGroupThreads) {
+          const uint32_t row = C.s2_rt0 * 16 + i;
+          int4* rr = (int4*)(red + i * kRedStride);
+          if (row < S.n) {
+            const long long Yi = 2 * row_value(red + i * kRedStride) - A;
+            double y = (double)__half2float(sc1[i]) *
+                       ((double)Yi * __longlong_as_double((long long)(1023 + E) << 52));  // packed.cpp:189
+            if (nonfinite) y = __longlong_as_double(0x7ff8000000000000ll);
+            if (yf32) {
+              const float yo = (float)y;
+              ((float*)Y)[row] = yo;
+              const uint32_t b = __float_as_uint(yo) & 0x7FFFFFFFu;
+              ymb = max(ymb, b >= 0x7F800000u ? 0x7F800000u : b);
+            } else {
+              const __half h = __float2half_rn((float)y);
+              ((__half*)Y)[row] = h;
+              ymb = max(ymb, (uint32_t)(__half_as_ushort(h) & 0x7FFFu));
+            }
+          }
+          rr[0] = make_int4(0, 0, 0, 0);
+          rr[1] = make_int4(0, 0, 0, 0);
+        }
+        if (D.flags & kStepPublish) {
+#pragma unroll
+          for (int o = 16; o; o >>= 1) ymb = max(ymb, __shfl_xor_sync(~0u, ymb, o));
+          if (lane == 0 && ymb)
+            atomicMax(amax + 4 * ((size_t)K + (size_t)k * kMaxSeg + C.s2_seg), ymb);
+        }
+      }
+    }
+    group_sync(gid);  // reds / outputs happen-before the sequencer's release
+    if (gt == 0) {
+      if (kTrace) PSTAMP(k, gid ? 3 : 1);
+      if (gid) {
+        tc::mbar_arrive(&tempty[slot]);
+        tc::mbar_arrive(&cdone2[k % kDoneRing]);
+        tc::mbar_arrive(&dempty[k % kDescSlots]);
+      } else {
+        tc::mbar_arrive(&cdone1[k % kDoneRing]);
+      }
+    }
   }
   if (kTrace && tid == 0) trp[kPassStamps * K + 1] = globaltimer();
 }
@@ -834,7 +769,9 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
   NQB_REQUIRE(steps != nullptr, NQB_E_VALIDATION, "null steps");
   const uint32_t G = (uint32_t)ctx->num_sms;
   std::vector<StepDesc> desc(K);
-  uint32_t bfrag = 0, xbytes = 16, s2bytes = 16, tbytes = 16, s1bytes = 16;
+  uint32_t bf1 = 0, bf2 = 0, xbytes = 16, s2bytes = 16, tbytes = 16, s1bytes = 16;
+  double bits1 = 0, bits2 = 0;  // stage-1 / stage-2 stream bytes (ring split)
+  uint32_t rt1 = 1, rt2 = 1;    // most row tiles of one CTA in stage 1 / stage 2
   uint64_t arena = 0, stream_bytes = 0;
   double algo = 0;
   bool has_pre = false;
@@ -864,18 +801,25 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
                   NQB_E_VALIDATION, "a pass step's output overlaps its own input");
       algo += (double)g->r[q] * (g->n[q] + g->m) / 8.0 + 2.0 * (g->n[q] + g->m) + esz * g->n[q];
       tbytes = std::max(tbytes, (((g->seg[q].t_off & 1u) + g->r[q] + 1) & ~1u) * 8u);
+      bf2 = std::max(bf2, kBytesPerK * kpad(g->r[q]));
+      bits1 += (double)g->r[q] * g->m;
+      bits2 += (double)g->r[q] * g->n[q];
     }
     algo += (double)esz * g->m;
-    bfrag = std::max(bfrag, g->bfrag_bytes);
     for (uint32_t c = 0; c < g->grid; ++c) {  // the CTA's stage-1 input slice
       const Cta& C = g->ctas[c];
       if (!C.s1_rtn || !C.s1_sln) continue;
       const Slab last = slab_of(g->m, C.s1_sl0 + C.s1_sln - 1);
       const uint32_t nk1 = last.k0 + 32 * last.nq - slab_of(g->m, C.s1_sl0).k0;
       xbytes = std::max(xbytes, esz * nk1);
+      bf1 = std::max(bf1, kBytesPerK * nk1);
       s2bytes = std::max(s2bytes, 2 * nk1);
     }
-    for (uint32_t c = 0; c < g->grid; ++c) s1bytes = std::max<uint32_t>(s1bytes, 32u * g->ctas[c].s2_rtn);
+    for (uint32_t c = 0; c < g->grid; ++c) {
+      s1bytes = std::max<uint32_t>(s1bytes, 32u * g->ctas[c].s2_rtn);
+      rt1 = std::max<uint32_t>(rt1, g->ctas[c].s1_rtn);
+      rt2 = std::max<uint32_t>(rt2, g->ctas[c].s2_rtn);
+    }
     stream_bytes += g->stream_bytes;
     D.t_off = arena;
     D.t_len = (g->R1 + 3) & ~1u;  // even, plus the odd-start overhang of a segment copy
@@ -894,6 +838,18 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
           exact = (int32_t)(K + j * kMaxSeg + q);
       }
     }
+    // an earlier step whose output overlaps this step's output: the stage-2 group
+    // runs step after step, but across CTAs only that step's output barrier
+    // orders the two writes
+    D.y_src = -1;
+    for (int j = (int)k - 1; j >= 0 && D.y_src < 0; --j) {
+      const uint32_t ej = (desc[j].flags & kStepYF32) ? 4 : 2;
+      for (uint32_t a = 0; a < desc[j].nseg && D.y_src < 0; ++a)
+        for (uint32_t b = 0; b < g->nseg && D.y_src < 0; ++b)
+          if (overlaps(desc[j].y[a], (size_t)desc[j].seg[a].n * ej, s.y[b], (size_t)g->n[b] * esz))
+            D.y_src = j;
+    }
+    if (D.y_src >= 0) desc[D.y_src].flags |= kStepPublish;
     if (D.x_src < 0) {
       D.flags |= kStepXPre;
       D.amax_idx = k;
@@ -904,28 +860,11 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       else D.flags |= kStepXSelf;
     }
   }
-  // phase order: stage 1 of step j may run before stage 2 of step i < j only if
-  // j reads or writes nothing that steps >= i write (RAW on x, WAW on y);
-  // s1_ahead[k] = stage-1 phases issued before stage 2 of k (non-decreasing)
-  // shared memory: head | 2 B-fragment buffers | x slots | t slots | weight ring.
-  // As many t slots as leave the ring >= NQB_PASS_RING_KB (default 64 KB: 4 x 16 KB
-  // bulk copies in flight already stream at the full per-SM HBM share).
-  const uint32_t bfrag_b = (bfrag + 127) / 128 * 128;
-  const uint32_t xs2_off = (16 + xbytes + 127) / 128 * 128;
-  const uint32_t xslot_b = (xs2_off + s2bytes + 127) / 128 * 128;
-  const uint32_t ts1_off = (tbytes + 127) / 128 * 128;
-  const uint32_t tslot_b = (ts1_off + s1bytes + 127) / 128 * 128;
-  const bool fuse_mode = env_u32p("NQB_PASS_FUSE", 0) != 0;
-  const uint32_t head = pass_head_bytes(fuse_mode);
-  const uint32_t ring_min = env_u32p("NQB_PASS_RING_KB", 128) * 1024;
-  const uint32_t base_b = head + (fuse_mode ? 2 : 1) * bfrag_b + kXSlots * xslot_b;
-  NQB_REQUIRE(base_b + 2 * tslot_b + ring_min / 2 <= 227u * 1024u, NQB_E_DIMENSION_MISMATCH,
-              "decode pass: staging buffers leave no room for the weight ring");
-  uint32_t TS = base_b + ring_min + 2 * tslot_b <= 227u * 1024u
-                    ? (227u * 1024u - base_b - ring_min) / tslot_b : 2u;
-  TS = std::max<uint32_t>(2, std::min<uint32_t>({TS, (uint32_t)kMaxTSlots,
-                                                 env_u32p("NQB_PASS_TSLOTS", 2)}));
-  const uint32_t L = std::min<uint32_t>(env_u32p("NQB_PASS_LOOKAHEAD", 2), kMaxLookahead);
+  // Producer order (stage-1 and stage-2 rings are filled in this interleaving):
+  // stage 1 of step j goes out before stage 2 of step i < j when j reads or
+  // writes nothing that steps >= i write (RAW on x, WAW on y);
+  // s1_ahead[k] = stage-1 issues before stage 2 of k (non-decreasing).
+  const uint32_t L = std::min<uint32_t>(env_u32p("NQB_PASS_LOOKAHEAD", 3), kMaxLookahead);
   std::vector<int32_t> dep(K, -1);
   for (uint32_t j = 0; j < K; ++j) {
     const uint32_t ej = (desc[j].flags & kStepYF32) ? 4 : 2;
@@ -949,16 +888,30 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       if (n1 < k + 1) n1 = k + 1;  // (dep[k] < k always holds)
       desc[k].s1_ahead = n1;
     }
-    // stage 2 of k shares a phase with the stage 1 that follows it in the order
-    // when that step does not depend on k (its x and y are independent of y_k)
-    if (fuse_mode)
-      for (uint32_t k = 0; k + 1 < K; ++k) {
-        const uint32_t j = desc[k].s1_ahead;  // the next stage-1 event after stage 2 of k
-        if (j < K && desc[k + 1].s1_ahead > j && dep[j] < (int32_t)k) desc[k].flags |= kStepFuse;
-      }
   }
-  NQB_REQUIRE(L + 4 < (uint32_t)kDescSlots && 2 * L + 6 <= (uint32_t)kDoneRing, NQB_E_INTERNAL,
-              "pass lookahead exceeds the descriptor / phase rings");
+  NQB_REQUIRE(L + 4 < (uint32_t)kDescSlots, NQB_E_INTERNAL,
+              "pass lookahead exceeds the descriptor ring");
+  // Shared memory: head | B fragments (x, t) | x slots | t slots | stage-1 ring |
+  // stage-2 ring.  The rings split what is left in proportion to the two stages'
+  // bytes (each >= 36 KB).
+  const uint32_t bf1_b = (std::max(bf1, 16u) + 127) / 128 * 128;
+  const uint32_t bf2_b = (std::max(bf2, 16u) + 127) / 128 * 128;
+  const uint32_t xs2_off = (16 + xbytes + 127) / 128 * 128;
+  const uint32_t xslot_b = (xs2_off + s2bytes + 127) / 128 * 128;
+  const uint32_t ts1_off = (tbytes + 127) / 128 * 128;
+  const uint32_t tslot_b = (ts1_off + s1bytes + 127) / 128 * 128;
+  const uint32_t head = pass_head_bytes();
+  const uint32_t TS = std::max<uint32_t>(2, std::min<uint32_t>(kMaxTSlots,
+                                                               env_u32p("NQB_PASS_TSLOTS", 2)));
+  const uint32_t red1_b = rt1 * 16 * kRedStride * 4, red2_b = rt2 * 16 * kRedStride * 4;
+  const uint32_t fixed = head + red1_b + red2_b + bf1_b + bf2_b + kXSlots * xslot_b + TS * tslot_b;
+  NQB_REQUIRE(fixed + 72u * 1024u <= 227u * 1024u, NQB_E_DIMENSION_MISMATCH,
+              "decode pass: staging buffers leave no room for the weight rings");
+  const uint32_t rings = (227u * 1024u - fixed) / 256 * 256;
+  const double f1 = bits1 + bits2 > 0 ? bits1 / (bits1 + bits2) : 0.5;
+  uint32_t ring1 = (uint32_t)(rings * f1) / 128 * 128;
+  ring1 = std::min(std::max(ring1, 36u * 1024u), rings - 36u * 1024u);
+  const uint32_t ring2 = rings - ring1;
 
   // ---- device memory: descriptors | CTA tables | counters | bounds | arena ----
   const uint32_t amax_words = K * (1 + kMaxSeg);
@@ -1002,31 +955,32 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     pp.arena_len = arena;
     pp.has_pre = has_pre ? 1 : 0;
     pp.debug = env_u32p("NQB_PASS_DEBUG", 0);
-    pp.bfrag_bytes = bfrag_b;
+    pp.red1_bytes = red1_b;
+    pp.red2_bytes = red2_b;
+    pp.bfrag1_bytes = bf1_b;
+    pp.bfrag2_bytes = bf2_b;
     pp.xs2_off = xs2_off;
     pp.xslot_bytes = xslot_b;
     pp.ts1_off = ts1_off;
     pp.tslot_bytes = tslot_b;
     pp.tslots = TS;
-    pp.fused = fuse_mode ? 1 : 0;
-    pp.head_bytes = head;
-    const uint32_t fixed = base_b + TS * tslot_b;
-    pp.ring_bytes = (227u * 1024u - fixed) / 128 * 128;
+    pp.ring1_bytes = ring1;
+    pp.ring2_bytes = ring2;
     const uint32_t cap_kb = env_u32p("NQB_PASS_CHUNK_KB", 0);
-    pp.chunk_cap = cap_kb ? cap_kb * 1024 : std::min<uint32_t>(32768, pp.ring_bytes / 3 / 128 * 128);
-    // a chunk is at most cap + the largest section (16 KB); the consumers hold one
-    // chunk at a time, so the ring must fit one
-    NQB_REQUIRE(pp.chunk_cap + 16384 <= pp.ring_bytes, NQB_E_VALIDATION,
-                "NQB_PASS_CHUNK_KB too large for the shared-memory ring");
-    P->smem_bytes = fixed + pp.ring_bytes;
+    // a chunk is at most cap + the largest section (16 KB); a group holds one
+    // chunk at a time, so its ring must fit one
+    pp.chunk1_cap = cap_kb ? cap_kb * 1024 : std::min<uint32_t>(32768, ring1 / 3 / 128 * 128);
+    pp.chunk2_cap = cap_kb ? cap_kb * 1024 : std::min<uint32_t>(32768, ring2 / 3 / 128 * 128);
+    NQB_REQUIRE(pp.chunk1_cap + 16384 <= ring1 && pp.chunk2_cap + 16384 <= ring2,
+                NQB_E_VALIDATION, "NQB_PASS_CHUNK_KB too large for the shared-memory rings");
+    P->smem_bytes = fixed + rings;
     if (env_u32p("NQB_PASS_VERBOSE", 0))
       std::fprintf(stderr,
-                   "nqb pass: K=%u G=%u smem=%u head=%u bfrag=%u xslot=%u tslot=%u ring=%u "
-                   "chunk_cap=%u lookahead=%u tslots=%u fused=%u\n",
-                   K, G, P->smem_bytes, head, pp.bfrag_bytes * (fuse_mode ? 2 : 1), pp.xslot_bytes, pp.tslot_bytes,
-                   pp.ring_bytes, pp.chunk_cap, L, TS,
-                   (unsigned)std::count_if(desc.begin(), desc.end(),
-                                           [](const StepDesc& d) { return (d.flags & kStepFuse) != 0; }));
+                   "nqb pass: K=%u G=%u smem=%u head=%u red=%u+%u bfrag=%u+%u xslot=%u tslot=%u x%u "
+                   "rings=%u+%u chunk caps=%u/%u lookahead=%u\n",
+                   K, G, P->smem_bytes, head, red1_b, red2_b, bf1_b, bf2_b, xslot_b, tslot_b, TS,
+                   ring1, ring2,
+                   pp.chunk1_cap, pp.chunk2_cap, L);
     P->stream_bytes = stream_bytes;
     P->algo_bytes = (uint64_t)algo;
     for (auto fn : {k_decode_pass<false>, k_decode_pass<true>})

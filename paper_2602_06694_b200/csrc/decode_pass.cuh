@@ -36,11 +36,11 @@ namespace dec {
 
 constexpr int kPassSlots = 16;   // weight ring chunks in flight (full/empty mbarrier pairs)
 constexpr int kDescSlots = 12;   // step descriptors in flight
-constexpr int kXSlots = 4;       // staged x slices in flight
+constexpr int kXSlots = 3;       // staged x slices in flight
 constexpr int kMaxTSlots = 6;    // staged t segments in flight (runtime count: PassParams::tslots)
 constexpr int kDoneRing = 24;    // consumer phase-completion mbarriers
 constexpr int kCtrStride = 16;   // u64 words per counter (own 128-byte line)
-constexpr int kPassHelpers = 4;  // producer, x stager, t loader, sequencer
+constexpr int kPassHelpers = 5;  // producer, x stager, t loader, sequencers 1 and 2
 constexpr int kPassStamps = 16;  // trace stamps per step
 constexpr int kMaxLookahead = 6;
 
@@ -51,7 +51,6 @@ enum : uint32_t {
   kStepPublish = 8u,   // a later step reads this step's output: output barrier + max|y|
   kStepXPre = 16u,     // |x| bound from the kernel-start prepass
   kStepXSelf = 32u,    // |x| bound computed by the x stager after the dependency
-  kStepFuse = 64u,     // stage 2 of this step shares a phase with the next stage 1
 };
 
 struct alignas(16) StepDesc {
@@ -62,10 +61,12 @@ struct alignas(16) StepDesc {
   Seg seg[kMaxSeg];
   uint32_t nseg, m, R1, flags;
   int32_t x_src;         // output barrier to pass before staging x (-1: none)
+  int32_t y_src;         // earlier step writing an overlapping output: its barrier gates stage 2
   uint32_t amax_idx;     // 16-byte bound word (per parity) holding max|x|
   uint64_t t_off;        // this step's t region (int64 index, even)
   uint32_t t_len;        // int64 words in the region (even)
-  uint32_t s1_ahead;     // stage-1 phases issued before this step's stage 2
+  uint32_t s1_ahead;     // stage-1 sections the producer issues before this step's stage 2
+  uint32_t pad[3];
 };
 static_assert(sizeof(StepDesc) % 16 == 0 && sizeof(StepDesc) <= 480, "step descriptor layout");
 constexpr uint32_t kDescSlotBytes = 512;  // descriptor + the CTA's 32-byte Cta entry at 480
@@ -79,22 +80,28 @@ struct PassParams {
   long long* arena;           // 2 parities x arena_len int64
   uint64_t arena_len;
   uint32_t amax_words;
-  uint32_t ring_bytes, bfrag_bytes, xslot_bytes, tslot_bytes, chunk_cap;
+  uint32_t ring1_bytes, ring2_bytes;     // stage-1 / stage-2 weight rings
+  uint32_t chunk1_cap, chunk2_cap;
+  uint32_t bfrag1_bytes, bfrag2_bytes;   // B fragments of x (stage 1) and t (stage 2)
+  uint32_t xslot_bytes, tslot_bytes;
+  uint32_t red1_bytes, red2_bytes;       // per-limb row sums (row tiles of the largest stage)
   uint32_t xs2_off;           // s2 slice offset in an x slot (header 16 B, then the x slice)
   uint32_t ts1_off;           // s1 slice offset in a t slot (after the t rows)
   uint32_t tslots;            // t slots (2..kMaxTSlots)
-  uint32_t fused;             // some phase runs two stages: second B-fragment / row-sum buffers
-  uint32_t head_bytes;        // pass_head_bytes(fused)
   uint32_t has_pre;
   uint32_t debug;  // NQB_PASS_DEBUG bits (experiments only): 1 skip MMA, 2 skip quantise, 4 suspend
                    // waits, 8 skip publish/outputs, 16 skip the t copy
   unsigned long long* trace;  // diagnostics: G x (kPassStamps K + 2) %globaltimer stamps
 };
 
-constexpr uint32_t kPassBars = 2 * kPassSlots + 2 * kDescSlots + 2 * kXSlots + 2 * kMaxTSlots + kDoneRing;
-__host__ __device__ __forceinline__ uint32_t pass_head_bytes(bool fused) {
-  return (8 * kPassBars + 64 + kDescSlots * kDescSlotBytes + 256 + 64 + 64 + 16 * kPassSlots +
-          (fused ? 2 : 1) * kRedBytes + 127) /
+constexpr int kGroupWarps = 6;                 // consumer warps per stage group
+constexpr int kGroupThreads = 32 * kGroupWarps;
+constexpr uint32_t kPassBars =
+    4 * kPassSlots + 2 * kDescSlots + 2 * kXSlots + 2 * kMaxTSlots + 2 * kDoneRing;
+// head: mbarriers | misc | descriptor slots | group partials | max|x| ring |
+// chunk records (2 rings)
+__host__ __device__ __forceinline__ uint32_t pass_head_bytes() {
+  return (8 * kPassBars + 64 + kDescSlots * kDescSlotBytes + 256 + 64 + 2 * 16 * kPassSlots + 127) /
          128 * 128;
 }
 
