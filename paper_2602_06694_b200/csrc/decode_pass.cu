@@ -42,22 +42,6 @@ __device__ __forceinline__ void poll_ctr(const unsigned long long* c, unsigned l
 __device__ __forceinline__ void arrive_ctr(unsigned long long* c) {
   asm volatile("red.release.gpu.global.add.u64 [%0], 1;\n" ::"l"(c) : "memory");
 }
-// LSU-path async copy (cp.async, not the TMA engine): small staging copies
-// must not queue behind the CTA's weight stream in the TMA unit.
-__device__ __forceinline__ void lsu_copy16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(smem_dst)),
-               "l"(gsrc)
-               : "memory");
-}
-// Copies `bytes` (multiple of 16, both ends 16-byte aligned) with all 32 lanes
-// and hooks completion onto `bar` (each lane's async arrive is pre-counted).
-__device__ __forceinline__ void lsu_copy(void* smem_dst, const void* gsrc, uint32_t bytes,
-                                         uint64_t* bar, int lane) {
-  for (uint32_t i = 16u * lane; i < bytes; i += 512u)
-    lsu_copy16((uint8_t*)smem_dst + i, (const uint8_t*)gsrc + i);
-  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(tc::smem_u32(bar))
-               : "memory");
-}
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* c) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(c) : "memory");
@@ -242,18 +226,6 @@ __device__ __forceinline__ void group_sync(int gid) {
 __device__ __forceinline__ void all_consumers_sync() {
   asm volatile("bar.sync 3, %0;\n" ::"n"(kConsumerThreads) : "memory");
 }
-__device__ __forceinline__ void gpartial(long long a, long long* red8g, int gw, int lane) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(~0u, a, o);
-  if (lane == 0) red8g[gw] = a;
-}
-__device__ __forceinline__ long long gsum(const long long* red8g) {
-  long long s = 0;
-#pragma unroll
-  for (int w = 0; w < kGroupWarps; ++w) s += red8g[w];
-  return s;
-}
-
 template <bool kTrace>
 __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_constant__ PassParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -263,26 +235,22 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   uint64_t* empty2 = full2 + kPassSlots;
   uint64_t* dfull = empty2 + kPassSlots;
   uint64_t* dempty = dfull + kDescSlots;
-  uint64_t* xfull = dempty + kDescSlots;
-  uint64_t* xempty = xfull + kXSlots;
-  uint64_t* tfull = xempty + kXSlots;
-  uint64_t* tempty = tfull + kMaxTSlots;
-  uint64_t* cdone1 = tempty + kMaxTSlots;
+  uint64_t* bfull1 = dempty + kDescSlots;  // quantised-x slots
+  uint64_t* bempty1 = bfull1 + kBSlots;
+  uint64_t* bfull2 = bempty1 + kBSlots;    // quantised-t slots
+  uint64_t* bempty2 = bfull2 + kBSlots;
+  uint64_t* cdone1 = bempty2 + kBSlots;
   uint64_t* cdone2 = cdone1 + kDoneRing;
   uint32_t* misc = (uint32_t*)(cdone2 + kDoneRing);  // [0] parity, [2..3] target
   uint8_t* dslots = (uint8_t*)misc + 64;
-  long long* red8 = (long long*)(dslots + kDescSlots * kDescSlotBytes);  // 2 x 16 partials
-  float* xmaxs = (float*)((uint8_t*)red8 + 256);  // max|x| of steps in flight (ring of 16)
+  float* xmaxs = (float*)(dslots + kDescSlots * kDescSlotBytes + 256);  // max|x| of steps in flight (ring of 16)
   ChunkRec* recs1 = (ChunkRec*)((uint8_t*)xmaxs + 64);
   ChunkRec* recs2 = recs1 + kPassSlots;
   int* red1 = (int*)(smem + pass_head_bytes());       // stage-1 row sums
   int* red2 = (int*)((uint8_t*)red1 + p.red1_bytes);  // stage-2 row sums
-  uint8_t* bfrag1 = (uint8_t*)red2 + p.red2_bytes;    // stage-1 B fragments (x limbs)
-  uint8_t* bfrag2 = bfrag1 + p.bfrag1_bytes;  // stage-2 B fragments (t limbs)
-  uint8_t* xslots = bfrag2 + p.bfrag2_bytes;
-  uint8_t* tslots = xslots + kXSlots * p.xslot_bytes;
-  const uint32_t TS = p.tslots;
-  uint8_t* ring1 = tslots + TS * p.tslot_bytes;
+  uint8_t* bslots1 = (uint8_t*)red2 + p.red2_bytes;   // header | B fragments of x
+  uint8_t* bslots2 = bslots1 + kBSlots * p.bslot1_bytes;  // header | B fragments of t | s1 slice
+  uint8_t* ring1 = bslots2 + kBSlots * p.bslot2_bytes;
   uint8_t* ring2 = ring1 + p.ring1_bytes;
 
   const int tid = threadIdx.x, lane = tid & 31;
@@ -306,15 +274,13 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     }
     for (int s = 0; s < kDescSlots; ++s) {
       tc::mbar_init(&dfull[s], 1);
-      tc::mbar_init(&dempty[s], 4);  // stage-2 group, producer, x stager, t loader
+      tc::mbar_init(&dempty[s], 7);  // stage-2 group, two producers, 2 x and 2 t quantisers
     }
-    for (int s = 0; s < kXSlots; ++s) {
-      tc::mbar_init(&xfull[s], 1);
-      tc::mbar_init(&xempty[s], 1);
-    }
-    for (int s = 0; s < kMaxTSlots; ++s) {
-      tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], 1);
+    for (int s = 0; s < kBSlots; ++s) {
+      tc::mbar_init(&bfull1[s], 2);  // the two quantiser warps
+      tc::mbar_init(&bempty1[s], 1);
+      tc::mbar_init(&bfull2[s], 2);
+      tc::mbar_init(&bempty2[s], 1);
     }
     for (int s = 0; s < kDoneRing; ++s) {
       tc::mbar_init(&cdone1[s], 1);
@@ -342,70 +308,69 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   // ============================================================= helper warps
   if (warp >= kConsumerWarps) {
     const int role = warp - kConsumerWarps;
-    if (role == 0) {
-      // ------------------------------------------------------------ producer
+    if (role == 0 || role == 7) {
+      // ----------------------------------------------- producers (one per ring)
+      // role 0 streams stage-1 sections step after step into ring 1, role 7
+      // stage-2 sections into ring 2.  The rings fill independently: stage 1 of
+      // later steps keeps streaming while stage 2 of a step waits for its t
+      // barrier (weights do not depend on x, so nothing orders the two streams).
       if (lane != 0) return;
-      uint64_t pos[2] = {0, 0}, starts[2][kPassSlots];
-      uint32_t chunk[2] = {0, 0}, rel[2] = {0, 0};
-      auto issue_stage = [&](uint32_t k, int stage) {
+      const int r = role == 0 ? 0 : 1;
+      const uint32_t RB = r ? p.ring2_bytes : p.ring1_bytes;
+      const uint32_t cap = r ? p.chunk2_cap : p.chunk1_cap;
+      uint64_t* fullr = r ? full2 : full1;
+      uint64_t* emptyr = r ? empty2 : empty1;
+      ChunkRec* recs = r ? recs2 : recs1;
+      uint8_t* ring = r ? ring2 : ring1;
+      uint64_t pos = 0, starts[kPassSlots];
+      uint32_t chunk = 0, rel = 0;
+      for (uint32_t k = 0; k < K; ++k) {
+        wait_desc(k);
         const StepDesc& D = desc_of(k);
         const Cta& C = cta_of(k);
-        const StageGeo g = stage == 1 ? stage1_geo(D, C) : stage2_geo(D, C);
-        const int r = stage - 1;
-        const uint32_t RB = r ? p.ring2_bytes : p.ring1_bytes;
-        const uint32_t cap = r ? p.chunk2_cap : p.chunk1_cap;
-        uint64_t* fullr = r ? full2 : full1;
-        uint64_t* emptyr = r ? empty2 : empty1;
-        ChunkRec* recs = r ? recs2 : recs1;
-        uint8_t* ring = r ? ring2 : ring1;
+        const StageGeo g = r ? stage2_geo(D, C) : stage1_geo(D, C);
+        if (kTrace) PSTAMP(k, r ? 14 : 11);
         uint32_t s0 = 0;
         uint64_t src = g.src_off;
         while (s0 < g.nsec) {
           uint32_t s1;
           const uint32_t sb = chunk_span(g, s0, cap, &s1);
-          const uint64_t start = ring_place(pos[r], sb, RB);
+          const uint64_t start = ring_place(pos, sb, RB);
           // wait for the slot and for every older chunk this range overwrites: chunks
           // are placed monotonically, so [start, pos) reaches older chunk c's bytes
           // in the ring exactly when pos > start_c + RB
-          while (rel[r] < chunk[r] && (chunk[r] - rel[r] >= (uint32_t)kPassSlots ||
-                                       starts[r][rel[r] % kPassSlots] + RB < pos[r])) {
-            mbar_wait_wd(&emptyr[rel[r] % kPassSlots], (rel[r] / kPassSlots) & 1, sus);
-            ++rel[r];
+          while (rel < chunk && (chunk - rel >= (uint32_t)kPassSlots ||
+                                 starts[rel % kPassSlots] + RB < pos)) {
+            mbar_wait_wd(&emptyr[rel % kPassSlots], (rel / kPassSlots) & 1, sus);
+            ++rel;
           }
-          const uint32_t slot = chunk[r] % kPassSlots;
-          starts[r][slot] = start;
+          const uint32_t slot = chunk % kPassSlots;
+          starts[slot] = start;
           const uint32_t roff = (uint32_t)(start % RB);
           recs[slot] = ChunkRec{roff, (uint16_t)s0, (uint16_t)s1, 0u, sb};
-          tc::mbar_arrive_expect_tx(&fullr[slot], sb);
-          tc::bulk_g2s(ring + roff, D.bits + src, sb, &fullr[slot]);
+          if (p.debug & 32u) {  // experiment: no copy, the consumers compute on stale bytes
+            tc::mbar_arrive(&fullr[slot]);
+          } else {
+            tc::mbar_arrive_expect_tx(&fullr[slot], sb);
+            tc::bulk_g2s(ring + roff, D.bits + src, sb, &fullr[slot]);
+          }
           src += sb;
           s0 = s1;
-          ++chunk[r];
+          ++chunk;
         }
-      };
-      uint32_t n1 = 0;
-      for (uint32_t k = 0; k < K; ++k) {
-        wait_desc(k);
-        const uint32_t ahead = desc_of(k).s1_ahead;
-        while (n1 < ahead) {
-          wait_desc(n1);
-          if (kTrace) PSTAMP(n1, 11);
-          issue_stage(n1, 1);
-          if (kTrace) PSTAMP(n1, 6);
-          ++n1;
-        }
-        if (kTrace) PSTAMP(k, 14);
-        issue_stage(k, 2);
-        if (kTrace) PSTAMP(k, 15);
+        if (kTrace) PSTAMP(k, r ? 15 : 6);
         tc::mbar_arrive(&dempty[k % kDescSlots]);
       }
       return;
     }
-    if (role == 1) {
-      // ----------------------------------------------------------- x stager
-      // clear this CTA's share of the other parity's bound words (used by the
-      // previous launch, which has completed)
-      {
+    if (role == 1 || role == 2) {
+      // ------------------------------------------------------ x quantisers
+      // Per step: the bound, then a = s2 * x (packed.cpp:160) of the CTA's
+      // stage-1 input slice as 38-bit fixed-point B fragments; the two warps
+      // take alternate quads and each adds its sum of the values to the header.
+      const int pw = role - 1;
+      if (pw == 0) {  // this CTA's share of the other parity's bound words (used by
+                      // the previous launch, which has completed)
         unsigned* other = p.amax + (size_t)(par ^ 1) * p.amax_words * 4;
         const uint32_t per = (p.amax_words + G - 1) / G;
         const uint32_t lo = min(p.amax_words, per * blockIdx.x), hi = min(p.amax_words, lo + per);
@@ -414,15 +379,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       bool pre_done = p.has_pre == 0;
       int32_t ywaited = -1;
       for (uint32_t j = 0; j < K; ++j) {
-        const uint32_t slot = j % kXSlots;
-        if (j >= (uint32_t)kXSlots) mbar_wait_wd(&xempty[slot], ((j / kXSlots) - 1) & 1, sus);
+        const uint32_t slot = j % kBSlots;
+        if (j >= (uint32_t)kBSlots) mbar_wait_wd(&bempty1[slot], ((j / kBSlots) - 1) & 1, sus);
         wait_desc(j);
         const StepDesc& D = desc_of(j);
         const Cta& C = cta_of(j);
-        const StageGeo g = stage1_geo(D, C);
-        uint8_t* xs = xslots + slot * p.xslot_bytes;
-        uint64_t* bar = &xfull[slot];
-        // every CTA needs the bound (stage 2 uses it), the slice only with stage-1 work
         if (lane == 0) {
           if (D.x_src >= 0 && D.x_src > ywaited) {
             poll_ctr(ybar + (size_t)D.x_src * kCtrStride, target);
@@ -434,45 +395,65 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
           }
         }
         __syncwarp();
-        const bool f32 = D.flags & kStepXF32;
-        const uint32_t esz = f32 ? 4 : 2;
+        const bool f32 = D.flags & kStepXF32, vec = (D.flags & kStepXVec) != 0;
+        uint32_t mb;
         if (D.flags & kStepXSelf) {  // whole-input bound, read after the dependency
-          uint32_t mb = absmax_bits(D.x, 0, D.m, f32, (D.flags & kStepXVec) != 0, lane, 32);
+          mb = absmax_bits(D.x, 0, D.m, f32, vec, lane, 32);
 #pragma unroll
           for (int o = 16; o; o >>= 1) mb = max(mb, __shfl_xor_sync(~0u, mb, o));
-          if (lane == 0) *(uint32_t*)xs = mb;
+        } else {
+          mb = __ldcg(amax + 4 * (size_t)D.amax_idx);
         }
-        uint32_t bulk = 0, s2b = 0;
-        const uint8_t* src = nullptr;
-        if (g.nsec) {
-          s2b = g.prefix;  // the segment's s2 slice (padded allocation, 128-byte aligned start)
-          const uint32_t hi = min(D.m, g.klo + g.prefix / 2);
-          const uint32_t nb = (hi - g.klo) * esz;
-          src = (const uint8_t*)D.x + (size_t)g.klo * esz;
-          if (D.flags & kStepXVec) bulk = nb / 16 * 16;
-          for (uint32_t b = bulk + lane; b < nb; b += 32) xs[16 + b] = __ldcg(src + b);
+        const float xmax = bound_value(mb, f32);
+        const StageGeo g = stage1_geo(D, C);
+        uint8_t* bs = bslots1 + slot * p.bslot1_bytes;
+        long long vsum = 0;
+        if (g.nsec && !(p.debug & 2u)) {
+          const Seg& S = D.seg[C.s1_seg];
+          const int ea = act_exponent(S.s2max, xmax);
+          const bool nonfinite = is_inf(xmax);
+          const uint32_t klo = g.klo, nquad = g.prefix / 8, m = D.m;
+          uint8_t* bf = bs + kBSlotHead;
+#pragma unroll 2
+          for (uint32_t qd = pw * 32 + lane; qd < nquad; qd += 64) {
+            const uint32_t k0 = klo + 4 * qd;
+            const XQuad xq = load_xquad(D.x, f32, vec, S.s2h, k0, m);
+            long long v[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float a = nonfinite ? 0.f : xq.s[e] * xq.x[e];
+              v[e] = __float2ll_rn(scale_pow2(a, kFix - ea));
+              vsum += v[e];
+            }
+            emit_quad(bf, klo, k0, q_of(k0, m), v);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) vsum += __shfl_xor_sync(~0u, vsum, o);
+        if (lane == 0) {
+          ((long long*)bs)[pw] = vsum;
+          if (pw == 0) xmaxs[j % 16] = xmax;
         }
         __syncwarp();
         if (lane == 0) {
-          const bool by_copy = !(D.flags & kStepXSelf);
-          tc::mbar_arrive_expect_tx(bar, bulk + s2b + (by_copy ? 16 : 0));
-          if (by_copy) tc::bulk_g2s(xs, amax + 4 * (size_t)D.amax_idx, 16, bar);
-          if (bulk) tc::bulk_g2s(xs + 16, src, bulk, bar);
-          if (s2b) tc::bulk_g2s(xs + p.xs2_off, D.seg[C.s1_seg].s2h + g.klo, s2b, bar);
+          if (kTrace && pw == 0) PSTAMP(j, 5);
+          tc::mbar_arrive(&bfull1[slot]);
+          tc::mbar_arrive(&dempty[j % kDescSlots]);
         }
-        if (kTrace && lane == 0) PSTAMP(j, 5);
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&dempty[j % kDescSlots]);
       }
       return;
     }
-    if (role == 2) {
-      // ------------------------------------------------------------ t loader
+    if (role == 3 || role == 4) {
+      // ------------------------------------------------------ t quantisers
+      // Per step: poll the t barrier, then the exact int64 t rows of the CTA's
+      // stage-2 segment -> 38-bit fixed-point B fragments (+ sum), and the
+      // segment's s1 slice; clear this CTA's share of the other parity's t.
+      const int pw = role - 3;
       int32_t ywaited = -1;
       for (uint32_t k = 0; k < K; ++k) {
-        const uint32_t slot = k % TS;
-        if (k >= TS) mbar_wait_wd(&tempty[slot], ((k / TS) - 1) & 1, sus);
-        if (kTrace && lane == 0) PSTAMP(k, 12);
+        const uint32_t slot = k % kBSlots;
+        if (k >= (uint32_t)kBSlots) mbar_wait_wd(&bempty2[slot], ((k / kBSlots) - 1) & 1, sus);
+        if (kTrace && lane == 0 && pw == 0) PSTAMP(k, 12);
         wait_desc(k);
         const StepDesc& D = desc_of(k);
         const Cta& C = cta_of(k);
@@ -484,26 +465,48 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
             ywaited = D.y_src;
           }
           // every CTA read the generation before its first arrival: advance it
-          if (k == 0 && blockIdx.x == 0) p.ctr[0] = target / G;
-          if (kTrace) PSTAMP(k, 4);
+          if (k == 0 && blockIdx.x == 0 && pw == 0) p.ctr[0] = target / G;
+          if (kTrace && pw == 0) PSTAMP(k, 4);
         }
         __syncwarp();
-        uint64_t* bar = &tfull[slot];
-        if (C.s2_rtn && !(p.debug & 16u)) {
+        uint8_t* bs = bslots2 + slot * p.bslot2_bytes;
+        long long vsum = 0;
+        if (C.s2_rtn && !(p.debug & 2u)) {
           const Seg& S = D.seg[C.s2_seg];
-          const uint32_t lo = S.t_off & ~1u, cnt = ((S.t_off & 1u) + S.r + 1) & ~1u;
-          uint8_t* ts = tslots + slot * p.tslot_bytes;
-          lsu_copy(ts, arena + D.t_off + lo, cnt * 8, bar, lane);
-          lsu_copy(ts + p.ts1_off, S.s1h + (size_t)C.s2_rt0 * 16, 32u * C.s2_rtn, bar, lane);
-          if (kTrace && lane == 0) PSTAMP(k, 13);
+          const long long* T = arena + D.t_off + S.t_off;
+          const int sh = t_shift(D.m);
+          const uint32_t nquad2 = kpad(S.r) / 4, r = S.r;
+          uint8_t* bf = bs + kBSlotHead;
+#pragma unroll 2
+          for (uint32_t qd = pw * 32 + lane; qd < nquad2; qd += 64) {
+            long long v[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t kk = 4 * qd + e;
+              const long long t = kk < r ? __ldcg(T + kk) : 0;
+              v[e] = (t + (1ll << (sh - 1))) >> sh;
+              vsum += v[e];
+            }
+            emit_quad(bf, 0, 4 * qd, q_of(4 * qd, r), v);
+          }
+          const uint4* s1src = (const uint4*)(S.s1h + (size_t)C.s2_rt0 * 16);
+          uint4* s1dst = (uint4*)(bs + p.bs2_s1_off);
+          for (uint32_t i = pw * 32 + lane; i < 2u * C.s2_rtn; i += 64) s1dst[i] = __ldg(s1src + i);
         }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) vsum += __shfl_xor_sync(~0u, vsum, o);
+        if (lane == 0) ((long long*)bs)[pw] = vsum;
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(bar);
+        if (lane == 0) {
+          if (kTrace && pw == 0) PSTAMP(k, 13);
+          tc::mbar_arrive(&bfull2[slot]);
+        }
         {  // clear this CTA's share of the step's region in the other parity
           long long* Z = p.arena + (size_t)(par ^ 1) * p.arena_len + D.t_off;
           const uint32_t pairs = D.t_len / 2, per = (pairs + G - 1) / G;
           const uint32_t lo = min(pairs, per * blockIdx.x), hi = min(pairs, lo + per);
-          for (uint32_t i = lo + lane; i < hi; i += 32) ((longlong2*)Z)[i] = make_longlong2(0, 0);
+          for (uint32_t i = lo + pw * 32 + lane; i < hi; i += 64)
+            ((longlong2*)Z)[i] = make_longlong2(0, 0);
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&dempty[k % kDescSlots]);
@@ -511,7 +514,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       return;
     }
     if (lane != 0) return;
-    if (role == 3) {
+    if (role == 5) {
       // ------------------------------------------- sequencer 1: t barriers
       for (uint32_t j = 0; j < K; ++j) {
         mbar_wait_wd(&cdone1[j % kDoneRing], (j / kDoneRing) & 1, sus);
@@ -543,10 +546,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
 
   // ================================================================ consumers
   const int gid = warp / kGroupWarps;  // 0: stage-1 group, 1: stage-2 group
-  const int gw = warp - gid * kGroupWarps;
   const int gt = tid - gid * kGroupThreads;
   int* const red = gid ? red2 : red1;
-  long long* const red8g = red8 + 16 * gid;
   for (uint32_t i = gt; i < (gid ? p.red2_bytes : p.red1_bytes) / 16; i += kGroupThreads)
     ((int4*)red)[i] = make_int4(0, 0, 0, 0);
   // ---- |x| prepass: this CTA's share of every independent input, one grid barrier
@@ -568,6 +569,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     if (tid == 0) arrive_ctr(xinit);
   }
   uint32_t chunk = 0;
+  const int gw = warp - gid * kGroupWarps;
   uint64_t* const fullr = gid ? full2 : full1;
   uint64_t* const emptyr = gid ? empty2 : empty1;
   const ChunkRec* const recs = gid ? recs2 : recs1;
@@ -604,89 +606,20 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     wait_desc(k);
     const StepDesc& D = desc_of(k);
     const Cta& C = cta_of(k);
-    const uint32_t slot = gid ? k % TS : k % kXSlots;
-    const uint8_t* st = gid ? tslots + slot * p.tslot_bytes : xslots + slot * p.xslot_bytes;
-    if (gid) mbar_wait_wd(&tfull[slot], (k / TS) & 1, sus);
-    else mbar_wait_wd(&xfull[slot], (k / kXSlots) & 1, sus);
-    if (kTrace && gt == 0) PSTAMP(k, gid ? 2 : 0);
+    const uint32_t slot = k % kBSlots;
+    mbar_wait_wd(gid ? &bfull2[slot] : &bfull1[slot], (k / kBSlots) & 1, sus);
+    const uint8_t* bs = gid ? bslots2 + slot * p.bslot2_bytes : bslots1 + slot * p.bslot1_bytes;
+    if (kTrace && gt == 0) {
+      PSTAMP(k, gid ? 2 : 0);
+      PSTAMP(k, gid ? 9 : 7);
+    }
     const StageGeo g = gid ? stage2_geo(D, C) : stage1_geo(D, C);
-    const float xmax = gid ? xmaxs[k % 16] : bound_value(*(const uint32_t*)st, (D.flags & kStepXF32) != 0);
-    const Seg& S = D.seg[gid ? C.s2_seg : C.s1_seg];
-    const int ea = act_exponent(S.s2max, xmax);
-    const bool nonfinite = is_inf(xmax);
-    const int sh = t_shift(D.m);
-    long long vsum = 0;  // sum of the quantised inputs (2 sum bit*v - sum v)
-    if (g.nsec && !(p.debug & 2u)) {
-      if (gid) {  // t (exact int64 sums) -> 38-bit fixed point
-        const long long* T = (const long long*)st + (S.t_off & 1u);
-        const uint32_t nquad2 = kpad(S.r) / 4;
-        for (uint32_t qd = gt; qd < nquad2; qd += kGroupThreads) {
-          long long v[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t kk = 4 * qd + e;
-            const long long t = kk < S.r ? T[kk] : 0;
-            v[e] = (t + (1ll << (sh - 1))) >> sh;
-            vsum += v[e];
-          }
-          emit_quad(bfrag2, 0, 4 * qd, q_of(4 * qd, S.r), v);
-        }
-      } else {  // a = s2 * x (packed.cpp:160) -> 38-bit fixed point
-        const bool xf32 = D.flags & kStepXF32;
-        const uint32_t klo = g.klo, nquad = g.prefix / 8, m = D.m;
-        const __half* s2s = (const __half*)(st + p.xs2_off) - klo;
-        for (uint32_t qd = gt; qd < nquad; qd += kGroupThreads) {
-          const uint32_t k0 = klo + 4 * qd;
-          float xv[4], sv[4];
-          if (k0 + 3 < m) {
-            const uint2 sh2 = *(const uint2*)(s2s + k0);
-            const float2 s01 = __half22float2(*(const __half2*)&sh2.x);
-            const float2 s23 = __half22float2(*(const __half2*)&sh2.y);
-            sv[0] = s01.x; sv[1] = s01.y; sv[2] = s23.x; sv[3] = s23.y;
-            if (xf32) {
-              const float4 v = *(const float4*)(st + 16 + 16 * qd);
-              xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
-            } else {
-              const uint2 v = *(const uint2*)(st + 16 + 8 * qd);
-              const float2 x01 = __half22float2(*(const __half2*)&v.x);
-              const float2 x23 = __half22float2(*(const __half2*)&v.y);
-              xv[0] = x01.x; xv[1] = x01.y; xv[2] = x23.x; xv[3] = x23.y;
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const uint32_t kk = k0 + e;
-              sv[e] = xv[e] = 0.f;
-              if (kk < m) {
-                sv[e] = __half2float(s2s[kk]);
-                xv[e] = xf32 ? ((const float*)(st + 16))[4 * qd + e]
-                             : __half2float(((const __half*)(st + 16))[4 * qd + e]);
-              }
-            }
-          }
-          long long v[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float a = nonfinite ? 0.f : sv[e] * xv[e];
-            v[e] = __float2ll_rn(scale_pow2(a, kFix - ea));
-            vsum += v[e];
-          }
-          emit_quad(bfrag1, klo, k0, q_of(k0, m), v);
-        }
-      }
-    }
-    gpartial(vsum, red8g, gw, lane);
-    group_sync(gid);  // fragments and partials visible; an x slot is consumed
-    if (gt == 0 && !gid) {
-      xmaxs[k % 16] = xmax;
-      tc::mbar_arrive(&xempty[slot]);
-    }
-    if (kTrace && gt == 0) PSTAMP(k, gid ? 9 : 7);
-    mma_stage(g, gid ? bfrag2 : bfrag1);
+    const long long A = ((const long long*)bs)[0] + ((const long long*)bs)[1];
+    mma_stage(g, bs + kBSlotHead);
     group_sync(gid);
     if (kTrace && gt == 0) PSTAMP(k, gid ? 10 : 8);
     if (g.nsec && !(p.debug & 8u)) {
-      const long long A = gsum(red8g);
+      const Seg& S = D.seg[gid ? C.s2_seg : C.s1_seg];
       if (!gid) {  // stage-1 publish: t rows (exact int64 reds)
         long long* Tseg = arena + D.t_off + S.t_off + (size_t)C.s1_rt0 * 16;
         for (uint32_t i = gt; i < (uint32_t)C.s1_rtn * 16; i += kGroupThreads) {
@@ -697,9 +630,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
           red_add_u64(&Tseg[i], v);
         }
       } else {  // stage-2 outputs (packed.cpp:174-190)
-        const int E = sh + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
+        const float xmax = xmaxs[k % 16];
+        const int ea = act_exponent(S.s2max, xmax);
+        const bool nonfinite = is_inf(xmax);
+        const int E = t_shift(D.m) + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
         const bool yf32 = D.flags & kStepYF32;
-        const __half* sc1 = (const __half*)(st + p.ts1_off);
+        const __half* sc1 = (const __half*)(bs + p.bs2_s1_off);
         void* Y = D.y[C.s2_seg];
         uint32_t ymb = 0;
         for (uint32_t i = gt; i < (uint32_t)C.s2_rtn * 16; i += kGroupThreads) {
@@ -736,10 +672,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     if (gt == 0) {
       if (kTrace) PSTAMP(k, gid ? 3 : 1);
       if (gid) {
-        tc::mbar_arrive(&tempty[slot]);
+        tc::mbar_arrive(&bempty2[slot]);
         tc::mbar_arrive(&cdone2[k % kDoneRing]);
         tc::mbar_arrive(&dempty[k % kDescSlots]);
       } else {
+        tc::mbar_arrive(&bempty1[slot]);
         tc::mbar_arrive(&cdone1[k % kDoneRing]);
       }
     }
@@ -769,7 +706,7 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
   NQB_REQUIRE(steps != nullptr, NQB_E_VALIDATION, "null steps");
   const uint32_t G = (uint32_t)ctx->num_sms;
   std::vector<StepDesc> desc(K);
-  uint32_t bf1 = 0, bf2 = 0, xbytes = 16, s2bytes = 16, tbytes = 16, s1bytes = 16;
+  uint32_t bf1 = 0, bf2 = 0, s1bytes = 16;
   double bits1 = 0, bits2 = 0;  // stage-1 / stage-2 stream bytes (ring split)
   uint32_t rt1 = 1, rt2 = 1;    // most row tiles of one CTA in stage 1 / stage 2
   uint64_t arena = 0, stream_bytes = 0;
@@ -800,7 +737,6 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       NQB_REQUIRE(!overlaps(s.y[q], (size_t)g->n[q] * esz, s.x, (size_t)g->m * esz),
                   NQB_E_VALIDATION, "a pass step's output overlaps its own input");
       algo += (double)g->r[q] * (g->n[q] + g->m) / 8.0 + 2.0 * (g->n[q] + g->m) + esz * g->n[q];
-      tbytes = std::max(tbytes, (((g->seg[q].t_off & 1u) + g->r[q] + 1) & ~1u) * 8u);
       bf2 = std::max(bf2, kBytesPerK * kpad(g->r[q]));
       bits1 += (double)g->r[q] * g->m;
       bits2 += (double)g->r[q] * g->n[q];
@@ -811,9 +747,7 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       if (!C.s1_rtn || !C.s1_sln) continue;
       const Slab last = slab_of(g->m, C.s1_sl0 + C.s1_sln - 1);
       const uint32_t nk1 = last.k0 + 32 * last.nq - slab_of(g->m, C.s1_sl0).k0;
-      xbytes = std::max(xbytes, esz * nk1);
       bf1 = std::max(bf1, kBytesPerK * nk1);
-      s2bytes = std::max(s2bytes, 2 * nk1);
     }
     for (uint32_t c = 0; c < g->grid; ++c) {
       s1bytes = std::max<uint32_t>(s1bytes, 32u * g->ctas[c].s2_rtn);
@@ -860,51 +794,15 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       else D.flags |= kStepXSelf;
     }
   }
-  // Producer order (stage-1 and stage-2 rings are filled in this interleaving):
-  // stage 1 of step j goes out before stage 2 of step i < j when j reads or
-  // writes nothing that steps >= i write (RAW on x, WAW on y);
-  // s1_ahead[k] = stage-1 issues before stage 2 of k (non-decreasing).
-  const uint32_t L = std::min<uint32_t>(env_u32p("NQB_PASS_LOOKAHEAD", 3), kMaxLookahead);
-  std::vector<int32_t> dep(K, -1);
-  for (uint32_t j = 0; j < K; ++j) {
-    const uint32_t ej = (desc[j].flags & kStepYF32) ? 4 : 2;
-    for (int i = (int)j - 1; i >= 0 && dep[j] < 0; --i) {
-      const uint32_t ei = (desc[i].flags & kStepYF32) ? 4 : 2;
-      bool d = desc[j].x_src == i;
-      for (uint32_t a = 0; a < desc[i].nseg && !d; ++a) {
-        d = overlaps(desc[i].y[a], (size_t)desc[i].seg[a].n * ei, desc[j].x,
-                     (size_t)desc[j].m * ((desc[j].flags & kStepXF32) ? 4 : 2));
-        for (uint32_t b = 0; b < desc[j].nseg && !d; ++b)
-          d = overlaps(desc[i].y[a], (size_t)desc[i].seg[a].n * ei, desc[j].y[b],
-                       (size_t)desc[j].seg[b].n * ej);
-      }
-      if (d) dep[j] = i;
-    }
-  }
-  {
-    uint32_t n1 = 0;
-    for (uint32_t k = 0; k < K; ++k) {
-      while (n1 < K && n1 <= k + L && dep[n1] < (int32_t)k) ++n1;
-      if (n1 < k + 1) n1 = k + 1;  // (dep[k] < k always holds)
-      desc[k].s1_ahead = n1;
-    }
-  }
-  NQB_REQUIRE(L + 4 < (uint32_t)kDescSlots, NQB_E_INTERNAL,
-              "pass lookahead exceeds the descriptor ring");
-  // Shared memory: head | B fragments (x, t) | x slots | t slots | stage-1 ring |
-  // stage-2 ring.  The rings split what is left in proportion to the two stages'
-  // bytes (each >= 36 KB).
-  const uint32_t bf1_b = (std::max(bf1, 16u) + 127) / 128 * 128;
-  const uint32_t bf2_b = (std::max(bf2, 16u) + 127) / 128 * 128;
-  const uint32_t xs2_off = (16 + xbytes + 127) / 128 * 128;
-  const uint32_t xslot_b = (xs2_off + s2bytes + 127) / 128 * 128;
-  const uint32_t ts1_off = (tbytes + 127) / 128 * 128;
-  const uint32_t tslot_b = (ts1_off + s1bytes + 127) / 128 * 128;
+  // Shared memory: head | row sums (stage 1, 2) | quantised-x slots | quantised-t
+  // slots | stage-1 ring | stage-2 ring.  The rings split what is left in
+  // proportion to the two stages' bytes (each >= 36 KB).
+  const uint32_t bslot1_b = (kBSlotHead + std::max(bf1, 16u) + 127) / 128 * 128;
+  const uint32_t bs2_s1_off = (kBSlotHead + std::max(bf2, 16u) + 127) / 128 * 128;
+  const uint32_t bslot2_b = (bs2_s1_off + s1bytes + 127) / 128 * 128;
   const uint32_t head = pass_head_bytes();
-  const uint32_t TS = std::max<uint32_t>(2, std::min<uint32_t>(kMaxTSlots,
-                                                               env_u32p("NQB_PASS_TSLOTS", 2)));
   const uint32_t red1_b = rt1 * 16 * kRedStride * 4, red2_b = rt2 * 16 * kRedStride * 4;
-  const uint32_t fixed = head + red1_b + red2_b + bf1_b + bf2_b + kXSlots * xslot_b + TS * tslot_b;
+  const uint32_t fixed = head + red1_b + red2_b + kBSlots * (bslot1_b + bslot2_b);
   NQB_REQUIRE(fixed + 72u * 1024u <= 227u * 1024u, NQB_E_DIMENSION_MISMATCH,
               "decode pass: staging buffers leave no room for the weight rings");
   const uint32_t rings = (227u * 1024u - fixed) / 256 * 256;
@@ -957,13 +855,9 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     pp.debug = env_u32p("NQB_PASS_DEBUG", 0);
     pp.red1_bytes = red1_b;
     pp.red2_bytes = red2_b;
-    pp.bfrag1_bytes = bf1_b;
-    pp.bfrag2_bytes = bf2_b;
-    pp.xs2_off = xs2_off;
-    pp.xslot_bytes = xslot_b;
-    pp.ts1_off = ts1_off;
-    pp.tslot_bytes = tslot_b;
-    pp.tslots = TS;
+    pp.bslot1_bytes = bslot1_b;
+    pp.bslot2_bytes = bslot2_b;
+    pp.bs2_s1_off = bs2_s1_off;
     pp.ring1_bytes = ring1;
     pp.ring2_bytes = ring2;
     const uint32_t cap_kb = env_u32p("NQB_PASS_CHUNK_KB", 0);
@@ -976,11 +870,10 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     P->smem_bytes = fixed + rings;
     if (env_u32p("NQB_PASS_VERBOSE", 0))
       std::fprintf(stderr,
-                   "nqb pass: K=%u G=%u smem=%u head=%u red=%u+%u bfrag=%u+%u xslot=%u tslot=%u x%u "
-                   "rings=%u+%u chunk caps=%u/%u lookahead=%u\n",
-                   K, G, P->smem_bytes, head, red1_b, red2_b, bf1_b, bf2_b, xslot_b, tslot_b, TS,
-                   ring1, ring2,
-                   pp.chunk1_cap, pp.chunk2_cap, L);
+                   "nqb pass: K=%u G=%u smem=%u head=%u red=%u+%u bslots=%ux(%u+%u) "
+                   "rings=%u+%u chunk caps=%u/%u\n",
+                   K, G, P->smem_bytes, head, red1_b, red2_b, kBSlots, bslot1_b, bslot2_b, ring1,
+                   ring2, pp.chunk1_cap, pp.chunk2_cap);
     P->stream_bytes = stream_bytes;
     P->algo_bytes = (uint64_t)algo;
     for (auto fn : {k_decode_pass<false>, k_decode_pass<true>})

@@ -3,26 +3,28 @@
 // A decode pass is a list of steps; a step is one decode group (1..kMaxSeg
 // layers that read the same input, e.g. q/k/v) with its input x and outputs y.
 // One launch of k_decode_pass runs every step of the pass on a grid of one CTA
-// per SM.  The consumer warps only compute from shared memory; every global
-// round trip lives in a helper warp that runs ahead of them:
-//   * producer: streams the CTA's weight bits for phase after phase (the same
-//     per-group plans and byte streams as the per-call kernel, decode_plan.cu)
-//     into a shared-memory ring, ahead of the consumers across steps and
-//     barriers: the weights do not depend on x, so HBM never waits for the
-//     layer chain;
-//   * x stager: per step, waits for the step's input (the producing step's
-//     output barrier, if any), then TMA-copies the CTA's x slice and the
-//     |x| bound into an x slot;
-//   * t loader: per step, polls the step's t barrier and TMA-copies the t rows
-//     of the CTA's stage-2 segment into a t slot; clears the other parity's
-//     accumulators for the next launch;
-//   * sequencer: turns consumer progress into the grid-barrier arrivals
-//     (release reductions) and prefetches step descriptors.
-// The consumers run, per step, stage 1 (x -> t, int64 red.add into the step's
-// t region) and stage 2 (t -> y) in a host-computed phase order: stage 1 of up
-// to `lookahead` later steps runs before a step's stage 2, so the t barrier and
-// t load hide behind MMA work; a step that depends on an earlier output (found
-// from the buffer ranges at build time) never moves ahead of it.
+// per SM.  The consumer warps only run MMAs from shared memory and finish rows;
+// every global round trip and all input quantisation live in helper warps that
+// run ahead of them:
+//   * producers (one per stage): stream the CTA's weight bits step after step
+//     (the same per-group plans and byte streams as the per-call kernel,
+//     decode_plan.cu) into that stage's shared-memory ring.  The weights do not
+//     depend on x, so HBM never waits for the layer chain, and the two rings
+//     fill independently;
+//   * x quantisers (2 warps): per step, wait for the step's input (the producing
+//     step's output barrier, if any), read the CTA's x and s2 slices from global
+//     memory and write a = s2*x as 38-bit fixed-point B fragments (+ their sum)
+//     into a stage-1 slot;
+//   * t quantisers (2 warps): per step, poll the step's t barrier, read the t
+//     rows of the CTA's stage-2 segment and write them as B fragments (+ sum, +
+//     the s1 slice) into a stage-2 slot; clear the other parity's accumulators
+//     for the next launch;
+//   * sequencers: turn consumer progress into the grid-barrier arrivals
+//     (release reductions) and prefetch step descriptors.
+// The consumers form two groups: group 0 runs stage 1 of step after step (x ->
+// t, int64 red.add into the step's t region), group 1 stage 2 (t -> y).  Group 0
+// runs ahead of group 1 as far as the descriptor ring allows, so the t barrier
+// of a step completes while group 1 still works on earlier steps.
 // |x| bounds: an independent input is reduced by a prepass at kernel start (one
 // grid barrier for all steps); a chained input takes the producing step's
 // published max|y|.  Accumulators and bounds are double-buffered by launch
@@ -36,13 +38,14 @@ namespace dec {
 
 constexpr int kPassSlots = 16;   // weight ring chunks in flight (full/empty mbarrier pairs)
 constexpr int kDescSlots = 12;   // step descriptors in flight
-constexpr int kXSlots = 3;       // staged x slices in flight
-constexpr int kMaxTSlots = 6;    // staged t segments in flight (runtime count: PassParams::tslots)
+constexpr int kBSlots = 2;       // quantised-input slots per stage (B fragments of x / t)
 constexpr int kDoneRing = 24;    // consumer phase-completion mbarriers
 constexpr int kCtrStride = 16;   // u64 words per counter (own 128-byte line)
-constexpr int kPassHelpers = 5;  // producer, x stager, t loader, sequencers 1 and 2
+// helper warps: producer 1, x quantisers (2), t quantisers (2), sequencers 1 and 2, producer 2
+constexpr int kPassHelpers = 8;
 constexpr int kPassStamps = 16;  // trace stamps per step
 constexpr int kMaxLookahead = 6;
+constexpr uint32_t kBSlotHead = 16;  // slot header: the two quantiser warps' sums of the values
 
 enum : uint32_t {
   kStepXF32 = 1u,      // x is fp32 (else binary16)
@@ -65,8 +68,7 @@ struct alignas(16) StepDesc {
   uint32_t amax_idx;     // 16-byte bound word (per parity) holding max|x|
   uint64_t t_off;        // this step's t region (int64 index, even)
   uint32_t t_len;        // int64 words in the region (even)
-  uint32_t s1_ahead;     // stage-1 sections the producer issues before this step's stage 2
-  uint32_t pad[3];
+  uint32_t pad[4];
 };
 static_assert(sizeof(StepDesc) % 16 == 0 && sizeof(StepDesc) <= 480, "step descriptor layout");
 constexpr uint32_t kDescSlotBytes = 512;  // descriptor + the CTA's 32-byte Cta entry at 480
@@ -82,22 +84,18 @@ struct PassParams {
   uint32_t amax_words;
   uint32_t ring1_bytes, ring2_bytes;     // stage-1 / stage-2 weight rings
   uint32_t chunk1_cap, chunk2_cap;
-  uint32_t bfrag1_bytes, bfrag2_bytes;   // B fragments of x (stage 1) and t (stage 2)
-  uint32_t xslot_bytes, tslot_bytes;
+  uint32_t bslot1_bytes, bslot2_bytes;   // quantised-input slots: header | B fragments (| s1)
   uint32_t red1_bytes, red2_bytes;       // per-limb row sums (row tiles of the largest stage)
-  uint32_t xs2_off;           // s2 slice offset in an x slot (header 16 B, then the x slice)
-  uint32_t ts1_off;           // s1 slice offset in a t slot (after the t rows)
-  uint32_t tslots;            // t slots (2..kMaxTSlots)
+  uint32_t bs2_s1_off;        // s1 slice offset in a stage-2 slot (after the t fragments)
   uint32_t has_pre;
   uint32_t debug;  // NQB_PASS_DEBUG bits (experiments only): 1 skip MMA, 2 skip quantise, 4 suspend
-                   // waits, 8 skip publish/outputs, 16 skip the t copy
+                   // waits, 8 skip publish/outputs, 32 no weight copies
   unsigned long long* trace;  // diagnostics: G x (kPassStamps K + 2) %globaltimer stamps
 };
 
 constexpr int kGroupWarps = 6;                 // consumer warps per stage group
 constexpr int kGroupThreads = 32 * kGroupWarps;
-constexpr uint32_t kPassBars =
-    4 * kPassSlots + 2 * kDescSlots + 2 * kXSlots + 2 * kMaxTSlots + 2 * kDoneRing;
+constexpr uint32_t kPassBars = 4 * kPassSlots + 2 * kDescSlots + 4 * kBSlots + 2 * kDoneRing;
 // head: mbarriers | misc | descriptor slots | group partials | max|x| ring |
 // chunk records (2 rings)
 __host__ __device__ __forceinline__ uint32_t pass_head_bytes() {
