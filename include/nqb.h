@@ -97,6 +97,15 @@ uint64_t nqb_kernel_launches(const nqb_context* ctx);
 int nqb_rank_for_target_bpw(uint64_t n, uint64_t m, double target_bpw, uint32_t* rank);
 
 /* ------------------------------------------------------------------------ */
+/* Synthetic weights (rng.hpp:25-58): out[i] = scale * Rng(seed).gaussian(),  */
+/* i-th call of one stream, rounded to fp32 and back when snap_f32 (NQMX      */
+/* precision, io.cpp:117-119).  SURVEY §8(d) rows 1 and 4: W = fp32(0.02 g).  */
+/* Host only, multi-threaded, bitwise equal to the reference stream.          */
+/* ------------------------------------------------------------------------ */
+int nqb_synthetic_weight_host(uint64_t seed, uint64_t count, double scale, int snap_f32,
+                              double* out);
+
+/* ------------------------------------------------------------------------ */
 /* Sign binarisation and packing (packed.cpp:51-103)                         */
 /* on_device != 0: pointers are device pointers (async on the ctx stream).   */
 /* ------------------------------------------------------------------------ */
@@ -129,6 +138,13 @@ int nqb_layer_upload(nqb_context* ctx, uint32_t n, uint32_t m, uint32_t r,
 int nqb_layer_upload_f16(nqb_context* ctx, uint32_t n, uint32_t m, uint32_t r,
                          const uint32_t* u_words, const uint32_t* v_words,
                          const uint16_t* s1_half, const uint16_t* s2_half, nqb_layer** out);
+/* Same as nqb_layer_upload, and the layer also keeps the exact fp64 scales, as
+ * the reference FactorizedLayer does in memory (packed.hpp:57-72): the exact
+ * paths (reconstruct_dense, gemv f64, gemm f64, gemv f32 host, download) use
+ * them, the binary16 hot kernels keep the snapped copy.  Used by the C++ shim. */
+int nqb_layer_upload_exact(nqb_context* ctx, uint32_t n, uint32_t m, uint32_t r,
+                           const uint32_t* u_words, const uint32_t* v_words,
+                           const double* s1, const double* s2, nqb_layer** out);
 int nqb_layer_free(nqb_layer* layer);
 int nqb_layer_shape(const nqb_layer* layer, uint32_t* n, uint32_t* m, uint32_t* r);
 /* Bytes the decode GEMV must stream for this layer (device layout). */
@@ -206,6 +222,13 @@ int nqb_pass_create(nqb_context* ctx, uint32_t count, const nqb_pass_step* steps
                     nqb_pass** out);
 int nqb_pass_launch(nqb_context* ctx, const nqb_pass* pass);
 int nqb_pass_free(nqb_pass* pass);
+/* One pass end to end with host buffers: hx[k] (or NULL: input left as is, e.g.
+ * produced by an earlier step) is copied into step k's input, the pass runs on
+ * the context stream, and hy[i] (one per layer of every step, in step order;
+ * NULL: not read back) receives the outputs; returns when they are on the
+ * host. */
+int nqb_pass_run_host(nqb_context* ctx, const nqb_pass* pass, const void* const* hx,
+                      void* const* hy);
 /* Bits streamed per launch, and the algorithmic bytes of the pass: per layer
  * r(n+m)/8 + 2(n+m) scales + y, plus x once per step. */
 uint64_t nqb_pass_stream_bytes(const nqb_pass* pass);
@@ -265,6 +288,12 @@ void nqb_admm_config_default(nqb_admm_config* cfg);
 int nqb_admm_factorize_host(nqb_context* ctx, const double* w, uint32_t n, uint32_t m,
                             const nqb_admm_config* cfg, double* consensus_u,
                             double* consensus_v, double* trace, nqb_admm_result* result);
+/* Same, plus the final AdmmState matrices (admm.hpp:53-62): state[0..5] = U (n x r),
+ * V (m x r), Z_U, Z_V, L_U, L_V host buffers, each may be NULL (state may be NULL). */
+int nqb_admm_factorize_state_host(nqb_context* ctx, const double* w, uint32_t n, uint32_t m,
+                                  const nqb_admm_config* cfg, double* consensus_u,
+                                  double* consensus_v, double* trace, nqb_admm_result* result,
+                                  double* const* state);
 /* Same on device buffers (w, consensus_u, consensus_v device; trace host or NULL). */
 int nqb_admm_factorize_device(nqb_context* ctx, const double* d_w, uint32_t n, uint32_t m,
                               const nqb_admm_config* cfg, double* d_consensus_u,

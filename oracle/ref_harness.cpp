@@ -5,6 +5,8 @@
 // oracle/_ref/libnqref.so.  Only tests/, __graft_entry__.smoke() and bench.py's
 // cpu_baseline / --impl reference leg load it.  Every function forwards to the
 // reference entry point it names; status codes follow include/nqb.h.
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -217,6 +219,59 @@ int nqref_gemv_f32_concurrent(std::uint32_t count, const std::uint32_t* n,
     for (auto& t : pool) t.join();
   })
 }
+
+// Decode-pass timing helper for the reference arm of bench.py: `count` layers
+// prebuilt once (nqref_pass_create), then one decode pass = gemv_packed_f32 on
+// every layer, spread over `threads` host threads that take layers from a
+// shared counter (the reference is single-threaded per call; host-core
+// parallelism = concurrent layers).  Only the gemv calls run inside
+// nqref_pass_run.
+struct RefPass {
+  std::vector<FactorizedLayer> layers;
+  std::vector<std::vector<float>> xs;
+};
+void* nqref_pass_create(std::uint32_t count, const std::uint32_t* n, const std::uint32_t* m,
+                        const std::uint32_t* r, const std::uint32_t* const* u,
+                        const std::uint32_t* const* v, const double* const* s1,
+                        const double* const* s2, const float* const* x) {
+  try {
+    auto* P = new RefPass();
+    for (std::uint32_t i = 0; i < count; ++i) {
+      P->layers.push_back(layer_of(n[i], m[i], r[i], u[i], v[i], s1[i], s2[i]));
+      P->xs.emplace_back(x[i], x[i] + m[i]);
+    }
+    return P;
+  } catch (const std::exception& e) {
+    code_of(e);
+    return nullptr;
+  }
+}
+int nqref_pass_run(void* h, float* const* y, std::uint32_t threads) {
+  GUARD({
+    auto* P = static_cast<RefPass*>(h);
+    const std::uint32_t count = (std::uint32_t)P->layers.size();
+    std::atomic<std::uint32_t> next{0};
+    std::atomic<int> failed{0};
+    auto work = [&]() {
+      for (;;) {
+        const std::uint32_t i = next.fetch_add(1);
+        if (i >= count) return;
+        try {
+          const std::vector<float> out = gemv_packed_f32(P->layers[i], P->xs[i]);
+          std::memcpy(y[i], out.data(), out.size() * sizeof(float));
+        } catch (...) {
+          failed = 1;
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (std::uint32_t t = 1; t < std::max<std::uint32_t>(1, threads); ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    if (failed) throw Error(ErrorKind::kNumerical, "gemv_packed_f32 failed in the pass");
+  })
+}
+void nqref_pass_destroy(void* h) { delete static_cast<RefPass*>(h); }
 
 // ---- linalg.cpp -------------------------------------------------------------
 int nqref_top_singular_pair(const double* mat, std::uint32_t rows, std::uint32_t cols,

@@ -60,6 +60,7 @@ PROTOTYPES = {
     "nqb_synchronize": (C.c_int, [P]),
     "nqb_kernel_launches": (U64, [P]),
     "nqb_rank_for_target_bpw": (C.c_int, [U64, U64, D, PU32]),
+    "nqb_synthetic_weight_host": (C.c_int, [U64, U64, D, C.c_int, P]),
     "nqb_binarize": (C.c_int, [P, P, U64, P, C.c_int]),
     "nqb_pack_signs": (C.c_int, [P, P, U32, U32, P, C.c_int]),
     "nqb_pack_latent": (C.c_int, [P, P, U32, U32, P, C.c_int]),
@@ -102,6 +103,7 @@ PROTOTYPES = {
     "nqb_pass_create": (C.c_int, [P, U32, P, PP]),
     "nqb_pass_launch": (C.c_int, [P, P]),
     "nqb_pass_free": (C.c_int, [P]),
+    "nqb_pass_run_host": (C.c_int, [P, P, P, P]),
     "nqb_pass_stream_bytes": (U64, [P]),
     "nqb_pass_algorithmic_bytes": (U64, [P]),
     "nqb_debug_pass_trace": (C.c_int, [P, P, P, PU32]),

@@ -57,6 +57,25 @@ enum { RED_SUMSQ = 0, RED_SUMSQ_DIFF = 1, RED_DOT = 2 };
 __global__ void k_scale(double* __restrict__ a, uint64_t n, double f) {
   GRID_STRIDE(i, n) a[i] *= f;  // DenseMatrix::scale (dense.cpp:56-58)
 }
+// Rebalance (admm.cpp:112-123) in one launch: U, Z_U, L_U scaled by c and V,
+// Z_V, L_V by 1/c (the same per-element products as six DenseMatrix::scale calls).
+__global__ void k_rebalance(double* __restrict__ u, double* __restrict__ zu,
+                            double* __restrict__ lu, uint64_t nr, double c,
+                            double* __restrict__ v, double* __restrict__ zv,
+                            double* __restrict__ lv, uint64_t mr, double ci) {
+  GRID_STRIDE(i, nr + mr) {
+    if (i < nr) {
+      u[i] *= c;
+      zu[i] *= c;
+      lu[i] *= c;
+    } else {
+      const uint64_t j = i - nr;
+      v[j] *= ci;
+      zv[j] *= ci;
+      lv[j] *= ci;
+    }
+  }
+}
 __global__ void k_add(const double* __restrict__ a, const double* __restrict__ b,
                       double* __restrict__ c, uint64_t n) {
   GRID_STRIDE(i, n) c[i] = a[i] + b[i];  // add (dense.cpp:108-115)
@@ -272,7 +291,7 @@ double spectral_norm_device(nqb_context* ctx, const double* d_m, uint32_t rows, 
 // ---------------------------------------------------------------------------
 void admm_device(nqb_context* ctx, const double* d_w, uint32_t n, uint32_t m,
                  const nqb_admm_config& cfg, double* d_cu, double* d_cv, double* h_trace,
-                 nqb_admm_result* res) {
+                 nqb_admm_result* res, double* const* h_state) {
   std::memset(res, 0, sizeof(*res));
   const uint64_t nm = (uint64_t)n * m;
   int flags = 0;
@@ -348,12 +367,7 @@ void admm_device(nqb_context* ctx, const double* d_w, uint32_t n, uint32_t m,
       const double nu = std::sqrt(norm2(ctx, u.p, nr)), nv = std::sqrt(norm2(ctx, v.p, mr));
       if (nu > 0.0 && nv > 0.0) {
         const double c = std::sqrt(nv / nu);
-        EW(ctx, k_scale, nr, u.p, nr, c);
-        EW(ctx, k_scale, nr, zu.p, nr, c);
-        EW(ctx, k_scale, nr, lu.p, nr, c);
-        EW(ctx, k_scale, mr, v.p, mr, 1.0 / c);
-        EW(ctx, k_scale, mr, zv.p, mr, 1.0 / c);
-        EW(ctx, k_scale, mr, lv.p, mr, 1.0 / c);
+        EW(ctx, k_rebalance, nr + mr, u.p, zu.p, lu.p, nr, c, v.p, zv.p, lv.p, mr, 1.0 / c);
       }
     }
     factor_solve_device(ctx, d_w, false, n, m, v.p, r, zu.p, lu.p, s.rho, cfg.ridge, u.p, sw);
@@ -373,6 +387,14 @@ void admm_device(nqb_context* ctx, const double* d_w, uint32_t n, uint32_t m,
   }
   EW(ctx, k_add, nr, u.p, lu.p, d_cu, nr);
   EW(ctx, k_add, mr, v.p, lv.p, d_cv, mr);
+  if (h_state) {  // AdmmState matrices (admm.hpp:53-62): U, V, Z_U, Z_V, L_U, L_V
+    const double* src[6] = {u.p, v.p, zu.p, zv.p, lu.p, lv.p};
+    const uint64_t len[6] = {nr, mr, nr, mr, nr, mr};
+    for (int i = 0; i < 6; ++i)
+      if (h_state[i])
+        NQB_CUDA(cudaMemcpyAsync(h_state[i], src[i], len[i] * 8, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  }
   NQB_CUDA(cudaEventRecord(e1, ctx->stream));
   NQB_CUDA(cudaEventSynchronize(e1));
   NQB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
@@ -449,13 +471,20 @@ int nqb_admm_factorize_device(nqb_context* ctx, const double* d_w, uint32_t n, u
   API_BEGIN
   need_ctx(ctx);
   NQB_REQUIRE(cfg && result, NQB_E_VALIDATION, "null config/result");
-  admm_device(ctx, d_w, n, m, *cfg, d_cu, d_cv, trace, result);
+  admm_device(ctx, d_w, n, m, *cfg, d_cu, d_cv, trace, result, nullptr);
   API_END
 }
 
 int nqb_admm_factorize_host(nqb_context* ctx, const double* w, uint32_t n, uint32_t m,
                             const nqb_admm_config* cfg, double* cu, double* cv, double* trace,
                             nqb_admm_result* result) {
+  return nqb_admm_factorize_state_host(ctx, w, n, m, cfg, cu, cv, trace, result, nullptr);
+}
+
+int nqb_admm_factorize_state_host(nqb_context* ctx, const double* w, uint32_t n, uint32_t m,
+                                  const nqb_admm_config* cfg, double* cu, double* cv,
+                                  double* trace, nqb_admm_result* result,
+                                  double* const* state) {
   API_BEGIN
   need_ctx(ctx);
   NQB_REQUIRE(cfg && result, NQB_E_VALIDATION, "null config/result");
@@ -466,7 +495,7 @@ int nqb_admm_factorize_host(nqb_context* ctx, const double* w, uint32_t n, uint3
   NQB_REQUIRE(r <= std::min(n, m) || nm == 0, NQB_E_RANK_TOO_LARGE,
               "admm_factorize: rank exceeds min(rows, cols)");
   Dev du((uint64_t)n * std::max(r, 1u)), dv((uint64_t)m * std::max(r, 1u));
-  admm_device(ctx, dw.p, n, m, *cfg, du.p, dv.p, trace, result);
+  admm_device(ctx, dw.p, n, m, *cfg, du.p, dv.p, trace, result, state);
   d2h(ctx, cu, du.p, (uint64_t)n * r);
   d2h(ctx, cv, dv.p, (uint64_t)m * r);
   API_END
@@ -515,7 +544,7 @@ int nqb_factorize_layer(nqb_context* ctx, const double* w, uint32_t n, uint32_t 
   nqb_admm_result local;
   nqb_admm_result* res = result ? result : &local;
   Dev cu((uint64_t)n * r), cv((uint64_t)m * r), s1(n), s2(m);
-  admm_device(ctx, dw, n, m, *cfg, cu.p, cv.p, nullptr, res);
+  admm_device(ctx, dw, n, m, *cfg, cu.p, cv.p, nullptr, res, nullptr);
   balance_device(ctx, cu.p, cv.p, n, m, r, nullptr, nullptr, scale_floor, s1.p, s2.p);
   const uint32_t wpr = ceil_div(r, 32);
   uint32_t* words = nullptr;

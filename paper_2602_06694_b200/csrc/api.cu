@@ -1,7 +1,10 @@
 // api.cu — extern "C" entry points of libnqb (include/nqb.h): context,
 // packing, layers and the forward.  ADMM entry points live in admm.cu.
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -230,6 +233,68 @@ int nqb_rank_for_target_bpw(uint64_t n, uint64_t m, double t, uint32_t* rank) {
   API_END
 }
 
+// Rng (rng.hpp:25-58): splitmix64; gaussian() = Box-Muller on two uniforms,
+// one value per call.  Draw j of the stream returns mix(seed + (j+1)*golden), so
+// gaussian i starts at draw 2i unless a uniform of 0 was rejected earlier
+// (probability 2^-53 per value): threads fill independent ranges by jumping
+// ahead, and any range that sees a rejection makes the whole fill sequential.
+namespace {
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+inline uint64_t splitmix_next(uint64_t& state) {
+  uint64_t z = (state += kGolden);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+inline double rng_uniform(uint64_t& state) { return (double)(splitmix_next(state) >> 11) * 0x1.0p-53; }
+// One gaussian; returns false if the first uniform was rejected (<= 0).
+inline bool rng_gaussian(uint64_t& state, double* g) {
+  double u1 = rng_uniform(state);
+  bool clean = true;
+  while (u1 <= 0.0) {
+    clean = false;
+    u1 = rng_uniform(state);
+  }
+  const double u2 = rng_uniform(state);
+  *g = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+  return clean;
+}
+inline double weight_value(double g, double scale, int snap_f32) {
+  const double w = scale * g;
+  return snap_f32 ? (double)(float)w : w;
+}
+}  // namespace
+
+int nqb_synthetic_weight_host(uint64_t seed, uint64_t count, double scale, int snap_f32,
+                              double* out) {
+  API_BEGIN
+  NQB_REQUIRE(out != nullptr || count == 0, NQB_E_VALIDATION, "null output");
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const uint64_t T = count < (1u << 16) ? 1 : std::min<uint64_t>(hw, 64);
+  std::atomic<int> dirty{0};
+  auto fill = [&](uint64_t a, uint64_t b) {
+    uint64_t st = seed + 2 * a * kGolden;
+    for (uint64_t i = a; i < b; ++i) {
+      double g;
+      if (!rng_gaussian(st, &g)) dirty = 1;
+      out[i] = weight_value(g, scale, snap_f32);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (uint64_t t = 1; t < T; ++t) pool.emplace_back(fill, count * t / T, count * (t + 1) / T);
+  fill(0, count / T);
+  for (auto& th : pool) th.join();
+  if (dirty && T > 1) {  // a rejected uniform shifts the stream: redo it in order
+    uint64_t st = seed;
+    for (uint64_t i = 0; i < count; ++i) {
+      double g;
+      rng_gaussian(st, &g);
+      out[i] = weight_value(g, scale, snap_f32);
+    }
+  }
+  API_END
+}
+
 // ---------------------------------------------------------------------------
 // binarize / pack / unpack
 // ---------------------------------------------------------------------------
@@ -418,11 +483,33 @@ int nqb_layer_upload(nqb_context* ctx, uint32_t n, uint32_t m, uint32_t r,
   return upload_impl(ctx, n, m, r, u_words, v_words, h1.data(), h2.data(), out);
 }
 
+int nqb_layer_upload_exact(nqb_context* ctx, uint32_t n, uint32_t m, uint32_t r,
+                           const uint32_t* u_words, const uint32_t* v_words, const double* s1,
+                           const double* s2, nqb_layer** out) {
+  const int st = nqb_layer_upload(ctx, n, m, r, u_words, v_words, s1, s2, out);
+  if (st != NQB_OK) return st;
+  API_BEGIN
+  nqb_layer* L = *out;
+  try {
+    NQB_CUDA(cudaMalloc(&L->s1d, 8 * ((size_t)n + m)));
+    L->s2d = L->s1d + n;
+    NQB_CUDA(cudaMemcpyAsync(L->s1d, s1, 8 * (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
+    NQB_CUDA(cudaMemcpyAsync(L->s2d, s2, 8 * (size_t)m, cudaMemcpyHostToDevice, ctx->stream));
+    NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  } catch (...) {
+    nqb_layer_free(L);
+    *out = nullptr;
+    throw;
+  }
+  API_END
+}
+
 int nqb_layer_free(nqb_layer* L) {
   API_BEGIN
   if (!L) return NQB_OK;
   cudaSetDevice(L->device);
   group_free(L->dec);
+  cudaFree(L->s1d);  // s2d shares the allocation
   cudaFree(L->hp_buf);
   cudaFree(L->u);
   cudaFree(L->vt);
@@ -465,7 +552,10 @@ int nqb_layer_download(nqb_context* ctx, const nqb_layer* L, uint32_t* u_words,
                              ctx->stream));
     NQB_CUDA(cudaStreamSynchronize(ctx->stream));
   }
-  if (s1 || s2) {
+  if ((s1 || s2) && L->s1d) {  // exact scales
+    if (s1) NQB_CUDA(cudaMemcpyAsync(s1, L->s1d, 8 * (size_t)L->n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (s2) NQB_CUDA(cudaMemcpyAsync(s2, L->s2d, 8 * (size_t)L->m, cudaMemcpyDeviceToHost, ctx->stream));
+  } else if (s1 || s2) {
     std::vector<uint16_t> h1(L->n), h2(L->m);
     NQB_CUDA(cudaMemcpyAsync(h1.data(), L->s1h, 2 * (size_t)L->n, cudaMemcpyDeviceToHost, ctx->stream));
     NQB_CUDA(cudaMemcpyAsync(h2.data(), L->s2h, 2 * (size_t)L->m, cudaMemcpyDeviceToHost, ctx->stream));
@@ -508,6 +598,13 @@ int nqb_gemv_f32_host(nqb_context* ctx, const nqb_layer* L, const float* x, floa
     NQB_CUDA(cudaMalloc(&ML->hp_buf, 4 * ((size_t)round_up(L->m, 4) + L->n)));
   float* dx = ML->hp_buf;
   float* dy = dx + round_up(L->m, 4);
+  if (L->s1d) {  // exact fp64 scales: gemv_two_stage<float> arithmetic on CUDA cores
+    NQB_CUDA(cudaMemcpyAsync(dx, x, 4 * (size_t)L->m, cudaMemcpyHostToDevice, ctx->stream));
+    simt_gemv<float, float>(ctx, L, dx, dy);
+    NQB_CUDA(cudaMemcpyAsync(y, dy, 4 * (size_t)L->n, cudaMemcpyDeviceToHost, ctx->stream));
+    NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return NQB_OK;
+  }
   // A pinned (page-locked, mapped) y is written by the kernel directly over the
   // host link: no separate device-to-host copy.  Pageable y goes through dy.
   // Checked every call (a cached answer could outlive the allocation).
@@ -709,6 +806,30 @@ int nqb_pass_launch(nqb_context* ctx, const nqb_pass* pass) {
 int nqb_pass_free(nqb_pass* pass) {
   API_BEGIN
   pass_free(pass);
+  API_END
+}
+
+// One pass end to end with host buffers: each non-NULL hx[k] is copied into
+// step k's device input, the pass runs, each non-NULL hy[i] (one per layer of
+// every step, in step order) receives that layer's output, and the call returns
+// when the outputs are on the host.  Pinned host buffers make the copies
+// asynchronous DMA; pageable ones go through the driver's staging.
+int nqb_pass_run_host(nqb_context* ctx, const nqb_pass* pass, const void* const* hx,
+                      void* const* hy) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_REQUIRE(pass != nullptr, NQB_E_VALIDATION, "null pass");
+  NQB_REQUIRE(pass->device == ctx->device, NQB_E_VALIDATION, "decode pass lives on another device");
+  for (uint32_t k = 0; hx && k < pass->K; ++k)
+    if (hx[k])
+      NQB_CUDA(cudaMemcpyAsync(pass->x_dev[k], hx[k], pass->x_bytes[k], cudaMemcpyHostToDevice,
+                               ctx->stream));
+  pass_launch(ctx, pass, nullptr);
+  for (size_t i = 0; hy && i < pass->y_dev.size(); ++i)
+    if (hy[i])
+      NQB_CUDA(cudaMemcpyAsync(hy[i], pass->y_dev[i], pass->y_bytes[i], cudaMemcpyDeviceToHost,
+                               ctx->stream));
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
   API_END
 }
 

@@ -97,6 +97,11 @@ struct nqb_layer {
   uint32_t* u = nullptr;
   __half* s1h = nullptr;
   __half* s2h = nullptr;
+  // exact fp64 scales (nqb_layer_upload_exact: the C++ drop-in's FactorizedLayer
+  // keeps double scales in memory, packed.hpp:57-72); the exact paths
+  // (reconstruct, gemv/gemm f64, gemv f32 host) use them when present
+  double* s1d = nullptr;
+  double* s2d = nullptr;
   int device = 0;
   nqb_group* dec = nullptr;  // decode plan of this layer alone (decode.cuh)
   float* hp_buf = nullptr;  // host drop-in path (nqb_gemv_f32_host): device x, y staging

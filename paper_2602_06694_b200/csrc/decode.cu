@@ -1,7 +1,6 @@
 // decode.cu — batch-1 BLR decode GEMV (gemv_packed_f32, packed.cpp:201-204)
 // as one fused two-stage sm_100a kernel.  Design: decode.cuh, DESIGN.md §4.
 #include <algorithm>
-#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -354,11 +353,21 @@ void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = g->smem_bytes;
   cfg.stream = ctx->stream;
-  cudaLaunchAttribute attr[1];
+  // Cooperative launch: the runtime guarantees that every CTA is co-resident
+  // (the in-kernel grid barrier needs it) or fails the launch, even when other
+  // streams or contexts hold SMs.  Programmatic serialization (PDL) still lets
+  // the launch start while the previous kernel drains.
+  static const bool coop = [] {
+    const char* v = std::getenv("NQB_DEC_COOP");
+    return !v || std::strtoul(v, nullptr, 10) != 0;
+  }();
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = coop ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   const bool big = g->big;
   if (p.trace) NQB_CUDA(cudaLaunchKernelEx(&cfg, big ? k_decode<true, true> : k_decode<true, false>, p));
   else NQB_CUDA(cudaLaunchKernelEx(&cfg, big ? k_decode<false, true> : k_decode<false, false>, p));

@@ -874,6 +874,15 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
                    "rings=%u+%u chunk caps=%u/%u\n",
                    K, G, P->smem_bytes, head, red1_b, red2_b, kBSlots, bslot1_b, bslot2_b, ring1,
                    ring2, pp.chunk1_cap, pp.chunk2_cap);
+    for (uint32_t k = 0; k < K; ++k) {
+      const uint32_t esz = steps[k].f32 ? 4 : 2;
+      P->x_dev.push_back(const_cast<void*>(steps[k].x));
+      P->x_bytes.push_back((size_t)desc[k].m * esz);
+      for (uint32_t q = 0; q < desc[k].nseg; ++q) {
+        P->y_dev.push_back(steps[k].y[q]);
+        P->y_bytes.push_back((size_t)desc[k].seg[q].n * esz);
+      }
+    }
     P->stream_bytes = stream_bytes;
     P->algo_bytes = (uint64_t)algo;
     for (auto fn : {k_decode_pass<false>, k_decode_pass<true>})

@@ -31,6 +31,8 @@
 // parity and the kernel clears the other parity itself, so the pass replays
 // (directly or in a CUDA graph) with no host work.
 #pragma once
+#include <vector>
+
 #include "decode.cuh"
 
 namespace nqb {
@@ -115,6 +117,9 @@ struct nqb_pass {
   void* dmem = nullptr;  // descriptors, CTA tables, counters, bounds, arena (one allocation)
   uint64_t stream_bytes = 0;   // bits streamed per launch
   uint64_t algo_bytes = 0;     // algorithmic bytes per launch
+  // step inputs and layer outputs (nqb_pass_run_host)
+  std::vector<void*> x_dev, y_dev;
+  std::vector<size_t> x_bytes, y_bytes;
 };
 
 namespace nqb {

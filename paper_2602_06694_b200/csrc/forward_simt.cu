@@ -20,7 +20,8 @@ namespace nqb {
 // a[j] = (Acc)s2[j] * (Acc)x[j] for j < m, 0 for m <= j < padded.
 template <typename Acc, typename In>
 __global__ void k_scale_input(const In* __restrict__ x, const __half* __restrict__ s2h,
-                              uint32_t m, uint32_t padded, Acc* __restrict__ a) {
+                              const double* __restrict__ s2d, uint32_t m, uint32_t padded,
+                              Acc* __restrict__ a) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < padded;
        j += gridDim.x * blockDim.x) {
     Acc v = Acc(0);
@@ -28,7 +29,7 @@ __global__ void k_scale_input(const In* __restrict__ x, const __half* __restrict
       Acc xv;
       if constexpr (std::is_same<In, __half>::value) xv = (Acc)__half2float(x[j]);
       else xv = (Acc)x[j];
-      v = (Acc)__half2float(s2h[j]) * xv;
+      v = (s2d ? (Acc)s2d[j] : (Acc)__half2float(s2h[j])) * xv;
     }
     a[j] = v;
   }
@@ -41,6 +42,7 @@ __global__ void __launch_bounds__(256) k_bitrow_dot(const uint32_t* __restrict__
                                                     uint32_t stride, uint32_t rows,
                                                     uint32_t words, const Acc* __restrict__ act,
                                                     const __half* __restrict__ row_scale,
+                                                    const double* __restrict__ row_scale_d,
                                                     Acc* __restrict__ out) {
   __shared__ Acc act_s[32][kChunkWords + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -67,7 +69,8 @@ __global__ void __launch_bounds__(256) k_bitrow_dot(const uint32_t* __restrict__
   }
   acc = warp_sum(acc);
   if (lane == 0 && row < rows) {
-    out[row] = row_scale ? (Acc)__half2float(row_scale[row]) * acc : acc;
+    out[row] = row_scale_d ? (Acc)row_scale_d[row] * acc
+                           : row_scale ? (Acc)__half2float(row_scale[row]) * acc : acc;
   }
 }
 
@@ -79,6 +82,7 @@ __global__ void __launch_bounds__(256) k_bitrow_gemm(const uint32_t* __restrict_
                                                      uint32_t nact, const Acc* __restrict__ act,
                                                      uint32_t ld, uint32_t b,
                                                      const __half* __restrict__ row_scale,
+                                                     const double* __restrict__ row_scale_d,
                                                      Acc* __restrict__ out, uint32_t ldo) {
   __shared__ Acc act_s[J][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -113,18 +117,21 @@ __global__ void __launch_bounds__(256) k_bitrow_gemm(const uint32_t* __restrict_
   for (int q = 0; q < 4; ++q) {
     const uint32_t row = row0 + warp * 4 + q;
     if (row < rows && c < b) {
-      const Acc s = row_scale ? (Acc)__half2float(row_scale[row]) : Acc(1);
-      out[(uint64_t)row * ldo + c] = row_scale ? s * acc[q] : acc[q];
+      const bool scaled = row_scale_d || row_scale;
+      const Acc s = row_scale_d ? (Acc)row_scale_d[row]
+                                : row_scale ? (Acc)__half2float(row_scale[row]) : Acc(1);
+      out[(uint64_t)row * ldo + c] = scaled ? s * acc[q] : acc[q];
     }
   }
 }
 
 __global__ void k_scale_rows(const double* __restrict__ x, const __half* __restrict__ s2h,
-                             uint32_t m, uint32_t b, double* __restrict__ a) {
+                             const double* __restrict__ s2d, uint32_t m, uint32_t b,
+                             double* __restrict__ a) {
   const uint64_t total = (uint64_t)m * b;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
        e += (uint64_t)gridDim.x * blockDim.x) {
-    a[e] = (double)__half2float(s2h[e / b]) * x[e];
+    a[e] = (s2d ? s2d[e / b] : (double)__half2float(s2h[e / b])) * x[e];
   }
 }
 
@@ -137,16 +144,16 @@ void simt_gemv(nqb_context* ctx, const nqb_layer* L, const In* d_x, Acc* d_y) {
   const uint32_t tpad = L->u_words * 32;
   Acc* a = (Acc*)scratch(ctx, 0, sizeof(Acc) * (apad + tpad));
   Acc* t = a + apad;
-  k_scale_input<Acc, In><<<ceil_div(apad, 256), 256, 0, ctx->stream>>>(d_x, L->s2h, L->m, apad, a);
+  k_scale_input<Acc, In><<<ceil_div(apad, 256), 256, 0, ctx->stream>>>(d_x, L->s2h, L->s2d, L->m, apad, a);
   NQB_LAUNCHED(ctx);
   if (tpad > L->r) {
     NQB_CUDA(cudaMemsetAsync(t + L->r, 0, sizeof(Acc) * (tpad - L->r), ctx->stream));
   }
   k_bitrow_dot<Acc><<<ceil_div(L->r, 8), 256, 0, ctx->stream>>>(L->vt, L->vt_words, L->r,
-                                                              L->vt_words, a, nullptr, t);
+                                                              L->vt_words, a, nullptr, nullptr, t);
   NQB_LAUNCHED(ctx);
   k_bitrow_dot<Acc><<<ceil_div(L->n, 8), 256, 0, ctx->stream>>>(L->u, L->u_words, L->n,
-                                                              L->u_words, t, L->s1h, d_y);
+                                                              L->u_words, t, L->s1h, L->s1d, d_y);
   NQB_LAUNCHED(ctx);
 }
 
@@ -161,15 +168,15 @@ void simt_gemm_f64(nqb_context* ctx, const nqb_layer* L, const double* d_x, uint
   double* a = (double*)scratch(ctx, 0, sizeof(double) * (a_elems + t_elems));
   double* t = a + a_elems;
   k_scale_rows<<<ceil_div(a_elems, 256) > 4096 ? 4096 : ceil_div(a_elems, 256), 256, 0,
-               ctx->stream>>>(d_x, L->s2h, L->m, b, a);
+               ctx->stream>>>(d_x, L->s2h, L->s2d, L->m, b, a);
   NQB_LAUNCHED(ctx);
   dim3 g1(ceil_div(L->r, 32), ceil_div(b, 32));
   k_bitrow_gemm<double><<<g1, 256, 0, ctx->stream>>>(L->vt, L->vt_words, L->r, L->m, a, b, b,
-                                                     nullptr, t, b);
+                                                     nullptr, nullptr, t, b);
   NQB_LAUNCHED(ctx);
   dim3 g2(ceil_div(L->n, 32), ceil_div(b, 32));
   k_bitrow_gemm<double><<<g2, 256, 0, ctx->stream>>>(L->u, L->u_words, L->n, L->r, t, b, b,
-                                                     L->s1h, d_y, b);
+                                                     L->s1h, L->s1d, d_y, b);
   NQB_LAUNCHED(ctx);
 }
 
@@ -185,11 +192,11 @@ void simt_gemm_f32(nqb_context* ctx, const nqb_layer* L, const float* d_a, uint3
   float* t = (float*)scratch(ctx, 1, sizeof(float) * (uint64_t)L->r * b);
   dim3 g1(ceil_div(L->r, 32), ceil_div(b, 32));
   k_bitrow_gemm<float><<<g1, 256, 0, ctx->stream>>>(L->vt, L->vt_words, L->r, L->m, d_a, b, b,
-                                                    nullptr, t, b);
+                                                    nullptr, nullptr, t, b);
   NQB_LAUNCHED(ctx);
   dim3 g2(ceil_div(L->n, 32), ceil_div(b, 32));
   k_bitrow_gemm<float><<<g2, 256, 0, ctx->stream>>>(L->u, L->u_words, L->n, L->r, t, b, b,
-                                                    L->s1h, d_y, b);
+                                                    L->s1h, L->s1d, d_y, b);
   NQB_LAUNCHED(ctx);
 }
 

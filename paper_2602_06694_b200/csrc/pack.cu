@@ -272,7 +272,7 @@ void launch_reconstruct(nqb_context* ctx, const nqb_layer* L, const uint32_t* d_
   dim3 grid(ceil_div(L->m, 16), ceil_div(L->n, 16));
   k_reconstruct<false><<<grid, 256, 0, ctx->stream>>>(L->u, d_vr, stride, L->n, L->m, L->r,
                                                       L->s1h, L->s2h, d_w, nullptr, nullptr,
-                                                      nullptr, nullptr);
+                                                      L->s1d, L->s2d);
   NQB_LAUNCHED(ctx);
 }
 
@@ -284,7 +284,7 @@ void launch_rel_error(nqb_context* ctx, const nqb_layer* L, const uint32_t* d_vr
   dim3 grid(ceil_div(L->m, 16), ceil_div(L->n, 16));
   k_reconstruct<true><<<grid, 256, 0, ctx->stream>>>(L->u, d_vr, stride, L->n, L->m, L->r,
                                                      L->s1h, L->s2h, nullptr, d_w, d_partial,
-                                                     d_s1, d_s2);
+                                                     d_s1 ? d_s1 : L->s1d, d_s2 ? d_s2 : L->s2d);
   NQB_LAUNCHED(ctx);
   k_sum_pairs<<<1, 1024, 0, ctx->stream>>>(d_partial, (uint64_t)grid.x * grid.y, d_out2);
   NQB_LAUNCHED(ctx);

@@ -268,6 +268,18 @@ def rank_for_target_bpw(n: int, m: int, target_bpw: float) -> int:
     return out.value
 
 
+def synthetic_weight(seed: int, n: int, m: int, scale: float = 0.02,
+                     snap_f32: bool = True) -> np.ndarray:
+    """W (n x m fp64, row-major) = fp32(scale * Rng(seed).gaussian()) per entry in
+    stream order (rng.hpp:25-58), generated on the host
+    by libnqb with the reference's splitmix64 / Box-Muller stream."""
+    out = np.empty((n, m), dtype=np.float64)
+    _check(L.load().nqb_synthetic_weight_host(int(seed) & 0xFFFFFFFFFFFFFFFF, n * m, float(scale),
+                                              1 if snap_f32 else 0, _ptr(out)),
+           "synthetic_weight")
+    return out
+
+
 # ---------------------------------------------------------------------------
 # packed.hpp
 # ---------------------------------------------------------------------------
@@ -580,6 +592,22 @@ class DecodePass:
     @property
     def algorithmic_bytes(self) -> int:
         return int(self.ctx.lib.nqb_pass_algorithmic_bytes(self.handle))
+
+    def run_host(self, xs, ys):
+        """One pass end to end through nqb_pass_run_host: xs[k] (numpy, or None
+        to keep step k's device input) -> device, the pass, device -> ys (numpy
+        arrays, one per layer of every step in step order, or None); returns
+        when the outputs are on the host.  Runs on the context's own stream."""
+        hx = (C.c_void_p * self.steps)(*[None if x is None else x.ctypes.data for x in xs])
+        ny = sum(len(k[2]) for k in self._keep)
+        if len(ys) != ny:
+            raise DimensionMismatch(f"run_host: {len(ys)} outputs for {ny} layers")
+        for (unit, x, outs), hxk in zip(self._keep, xs):
+            if hxk is not None and hxk.nbytes != x.numel() * x.element_size():
+                raise DimensionMismatch("run_host: host input size differs from the step input")
+        hy = (C.c_void_p * ny)(*[None if y is None else y.ctypes.data for y in ys])
+        _check(self.ctx.lib.nqb_pass_run_host(self.ctx.handle, self.handle, hx, hy),
+               "nqb_pass_run_host")
 
     def launch(self):
         """Enqueues the pass on torch's current stream."""

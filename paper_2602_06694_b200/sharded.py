@@ -88,19 +88,27 @@ class PackedMatrix:
     iterations: int = 0
     converged: bool = False
     seconds: float = 0.0
+    # phase statistics of the device ADMM (nqb_admm_result)
+    svd_steps: int = 0
+    svd_power_iters: int = 0
+    seconds_svd: float = 0.0
+    seconds_iter: float = 0.0
 
-    _HDR = struct.Struct("<IIIIdIIdI")  # index n m r err iters conv secs pad
+    # index n m r err iters conv secs svd_steps svd_power_iters secs_svd secs_iter
+    _HDR = struct.Struct("<IIIIdIIdIQdd")
 
     def to_bytes(self) -> bytes:
         h = self._HDR.pack(self.index, self.n, self.m, self.r, float(self.rel_error),
-                           int(self.iterations), int(self.converged), float(self.seconds), 0)
+                           int(self.iterations), int(self.converged), float(self.seconds),
+                           int(self.svd_steps), int(self.svd_power_iters), float(self.seconds_svd),
+                           float(self.seconds_iter))
         return h + np.ascontiguousarray(self.u, "<u4").tobytes() + \
             np.ascontiguousarray(self.v, "<u4").tobytes() + \
             np.ascontiguousarray(self.s1, "<u2").tobytes() + np.ascontiguousarray(self.s2, "<u2").tobytes()
 
     @classmethod
     def from_bytes(cls, buf: memoryview) -> Tuple["PackedMatrix", int]:
-        idx, n, m, r, err, iters, conv, secs, _ = cls._HDR.unpack_from(buf, 0)
+        idx, n, m, r, err, iters, conv, secs, ss, spi, tsvd, tit = cls._HDR.unpack_from(buf, 0)
         off = cls._HDR.size
         k = (r + 31) // 32
         u = np.frombuffer(buf, "<u4", n * k, off).reshape(n, k).copy()
@@ -111,7 +119,7 @@ class PackedMatrix:
         off += 2 * n
         s2 = np.frombuffer(buf, "<u2", m, off).copy()
         off += 2 * m
-        return cls(idx, n, m, r, u, v, s1, s2, err, iters, bool(conv), secs), off
+        return cls(idx, n, m, r, u, v, s1, s2, err, iters, bool(conv), secs, ss, spi, tsvd, tit), off
 
 
 def pack_shard(items: Sequence[PackedMatrix]) -> np.ndarray:
@@ -135,9 +143,11 @@ def unpack_shard(buf: np.ndarray) -> List[PackedMatrix]:
 
 
 def synthetic_weight(spec: MatrixSpec) -> np.ndarray:
-    """W = fp32(0.02 * N(0,1)) seeded by the spec (promoted to double like NQMX, io.cpp:118)."""
-    rng = np.random.default_rng(spec.seed)
-    return (0.02 * rng.standard_normal((spec.n, spec.m))).astype(np.float32).astype(np.float64)
+    """W_ij = fp32(0.02 * g), g from the reference Rng(spec.seed) in row-major order,
+    promoted to double like NQMX (io.cpp:117-119): SURVEY §8(d) row 4, so the
+    reference can regenerate exactly these inputs (nqb_synthetic_weight_host)."""
+    from . import nanoquant as nq
+    return nq.synthetic_weight(spec.seed, spec.n, spec.m, 0.02)
 
 
 def device_factorize(spec: MatrixSpec, index: int, bpw: float, max_iters: int = 400,
@@ -154,8 +164,11 @@ def device_factorize(spec: MatrixSpec, index: int, bpw: float, max_iters: int = 
     got = lay.download()
     h1 = got.s1.astype(np.float16).view(np.uint16)
     h2 = got.s2.astype(np.float16).view(np.uint16)
+    st = state.stats
     return PackedMatrix(index, spec.n, spec.m, r, got.u, got.v, h1, h2, err, state.iteration,
-                        state.converged, secs)
+                        state.converged, secs, int(st.get("svd_steps", 0)),
+                        int(st.get("svd_power_iters", 0)), float(st.get("seconds_svd_init", 0.0)),
+                        float(st.get("seconds_iterations", 0.0)))
 
 
 @dataclass

@@ -322,3 +322,40 @@ def test_graph_then_bigger_upload_keeps_graph_valid(nq, chk):
     torch.cuda.synchronize()
     ctx.bind_torch_stream()
     del grp
+
+
+def test_decode_co_resident_under_busy_stream_and_two_contexts(nq, chk):
+    """The per-call kernel's grid barrier needs every CTA resident: the launch is
+    cooperative, so decode completes correctly while another stream keeps the
+    SMs busy, and while a second context (own stream) decodes concurrently."""
+    import threading
+
+    import torch
+    n, m, r = 4096, 4096, 1622
+    lay = O.synthetic_layer(chk, 0xC0, n, m, r)
+    x = chk.rng(0xC1).gaussian(m).astype(np.float32)
+    want = chk.gemv_packed_f32(lay, x)
+    fl = nq.FactorizedLayer(n, m, r, lay.u, lay.v, lay.s1, lay.s2)
+    ctx2 = nq.Context(0)
+    d1 = nq.DeviceLayer.upload(fl, nq.context(0))
+    d2 = nq.DeviceLayer.upload(fl, ctx2)
+    busy = torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda")
+    with torch.cuda.stream(busy):
+        for _ in range(40):
+            a = torch.tanh(a @ a)  # keeps every SM occupied for a while
+    outs = {}
+
+    def run(dev, key):
+        outs[key] = [dev.gemv_f32(x) for _ in range(20)]
+
+    th = threading.Thread(target=run, args=(d2, "b"))
+    th.start()
+    run(d1, "a")
+    th.join(timeout=120)
+    torch.cuda.synchronize()
+    for key in ("a", "b"):
+        assert len(outs[key]) == 20
+        for y in outs[key]:
+            assert rel(y, want) <= 2e-5
+    ctx2.close()

@@ -212,3 +212,35 @@ def test_sign_bits_helper_on_device_layer(nq, chk):
     lay = O.synthetic_layer(chk, 2, 40, 70, 45)
     back = nq.DeviceLayer.upload(to_nq(nq, lay)).download()
     assert np.array_equal(bits_of(back.u, 45), bits_of(lay.u, 45))
+
+
+# BASELINE config 3: the benchmarked Llama-2-70B shapes at 0.55 bit, b = 2048
+# tokens.  The GPU computes all 2048 columns; a deterministic 64-column subset
+# (columns are independent in gemm_packed, packed.cpp:260-287) is checked against
+# the unmodified reference with NQ_THREADS = nproc.
+CFG3 = [("l70_q", 8192, 8192), ("l70_gate", 28672, 8192), ("l70_down", 8192, 28672)]
+
+
+@pytest.mark.parametrize("name,n,m", CFG3)
+def test_prefill_config3_shapes_b2048_vs_gemm_packed(nq, chk, name, n, m):
+    import os
+
+    import torch
+    r = chk.rank_for_target_bpw(n, m, 0.55)
+    assert r == {8192: 2237, 28672: 3488}[max(n, m)]
+    b = 2048
+    lay = O.synthetic_layer(chk, 0xC3 + n + m, n, m, r)
+    # activations at 1/8 of unit variance: with N(0,1) x the 8192 x 28672 (down)
+    # outputs reach ~7e4 and overflow binary16 I/O (65504), on any fp16 path
+    X16 = (0.125 * chk.rng(0xC3).gaussian(m * b)).reshape(b, m).astype(np.float16)  # token-major
+    dev = nq.DeviceLayer.upload(to_nq(nq, lay))
+    y = torch.empty((b, n), dtype=torch.float16, device="cuda")
+    dev.gemm_device(torch.from_numpy(X16).cuda(), y)
+    torch.cuda.synchronize()
+    cols = np.sort(np.random.default_rng(n * 7 + m).choice(b, 64, replace=False))
+    want = chk.gemm_packed(lay, X16[cols].astype(np.float64).T, threads=os.cpu_count() or 1)
+    got = y.float().cpu().numpy()[cols].T
+    assert np.isfinite(got).all()
+    assert rel(got, want) <= FWD_TOL
+    for j in range(0, 64, 16):  # per column, too (tokens are independent)
+        assert rel(got[:, j], want[:, j]) <= FWD_TOL

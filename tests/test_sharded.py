@@ -112,3 +112,65 @@ def test_device_factorize_small_matrix_matches_layer_path():
     assert 0 < pm.rel_error < 1.5 and pm.iterations >= 1
     rt = S.unpack_shard(S.pack_shard([pm]))[0]
     assert np.array_equal(rt.u, pm.u) and np.array_equal(rt.s2, pm.s2)
+
+
+def _device_worker(rank, world, port, out):
+    """One rank of a real multi-rank run: the device factorisation (libnqb on
+    cuda:0, both ranks share the GPU) + the gloo gather of packed factors."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rep = S.sharded_init(device_specs(), 1.0)
+        if rank == 0:
+            out.put({i: (p.u.tobytes(), p.v.tobytes(), p.s1.tobytes(), p.s2.tobytes(), p.r,
+                         p.rel_error, p.iterations) for i, p in rep.matrices.items()})
+        else:
+            assert rep is None
+    finally:
+        dist.destroy_process_group()
+
+
+def device_specs():
+    """Four small matrices, W from the reference Rng (SURVEY §8(d) row 4 seeds)."""
+    shapes = [(64, 48), (96, 160), (128, 128), (200, 64)]
+    return [S.MatrixSpec(f"d{i}", n, m, 0x7B000000 + i) for i, (n, m) in enumerate(shapes)]
+
+
+@pytest.mark.gpu
+def test_device_sharded_world2_gather_bitwise_equals_world1():
+    """SURVEY §8(d) protocol: the gathered packed factors of a 2-rank device run
+    equal a single-rank run bit for bit (same matrices, same metrics)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_device_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = S.sharded_init(device_specs(), 1.0)
+    assert sorted(got) == sorted(want.matrices) == [0, 1, 2, 3]
+    for i, pm in want.matrices.items():
+        assert got[i] == (pm.u.tobytes(), pm.v.tobytes(), pm.s1.tobytes(), pm.s2.tobytes(), pm.r,
+                          pm.rel_error, pm.iterations)
+        assert pm.svd_power_iters > 0 and pm.seconds_svd > 0
+
+
+def test_synthetic_weight_matches_reference_rng():
+    """The product's W generator (libnqb host code) is the reference Rng stream:
+    bitwise equal to rng.hpp via oracle/_ref, including the fp32 snap."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle"))
+    import oracle as O
+    from paper_2602_06694_b200 import nanoquant as nq
+    chk = O.reference() if O.reference_available() else O.restated()
+    for seed, n, m in [(0x7B000000, 3, 5), (0x7B000000 + 7 * 3 + 4, 257, 300),
+                       (0xB1A5E001, 64, 4096)]:
+        w = nq.synthetic_weight(seed, n, m)
+        ref = O.synthetic_weight(chk, seed, n, m)
+        assert np.array_equal(w.view(np.uint64), ref.view(np.uint64))
+    spec = S.MatrixSpec("b3.up", 64, 96, 0x7B000000 + 7 * 3 + 5)
+    assert np.array_equal(S.synthetic_weight(spec), O.synthetic_weight(chk, spec.seed, 64, 96))
