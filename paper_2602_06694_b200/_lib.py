@@ -66,6 +66,7 @@ PROTOTYPES = {
     "nqb_pack_latent": (C.c_int, [P, P, U32, U32, P, C.c_int]),
     "nqb_unpack_signs": (C.c_int, [P, P, U32, U32, P, C.c_int]),
     "nqb_layer_upload": (C.c_int, [P, U32, U32, U32, P, P, P, P, PP]),
+    "nqb_layer_upload_exact": (C.c_int, [P, U32, U32, U32, P, P, P, P, PP]),
     "nqb_layer_upload_f16": (C.c_int, [P, U32, U32, U32, P, P, P, P, PP]),
     "nqb_layer_free": (C.c_int, [P]),
     "nqb_layer_shape": (C.c_int, [P, PU32, PU32, PU32]),
@@ -81,6 +82,8 @@ PROTOTYPES = {
     "nqb_admm_config_default": (None, [C.POINTER(AdmmConfig)]),
     "nqb_admm_factorize_host": (C.c_int, [P, P, U32, U32, C.POINTER(AdmmConfig), P, P, P,
                                           C.POINTER(AdmmResultC)]),
+    "nqb_admm_factorize_state_host": (C.c_int, [P, P, U32, U32, C.POINTER(AdmmConfig), P, P,
+                                                P, C.POINTER(AdmmResultC), P]),
     "nqb_admm_factorize_device": (C.c_int, [P, P, U32, U32, C.POINTER(AdmmConfig), P, P, P,
                                             C.POINTER(AdmmResultC)]),
     "nqb_balance_host": (C.c_int, [P, P, P, U32, U32, U32, P, P, D, P, P, P, P, PD]),
