@@ -56,7 +56,15 @@ def main():
                           "per_rank_compute_s": rep.per_rank_seconds,
                           "mean_rel_error": sum(errs) / len(errs),
                           "mean_admm_iterations": sum(its) / len(its),
-                          "shapes": sorted({(p.n, p.m, p.r) for p in rep.matrices.values()})}),
+                          "shapes": sorted({(p.n, p.m, p.r) for p in rep.matrices.values()}),
+                          "weights": "W = fp32(0.02 g), g from the reference Rng(0x7B000000 + 7b + p)",
+                          "per_matrix": [{"name": specs[i].name, "n": p.n, "m": p.m, "r": p.r,
+                                          "seconds": p.seconds, "svd_init_s": p.seconds_svd,
+                                          "iterations_s": p.seconds_iter,
+                                          "svd_power_iterations": p.svd_power_iters,
+                                          "admm_iterations": p.iterations,
+                                          "converged": p.converged, "rel_error": p.rel_error}
+                                         for i, p in sorted(rep.matrices.items())]}),
               flush=True)
     if ws > 1:
         dist.destroy_process_group()
