@@ -3,8 +3,8 @@
 // y = s1 .* U (V^T (s2 .* x))  (gemv_two_stage, packed.cpp:153-192)
 //
 // The signs are consumed as {0,1} bits: sum_j sign_j a_j = 2 sum_j bit_j a_j -
-// sum_j a_j.  Activations are quantised once per call to 22-bit fixed point
-// against a per-segment power-of-two bound, split into four signed 8-bit limbs
+// sum_j a_j.  Activations are quantised once per call to 38-bit fixed point
+// against a power-of-two bound from max|x| (kFix), split into six signed 8-bit limbs
 // and fed to the tensor cores as the B operand of `mma.sync m16n8k32 u8.s8`;
 // the bits are the A operand, expanded in registers with ONE LOP3 per four
 // bits: tile q of a 256-wide K slab uses A bytes {0, 2^q} (word & 0x01010101<<q)
