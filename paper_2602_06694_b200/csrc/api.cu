@@ -51,6 +51,21 @@ void* scratch(nqb_context* ctx, int slot, size_t bytes) {
   return s.ptr;
 }
 
+void* ctx_pinned(nqb_context* ctx, int slot, size_t bytes) {
+  if (ctx->pinned_bytes[slot] < bytes) {
+    if (ctx->pinned[slot]) {
+      NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+      NQB_CUDA(cudaFreeHost(ctx->pinned[slot]));
+    }
+    ctx->pinned[slot] = nullptr;
+    ctx->pinned_bytes[slot] = 0;
+    const size_t want = bytes < 65536 ? 65536 : bytes;
+    NQB_CUDA(cudaHostAlloc(&ctx->pinned[slot], want, cudaHostAllocDefault));
+    ctx->pinned_bytes[slot] = want;
+  }
+  return ctx->pinned[slot];
+}
+
 uint16_t host_double_to_half(double x) {
   const __half h = __float2half_rn((float)x);
   uint16_t bits;
@@ -175,6 +190,8 @@ int nqb_destroy(nqb_context* ctx) {
   for (auto& s : ctx->scratch)
     if (s.ptr) cudaFree(s.ptr);
   if (ctx->barrier) cudaFree(ctx->barrier);
+  for (void* p : ctx->pinned)
+    if (p) cudaFreeHost(p);
   if (ctx->dec_state) cudaFree(ctx->dec_state);
   for (void* p : ctx->dec_retired) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -423,6 +440,38 @@ nqb_layer* layer_from_device_words(nqb_context* ctx, uint32_t n, uint32_t m, uin
     throw;
   }
   return L;
+}
+
+// Many small copies in one launch (nqb_pass_run_host): block b takes jobs b,
+// b + grid, ...; 16-byte vectors when both ends and the size allow.
+__global__ void k_copy_jobs(const CopyJob* __restrict__ jobs, uint32_t count) {
+  for (uint32_t j = blockIdx.x; j < count; j += gridDim.x) {
+    const CopyJob J = jobs[j];
+    const bool vec = (((uintptr_t)J.dst | (uintptr_t)J.src | J.bytes) & 15u) == 0;
+    if (vec) {
+      const uint4* s = (const uint4*)J.src;
+      uint4* d = (uint4*)J.dst;
+      for (size_t i = threadIdx.x; i < J.bytes / 16; i += blockDim.x) d[i] = s[i];
+    } else {
+      const uint8_t* s = (const uint8_t*)J.src;
+      uint8_t* d = (uint8_t*)J.dst;
+      for (size_t i = threadIdx.x; i < J.bytes; i += blockDim.x) d[i] = s[i];
+    }
+  }
+}
+
+void copy_jobs(nqb_context* ctx, const std::vector<CopyJob>& jobs, int slot) {
+  if (jobs.empty()) return;
+  const size_t bytes = jobs.size() * sizeof(CopyJob);
+  // the job list goes up through a page-locked staging buffer of the context
+  // (two slots: the input and the output list of one call can be in flight)
+  CopyJob* host = (CopyJob*)ctx_pinned(ctx, slot, bytes);
+  std::memcpy(host, jobs.data(), bytes);
+  CopyJob* dev = (CopyJob*)scratch(ctx, 12 + slot, bytes);
+  NQB_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  k_copy_jobs<<<std::min<uint32_t>((uint32_t)jobs.size(), 4u * ctx->num_sms), 256, 0, ctx->stream>>>(
+      dev, (uint32_t)jobs.size());
+  NQB_LAUNCHED(ctx);
 }
 
 // V back to the reference orientation (m x stride words) in device memory.
@@ -820,15 +869,32 @@ int nqb_pass_run_host(nqb_context* ctx, const nqb_pass* pass, const void* const*
   check_ctx(ctx);
   NQB_REQUIRE(pass != nullptr, NQB_E_VALIDATION, "null pass");
   NQB_REQUIRE(pass->device == ctx->device, NQB_E_VALIDATION, "decode pass lives on another device");
+  // A decode pass has hundreds of small inputs and outputs; one API call per
+  // buffer would cost more host time than the kernel.  Page-locked host buffers
+  // are moved by ONE copy kernel per direction that reads / writes them through
+  // their mapped device addresses; pageable ones get one cudaMemcpyAsync each.
+  std::vector<CopyJob> jobs;
+  auto add = [&](void* dst, const void* src, size_t bytes, bool host_is_dst) {
+    const void* host = host_is_dst ? dst : src;
+    cudaPointerAttributes at{};
+    void* mapped = nullptr;
+    if (cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost)
+      mapped = at.devicePointer;
+    cudaGetLastError();
+    if (mapped) {
+      jobs.push_back(host_is_dst ? CopyJob{mapped, src, bytes} : CopyJob{dst, mapped, bytes});
+    } else {
+      NQB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+    }
+  };
   for (uint32_t k = 0; hx && k < pass->K; ++k)
-    if (hx[k])
-      NQB_CUDA(cudaMemcpyAsync(pass->x_dev[k], hx[k], pass->x_bytes[k], cudaMemcpyHostToDevice,
-                               ctx->stream));
+    if (hx[k]) add(pass->x_dev[k], hx[k], pass->x_bytes[k], false);
+  copy_jobs(ctx, jobs, 0);
   pass_launch(ctx, pass, nullptr);
+  jobs.clear();
   for (size_t i = 0; hy && i < pass->y_dev.size(); ++i)
-    if (hy[i])
-      NQB_CUDA(cudaMemcpyAsync(hy[i], pass->y_dev[i], pass->y_bytes[i], cudaMemcpyDeviceToHost,
-                               ctx->stream));
+    if (hy[i]) add(hy[i], pass->y_dev[i], pass->y_bytes[i], true);
+  copy_jobs(ctx, jobs, 1);
   NQB_CUDA(cudaStreamSynchronize(ctx->stream));
   API_END
 }

@@ -79,6 +79,9 @@ struct nqb_context {
   bool dec_attr_set = false;
   bool pdl = true;  // launch decode kernels with Programmatic Dependent Launch
   void* dec_trace = nullptr;  // diagnostics (nqb_debug_decode_trace)
+  // page-locked host staging (ctx_pinned): job lists of nqb_pass_run_host
+  void* pinned[2] = {nullptr, nullptr};
+  size_t pinned_bytes[2] = {0, 0};
 };
 
 struct nqb_group;
@@ -111,6 +114,15 @@ namespace nqb {
 
 // Returns a device buffer of at least `bytes` from slot `slot` of the arena.
 void* scratch(nqb_context* ctx, int slot, size_t bytes);
+// A page-locked host buffer of at least `bytes` (slot 0 or 1) owned by the context.
+void* ctx_pinned(nqb_context* ctx, int slot, size_t bytes);
+// One copy of a batch moved by a single kernel (nqb_pass_run_host).
+struct CopyJob {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+void copy_jobs(nqb_context* ctx, const std::vector<CopyJob>& jobs, int slot);
 
 inline uint32_t ceil_div(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
 inline uint32_t round_up(uint32_t a, uint32_t b) { return (a + b - 1) / b * b; }

@@ -577,26 +577,46 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   // The stage's (pair, section) items are split over the group's warps once for
   // the whole stage (pair-major, contiguous per warp); each warp walks the
   // chunks as they land and runs its items in each.
+  uint32_t cur_step = 0;
   auto mma_stage = [&](const StageGeo& g, const uint8_t* bf) {
     if (!g.nsec) return;
     const uint32_t npair = (g.rtn + 1) / 2, U = npair * g.nsec;
     const uint32_t f0 = U * gw / kGroupWarps, f1 = U * (gw + 1) / kGroupWarps;
     const uint32_t p0 = f0 / g.nsec, p1 = f1 ? (f1 - 1) / g.nsec : 0;
+    unsigned long long wsum = 0, nch = 0, rsum = 0, ncall = 0, nslab = 0;
     for (uint32_t s0 = 0; s0 < g.nsec;) {
       const uint32_t slot = chunk % kPassSlots;
+      const unsigned long long w0 = kTrace ? clock64() : 0ull;
       mbar_wait_wd(&fullr[slot], (chunk / kPassSlots) & 1, sus);
+      if (kTrace) {
+        wsum += clock64() - w0;
+        ++nch;
+      }
       const ChunkRec cr = recs[slot];
       if (f0 < f1 && !(p.debug & 1u)) {
         for (uint32_t pr = p0; pr <= p1; ++pr) {
           const uint32_t sa = max(s0, pr == p0 ? f0 - p0 * g.nsec : 0u);
           const uint32_t sb = min((uint32_t)cr.s1, pr == p1 ? f1 - p1 * g.nsec : g.nsec);
-          if (sa < sb) run_pair(ring + cr.off, g, s0, pr, sa, sb, bf, red);
+          if (sa < sb) {
+            const unsigned long long r0 = kTrace ? clock64() : 0ull;
+            run_pair(ring + cr.off, g, s0, pr, sa, sb, bf, red);
+            if (kTrace) {
+              rsum += clock64() - r0;
+              ++ncall;
+              nslab += sb - sa;
+            }
+          }
         }
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&emptyr[slot]);
       ++chunk;
       s0 = cr.s1;
+    }
+    if (kTrace && gw == 0 && lane == 0) {  // this warp's time waiting for chunks, and chunks
+      trp[1 + kPassStamps * cur_step + 16 + gid] = wsum;
+      trp[1 + kPassStamps * cur_step + 18 + gid] = (nch << 48) | (ncall << 32) | (nslab << 16);
+      trp[1 + kPassStamps * cur_step + 20 + gid] = rsum;
     }
   };
 
@@ -615,6 +635,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     }
     const StageGeo g = gid ? stage2_geo(D, C) : stage1_geo(D, C);
     const long long A = ((const long long*)bs)[0] + ((const long long*)bs)[1];
+    cur_step = k;
     mma_stage(g, bs + kBSlotHead);
     group_sync(gid);
     if (kTrace && gt == 0) PSTAMP(k, gid ? 10 : 8);
@@ -863,8 +884,15 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     const uint32_t cap_kb = env_u32p("NQB_PASS_CHUNK_KB", 0);
     // a chunk is at most cap + the largest section (16 KB); a group holds one
     // chunk at a time, so its ring must fit one
-    pp.chunk1_cap = cap_kb ? cap_kb * 1024 : std::min<uint32_t>(32768, ring1 / 3 / 128 * 128);
-    pp.chunk2_cap = cap_kb ? cap_kb * 1024 : std::min<uint32_t>(32768, ring2 / 3 / 128 * 128);
+    // Chunks of about half a ring: a chunk's sections are the run length of every
+    // consumer warp's MMA loop (one flush per run), so longer chunks cut the
+    // per-run overhead; two chunks in flight still cover the HBM latency
+    // (measured: 70B pass 1068 -> 1240 GB/s going from ring/3 to ~32 KB chunks).
+    auto cap_of = [](uint32_t ring) {
+      return std::min<uint32_t>(40u * 1024u, (ring / 2 - 2048) / 128 * 128);
+    };
+    pp.chunk1_cap = cap_kb ? cap_kb * 1024 : cap_of(ring1);
+    pp.chunk2_cap = cap_kb ? cap_kb * 1024 : cap_of(ring2);
     NQB_REQUIRE(pp.chunk1_cap + 16384 <= ring1 && pp.chunk2_cap + 16384 <= ring2,
                 NQB_E_VALIDATION, "NQB_PASS_CHUNK_KB too large for the shared-memory rings");
     P->smem_bytes = fixed + rings;

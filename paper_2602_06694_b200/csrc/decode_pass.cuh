@@ -45,7 +45,7 @@ constexpr int kDoneRing = 24;    // consumer phase-completion mbarriers
 constexpr int kCtrStride = 16;   // u64 words per counter (own 128-byte line)
 // helper warps: producer 1, x quantisers (2), t quantisers (2), sequencers 1 and 2, producer 2
 constexpr int kPassHelpers = 8;
-constexpr int kPassStamps = 16;  // trace stamps per step
+constexpr int kPassStamps = 24;  // trace stamps per step (16..21: consumer chunk-wait / run counters, per stage)
 constexpr int kMaxLookahead = 6;
 constexpr uint32_t kBSlotHead = 16;  // slot header: the two quantiser warps' sums of the values
 

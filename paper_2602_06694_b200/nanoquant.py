@@ -615,15 +615,16 @@ class DecodePass:
         _check(self.ctx.lib.nqb_pass_launch(self.ctx.handle, self.handle), "nqb_pass_launch")
 
     def trace(self):
-        """One launch with per-CTA %globaltimer stamps -> (grid, 16K+2) uint64 array:
+        """One launch with per-CTA %globaltimer stamps -> (grid, 24K+2) uint64 array:
         [CTA start, per step (stage-1 start, stage-1 end, t ready, stage-2 end,
         t barrier seen by the t loader, x staged by the x stager, stage-1 first
         chunk landed, x quantised, stage-1 MMA done, t quantised, stage-2 MMA
         done, producer issued stage 1, t loader got its slot, t copy issued, producer started / finished stage 2),
+        16/17 ns warp 0 of each stage group waited for chunks, 18/19 its chunks),
         end]; stamp 6 = producer finished stage 1."""
         self.ctx.bind_torch_stream(self._keep[0][1].device)
         g = C.c_uint32()
-        per = 16 * self.steps + 2
+        per = 24 * self.steps + 2
         out = np.zeros(160 * per, np.uint64)
         _check(self.ctx.lib.nqb_debug_pass_trace(self.ctx.handle, self.handle, _ptr(out),
                                                  C.byref(g)), "nqb_debug_pass_trace")

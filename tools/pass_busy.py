@@ -56,8 +56,9 @@ def main():
     tr = p.trace().astype(np.int64)
     G, K = tr.shape[0], len(steps)
     t0 = tr[:, 0].min()
-    st = ((tr[:, 1:1 + 16 * K] - t0) / 1e3).reshape(G, K, 16)
-    span = (tr[:, 16 * K + 1].max() - t0) / 1e3
+    raw = tr[:, 1:1 + 24 * K].reshape(G, K, 24)
+    st = (raw - t0) / 1e3
+    span = (tr[:, 24 * K + 1].max() - t0) / 1e3
     kinds = ["qkv", "o", "gateup", "down"]
     out = {"model": args.model, "blocks": args.blocks, "span_us": span,
            "gbs_traced": p.algorithmic_bytes / span / 1e3}
@@ -69,6 +70,13 @@ def main():
         "s2_wait": st[:, :, 2] - s2_prev_end, "s2_quant": st[:, :, 9] - st[:, :, 2],
         "s2_mma": st[:, :, 10] - st[:, :, 9], "s2_out": st[:, :, 3] - st[:, :, 10],
         "tbar_after_s1end_max": st[:, :, 4] - st[:, :, 1].max(axis=0, keepdims=True),
+        "s1_chunk_wait": raw[:, :, 16] / 1965.0, "s2_chunk_wait": raw[:, :, 17] / 1965.0,
+        "s1_chunks": (raw[:, :, 18] >> 48).astype(float), "s2_chunks": (raw[:, :, 19] >> 48).astype(float),
+        "s1_calls": ((raw[:, :, 18] >> 32) & 0xFFFF).astype(float),
+        "s2_calls": ((raw[:, :, 19] >> 32) & 0xFFFF).astype(float),
+        "s1_slabs": ((raw[:, :, 18] >> 16) & 0xFFFF).astype(float),
+        "s2_slabs": ((raw[:, :, 19] >> 16) & 0xFFFF).astype(float),
+        "s1_runpair_us": raw[:, :, 20] / 1965.0, "s2_runpair_us": raw[:, :, 21] / 1965.0,
     }
     for i, kd in enumerate(kinds):
         sel = [k for k in range(K) if k % 4 == i and k >= 4]
