@@ -41,6 +41,7 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+admm_layer_for_cpu = None  # config 1: the ADMM's layer, for the CPU forward baseline
 sys.path.insert(0, ROOT)
 
 METRIC = "BLR-linear decode GB/s"
@@ -445,6 +446,8 @@ def admm_leg(nq, torch, ws, rank, local, hbm, fp64_peak):
     wall = time.perf_counter() - t0
     if rank != 0:
         return None
+    global admm_layer_for_cpu
+    admm_layer_for_cpu = rep.matrices[min(rep.matrices)]
     mats = [rep.matrices[i] for i in sorted(rep.matrices)]
     n = m = 4096
     r = mats[0].r
@@ -469,7 +472,30 @@ def admm_leg(nq, torch, ws, rank, local, hbm, fp64_peak):
                                "unit": "TFLOP/s", "frac": it_tf / fp64_peak,
                                "flops_per_iteration": flops_iter,
                                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"}},
-            "weights": "W = fp32(0.02 g), g from the reference Rng(0x7B000000 + 7b) (rng.hpp:25-58)"}
+            "weights": "W = fp32(0.02 g), g from the reference Rng(0x7B000000 + 7b) (rng.hpp:25-58)",
+            "forward": config1_forward(nq, torch, pm)}
+
+
+def config1_forward(nq, torch, pm, reps=200):
+    """BASELINE config 1's batch-1 forward on the layer the ADMM just produced
+    (binary16 scales, NQPK precision): x fp32 from Rng(0xB1A5E002) (SURVEY §8(d)
+    row 1), the reference-facing drop-in nqb_gemv_f32_host and the device kernel."""
+    lay = nq.DeviceLayer.upload_f16(pm.n, pm.m, pm.r, pm.u, pm.v, pm.s1, pm.s2)
+    x = nq.synthetic_weight(0xB1A5E002, 1, pm.m, 1.0, snap_f32=True).astype(np.float32).ravel()
+    y = lay.gemv_f32(x)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty(pm.n, device="cuda", dtype=torch.float32)
+    stream = torch.cuda.Stream()
+    sec = time_launches(torch, stream, lambda: lay.gemv_device(xd, yd), reps, 10)
+    t0 = time.perf_counter()
+    for _ in range(50):
+        lay.gemv_f32(x, out=y)
+    host = (time.perf_counter() - t0) / 50
+    nbytes = algo_bytes(pm.n, pm.m, pm.r) + 2 * pm.n  # fp32 x / y
+    return {"layer": f"{pm.n}x{pm.m} r={pm.r} from the ADMM above", "device_us": sec * 1e6,
+            "device_gbs_l2_resident": nbytes / sec / 1e9, "host_dropin_us": host * 1e6,
+            "y": y, "x": x, "note": "one 2.1 MB layer re-read per call stays in L2; the HBM-bound "
+                                   "numbers are the pass and per-shape lines"}
 
 
 def admm_small_gpu(nq, ws_cpu, r):
@@ -674,12 +700,28 @@ def main():
                 for k, v in cp.items():
                     extra["prefill_tcgen05"][k]["cpu_baseline"] = v
             if admm is not None:
+                fw = admm["forward"]
+                pm0 = admm_layer_for_cpu
+                O = _oracle()
+                ref = O.reference()
+                L = O.Layer(pm0.n, pm0.m, pm0.r, pm0.u, pm0.v,
+                            pm0.s1.view(np.float16).astype(np.float64),
+                            pm0.s2.view(np.float16).astype(np.float64))
+                t0 = time.perf_counter()
+                yr = ref.gemv_packed_f32(L, fw["x"])
+                fw["cpu_baseline"] = {"seconds": time.perf_counter() - t0, "cores": 1,
+                                      "kind": "reference", "call": "gemv_packed_f32"}
+                fw["rel_error_vs_reference"] = float(np.linalg.norm(fw["y"] - yr) /
+                                                     max(np.linalg.norm(yr), 1e-300))
                 ca, ws_cpu, r256 = cpu_admm_baseline()
                 ca["gpu_same_256_matrices"] = admm_small_gpu(nq, ws_cpu, r256)
                 admm["cpu_baseline"] = ca
         except Exception as e:  # noqa: BLE001
             extra["cpu_baseline_error"] = str(e)
 
+    if admm is not None and "forward" in admm:
+        admm["forward"].pop("x", None)
+        admm["forward"].pop("y", None)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,

@@ -59,6 +59,7 @@ typedef enum nqb_status {
   /* ErrorKind::kNumerical (CLI exit 3) */
   NQB_E_ZERO_MATRIX = 32,         /* ZeroMatrix          errors.hpp:53-57 */
   NQB_E_NOT_POSITIVE_DEFINITE = 33, /* NotPositiveDefinite errors.hpp:47-51 */
+  NQB_E_NON_FINITE_LOSS = 34,       /* NonFiniteLoss       refine.hpp:72-77 */
   /* runtime (no reference counterpart) */
   NQB_E_CUDA = 64,
   NQB_E_OUT_OF_MEMORY = 65,
@@ -319,6 +320,29 @@ int nqb_factorize_layer(nqb_context* ctx, const double* w, uint32_t n, uint32_t 
  * W on host (on_device = 0) or device. */
 int nqb_layer_rel_error(nqb_context* ctx, const nqb_layer* layer, const double* w,
                         int on_device, double* rel_error);
+
+/* ------------------------------------------------------------------------ */
+/* STE refinement on the device (refine.cpp:285-384, 420-425) */
+/* ------------------------------------------------------------------------ */
+typedef struct nqb_tune_config {  /* TuneConfig, refine.hpp:55-64 */
+  int32_t epochs;          /* default 8 */
+  int32_t batch_size;      /* default 4 */
+  double learning_rate;    /* default 1e-4 */
+  int32_t schedule;        /* 0 constant, 1 cosine (default) */
+  int32_t reserved;
+  uint64_t seed;
+} nqb_tune_config;
+
+/* ste_refine on one factorized latent layer (the pipeline's per-layer group,
+ * pipeline.cpp:128-135): Adam on latent_u (n x r), latent_v (m x r), s1 (n), s2 (m)
+ * against sum_c w_c ||teacher - forward(x)||^2 with the straight-through sign,
+ * x (m x b) and teacher (n x b) as columns, column_weights (b) or NULL.  The four
+ * host buffers are overwritten with the best-loss checkpoint (also on
+ * NQB_E_NON_FINITE_LOSS, like NonFiniteLoss::best_chain); best_loss may be NULL. */
+int nqb_ste_refine_layer_host(nqb_context* ctx, double* latent_u, double* latent_v, double* s1,
+                              double* s2, uint32_t n, uint32_t m, uint32_t r, const double* x,
+                              const double* teacher, uint32_t b, const double* column_weights,
+                              const nqb_tune_config* cfg, double* best_loss);
 
 /* ------------------------------------------------------------------------ */
 /* Linear-algebra building blocks (linalg.hpp:35-51, admm.hpp:30-38, 65-67)  */

@@ -377,6 +377,24 @@ class Checker:
         layer = Layer(n, m, cfg.rank, u, v, s1, s2)
         return layer, err.value, trace[: res.trace_len].copy(), res.as_dict()
 
+    def ste_refine(self, lu, lv, s1, s2, x, teacher, epochs=8, lr=1e-4, batch=4, cosine=True,
+                   seed=0, column_weights=None):
+        """ste_refine (refine.cpp:420-425) on a one-layer chain; returns
+        (latent_u, latent_v, s1, s2, status)."""
+        self._ref_only("ste_refine")
+        lu, lv = _f64(lu).copy(), _f64(lv).copy()
+        s1, s2 = _f64(s1).copy(), _f64(s2).copy()
+        x, t = _f64(x), _f64(teacher)
+        n, r = lu.shape
+        m, b = x.shape
+        w = None if column_weights is None else _f64(column_weights)
+        fn = self.lib.nqref_ste_refine
+        fn.restype = C.c_int
+        st = fn(_ptr(lu), _ptr(lv), _ptr(s1), _ptr(s2), _U32(n), _U32(m), _U32(r), _ptr(x), _ptr(t),
+                _U32(b), None if w is None else _ptr(w), _I32(epochs), _D(lr), _I32(batch),
+                _I32(1 if cosine else 0), _U64(seed))
+        return lu, lv, s1, s2, st
+
     def layer_rel_error(self, L: Layer, w):
         w = _f64(w)
         out = _D()

@@ -24,6 +24,7 @@
 #include "nanoquant/linalg.hpp"
 #include "nanoquant/packed.hpp"
 #include "nanoquant/precondition.hpp"
+#include "nanoquant/refine.hpp"
 #include "nanoquant/rng.hpp"
 #include "nanoquant/storage.hpp"
 #include "nqb.h"
@@ -272,6 +273,44 @@ int nqref_pass_run(void* h, float* const* y, std::uint32_t threads) {
   })
 }
 void nqref_pass_destroy(void* h) { delete static_cast<RefPass*>(h); }
+
+// ---- refine.cpp --------------------------------------------------------------
+// ste_refine (refine.cpp:420-425) on a ToyChain of one FactorizedLatentLayer,
+// the pipeline's per-layer group (pipeline.cpp:128-135); latents and scales are
+// overwritten with the result (the best checkpoint, also on NonFiniteLoss).
+int nqref_ste_refine(double* lu, double* lv, double* s1, double* s2, std::uint32_t n,
+                     std::uint32_t m, std::uint32_t r, const double* x, const double* teacher,
+                     std::uint32_t b, const double* colw, std::int32_t epochs, double lr,
+                     std::int32_t batch, std::int32_t cosine, std::uint64_t seed) {
+  auto put_layer = [&](const ToyChain& c) {
+    const auto& f = std::get<FactorizedLatentLayer>(c.layers[0]);
+    put(f.latent_u, lu);
+    put(f.latent_v, lv);
+    std::memcpy(s1, f.s1.data(), n * sizeof(double));
+    std::memcpy(s2, f.s2.data(), m * sizeof(double));
+  };
+  try {
+    ToyChain chain;
+    chain.layers.push_back(FactorizedLatentLayer{dm(lu, n, r), dm(lv, m, r),
+                                                 std::vector<double>(s1, s1 + n),
+                                                 std::vector<double>(s2, s2 + m)});
+    TuneConfig cfg;
+    cfg.epochs = epochs;
+    cfg.learning_rate = lr;
+    cfg.batch_size = batch;
+    cfg.schedule = cosine ? LrSchedule::kCosine : LrSchedule::kConstant;
+    cfg.seed = seed;
+    if (colw) cfg.column_weights.assign(colw, colw + b);
+    put_layer(ste_refine(chain, dm(x, m, b), dm(teacher, n, b), cfg));
+    return NQB_OK;
+  } catch (const NonFiniteLoss& e) {
+    put_layer(e.best_chain);
+    g_err = e.what();
+    return NQB_E_NON_FINITE_LOSS;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
 
 // ---- linalg.cpp -------------------------------------------------------------
 int nqref_top_singular_pair(const double* mat, std::uint32_t rows, std::uint32_t cols,

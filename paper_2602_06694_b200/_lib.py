@@ -41,6 +41,13 @@ class AdmmResultC(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
 
 
+class TuneConfig(C.Structure):
+    """nqb_tune_config (TuneConfig, refine.hpp:55-64)."""
+
+    _fields_ = [("epochs", I32), ("batch_size", I32), ("learning_rate", C.c_double),
+                ("schedule", I32), ("reserved", I32), ("seed", C.c_uint64)]
+
+
 class PassStep(C.Structure):
     """nqb_pass_step."""
 
@@ -80,6 +87,8 @@ PROTOTYPES = {
     "nqb_gemm_f16_device": (C.c_int, [P, P, P, U32, P]),
     "nqb_reconstruct_dense_host": (C.c_int, [P, P, P]),
     "nqb_admm_config_default": (None, [C.POINTER(AdmmConfig)]),
+    "nqb_ste_refine_layer_host": (C.c_int, [P, P, P, P, P, U32, U32, U32, P, P, U32, P,
+                                            C.POINTER(TuneConfig), PD]),
     "nqb_admm_factorize_host": (C.c_int, [P, P, U32, U32, C.POINTER(AdmmConfig), P, P, P,
                                           C.POINTER(AdmmResultC)]),
     "nqb_admm_factorize_state_host": (C.c_int, [P, P, U32, U32, C.POINTER(AdmmConfig), P, P,

@@ -104,6 +104,11 @@ class NotPositiveDefinite(Error):
     code = 33
 
 
+class NonFiniteLoss(Error):  # refine.hpp:72-77; best_chain is the checkpoint written back
+    kind = KIND_NUMERICAL
+    code = 34
+
+
 class DeviceError(Error):
     """CUDA / allocation / missing-device failures (no reference counterpart)."""
 
@@ -114,7 +119,7 @@ class DeviceError(Error):
 _BY_CODE = {cls.code: cls for cls in (DimensionMismatch, NonFiniteInput, NonBinaryEntry,
                                        CorruptPadding, RankTooLarge, InvalidRank,
                                        NotSymmetric, TargetTooSmall, ParseError, IoError, EmptyStats,
-                                       ZeroMatrix, NotPositiveDefinite)}
+                                       ZeroMatrix, NotPositiveDefinite, NonFiniteLoss)}
 
 
 def _check(status: int, where: str):
@@ -1125,3 +1130,64 @@ def unprecondition_rows(factor, diag, ctx: Context | None = None) -> np.ndarray:
     _check(ctx.lib.nqb_unprecondition_rows_host(ctx.handle, out.ctypes.data, out.shape[0],
                                                 out.shape[1], _ptr(_f64(d))), "unprecondition_rows")
     return out
+
+
+# ---------------------------------------------------------------------------
+# refine.hpp: STE refinement of one factorized latent layer on the device
+#
+# ---------------------------------------------------------------------------
+@dataclass
+class TuneConfig:  # refine.hpp:55-64
+    epochs: int = 8
+    learning_rate: float = 1e-4
+    batch_size: int = 4
+    schedule: str = "cosine"  # or "constant"
+    seed: int = 0
+
+    def c(self):
+        return L.TuneConfig(self.epochs, self.batch_size, self.learning_rate,
+                            1 if self.schedule == "cosine" else 0, 0, self.seed & 0xFFFFFFFFFFFFFFFF)
+
+
+@dataclass
+class FactorizedLatentLayer:  # refine.hpp:28-34
+    latent_u: np.ndarray
+    latent_v: np.ndarray
+    s1: np.ndarray
+    s2: np.ndarray
+
+
+def ste_refine(layer: FactorizedLatentLayer, x, teacher_outputs, config: TuneConfig,
+               column_weights=None, ctx: Context | None = None):
+    """ste_refine (refine.cpp:420-425) on a one-layer chain, on the device: returns
+    (refined FactorizedLatentLayer, best loss).  x is (m, b) and teacher_outputs
+    (n, b), inputs as columns.  Raises NonFiniteLoss (with .best_chain) on
+    divergence, like the reference."""
+    ctx = ctx or context()
+    lu, lv = _mat(layer.latent_u).copy(), _mat(layer.latent_v).copy()
+    s1, s2 = _f64(layer.s1).copy(), _f64(layer.s2).copy()
+    n, r = lu.shape
+    m = lv.shape[0]
+    X, T = _mat(x), _mat(teacher_outputs)
+    if lv.shape[1] != r or s1.size != n or s2.size != m or X.shape[0] != m:
+        raise DimensionMismatch("chain input dim does not match X rows")
+    if T.shape != (n, X.shape[1]):
+        raise DimensionMismatch("teacher outputs do not match chain output shape")
+    w = None
+    if column_weights is not None and len(column_weights):
+        w = _f64(column_weights)
+        if w.size != X.shape[1]:
+            raise DimensionMismatch("column weight count does not match batch")
+    best = C.c_double()
+    cfg = config.c()
+    st = ctx.lib.nqb_ste_refine_layer_host(ctx.handle, _ptr(lu), _ptr(lv), _ptr(s1), _ptr(s2), n, m, r,
+                                           _ptr(X), _ptr(T), X.shape[1],
+                                           None if w is None else _ptr(w), C.byref(cfg), C.byref(best))
+    out = FactorizedLatentLayer(lu, lv, s1, s2)
+    if st == NonFiniteLoss.code:
+        err = NonFiniteLoss("ste_refine: " + L.load().nqb_last_error().decode(errors="replace"),
+                            code=st)
+        err.best_chain = out
+        raise err
+    _check(st, "ste_refine")
+    return out, best.value

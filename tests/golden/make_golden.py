@@ -37,6 +37,20 @@ CASES = {
     "l13s16_q_b0.55": (320, 320, 0.55, 0x13B00000, 400),
     "l13s16_gate_b0.55": (864, 320, 0.55, 0x13B00004, 400),
     "l13s16_down_b0.55": (320, 864, 0.55, 0x13B00006, 400),
+    "l13s16_gate_b0.8": (864, 320, 0.8, 0x13B00004, 400),
+    "l13s16_gate_b1.0": (864, 320, 1.0, 0x13B00004, 400),
+    "l13s16_down_b0.8": (320, 864, 0.8, 0x13B00006, 400),
+    "l13s16_down_b1.0": (320, 864, 1.0, 0x13B00006, 400),
+    # Llama-2-13B shapes scaled 1/8
+    "l13s8_q_b1.0": (640, 640, 1.0, 0x13B80000, 400),
+    "l13s8_q_b0.8": (640, 640, 0.8, 0x13B80000, 400),
+    "l13s8_q_b0.55": (640, 640, 0.55, 0x13B80000, 400),
+    "l13s8_gate_b1.0": (1728, 640, 1.0, 0x13B80004, 400),
+    "l13s8_gate_b0.8": (1728, 640, 0.8, 0x13B80004, 400),
+    "l13s8_gate_b0.55": (1728, 640, 0.55, 0x13B80004, 400),
+    "l13s8_down_b1.0": (640, 1728, 1.0, 0x13B80006, 400),
+    "l13s8_down_b0.8": (640, 1728, 0.8, 0x13B80006, 400),
+    "l13s8_down_b0.55": (640, 1728, 0.55, 0x13B80006, 400),
     "w512_b1.0": (512, 512, 1.0, 0xB1A5E001, 400),
     "w512_b0.55": (512, 512, 0.55, 0xB1A5E001, 400),
     "w1024_b1.0": (1024, 1024, 1.0, 0xB1A5E001, 400),
