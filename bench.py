@@ -499,12 +499,23 @@ def config1_forward(nq, torch, pm, reps=200):
 
 
 def admm_small_gpu(nq, ws_cpu, r):
-    """Our device path on the same 256^2 matrices the CPU baseline factorised."""
+    """Our device path on the same 256^2 matrices the CPU baseline factorised (W from
+    the same Rng seeds): one after another, and `workers` at a time on one GPU (one
+    context per worker, each confined to an equal share of the SMs, sharded.run_local)
+    -- a 256^2 matrix alone is latency-bound on the per-iteration grid barriers."""
+    from paper_2602_06694_b200 import sharded as S
     t0 = time.perf_counter()
     for w in ws_cpu:
         nq.factorize_layer(w, nq.AdmmConfig(rank=r))
     secs = time.perf_counter() - t0
-    return {"matrices_per_s_256": len(ws_cpu) / secs, "seconds": secs, "matrices": len(ws_cpu)}
+    specs = [S.MatrixSpec(f"w{i}", 256, 256, 0x7B000000 + i) for i in range(len(ws_cpu))]
+    out = {"matrices_per_s_256": len(ws_cpu) / secs, "seconds": secs, "matrices": len(ws_cpu)}
+    for workers in (4, 8):
+        t0 = time.perf_counter()
+        S.run_local(specs, list(range(len(specs))), 1.0, workers=workers)
+        sec_w = time.perf_counter() - t0
+        out[f"concurrent_{workers}"] = {"matrices_per_s_256": len(specs) / sec_w, "seconds": sec_w}
+    return out
 
 
 def reference_arm(args, ws, rank):
