@@ -584,6 +584,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     const uint32_t f0 = U * gw / kGroupWarps, f1 = U * (gw + 1) / kGroupWarps;
     const uint32_t p0 = f0 / g.nsec, p1 = f1 ? (f1 - 1) / g.nsec : 0;
     unsigned long long wsum = 0, nch = 0, rsum = 0, ncall = 0, nslab = 0;
+    const unsigned long long l0 = kTrace ? clock64() : 0ull;
     for (uint32_t s0 = 0; s0 < g.nsec;) {
       const uint32_t slot = chunk % kPassSlots;
       const unsigned long long w0 = kTrace ? clock64() : 0ull;
@@ -617,6 +618,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       trp[1 + kPassStamps * cur_step + 16 + gid] = wsum;
       trp[1 + kPassStamps * cur_step + 18 + gid] = (nch << 48) | (ncall << 32) | (nslab << 16);
       trp[1 + kPassStamps * cur_step + 20 + gid] = rsum;
+      trp[1 + kPassStamps * cur_step + 22 + gid] = clock64() - l0;  // the whole chunk loop
     }
   };
 

@@ -77,6 +77,7 @@ def main():
         "s1_slabs": ((raw[:, :, 18] >> 16) & 0xFFFF).astype(float),
         "s2_slabs": ((raw[:, :, 19] >> 16) & 0xFFFF).astype(float),
         "s1_runpair_us": raw[:, :, 20] / 1965.0, "s2_runpair_us": raw[:, :, 21] / 1965.0,
+        "s1_loop_us": raw[:, :, 22] / 1965.0, "s2_loop_us": raw[:, :, 23] / 1965.0,
     }
     for i, kd in enumerate(kinds):
         sel = [k for k in range(K) if k % 4 == i and k >= 4]
