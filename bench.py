@@ -422,6 +422,35 @@ def prefill_leg(nq, ctx, torch, stream, tpk, b=2048, reps=10):
     return out, arrays
 
 
+def dgemm_ours(nq, torch, ctx, r=2032, n=4096):
+    """Our fp64 DMMA GEMM (dgemm.cu, nqb_dgemm_device) at the ADMM factor-solve
+    shapes of 4096^2 r = 2032 (admm.cpp:62-78): the Gram fixed^T fixed (r x r, K = n)
+    and the right-hand side fixed^T target^T (r x n, K = n); TF/s of 2MNK."""
+    import ctypes as C
+    lib = ctx.lib
+    out = {}
+    stream = torch.cuda.Stream()
+    for name, (M, N, K, ta, tb) in {"gram": (r, r, n, True, False),
+                                    "rhs": (r, n, n, True, True)}.items():
+        a = torch.randn(K, M, device="cuda", dtype=torch.float64)  # op(A) = A^T (M x K)
+        b = torch.randn(N, K, device="cuda", dtype=torch.float64) if tb else \
+            torch.randn(K, N, device="cuda", dtype=torch.float64)
+        c = torch.empty(M, N, device="cuda", dtype=torch.float64)
+        ldb = K if tb else N
+
+        def run():
+            ctx.bind_torch_stream()
+            st = lib.nqb_dgemm_device(ctx.handle, int(ta), int(tb), M, N, K, C.c_double(1.0),
+                                      C.c_void_p(a.data_ptr()), M, C.c_void_p(b.data_ptr()), ldb,
+                                      C.c_double(0.0), C.c_void_p(c.data_ptr()), N)
+            assert st == 0
+        sec = time_launches(torch, stream, run, 5, 2)
+        out[name] = {"M": M, "N": N, "K": K, "ms": sec * 1e3, "tflops": 2.0 * M * N * K / sec / 1e12}
+    torch.cuda.synchronize()
+    ctx.set_stream(None)  # the context must not keep this local stream
+    return out
+
+
 def dgemm_peak(torch):
     """Measured FP64 tensor (DMMA) peak on this GPU: cuBLAS DGEMM 8192^3 (the
     denominator of the ADMM iteration-phase roofline; MEASURED_PEAKS.json has no
@@ -697,6 +726,10 @@ def main():
         admm = admm_leg(nq, torch, ws, rank, local, hbm, fp64_peak)
         if rank == 0:
             admm["fp64_dgemm_peak_tflops"] = fp64_peak
+            ours = dgemm_ours(nq, torch, ctx)
+            for v in ours.values():
+                v["frac_of_cublas_dgemm_peak"] = v["tflops"] / fp64_peak
+            admm["dmma_gemm"] = ours
             extra["admm_init"] = admm
 
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
