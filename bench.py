@@ -641,6 +641,8 @@ def main():
     #      pinned host x -> device, one pass launch, device -> pinned host y, synchronous ----
     hx = [torch.from_numpy(x).pin_memory().numpy() for _, _, x in steps]
     hy = [torch.empty(l[1], dtype=torch.float16).pin_memory().numpy() for _, ls, _ in steps for l in ls]
+    for a in hx + hy:  # explicit registration: no per-call pointer probing
+        ctx.register_host(a)
     h2d = sum(x.nbytes for x in hx)
     d2h = sum(y.nbytes for y in hy)
     dpass.run_host(hx, hy)
@@ -655,7 +657,8 @@ def main():
         e2e_secs = float(t.item())
     e2e = {"value": ws * step_bytes * e2e_steps / e2e_secs / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "api": "nqb_pass_run_host (C ABI, pinned host x/y, one decode-pass launch, synchronous)",
+           "api": "nqb_pass_run_host (C ABI, registered pinned host x/y, one decode-pass launch, "
+                  "synchronous)",
            "steps": e2e_steps}
 
     extra = {}
@@ -666,6 +669,8 @@ def main():
         hxf = [torch.randn(l.m, dtype=torch.float32).pin_memory().numpy() for l in all_layers]
         hyf = [torch.empty(l.n, dtype=torch.float32).pin_memory().numpy() for l in all_layers]
         ctx.set_stream(None)
+        for a in hxf + hyf:
+            ctx.register_host(a)
         for l, x, y in zip(all_layers, hxf, hyf):
             l.gemv_f32(x, out=y)
         t0 = time.perf_counter()
@@ -675,7 +680,8 @@ def main():
         dt = (time.perf_counter() - t0) / 2
         extra["e2e_dropin_per_layer"] = {
             "value": step_bytes / dt / 1e9, "unit": UNIT,
-            "api": "nqb_gemv_f32_host per layer (gemv_packed_f32 drop-in, pinned fp32 host x/y)",
+            "api": "nqb_gemv_f32_host per layer (gemv_packed_f32 drop-in, registered pinned fp32 "
+                   "host x/y)",
             "h2d_bytes_per_step": sum(4 * l.m for l in all_layers),
             "d2h_bytes_per_step": sum(4 * l.n for l in all_layers)}
         extra["per_call_graph"] = per_call_graph_gbs(nq, ctx, torch, stream, pass_steps, step_bytes)

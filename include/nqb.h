@@ -83,6 +83,14 @@ int nqb_create(int device, nqb_context** out);
 int nqb_destroy(nqb_context* ctx);
 /* Use an external cudaStream_t (NULL = the context's own stream). */
 int nqb_set_stream(nqb_context* ctx, void* cuda_stream);
+/* Registers a host range for the _host entry points: page-locks and maps it if it
+ * is not already page-locked, and remembers its device alias, so those calls move
+ * it by DMA or zero-copy without probing the pointer each call (outputs of
+ * nqb_gemv_f32_host are written through the alias; nqb_pass_run_host moves
+ * registered buffers with one copy kernel per direction).  Unregister before
+ * freeing the memory. */
+int nqb_host_register(nqb_context* ctx, void* ptr, size_t bytes);
+int nqb_host_unregister(nqb_context* ctx, void* ptr);
 void* nqb_get_stream(nqb_context* ctx);
 int nqb_synchronize(nqb_context* ctx);
 /* Limit the persistent ADMM kernels of this context to `sms` SMs (<= 0: all),

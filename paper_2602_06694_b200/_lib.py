@@ -63,6 +63,8 @@ PROTOTYPES = {
     "nqb_create": (C.c_int, [C.c_int, PP]),
     "nqb_destroy": (C.c_int, [P]),
     "nqb_set_stream": (C.c_int, [P, P]),
+    "nqb_host_register": (C.c_int, [P, P, C.c_size_t]),
+    "nqb_host_unregister": (C.c_int, [P, P]),
     "nqb_get_stream": (P, [P]),
     "nqb_synchronize": (C.c_int, [P]),
     "nqb_kernel_launches": (U64, [P]),

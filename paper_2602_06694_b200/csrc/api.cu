@@ -66,6 +66,22 @@ void* ctx_pinned(nqb_context* ctx, int slot, size_t bytes) {
   return ctx->pinned[slot];
 }
 
+void* host_alias(nqb_context* ctx, const void* p, size_t bytes) {
+  const uintptr_t a = (uintptr_t)p;
+  auto it = ctx->host_ranges.upper_bound(a);
+  if (it != ctx->host_ranges.begin()) {
+    --it;
+    if (a >= it->first && a + bytes <= it->first + it->second.bytes)
+      return it->second.dev + (a - it->first);
+  }
+  cudaPointerAttributes at{};
+  void* dev = nullptr;
+  if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost)
+    dev = at.devicePointer;
+  cudaGetLastError();
+  return dev;
+}
+
 uint16_t host_double_to_half(double x) {
   const __half h = __float2half_rn((float)x);
   uint16_t bits;
@@ -192,12 +208,42 @@ int nqb_destroy(nqb_context* ctx) {
   if (ctx->barrier) cudaFree(ctx->barrier);
   for (void* p : ctx->pinned)
     if (p) cudaFreeHost(p);
+  for (auto& kv : ctx->host_ranges)
+    if (kv.second.ours) cudaHostUnregister((void*)kv.first);
   if (ctx->dec_state) cudaFree(ctx->dec_state);
   for (void* p : ctx->dec_retired) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
+  API_END
+}
+
+int nqb_host_register(nqb_context* ctx, void* ptr, size_t bytes) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_REQUIRE(ptr != nullptr && bytes > 0, NQB_E_VALIDATION, "empty host range");
+  bool ours = false;
+  cudaPointerAttributes at{};
+  if (!(cudaPointerGetAttributes(&at, ptr) == cudaSuccess && at.type == cudaMemoryTypeHost)) {
+    cudaGetLastError();
+    NQB_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterMapped));
+    ours = true;
+    NQB_CUDA(cudaPointerGetAttributes(&at, ptr));
+  }
+  NQB_REQUIRE(at.devicePointer != nullptr, NQB_E_VALIDATION, "host range has no device mapping");
+  ctx->host_ranges[(uintptr_t)ptr] = nqb_context::HostRange{bytes, (char*)at.devicePointer, ours};
+  API_END
+}
+
+int nqb_host_unregister(nqb_context* ctx, void* ptr) {
+  API_BEGIN
+  check_ctx(ctx);
+  auto it = ctx->host_ranges.find((uintptr_t)ptr);
+  NQB_REQUIRE(it != ctx->host_ranges.end(), NQB_E_VALIDATION, "host range was not registered");
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (it->second.ours) NQB_CUDA(cudaHostUnregister(ptr));
+  ctx->host_ranges.erase(it);
   API_END
 }
 
@@ -657,13 +703,9 @@ int nqb_gemv_f32_host(nqb_context* ctx, const nqb_layer* L, const float* x, floa
   // A pinned (page-locked, mapped) y is written by the kernel directly over the
   // host link: no separate device-to-host copy.  Pageable y goes through dy.
   // Checked every call (a cached answer could outlive the allocation).
-  float* y_dev = nullptr;
-  {
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, y) == cudaSuccess && at.type == cudaMemoryTypeHost)
-      y_dev = (float*)at.devicePointer;
-    cudaGetLastError();
-  }
+  // Registered ranges (nqb_host_register) are a map lookup; anything else is
+  // probed once per call (a cached answer could outlive the allocation).
+  float* y_dev = (float*)host_alias(ctx, y, 4 * (size_t)L->n);
   NQB_CUDA(cudaMemcpyAsync(dx, x, 4 * (size_t)L->m, cudaMemcpyHostToDevice, ctx->stream));
   if (y_dev) {
     decode_gemv_f32(ctx, L, dx, y_dev);
@@ -875,12 +917,7 @@ int nqb_pass_run_host(nqb_context* ctx, const nqb_pass* pass, const void* const*
   // their mapped device addresses; pageable ones get one cudaMemcpyAsync each.
   std::vector<CopyJob> jobs;
   auto add = [&](void* dst, const void* src, size_t bytes, bool host_is_dst) {
-    const void* host = host_is_dst ? dst : src;
-    cudaPointerAttributes at{};
-    void* mapped = nullptr;
-    if (cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost)
-      mapped = at.devicePointer;
-    cudaGetLastError();
+    void* mapped = host_alias(ctx, host_is_dst ? dst : src, bytes);
     if (mapped) {
       jobs.push_back(host_is_dst ? CopyJob{mapped, src, bytes} : CopyJob{dst, mapped, bytes});
     } else {

@@ -7,6 +7,7 @@
 
 #include <cstdio>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "nqb.h"
@@ -79,6 +80,14 @@ struct nqb_context {
   bool dec_attr_set = false;
   bool pdl = true;  // launch decode kernels with Programmatic Dependent Launch
   void* dec_trace = nullptr;  // diagnostics (nqb_debug_decode_trace)
+  // host ranges registered with nqb_host_register: base -> (bytes, device alias,
+  // whether the library page-locked it)
+  struct HostRange {
+    size_t bytes;
+    char* dev;
+    bool ours;
+  };
+  std::map<uintptr_t, HostRange> host_ranges;
   // page-locked host staging (ctx_pinned): job lists of nqb_pass_run_host
   void* pinned[2] = {nullptr, nullptr};
   size_t pinned_bytes[2] = {0, 0};
@@ -123,6 +132,9 @@ struct CopyJob {
   size_t bytes;
 };
 void copy_jobs(nqb_context* ctx, const std::vector<CopyJob>& jobs, int slot);
+// Device alias of a page-locked host address: the registry (nqb_host_register)
+// first, else one cudaPointerGetAttributes probe; nullptr for pageable memory.
+void* host_alias(nqb_context* ctx, const void* p, size_t bytes);
 
 inline uint32_t ceil_div(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
 inline uint32_t round_up(uint32_t a, uint32_t b) { return (a + b - 1) / b * b; }

@@ -146,6 +146,16 @@ class Context:
         self.device = device
         self._stream = 0
 
+    def register_host(self, arr) -> None:
+        """nqb_host_register: page-locks (if needed) and maps a host numpy array for the
+        _host entry points; keep the array alive until unregister_host."""
+        _check(self.lib.nqb_host_register(self.handle, C.c_void_p(arr.ctypes.data), arr.nbytes),
+               "nqb_host_register")
+
+    def unregister_host(self, arr) -> None:
+        _check(self.lib.nqb_host_unregister(self.handle, C.c_void_p(arr.ctypes.data)),
+               "nqb_host_unregister")
+
     def close(self):
         if self.handle:
             self.lib.nqb_destroy(self.handle)

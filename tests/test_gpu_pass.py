@@ -230,3 +230,33 @@ def test_pass_rejects_bad_steps(nq):
         nq.DecodePass([(a, x, [torch.empty(63, device="cuda", dtype=torch.float16)])])
     with pytest.raises(nq.Error):  # output aliases its own input
         nq.DecodePass([(a, x, [x])])
+
+
+def test_pass_run_host_registered_and_pageable_agree(nq, chk):
+    """nqb_pass_run_host with registered (nqb_host_register), plain pinned and
+    pageable host buffers gives the device pass's outputs bit for bit."""
+    import torch
+    rng = np.random.default_rng(33)
+    steps, host, keep = block_model(nq, rng, (1024, 2752, 400, 600), torch.float16, False)
+    p = nq.DecodePass(steps)
+    p.launch()
+    torch.cuda.synchronize()
+    want = [y.cpu().numpy().copy() for _, _, ys in steps for y in ys]
+    ctx = p.ctx
+    for mode in ("pageable", "pinned", "registered"):
+        if mode == "pageable":
+            hx = [x.cpu().numpy().copy() for _, x, _ in steps]
+            hy = [np.empty_like(w) for w in want]
+        else:
+            hx = [x.cpu().pin_memory().numpy() for _, x, _ in steps]
+            hy = [torch.empty(w.shape, dtype=torch.float16).pin_memory().numpy() for w in want]
+        if mode == "registered":
+            for a in hx + hy:
+                ctx.register_host(a)
+        p.run_host(hx, hy)
+        for a, b in zip(hy, want):
+            assert np.array_equal(a.view(np.uint16), b.view(np.uint16)), mode
+        if mode == "registered":
+            for a in hx + hy:
+                ctx.unregister_host(a)
+    p.free()
