@@ -13,6 +13,8 @@ import os
 import sys
 import time
 
+import numpy as np
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
@@ -23,6 +25,8 @@ def main():
     ap.add_argument("--workers", type=int, default=1)
     ap.add_argument("--shape", default=None, help="n,m: uniform synthetic matrices instead of Llama-2-7B")
     ap.add_argument("--count", type=int, default=8)
+    ap.add_argument("--repro", action="store_true",
+                    help="re-run the first matrix and check the packed factors are bitwise equal")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -66,6 +70,13 @@ def main():
                                           "converged": p.converged, "rel_error": p.rel_error}
                                          for i, p in sorted(rep.matrices.items())]}),
               flush=True)
+        if args.repro:  # GPU-vs-GPU bitwise reproducibility at full size (SURVEY §8(d) protocol)
+            i0 = min(rep.matrices)
+            again = S.device_factorize(specs[i0], i0, args.bpw)
+            first = rep.matrices[i0]
+            same = all(np.array_equal(getattr(first, f), getattr(again, f)) for f in ("u", "v", "s1", "s2"))
+            print(json.dumps({"repro_matrix": specs[i0].name, "bitwise_equal": bool(same),
+                              "rel_error": [first.rel_error, again.rel_error]}), flush=True)
     if ws > 1:
         dist.destroy_process_group()
 
