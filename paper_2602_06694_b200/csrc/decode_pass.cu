@@ -220,13 +220,13 @@ __device__ __forceinline__ void share_of(uint32_t m, uint32_t b, uint32_t G, uin
   } while (0)
 
 // Named barriers of the two consumer groups (ids 1, 2) and of all consumers (3).
-__device__ __forceinline__ void group_sync(int gid) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(1 + gid), "n"(kGroupThreads) : "memory");
+__device__ __forceinline__ void group_sync(int gid, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(1 + gid), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void all_consumers_sync() {
   asm volatile("bar.sync 3, %0;\n" ::"n"(kConsumerThreads) : "memory");
 }
-template <bool kTrace>
+template <bool kTrace, int kW1>
 __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_constant__ PassParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full1 = (uint64_t*)smem;  // stage-1 ring
@@ -249,8 +249,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   int* red1 = (int*)(smem + pass_head_bytes());       // stage-1 row sums
   int* red2 = (int*)((uint8_t*)red1 + p.red1_bytes);  // stage-2 row sums
   uint8_t* bslots1 = (uint8_t*)red2 + p.red2_bytes;   // header | B fragments of x
-  uint8_t* bslots2 = bslots1 + kBSlots * p.bslot1_bytes;  // header | B fragments of t | s1 slice
-  uint8_t* ring1 = bslots2 + kBSlots * p.bslot2_bytes;
+  constexpr uint32_t NB = kBSlots;
+  uint8_t* bslots2 = bslots1 + NB * p.bslot1_bytes;  // header | B fragments of t | s1 slice
+  uint8_t* ring1 = bslots2 + NB * p.bslot2_bytes;
   uint8_t* ring2 = ring1 + p.ring1_bytes;
 
   const int tid = threadIdx.x, lane = tid & 31;
@@ -268,9 +269,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   if (tid == 0) {
     for (int s = 0; s < kPassSlots; ++s) {
       tc::mbar_init(&full1[s], 1);
-      tc::mbar_init(&empty1[s], kGroupWarps);
+      tc::mbar_init(&empty1[s], kW1);
       tc::mbar_init(&full2[s], 1);
-      tc::mbar_init(&empty2[s], kGroupWarps);
+      tc::mbar_init(&empty2[s], kConsumerWarps - kW1);
     }
     for (int s = 0; s < kDescSlots; ++s) {
       tc::mbar_init(&dfull[s], 1);
@@ -379,8 +380,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       bool pre_done = p.has_pre == 0;
       int32_t ywaited = -1;
       for (uint32_t j = 0; j < K; ++j) {
-        const uint32_t slot = j % kBSlots;
-        if (j >= (uint32_t)kBSlots) mbar_wait_wd(&bempty1[slot], ((j / kBSlots) - 1) & 1, sus);
+        const uint32_t slot = j % NB;
+        if (j >= NB) mbar_wait_wd(&bempty1[slot], ((j / NB) - 1) & 1, sus);
         wait_desc(j);
         const StepDesc& D = desc_of(j);
         const Cta& C = cta_of(j);
@@ -451,8 +452,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       const int pw = role - 3;
       int32_t ywaited = -1;
       for (uint32_t k = 0; k < K; ++k) {
-        const uint32_t slot = k % kBSlots;
-        if (k >= (uint32_t)kBSlots) mbar_wait_wd(&bempty2[slot], ((k / kBSlots) - 1) & 1, sus);
+        const uint32_t slot = k % NB;
+        if (k >= NB) mbar_wait_wd(&bempty2[slot], ((k / NB) - 1) & 1, sus);
         if (kTrace && lane == 0 && pw == 0) PSTAMP(k, 12);
         wait_desc(k);
         const StepDesc& D = desc_of(k);
@@ -545,10 +546,15 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   }
 
   // ================================================================ consumers
-  const int gid = warp / kGroupWarps;  // 0: stage-1 group, 1: stage-2 group
-  const int gt = tid - gid * kGroupThreads;
+  // the consumer warps split into a stage-1 group (warps1) and a stage-2 group,
+  // sized by the host in proportion to the two stages' bytes (pass_build)
+  constexpr int W1 = kW1;
+  const int gid = warp < W1 ? 0 : 1;  // 0: stage-1 group, 1: stage-2 group
+  const int GW = gid ? kConsumerWarps - W1 : W1;  // warps in this group
+  const uint32_t GT = 32u * GW;                   // threads in this group
+  const int gt = tid - gid * 32 * W1;
   int* const red = gid ? red2 : red1;
-  for (uint32_t i = gt; i < (gid ? p.red2_bytes : p.red1_bytes) / 16; i += kGroupThreads)
+  for (uint32_t i = gt; i < (gid ? p.red2_bytes : p.red1_bytes) / 16; i += GT)
     ((int4*)red)[i] = make_int4(0, 0, 0, 0);
   // ---- |x| prepass: this CTA's share of every independent input, one grid barrier
   if (p.has_pre) {
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     if (tid == 0) arrive_ctr(xinit);
   }
   uint32_t chunk = 0;
-  const int gw = warp - gid * kGroupWarps;
+  const int gw = warp - gid * W1;
   uint64_t* const fullr = gid ? full2 : full1;
   uint64_t* const emptyr = gid ? empty2 : empty1;
   const ChunkRec* const recs = gid ? recs2 : recs1;
@@ -581,7 +587,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   auto mma_stage = [&](const StageGeo& g, const uint8_t* bf) {
     if (!g.nsec) return;
     const uint32_t npair = (g.rtn + 1) / 2, U = npair * g.nsec;
-    const uint32_t f0 = U * gw / kGroupWarps, f1 = U * (gw + 1) / kGroupWarps;
+    const uint32_t f0 = U * gw / GW, f1 = U * (gw + 1) / GW;
     const uint32_t p0 = f0 / g.nsec, p1 = f1 ? (f1 - 1) / g.nsec : 0;
     unsigned long long wsum = 0, nch = 0, rsum = 0, ncall = 0, nslab = 0;
     const unsigned long long l0 = kTrace ? clock64() : 0ull;
@@ -628,8 +634,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     wait_desc(k);
     const StepDesc& D = desc_of(k);
     const Cta& C = cta_of(k);
-    const uint32_t slot = k % kBSlots;
-    mbar_wait_wd(gid ? &bfull2[slot] : &bfull1[slot], (k / kBSlots) & 1, sus);
+    const uint32_t slot = k % NB;
+    mbar_wait_wd(gid ? &bfull2[slot] : &bfull1[slot], (k / NB) & 1, sus);
     const uint8_t* bs = gid ? bslots2 + slot * p.bslot2_bytes : bslots1 + slot * p.bslot1_bytes;
     if (kTrace && gt == 0) {
       PSTAMP(k, gid ? 2 : 0);
@@ -639,13 +645,13 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     const long long A = ((const long long*)bs)[0] + ((const long long*)bs)[1];
     cur_step = k;
     mma_stage(g, bs + kBSlotHead);
-    group_sync(gid);
+    group_sync(gid, GT);
     if (kTrace && gt == 0) PSTAMP(k, gid ? 10 : 8);
     if (g.nsec && !(p.debug & 8u)) {
       const Seg& S = D.seg[gid ? C.s2_seg : C.s1_seg];
       if (!gid) {  // stage-1 publish: t rows (exact int64 reds)
         long long* Tseg = arena + D.t_off + S.t_off + (size_t)C.s1_rt0 * 16;
-        for (uint32_t i = gt; i < (uint32_t)C.s1_rtn * 16; i += kGroupThreads) {
+        for (uint32_t i = gt; i < (uint32_t)C.s1_rtn * 16; i += GT) {
           const long long v = 2 * row_value(red + i * kRedStride) - A;
           int4* rr = (int4*)(red + i * kRedStride);
           rr[0] = make_int4(0, 0, 0, 0);
@@ -661,7 +667,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         const __half* sc1 = (const __half*)(bs + p.bs2_s1_off);
         void* Y = D.y[C.s2_seg];
         uint32_t ymb = 0;
-        for (uint32_t i = gt; i < (uint32_t)C.s2_rtn * 16; i += kGroupThreads) {
+        for (uint32_t i = gt; i < (uint32_t)C.s2_rtn * 16; i += GT) {
           const uint32_t row = C.s2_rt0 * 16 + i;
           int4* rr = (int4*)(red + i * kRedStride);
           if (row < S.n) {
@@ -691,7 +697,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         }
       }
     }
-    group_sync(gid);  // reds / outputs happen-before the sequencer's release
+    group_sync(gid, GT);  // reds / outputs happen-before the sequencer's release
     if (gt == 0) {
       if (kTrace) PSTAMP(k, gid ? 3 : 1);
       if (gid) {
@@ -732,7 +738,7 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
   uint32_t bf1 = 0, bf2 = 0, s1bytes = 16;
   double bits1 = 0, bits2 = 0;  // stage-1 / stage-2 stream bytes (ring split)
   uint32_t rt1 = 1, rt2 = 1;    // most row tiles of one CTA in stage 1 / stage 2
-  uint64_t arena = 0, stream_bytes = 0;
+  uint64_t arena = 0, stream_bytes = 0, max_s2_cta_bytes = 0;
   double algo = 0;
   bool has_pre = false;
   for (uint32_t k = 0; k < K; ++k) {
@@ -771,6 +777,15 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       const Slab last = slab_of(g->m, C.s1_sl0 + C.s1_sln - 1);
       const uint32_t nk1 = last.k0 + 32 * last.nq - slab_of(g->m, C.s1_sl0).k0;
       bf1 = std::max(bf1, kBytesPerK * nk1);
+    }
+    for (uint32_t c = 0; c < g->grid; ++c) {
+      const Cta& C = g->ctas[c];
+      if (C.s2_rtn) {
+        uint64_t b2 = 0;
+        const uint32_t r2 = g->seg[C.s2_seg].r;
+        for (uint32_t q = 0, ns = nslabs(r2); q < ns; ++q) b2 += (uint64_t)C.s2_rtn * unit_bytes(slab_of(r2, q).nq);
+        max_s2_cta_bytes = std::max<uint64_t>(max_s2_cta_bytes, b2);
+      }
     }
     for (uint32_t c = 0; c < g->grid; ++c) {
       s1bytes = std::max<uint32_t>(s1bytes, 32u * g->ctas[c].s2_rtn);
@@ -825,7 +840,10 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
   const uint32_t bslot2_b = (bs2_s1_off + s1bytes + 127) / 128 * 128;
   const uint32_t head = pass_head_bytes();
   const uint32_t red1_b = rt1 * 16 * kRedStride * 4, red2_b = rt2 * 16 * kRedStride * 4;
-  const uint32_t fixed = head + red1_b + red2_b + kBSlots * (bslot1_b + bslot2_b);
+  // two quantised-input slots per stage (three measured no better on 7B:
+  // 884 vs 860-905 GB/s across runs, and cost 33 KB of ring at 70B)
+  const uint32_t nb = kBSlots;
+  const uint32_t fixed = head + red1_b + red2_b + nb * (bslot1_b + bslot2_b);
   NQB_REQUIRE(fixed + 72u * 1024u <= 227u * 1024u, NQB_E_DIMENSION_MISMATCH,
               "decode pass: staging buffers leave no room for the weight rings");
   const uint32_t rings = (227u * 1024u - fixed) / 256 * 256;
@@ -881,6 +899,16 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     pp.bslot1_bytes = bslot1_b;
     pp.bslot2_bytes = bslot2_b;
     pp.bs2_s1_off = bs2_s1_off;
+    // Consumer warps per stage group.  Measured (tools/gpu_pass_ab.sh): an even
+    // 6 + 6 split is best when every step is small (7B: 886 vs 841 GB/s for 4 + 8),
+    // while a pass whose largest step puts > 96 KB of stage-2 bits on each CTA
+    // (70B gate/up: 169 KB) is bound by the stage-2 group, and 4 + 8 gives
+    // 1495 vs 1234 GB/s.
+    {
+      const uint32_t w1 = max_s2_cta_bytes > 96u * 1024u ? 4u : 6u;
+      const uint32_t ew = env_u32p("NQB_PASS_WARPS1", 0);
+      pp.warps1 = ew == 4 || ew == 6 ? ew : w1;  // the kernel is instantiated for 4 and 6
+    }
     pp.ring1_bytes = ring1;
     pp.ring2_bytes = ring2;
     const uint32_t cap_kb = env_u32p("NQB_PASS_CHUNK_KB", 0);
@@ -902,7 +930,7 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       std::fprintf(stderr,
                    "nqb pass: K=%u G=%u smem=%u head=%u red=%u+%u bslots=%ux(%u+%u) "
                    "rings=%u+%u chunk caps=%u/%u\n",
-                   K, G, P->smem_bytes, head, red1_b, red2_b, kBSlots, bslot1_b, bslot2_b, ring1,
+                   K, G, P->smem_bytes, head, red1_b, red2_b, nb, bslot1_b, bslot2_b, ring1,
                    ring2, pp.chunk1_cap, pp.chunk2_cap);
     for (uint32_t k = 0; k < K; ++k) {
       const uint32_t esz = steps[k].f32 ? 4 : 2;
@@ -915,11 +943,12 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     }
     P->stream_bytes = stream_bytes;
     P->algo_bytes = (uint64_t)algo;
-    for (auto fn : {k_decode_pass<false>, k_decode_pass<true>})
+    for (auto fn : {k_decode_pass<false, 6>, k_decode_pass<true, 6>, k_decode_pass<false, 4>,
+                    k_decode_pass<true, 4>})
       NQB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)P->smem_bytes));
     int per_sm = 0;
-    NQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_pass<false>,
+    NQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_pass<false, 6>,
                                                            kPassThreads, P->smem_bytes));
     NQB_REQUIRE(per_sm >= 1, NQB_E_INTERNAL, "decode pass kernel does not fit an SM");
   } catch (...) {
@@ -945,8 +974,9 @@ void pass_launch(nqb_context* ctx, const nqb_pass* P, unsigned long long* trace)
   attr[0].val.cooperative = env_u32p("NQB_PASS_COOP", 1) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (trace) NQB_CUDA(cudaLaunchKernelEx(&cfg, k_decode_pass<true>, pp));
-  else NQB_CUDA(cudaLaunchKernelEx(&cfg, k_decode_pass<false>, pp));
+  const bool w4 = pp.warps1 == 4;
+  if (trace) NQB_CUDA(cudaLaunchKernelEx(&cfg, w4 ? k_decode_pass<true, 4> : k_decode_pass<true, 6>, pp));
+  else NQB_CUDA(cudaLaunchKernelEx(&cfg, w4 ? k_decode_pass<false, 4> : k_decode_pass<false, 6>, pp));
   NQB_LAUNCHED(ctx);
 }
 

@@ -89,14 +89,15 @@ struct PassParams {
   uint32_t bslot1_bytes, bslot2_bytes;   // quantised-input slots: header | B fragments (| s1)
   uint32_t red1_bytes, red2_bytes;       // per-limb row sums (row tiles of the largest stage)
   uint32_t bs2_s1_off;        // s1 slice offset in a stage-2 slot (after the t fragments)
+  uint32_t warps1;            // consumer warps of the stage-1 group (4 or 6; the rest run stage 2)
   uint32_t has_pre;
   uint32_t debug;  // NQB_PASS_DEBUG bits (experiments only): 1 skip MMA, 2 skip quantise, 4 suspend
                    // waits, 8 skip publish/outputs, 32 no weight copies
   unsigned long long* trace;  // diagnostics: G x (kPassStamps K + 2) %globaltimer stamps
 };
 
-constexpr int kGroupWarps = 6;                 // consumer warps per stage group
-constexpr int kGroupThreads = 32 * kGroupWarps;
+// the kConsumerWarps consumer warps form a stage-1 group (PassParams::warps1) and a
+// stage-2 group
 constexpr uint32_t kPassBars = 4 * kPassSlots + 2 * kDescSlots + 4 * kBSlots + 2 * kDoneRing;
 // head: mbarriers | misc | descriptor slots | group partials | max|x| ring |
 // chunk records (2 rings)
