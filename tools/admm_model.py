@@ -21,6 +21,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--blocks", type=int, default=32)
+    ap.add_argument("--first-block", type=int, default=0, help="run blocks first .. first+blocks-1")
     ap.add_argument("--bpw", type=float, default=1.0)
     ap.add_argument("--workers", type=int, default=1)
     ap.add_argument("--shape", default=None, help="n,m: uniform synthetic matrices instead of Llama-2-7B")
@@ -42,7 +43,7 @@ def main():
         n, m = map(int, args.shape.split(","))
         specs = [S.MatrixSpec(f"w{i}", n, m, 0xA000 + i) for i in range(args.count)]
     else:
-        specs = S.llama2_7b_specs(args.blocks)
+        specs = S.llama2_7b_specs(args.first_block + args.blocks)[7 * args.first_block:]
     if ws > 1:
         dist.barrier()
     t0 = time.perf_counter()
