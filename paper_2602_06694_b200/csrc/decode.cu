@@ -312,6 +312,7 @@ void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32
                 void* const* d_ys, int y_f32) {
   NQB_REQUIRE(g->device == ctx->device, NQB_E_VALIDATION, "decode group lives on another device");
   NQB_REQUIRE(d_x != nullptr, NQB_E_VALIDATION, "null input");
+  NQB_REQUIRE(!g->pass_only, NQB_E_VALIDATION, "a pass-only decode plan cannot run per call");
   dec_state_reserve(ctx, g->R1);
   Params p{};
   p.bits = g->bits;

@@ -160,6 +160,8 @@ struct nqb_group {
   uint32_t buf_bytes = 0, slot_bytes = 0, nbar = 0, bfrag_bytes = 0, smem_bytes = 0;
   uint64_t stream_bytes = 0;
   bool big = false;                    // long per-CTA streams: pipelined MMA instance
+  bool pass_only = false;              // planned for k_decode_pass only (pass_build)
+  const nqb_layer* layers[nqb::dec::kMaxSeg] = {nullptr};  // the planned layers (re-planning)
   uint8_t* bits = nullptr;             // device, stream_bytes
   nqb::dec::Cta* ctas = nullptr;       // host copy of the CTA table (grid entries)
   nqb::dec::Seg seg[nqb::dec::kMaxSeg];
@@ -168,7 +170,11 @@ struct nqb_group {
 
 namespace nqb {
 // decode_plan.cu
-nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_t count);
+// grid_cap / max_rt: 0 = the context's SMs / kMaxRt.  pass_only: a plan for the
+// decode-pass kernel only: row-tile blocks above kMaxRt and the pair-major
+// stream layout (k_relayout); group_gemv refuses it.
+nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_t count,
+                       uint32_t grid_cap = 0, uint32_t max_rt = 0, bool pass_only = false);
 void group_free(nqb_group* g);
 // decode.cu
 void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32,

@@ -87,21 +87,78 @@ __device__ __forceinline__ StageGeo stage2_geo(const StepDesc& D, const Cta& C) 
   return g;
 }
 
-__device__ __forceinline__ uint32_t sec_width(const StageGeo& g, uint32_t s) {
-  return 32u * slab_of(g.K, g.slab0 + s).nq;
+// Bytes of one row tile over the stage's first i slabs (U_i of the pair-major
+// layout, k_relayout): the full 256-wide slabs come first, then <= 2 tails.
+__device__ __forceinline__ uint32_t cum_bytes(const StageGeo& g, uint32_t i) {
+  uint32_t F, rem;
+  slab_split(g.K, F, rem);
+  const uint32_t nf = F > g.slab0 ? min(F - g.slab0, i) : 0u;
+  uint32_t bytes = 512u * nf;
+  for (uint32_t s = nf; s < i; ++s) bytes += unit_bytes(slab_of(g.K, g.slab0 + s).nq);
+  return bytes;
 }
 
-// Sections [s0, *s1) of a chunk (at least one, at most `cap` bytes unless one
-// section alone is larger); returns the chunk's section bytes.
-__device__ __forceinline__ uint32_t chunk_span(const StageGeo& g, uint32_t s0, uint32_t cap,
-                                               uint32_t* s1) {
-  uint32_t s = s0, bytes = 0;
-  do {
-    bytes += 2u * g.rtn * sec_width(g, s);
-    ++s;
-  } while (s < g.nsec && bytes + 2u * g.rtn * sec_width(g, s) <= cap);
-  *s1 = s;
-  return bytes;
+// Work items of a stage: (row-tile pair, run of <= S slabs), pair-major; item i
+// is ring chunk (stage chunk base + i) and goes to consumer warp (chunk % GW).
+struct Item {
+  uint32_t pr, a, b, nt;
+};
+__device__ __forceinline__ Item item_of(const StageGeo& g, uint32_t S, uint32_t i) {
+  const uint32_t ipp = (g.nsec + S - 1) / S;
+  Item it;
+  it.pr = i / ipp;
+  it.a = (i % ipp) * S;
+  it.b = min(g.nsec, it.a + S);
+  it.nt = 2 * it.pr + 1 < g.rtn ? 2u : 1u;
+  return it;
+}
+__device__ __forceinline__ uint32_t items_of(const StageGeo& g, uint32_t S) {
+  return g.nsec ? (g.rtn + 1) / 2 * ((g.nsec + S - 1) / S) : 0u;
+}
+// Item cursor for walking a stage's items in steps of a wave (no divisions in
+// the loop): item i = pr * ipp + h.
+struct ItemCur {
+  uint32_t pr, h;
+};
+struct StageItems {
+  uint32_t S, ipp, nitems, nf, utot;  // slabs per item, items per pair, items, full slabs, tile bytes
+};
+__device__ __forceinline__ StageItems stage_items(const StageGeo& g, uint32_t S) {
+  StageItems t;
+  t.S = S;
+  t.ipp = g.nsec ? (g.nsec + S - 1) / S : 1u;
+  t.nitems = items_of(g, S);
+  uint32_t F, rem;
+  slab_split(g.K, F, rem);
+  t.nf = F > g.slab0 ? min(F - g.slab0, g.nsec) : 0u;
+  t.utot = cum_bytes(g, g.nsec);
+  return t;
+}
+__device__ __forceinline__ ItemCur item_cur(const StageItems& t, uint32_t i) {
+  return ItemCur{i / t.ipp, i % t.ipp};
+}
+__device__ __forceinline__ void item_advance(ItemCur& c, const StageItems& t, uint32_t n) {
+  c.h += n;
+  while (c.h >= t.ipp) {
+    c.h -= t.ipp;
+    ++c.pr;
+  }
+}
+// byte offset of the item at cursor c in the stage's pair-major stream (past the
+// last pair: the stage's bytes)
+__device__ __forceinline__ uint32_t cur_off(const StageGeo& g, const StageItems& t, const ItemCur& c) {
+  const uint32_t npair = (g.rtn + 1) / 2;
+  if (c.pr >= npair) return g.rtn * t.utot;
+  const uint32_t a = c.h * t.S, nt = 2 * c.pr + 1 < g.rtn ? 2u : 1u;
+  return 2 * c.pr * t.utot + nt * (a <= t.nf ? 512u * a : cum_bytes(g, a));
+}
+
+// Byte offset of item i in the stage's pair-major stream (i = items: the end).
+__device__ __forceinline__ uint32_t item_off(const StageGeo& g, uint32_t S, uint32_t i,
+                                             uint32_t utot) {
+  if (i >= items_of(g, S)) return g.rtn * utot;
+  const Item it = item_of(g, S, i);
+  return 2 * it.pr * utot + it.nt * cum_bytes(g, it.a);
 }
 
 // Ring placement shared by producer and consumers: chunks never wrap.
@@ -113,21 +170,20 @@ __device__ __forceinline__ uint64_t ring_place(uint64_t& pos, uint32_t bytes, ui
   return start;
 }
 
-// Where the producer put a chunk (written before the chunk's copies are issued;
-// the consumers read it after the chunk's full barrier): the consumers never
-// repeat the section / ring arithmetic.
+// Where the producer put a chunk (one work item; written before the chunk's
+// copy is issued, read by the consuming warp after the chunk's full barrier).
 struct ChunkRec {
-  uint32_t off;     // ring byte offset of the chunk (prefix first)
-  uint16_t s0, s1;  // sections [s0, s1) of the stage
-  uint32_t pre;     // prefix bytes (stage-1 s2 scales) before the sections
-  uint32_t sb;      // section bytes (the stage-2 s1 scales follow them in the last chunk)
+  uint32_t off;      // ring byte offset
+  uint32_t i0;       // first work item of the wave
 };
+static_assert(sizeof(ChunkRec) <= 16, "chunk record slot");
 
-// Sections [sa, sb) of row-tile pair pr inside a resident chunk whose first
-// section is s0c, accumulated and flushed into red[] (the pair's rows).
-__device__ __forceinline__ void run_pair(const uint8_t* base, const StageGeo& g, uint32_t s0c,
-                                         uint32_t pr, uint32_t sa, uint32_t sb,
-                                         const uint8_t* bfrag, int* red) {
+// One work item resident at `base` (pair-major: the pair's units of slab a, then
+// of slab a+1, ...): its MMAs, flushed into red[] (the pair's rows).  The full
+// slabs run software-pipelined (full_run; the next slab of a tile is nt * 512
+// bytes on), then the 128 / 64 tails.
+__device__ __forceinline__ void run_item(const uint8_t* base, const StageGeo& g, uint32_t pr,
+                                         uint32_t a, uint32_t b, const uint8_t* bfrag, int* red) {
   const int lane = threadIdx.x & 31;
   int acc[2][4][4];
 #pragma unroll
@@ -135,31 +191,27 @@ __device__ __forceinline__ void run_pair(const uint8_t* base, const StageGeo& g,
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[j][q][0] = acc[j][q][1] = acc[j][q][2] = acc[j][q][3] = 0;
   const uint32_t gq = lane >> 2, c = lane & 3;
-  const uint32_t rtn = g.rtn, t0 = 2 * pr;
-  const bool two = t0 + 1 < rtn;
+  const uint32_t t0 = 2 * pr;
+  const bool two = t0 + 1 < g.rtn;
   uint32_t F, rem;
   slab_split(g.K, F, rem);
-  const uint32_t sl0 = g.slab0 + s0c;  // absolute slab of the chunk's first section
-  const uint32_t k_first = slab_of(g.K, sl0).k0;
-  const uint32_t nfull = F > sl0 ? F - sl0 : 0;  // chunk-relative sections that are full slabs
-  uint32_t s = sa - s0c;
-  const uint32_t send = sb - s0c, sf = min(send, nfull);
-  if (s < sf) {
-    const uint32_t k0 = 256 * (sl0 + s);
-    const uint8_t* unit = base + 2u * rtn * (k0 - k_first) + t0 * 512;
-    const uint8_t* bp = bfrag + kBytesPerK * (k0 - g.klo) + (gq * 4 + c) * 16;
-    if (two) full_run<2>(unit, 512u * rtn, bp, sf - s, lane, gq < (uint32_t)kLimbs, acc);
-    else full_run<1>(unit, 512u * rtn, bp, sf - s, lane, gq < (uint32_t)kLimbs, acc);
-    s = sf;
+  const uint32_t sl0 = g.slab0 + a;  // absolute slab of the item's first slab
+  const uint32_t nfull = F > sl0 ? min(F - sl0, b - a) : 0u;
+  const uint8_t* unit = base;
+  if (nfull) {
+    const uint8_t* bp = bfrag + kBytesPerK * (256 * sl0 - g.klo) + (gq * 4 + c) * 16;
+    if (two) full_run<2>(unit, 1024u, bp, nfull, lane, gq < (uint32_t)kLimbs, acc);
+    else full_run<1>(unit, 512u, bp, nfull, lane, gq < (uint32_t)kLimbs, acc);
+    unit += (two ? 1024u : 512u) * nfull;
   }
-  for (; s < send; ++s) {  // the 128 / 64 tails
-    uint2 b[8];
-    const Slab sl = slab_of(g.K, sl0 + s);
+  for (uint32_t s = a + nfull; s < b; ++s) {  // the 128 / 64 tails
+    uint2 bv[8];
+    const Slab sl = slab_of(g.K, g.slab0 + s);
     const uint32_t ub = unit_bytes(sl.nq);
-    const uint8_t* unit = base + 2u * rtn * (sl.k0 - k_first) + t0 * ub;
-    load_b(bfrag, g.klo, sl, gq, c, b);
-    if (two) tiles_mma<2>(unit, ub, sl.nq, lane, b, acc);
-    else tiles_mma<1>(unit, ub, sl.nq, lane, b, acc);
+    load_b(bfrag, g.klo, sl, gq, c, bv);
+    if (two) tiles_mma<2>(unit, ub, sl.nq, lane, bv, acc);
+    else tiles_mma<1>(unit, ub, sl.nq, lane, bv, acc);
+    unit += (two ? 2u : 1u) * ub;
   }
   flush_rows(acc[0], red + t0 * 16 * kRedStride, lane);
   if (two) flush_rows(acc[1], red + (t0 + 1) * 16 * kRedStride, lane);
@@ -256,7 +308,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
 
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(~0u, tid >> 5, 0);
-  const uint32_t K = p.K, G = p.G;
+  const uint32_t K = p.K, G = p.G, P = p.P;
   const bool sus = (p.debug & 4u) != 0;
   auto desc_of = [&](uint32_t k) -> const StepDesc& {
     return *(const StepDesc*)(dslots + (k % kDescSlots) * kDescSlotBytes);
@@ -269,7 +321,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   if (tid == 0) {
     for (int s = 0; s < kPassSlots; ++s) {
       tc::mbar_init(&full1[s], 1);
-      tc::mbar_init(&empty1[s], kW1);
+      tc::mbar_init(&empty1[s], kW1);  // a chunk is a wave: one item per warp of the group
       tc::mbar_init(&full2[s], 1);
       tc::mbar_init(&empty2[s], kConsumerWarps - kW1);
     }
@@ -290,11 +342,17 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     tc::fence_mbar_init();
     const unsigned long long gen = ld_relaxed_u64(p.ctr);
     misc[0] = (uint32_t)(gen & 1);
-    *(unsigned long long*)(misc + 2) = (gen + 1) * G;
+    *(unsigned long long*)(misc + 2) = (gen + 1) * p.P;  // step barriers: the partition's CTAs
+    *(unsigned long long*)(misc + 4) = (gen + 1) * G;    // kernel-start barrier: every CTA
   }
   __syncthreads();
   const uint32_t par = misc[0];
   const unsigned long long target = *(const unsigned long long*)(misc + 2);
+  const unsigned long long target_all = *(const unsigned long long*)(misc + 4);
+  // this CTA's partition and its step list (local index j -> step D.idx)
+  const uint32_t sub = blockIdx.x / p.P;
+  const uint32_t Kc = sub < p.nsub ? p.list_off[sub + 1] - p.list_off[sub] : 0u;
+  const uint32_t prank = blockIdx.x - sub * p.P;  // rank inside the partition
   unsigned long long* xinit = p.ctr + kCtrStride;
   unsigned long long* tbar = p.ctr + 2 * kCtrStride;
   unsigned long long* ybar = tbar + (size_t)K * kCtrStride;
@@ -318,24 +376,31 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       if (lane != 0) return;
       const int r = role == 0 ? 0 : 1;
       const uint32_t RB = r ? p.ring2_bytes : p.ring1_bytes;
-      const uint32_t cap = r ? p.chunk2_cap : p.chunk1_cap;
+      const uint32_t S = p.item_slabs;
       uint64_t* fullr = r ? full2 : full1;
       uint64_t* emptyr = r ? empty2 : empty1;
       ChunkRec* recs = r ? recs2 : recs1;
       uint8_t* ring = r ? ring2 : ring1;
       uint64_t pos = 0, starts[kPassSlots];
       uint32_t chunk = 0, rel = 0;
-      for (uint32_t k = 0; k < K; ++k) {
-        wait_desc(k);
-        const StepDesc& D = desc_of(k);
-        const Cta& C = cta_of(k);
+      for (uint32_t j = 0; j < Kc; ++j) {
+        wait_desc(j);
+        const StepDesc& D = desc_of(j);
+        const Cta& C = cta_of(j);
+        const uint32_t k = D.idx;
         const StageGeo g = r ? stage2_geo(D, C) : stage1_geo(D, C);
         if (kTrace) PSTAMP(k, r ? 14 : 11);
-        uint32_t s0 = 0;
         uint64_t src = g.src_off;
-        while (s0 < g.nsec) {
-          uint32_t s1;
-          const uint32_t sb = chunk_span(g, s0, cap, &s1);
+        const StageItems T = stage_items(g, S);
+        const uint32_t GWr = r ? kConsumerWarps - kW1 : kW1;  // items per wave
+        ItemCur c0{0, 0}, c1 = item_cur(T, min(GWr, T.nitems));
+        uint32_t o0 = 0;
+        for (uint32_t i0 = 0; i0 < T.nitems; i0 += GWr) {
+          const uint32_t o1 = cur_off(g, T, c1);
+          const uint32_t sb = o1 - o0;
+          o0 = o1;
+          item_advance(c1, T, GWr);
+          (void)c0;
           const uint64_t start = ring_place(pos, sb, RB);
           // wait for the slot and for every older chunk this range overwrites: chunks
           // are placed monotonically, so [start, pos) reaches older chunk c's bytes
@@ -348,7 +413,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
           const uint32_t slot = chunk % kPassSlots;
           starts[slot] = start;
           const uint32_t roff = (uint32_t)(start % RB);
-          recs[slot] = ChunkRec{roff, (uint16_t)s0, (uint16_t)s1, 0u, sb};
+          recs[slot] = ChunkRec{roff, i0};
           if (p.debug & 32u) {  // experiment: no copy, the consumers compute on stale bytes
             tc::mbar_arrive(&fullr[slot]);
           } else {
@@ -356,11 +421,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
             tc::bulk_g2s(ring + roff, D.bits + src, sb, &fullr[slot]);
           }
           src += sb;
-          s0 = s1;
           ++chunk;
         }
         if (kTrace) PSTAMP(k, r ? 15 : 6);
-        tc::mbar_arrive(&dempty[k % kDescSlots]);
+        tc::mbar_arrive(&dempty[j % kDescSlots]);
       }
       return;
     }
@@ -379,7 +443,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       }
       bool pre_done = p.has_pre == 0;
       int32_t ywaited = -1;
-      for (uint32_t j = 0; j < K; ++j) {
+      for (uint32_t j = 0; j < Kc; ++j) {
         const uint32_t slot = j % NB;
         if (j >= NB) mbar_wait_wd(&bempty1[slot], ((j / NB) - 1) & 1, sus);
         wait_desc(j);
@@ -391,7 +455,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
             ywaited = D.x_src;
           }
           if ((D.flags & kStepXPre) && !pre_done) {
-            poll_ctr(xinit, target);
+            poll_ctr(xinit, target_all);
             pre_done = true;
           }
         }
@@ -437,7 +501,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         }
         __syncwarp();
         if (lane == 0) {
-          if (kTrace && pw == 0) PSTAMP(j, 5);
+          if (kTrace && pw == 0) PSTAMP(D.idx, 5);
           tc::mbar_arrive(&bfull1[slot]);
           tc::mbar_arrive(&dempty[j % kDescSlots]);
         }
@@ -451,22 +515,21 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       // segment's s1 slice; clear this CTA's share of the other parity's t.
       const int pw = role - 3;
       int32_t ywaited = -1;
-      for (uint32_t k = 0; k < K; ++k) {
-        const uint32_t slot = k % NB;
-        if (k >= NB) mbar_wait_wd(&bempty2[slot], ((k / NB) - 1) & 1, sus);
+      for (uint32_t j = 0; j < Kc; ++j) {
+        const uint32_t slot = j % NB;
+        if (j >= NB) mbar_wait_wd(&bempty2[slot], ((j / NB) - 1) & 1, sus);
+        wait_desc(j);
+        const StepDesc& D = desc_of(j);
+        const Cta& C = cta_of(j);
+        const uint32_t k = D.idx;
         if (kTrace && lane == 0 && pw == 0) PSTAMP(k, 12);
-        wait_desc(k);
-        const StepDesc& D = desc_of(k);
-        const Cta& C = cta_of(k);
         if (lane == 0) {
-          if (C.s2_rtn || (k == 0 && blockIdx.x == 0)) poll_ctr(tbar + (size_t)k * kCtrStride, target);
+          if (C.s2_rtn) poll_ctr(tbar + (size_t)k * kCtrStride, target);
           // an earlier step writing an overlapping output must be done everywhere
           if (D.y_src >= 0 && D.y_src > ywaited) {
             poll_ctr(ybar + (size_t)D.y_src * kCtrStride, target);
             ywaited = D.y_src;
           }
-          // every CTA read the generation before its first arrival: advance it
-          if (k == 0 && blockIdx.x == 0 && pw == 0) p.ctr[0] = target / G;
           if (kTrace && pw == 0) PSTAMP(k, 4);
         }
         __syncwarp();
@@ -504,42 +567,57 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         }
         {  // clear this CTA's share of the step's region in the other parity
           long long* Z = p.arena + (size_t)(par ^ 1) * p.arena_len + D.t_off;
-          const uint32_t pairs = D.t_len / 2, per = (pairs + G - 1) / G;
-          const uint32_t lo = min(pairs, per * blockIdx.x), hi = min(pairs, lo + per);
+          const uint32_t pairs = D.t_len / 2, per = (pairs + P - 1) / P;
+          const uint32_t lo = min(pairs, per * prank), hi = min(pairs, lo + per);
           for (uint32_t i = lo + pw * 32 + lane; i < hi; i += 64)
             ((longlong2*)Z)[i] = make_longlong2(0, 0);
         }
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&dempty[k % kDescSlots]);
+        if (lane == 0) tc::mbar_arrive(&dempty[j % kDescSlots]);
+      }
+      // every CTA has read the generation (it arrived on the kernel-start barrier
+      // after reading it): advance it for the next launch
+      if (blockIdx.x == 0 && pw == 0 && lane == 0) {
+        poll_ctr(xinit, target_all);
+        p.ctr[0] = target_all / G;
       }
       return;
     }
     if (lane != 0) return;
     if (role == 5) {
       // ------------------------------------------- sequencer 1: t barriers
-      for (uint32_t j = 0; j < K; ++j) {
+      // step indices from the partition's list (not the descriptor slot, which
+      // the stage-2 group may release as soon as stage 1 of the step is done)
+      const uint32_t* list = Kc ? p.list + p.list_off[sub] : nullptr;
+      uint32_t knext = Kc ? __ldg(list) : 0u;
+      for (uint32_t j = 0; j < Kc; ++j) {
+        const uint32_t k = knext;
+        if (j + 1 < Kc) knext = __ldg(list + j + 1);
         mbar_wait_wd(&cdone1[j % kDoneRing], (j / kDoneRing) & 1, sus);
-        arrive_ctr(tbar + (size_t)j * kCtrStride);  // stage-1 t reds ordered before it
+        arrive_ctr(tbar + (size_t)k * kCtrStride);  // stage-1 t reds ordered before it
       }
       return;
     }
     // --------------------- sequencer 2: output barriers, descriptor prefetch
-    auto issue_desc = [&](uint32_t k) {
-      const uint32_t slot = k % kDescSlots;
+    const uint32_t* list = Kc ? p.list + p.list_off[sub] : nullptr;
+    auto issue_desc = [&](uint32_t j) {
+      const uint32_t slot = j % kDescSlots, k = __ldg(list + j);
       uint8_t* dst = dslots + slot * kDescSlotBytes;
       tc::mbar_arrive_expect_tx(&dfull[slot], (uint32_t)sizeof(StepDesc) + 32);
       tc::bulk_g2s(dst, p.desc + k, (uint32_t)sizeof(StepDesc), &dfull[slot]);
       tc::bulk_g2s(dst + 480, p.ctas + (size_t)k * G + blockIdx.x, 32, &dfull[slot]);
     };
-    for (uint32_t k = 0; k < min(K, (uint32_t)kDescSlots); ++k) issue_desc(k);
-    for (uint32_t k = 0; k < K; ++k) {
-      wait_desc(k);
-      const bool publish = desc_of(k).flags & kStepPublish;
-      mbar_wait_wd(&cdone2[k % kDoneRing], (k / kDoneRing) & 1, sus);
+    for (uint32_t j = 0; j < min(Kc, (uint32_t)kDescSlots); ++j) issue_desc(j);
+    for (uint32_t j = 0; j < Kc; ++j) {
+      wait_desc(j);
+      const StepDesc& D = desc_of(j);
+      const bool publish = D.flags & kStepPublish;
+      const uint32_t k = D.idx;
+      mbar_wait_wd(&cdone2[j % kDoneRing], (j / kDoneRing) & 1, sus);
       if (publish) arrive_ctr(ybar + (size_t)k * kCtrStride);
-      if (k + kDescSlots < K) {
-        mbar_wait_wd(&dempty[k % kDescSlots], (k / kDescSlots) & 1, sus);
-        issue_desc(k + kDescSlots);
+      if (j + kDescSlots < Kc) {
+        mbar_wait_wd(&dempty[j % kDescSlots], (j / kDescSlots) & 1, sus);
+        issue_desc(j + kDescSlots);
       }
     }
     return;
@@ -571,27 +649,29 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         atomicMax(amax + 4 * (size_t)__ldg(&Dg->amax_idx), mb);
       }
     }
-    all_consumers_sync();
-    if (tid == 0) arrive_ctr(xinit);
   }
-  uint32_t chunk = 0;
+  // kernel-start barrier (every CTA, after it read the generation): the
+  // prepass bounds, and the generation advance at the end of CTA 0
+  all_consumers_sync();
+  if (tid == 0) arrive_ctr(xinit);
+  uint32_t chunk = 0;  // the group's ring chunks (work items) consumed so far
   const int gw = warp - gid * W1;
   uint64_t* const fullr = gid ? full2 : full1;
   uint64_t* const emptyr = gid ? empty2 : empty1;
   const ChunkRec* const recs = gid ? recs2 : recs1;
   const uint8_t* const ring = gid ? ring2 : ring1;
-  // The stage's (pair, section) items are split over the group's warps once for
-  // the whole stage (pair-major, contiguous per warp); each warp walks the
-  // chunks as they land and runs its items in each.
+  // A ring chunk is a wave of GW consecutive work items (pair-major, so one
+  // contiguous byte range); warp w runs item w of each wave and flushes once per
+  // item (a tile pair over a run of up to item_slabs slabs).
   uint32_t cur_step = 0;
   auto mma_stage = [&](const StageGeo& g, const uint8_t* bf) {
-    if (!g.nsec) return;
-    const uint32_t npair = (g.rtn + 1) / 2, U = npair * g.nsec;
-    const uint32_t f0 = U * gw / GW, f1 = U * (gw + 1) / GW;
-    const uint32_t p0 = f0 / g.nsec, p1 = f1 ? (f1 - 1) / g.nsec : 0;
-    unsigned long long wsum = 0, nch = 0, rsum = 0, ncall = 0, nslab = 0;
+    const StageItems T = stage_items(g, p.item_slabs);
+    const uint32_t nitems = T.nitems;
+    if (!nitems) return;
+    ItemCur c0{0, 0}, ci = item_cur(T, (uint32_t)gw);  // the wave's first item, this warp's
+    unsigned long long wsum = 0, nch = 0, rsum = 0;
     const unsigned long long l0 = kTrace ? clock64() : 0ull;
-    for (uint32_t s0 = 0; s0 < g.nsec;) {
+    for (uint32_t i0 = 0; i0 < nitems; i0 += GW) {
       const uint32_t slot = chunk % kPassSlots;
       const unsigned long long w0 = kTrace ? clock64() : 0ull;
       mbar_wait_wd(&fullr[slot], (chunk / kPassSlots) & 1, sus);
@@ -599,30 +679,24 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         wsum += clock64() - w0;
         ++nch;
       }
-      const ChunkRec cr = recs[slot];
-      if (f0 < f1 && !(p.debug & 1u)) {
-        for (uint32_t pr = p0; pr <= p1; ++pr) {
-          const uint32_t sa = max(s0, pr == p0 ? f0 - p0 * g.nsec : 0u);
-          const uint32_t sb = min((uint32_t)cr.s1, pr == p1 ? f1 - p1 * g.nsec : g.nsec);
-          if (sa < sb) {
-            const unsigned long long r0 = kTrace ? clock64() : 0ull;
-            run_pair(ring + cr.off, g, s0, pr, sa, sb, bf, red);
-            if (kTrace) {
-              rsum += clock64() - r0;
-              ++ncall;
-              nslab += sb - sa;
-            }
-          }
-        }
+      const uint32_t i = i0 + gw;
+      if (i < nitems && !(p.debug & 1u)) {
+        const ChunkRec cr = recs[slot];
+        const uint32_t off = cur_off(g, T, ci) - cur_off(g, T, c0);
+        const uint32_t a = ci.h * T.S;
+        const unsigned long long r0 = kTrace ? clock64() : 0ull;
+        run_item(ring + cr.off + off, g, ci.pr, a, min(g.nsec, a + T.S), bf, red);
+        if (kTrace) rsum += clock64() - r0;
       }
+      item_advance(c0, T, GW);
+      item_advance(ci, T, GW);
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&emptyr[slot]);
       ++chunk;
-      s0 = cr.s1;
     }
     if (kTrace && gw == 0 && lane == 0) {  // this warp's time waiting for chunks, and chunks
       trp[1 + kPassStamps * cur_step + 16 + gid] = wsum;
-      trp[1 + kPassStamps * cur_step + 18 + gid] = (nch << 48) | (ncall << 32) | (nslab << 16);
+      trp[1 + kPassStamps * cur_step + 18 + gid] = (nch << 48) | (nch << 32) | ((unsigned long long)nitems << 16);
       trp[1 + kPassStamps * cur_step + 20 + gid] = rsum;
       trp[1 + kPassStamps * cur_step + 22 + gid] = clock64() - l0;  // the whole chunk loop
     }
@@ -630,12 +704,13 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
 
   // Both groups run the same loop (one copy of the MMA code in the kernel):
   // group 0 does stage 1 of step k (x -> t), group 1 stage 2 (t -> y).
-  for (uint32_t k = 0; k < K; ++k) {
-    wait_desc(k);
-    const StepDesc& D = desc_of(k);
-    const Cta& C = cta_of(k);
-    const uint32_t slot = k % NB;
-    mbar_wait_wd(gid ? &bfull2[slot] : &bfull1[slot], (k / NB) & 1, sus);
+  for (uint32_t j = 0; j < Kc; ++j) {
+    wait_desc(j);
+    const StepDesc& D = desc_of(j);
+    const Cta& C = cta_of(j);
+    const uint32_t k = D.idx;
+    const uint32_t slot = j % NB;
+    mbar_wait_wd(gid ? &bfull2[slot] : &bfull1[slot], (j / NB) & 1, sus);
     const uint8_t* bs = gid ? bslots2 + slot * p.bslot2_bytes : bslots1 + slot * p.bslot1_bytes;
     if (kTrace && gt == 0) {
       PSTAMP(k, gid ? 2 : 0);
@@ -659,7 +734,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
           red_add_u64(&Tseg[i], v);
         }
       } else {  // stage-2 outputs (packed.cpp:174-190)
-        const float xmax = xmaxs[k % 16];
+        const float xmax = xmaxs[j % 16];
         const int ea = act_exponent(S.s2max, xmax);
         const bool nonfinite = is_inf(xmax);
         const int E = t_shift(D.m) + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
@@ -702,11 +777,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       if (kTrace) PSTAMP(k, gid ? 3 : 1);
       if (gid) {
         tc::mbar_arrive(&bempty2[slot]);
-        tc::mbar_arrive(&cdone2[k % kDoneRing]);
-        tc::mbar_arrive(&dempty[k % kDescSlots]);
+        tc::mbar_arrive(&cdone2[j % kDoneRing]);
+        // the stage-1 group also reads this descriptor slot; a CTA without stage-2
+        // rows in the step does not wait for the t barrier, so wait for it here
+        mbar_wait_wd(&cdone1[j % kDoneRing], (j / kDoneRing) & 1, sus);
+        tc::mbar_arrive(&dempty[j % kDescSlots]);
       } else {
         tc::mbar_arrive(&bempty1[slot]);
-        tc::mbar_arrive(&cdone1[k % kDoneRing]);
+        tc::mbar_arrive(&cdone1[j % kDoneRing]);
       }
     }
   }
@@ -730,17 +808,73 @@ bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
 }
 }  // namespace
 
+namespace {
+
+// Geometry of a pass over a given set of plans (one per step), and the
+// shared-memory split it needs.
+struct PassGeo {
+  uint32_t bf1 = 0, bf2 = 0, s1bytes = 16, rt1 = 1, rt2 = 1, maxsec1 = 0, maxsec2 = 0;
+  double bits1 = 0, bits2 = 0;
+  uint64_t max_s2_cta_bytes = 0;
+  uint32_t bslot1_b = 0, bs2_s1_off = 0, bslot2_b = 0, red1_b = 0, red2_b = 0, fixed = 0;
+  uint32_t min1 = 0, min2 = 0;  // smallest rings
+  bool fits = false;
+};
+
+PassGeo pass_geo(uint32_t K, const std::vector<const nqb_group*>& plan, uint32_t item_slabs) {
+  PassGeo q;
+  for (uint32_t k = 0; k < K; ++k) {
+    const nqb_group* g = plan[k];
+    for (uint32_t s = 0; s < g->nseg; ++s) {
+      q.bf2 = std::max(q.bf2, kBytesPerK * kpad(g->r[s]));
+      q.bits1 += (double)g->r[s] * g->m;
+      q.bits2 += (double)g->r[s] * g->n[s];
+    }
+    for (uint32_t c = 0; c < g->grid; ++c) {
+      const Cta& C = g->ctas[c];
+      if (C.s1_rtn && C.s1_sln) {  // the CTA's stage-1 input slice and sections
+        const Slab last = slab_of(g->m, C.s1_sl0 + C.s1_sln - 1);
+        const uint32_t nk1 = last.k0 + 32 * last.nq - slab_of(g->m, C.s1_sl0).k0;
+        q.bf1 = std::max(q.bf1, kBytesPerK * nk1);
+        q.maxsec1 = std::max<uint32_t>(q.maxsec1, C.s1_rtn * 512u);
+      }
+      if (C.s2_rtn) {
+        uint64_t b2 = 0;
+        const uint32_t r2 = g->seg[C.s2_seg].r;
+        for (uint32_t i = 0, ns = nslabs(r2); i < ns; ++i)
+          b2 += (uint64_t)C.s2_rtn * unit_bytes(slab_of(r2, i).nq);
+        q.max_s2_cta_bytes = std::max<uint64_t>(q.max_s2_cta_bytes, b2);
+        q.maxsec2 = std::max<uint32_t>(q.maxsec2, C.s2_rtn * 512u);
+      }
+      q.s1bytes = std::max<uint32_t>(q.s1bytes, 32u * C.s2_rtn);
+      q.rt1 = std::max<uint32_t>(q.rt1, C.s1_rtn);
+      q.rt2 = std::max<uint32_t>(q.rt2, C.s2_rtn);
+    }
+  }
+  // Shared memory: head | row sums (stage 1, 2) | quantised-x slots | quantised-t
+  // slots | stage-1 ring | stage-2 ring.
+  q.bslot1_b = (kBSlotHead + std::max(q.bf1, 16u) + 127) / 128 * 128;
+  q.bs2_s1_off = (kBSlotHead + std::max(q.bf2, 16u) + 127) / 128 * 128;
+  q.bslot2_b = (q.bs2_s1_off + q.s1bytes + 127) / 128 * 128;
+  q.red1_b = q.rt1 * 16 * kRedStride * 4;
+  q.red2_b = q.rt2 * 16 * kRedStride * 4;
+  q.fixed = pass_head_bytes() + q.red1_b + q.red2_b + kBSlots * (q.bslot1_b + q.bslot2_b);
+  // a ring chunk is a wave of work items (<= 8 tile pairs over <= item_slabs
+  // slabs); each ring holds at least one
+  q.min1 = q.min2 = std::max<uint32_t>(24u * 1024u, 8 * 1024u * item_slabs);
+  q.fits = q.fixed + q.min1 + q.min2 <= 227u * 1024u;
+  return q;
+}
+
+}  // namespace
+
 nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
   NQB_REQUIRE(K >= 1 && K <= 65536, NQB_E_VALIDATION, "a decode pass holds 1..65536 steps");
   NQB_REQUIRE(steps != nullptr, NQB_E_VALIDATION, "null steps");
   const uint32_t G = (uint32_t)ctx->num_sms;
   std::vector<StepDesc> desc(K);
-  uint32_t bf1 = 0, bf2 = 0, s1bytes = 16;
-  double bits1 = 0, bits2 = 0;  // stage-1 / stage-2 stream bytes (ring split)
-  uint32_t rt1 = 1, rt2 = 1;    // most row tiles of one CTA in stage 1 / stage 2
-  uint64_t arena = 0, stream_bytes = 0, max_s2_cta_bytes = 0;
-  double algo = 0;
-  bool has_pre = false;
+  bool has_pre = false, chained = false;
+  // ---- dependencies from buffer ranges (geometry only: any plan of the group) ----
   for (uint32_t k = 0; k < K; ++k) {
     const PassStepIn& s = steps[k];
     const nqb_group* g = s.group;
@@ -751,11 +885,10 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     NQB_REQUIRE(s.x != nullptr, NQB_E_VALIDATION, "null pass input");
     StepDesc& D = desc[k];
     std::memset(&D, 0, sizeof(D));
-    D.bits = g->bits;
+    D.idx = k;
     D.x = s.x;
     D.nseg = g->nseg;
     D.m = g->m;
-    D.R1 = g->R1;
     const uint32_t esz = s.f32 ? 4 : 2;
     D.flags = (s.f32 ? (kStepXF32 | kStepYF32) : 0u) |
               (((uintptr_t)s.x % 16 == 0) ? kStepXVec : 0u);
@@ -765,39 +898,9 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       D.y[q] = s.y[q];
       NQB_REQUIRE(!overlaps(s.y[q], (size_t)g->n[q] * esz, s.x, (size_t)g->m * esz),
                   NQB_E_VALIDATION, "a pass step's output overlaps its own input");
-      algo += (double)g->r[q] * (g->n[q] + g->m) / 8.0 + 2.0 * (g->n[q] + g->m) + esz * g->n[q];
-      bf2 = std::max(bf2, kBytesPerK * kpad(g->r[q]));
-      bits1 += (double)g->r[q] * g->m;
-      bits2 += (double)g->r[q] * g->n[q];
     }
-    algo += (double)esz * g->m;
-    for (uint32_t c = 0; c < g->grid; ++c) {  // the CTA's stage-1 input slice
-      const Cta& C = g->ctas[c];
-      if (!C.s1_rtn || !C.s1_sln) continue;
-      const Slab last = slab_of(g->m, C.s1_sl0 + C.s1_sln - 1);
-      const uint32_t nk1 = last.k0 + 32 * last.nq - slab_of(g->m, C.s1_sl0).k0;
-      bf1 = std::max(bf1, kBytesPerK * nk1);
-    }
-    for (uint32_t c = 0; c < g->grid; ++c) {
-      const Cta& C = g->ctas[c];
-      if (C.s2_rtn) {
-        uint64_t b2 = 0;
-        const uint32_t r2 = g->seg[C.s2_seg].r;
-        for (uint32_t q = 0, ns = nslabs(r2); q < ns; ++q) b2 += (uint64_t)C.s2_rtn * unit_bytes(slab_of(r2, q).nq);
-        max_s2_cta_bytes = std::max<uint64_t>(max_s2_cta_bytes, b2);
-      }
-    }
-    for (uint32_t c = 0; c < g->grid; ++c) {
-      s1bytes = std::max<uint32_t>(s1bytes, 32u * g->ctas[c].s2_rtn);
-      rt1 = std::max<uint32_t>(rt1, g->ctas[c].s1_rtn);
-      rt2 = std::max<uint32_t>(rt2, g->ctas[c].s2_rtn);
-    }
-    stream_bytes += g->stream_bytes;
-    D.t_off = arena;
-    D.t_len = (g->R1 + 3) & ~1u;  // even, plus the odd-start overhang of a segment copy
-    arena += D.t_len;
-    // dependencies from buffer ranges: the latest earlier step whose output
-    // overlaps this input must have finished (output barrier) before stage 1
+    // the latest earlier step whose output overlaps this input must have finished
+    // (output barrier) before stage 1
     D.x_src = -1;
     int32_t exact = -1;
     for (int j = (int)k - 1; j >= 0 && D.x_src < 0; --j) {
@@ -821,72 +924,167 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
           if (overlaps(desc[j].y[a], (size_t)desc[j].seg[a].n * ej, s.y[b], (size_t)g->n[b] * esz))
             D.y_src = j;
     }
-    if (D.y_src >= 0) desc[D.y_src].flags |= kStepPublish;
+    if (D.y_src >= 0) {
+      desc[D.y_src].flags |= kStepPublish;
+      chained = true;
+    }
     if (D.x_src < 0) {
       D.flags |= kStepXPre;
       D.amax_idx = k;
       has_pre = true;
     } else {
+      chained = true;
       desc[D.x_src].flags |= kStepPublish;
       if (exact >= 0) D.amax_idx = (uint32_t)exact;
       else D.flags |= kStepXSelf;
     }
   }
-  // Shared memory: head | row sums (stage 1, 2) | quantised-x slots | quantised-t
-  // slots | stage-1 ring | stage-2 ring.  The rings split what is left in
-  // proportion to the two stages' bytes (each >= 36 KB).
-  const uint32_t bslot1_b = (kBSlotHead + std::max(bf1, 16u) + 127) / 128 * 128;
-  const uint32_t bs2_s1_off = (kBSlotHead + std::max(bf2, 16u) + 127) / 128 * 128;
-  const uint32_t bslot2_b = (bs2_s1_off + s1bytes + 127) / 128 * 128;
-  const uint32_t head = pass_head_bytes();
-  const uint32_t red1_b = rt1 * 16 * kRedStride * 4, red2_b = rt2 * 16 * kRedStride * 4;
-  // two quantised-input slots per stage (three measured no better on 7B:
-  // 884 vs 860-905 GB/s across runs, and cost 33 KB of ring at 70B)
-  const uint32_t nb = kBSlots;
-  const uint32_t fixed = head + red1_b + red2_b + nb * (bslot1_b + bslot2_b);
-  NQB_REQUIRE(fixed + 72u * 1024u <= 227u * 1024u, NQB_E_DIMENSION_MISMATCH,
-              "decode pass: staging buffers leave no room for the weight rings");
-  const uint32_t rings = (227u * 1024u - fixed) / 256 * 256;
-  const double f1 = bits1 + bits2 > 0 ? bits1 / (bits1 + bits2) : 0.5;
-  uint32_t ring1 = (uint32_t)(rings * f1) / 128 * 128;
-  ring1 = std::min(std::max(ring1, 36u * 1024u), rings - 36u * 1024u);
-  const uint32_t ring2 = rings - ring1;
 
-  // ---- device memory: descriptors | CTA tables | counters | bounds | arena ----
-  const uint32_t amax_words = K * (1 + kMaxSeg);
-  const size_t desc_b = sizeof(StepDesc) * K;
-  const size_t cta_b = sizeof(Cta) * (size_t)K * G;
-  const size_t ctr_b = sizeof(unsigned long long) * kCtrStride * (2 + 2 * (size_t)K);
-  const size_t amax_b = 2ull * amax_words * 16;
-  const size_t arena_b = 2ull * arena * 8;
   auto* P = new nqb_pass();
   P->device = ctx->device;
   P->K = K;
   P->G = G;
   try {
-    NQB_CUDA(cudaMalloc(&P->dmem, desc_b + cta_b + ctr_b + amax_b + arena_b));
+    // ---- SM partitions.  When no step reads or overwrites another step's output,
+    // the steps are independent: the grid splits into nsub partitions of P CTAs
+    // and each runs its share of the steps on plans built for P CTAs, so every CTA
+    // sees nsub times the bytes per step and the per-step handoff chain (x
+    // quantisation, t barrier, epilogues) is amortised over that much more work
+    // (measured: a 7B pass on 74 SMs runs at 77 % of the rate on 148).  A chained
+    // pass keeps one partition of G CTAs (the steps run one after the other).
+    // The pass runs on its own plans (pair-major stream layout, k_relayout; the
+    // groups' per-call plans stay untouched), one per distinct group.
+    const uint32_t item_slabs = std::min<uint32_t>(std::max<uint32_t>(env_u32p("NQB_PASS_ITEM_SLABS", 4), 1), 64);
+    uint32_t nsub = 0;
+    std::vector<const nqb_group*> plan(K);
+    PassGeo geo;
+    {
+      const uint32_t want = chained ? 1u : std::min<uint32_t>(std::max<uint32_t>(env_u32p("NQB_PASS_SPLIT", 4), 1), kMaxSub);
+      for (uint32_t ns = want; ns >= 1; --ns) {
+        const uint32_t Pc = G / ns;
+        std::vector<nqb_group*> made;
+        std::vector<const nqb_group*> pl(K);
+        bool ok = Pc >= 8 || ns == 1;
+        try {
+          std::vector<std::pair<const nqb_group*, nqb_group*>> memo;
+          for (uint32_t k = 0; k < K && ok; ++k) {
+            const nqb_group* g = steps[k].group;
+            nqb_group* h = nullptr;
+            for (auto& pr : memo)
+              if (pr.first == g) h = pr.second;
+            if (!h) {
+              h = group_build(ctx, g->layers, g->nseg, Pc, kPassMaxRt, true);
+              made.push_back(h);
+              memo.push_back({g, h});
+            }
+            pl[k] = h;
+          }
+        } catch (const nqb::Failure& f) {
+          ok = false;
+          if (env_u32p("NQB_PASS_VERBOSE", 0))
+            std::fprintf(stderr, "nqb pass: %u partitions: plan failed: %s\n", ns, f.msg.c_str());
+        }
+        PassGeo gq;
+        if (ok) gq = pass_geo(K, pl, item_slabs);
+        if (ok && !gq.fits && env_u32p("NQB_PASS_VERBOSE", 0))
+          std::fprintf(stderr, "nqb pass: %u partitions: staging %u B + rings %u + %u B > 227 KB\n",
+                       ns, gq.fixed, gq.min1, gq.min2);
+        if (ok && gq.fits) {
+          nsub = ns;
+          plan = pl;
+          geo = gq;
+          P->owned = made;
+          break;
+        }
+        for (auto* h : made) group_free(h);
+      }
+    }
+    NQB_REQUIRE(nsub >= 1, NQB_E_DIMENSION_MISMATCH,
+                "decode pass: no partition of the grid fits the steps' plans in shared memory");
+    const uint32_t Pn = G / nsub;
+    NQB_REQUIRE(geo.fits, NQB_E_DIMENSION_MISMATCH,
+                "decode pass: staging buffers leave no room for the weight rings");
+
+    // ---- per-step plan data, t regions, algorithmic bytes ----
+    uint64_t arena = 0, stream_bytes = 0;
+    double algo = 0;
+    std::vector<uint64_t> load(nsub, 0);
+    std::vector<std::vector<uint32_t>> lists(nsub);
+    std::vector<uint32_t> part(K, 0);
+    for (uint32_t k = 0; k < K; ++k) {
+      const nqb_group* g = plan[k];
+      NQB_REQUIRE(g->grid <= Pn, NQB_E_INTERNAL, "decode plan larger than its partition");
+      StepDesc& D = desc[k];
+      D.bits = g->bits;
+      D.R1 = g->R1;
+      const uint32_t esz = steps[k].f32 ? 4 : 2;
+      for (uint32_t q = 0; q < g->nseg; ++q) {
+        D.seg[q] = g->seg[q];
+        algo += (double)g->r[q] * (g->n[q] + g->m) / 8.0 + 2.0 * (g->n[q] + g->m) + esz * g->n[q];
+      }
+      algo += (double)esz * g->m;
+      stream_bytes += g->stream_bytes;
+      D.t_off = arena;
+      D.t_len = (g->R1 + 3) & ~1u;  // even, plus the odd-start overhang of a segment copy
+      arena += D.t_len;
+      // partition: the least-loaded one (steps stay in pass order inside it)
+      uint32_t best = 0;
+      for (uint32_t i = 1; i < nsub; ++i)
+        if (load[i] < load[best]) best = i;
+      load[best] += g->stream_bytes;
+      lists[best].push_back(k);
+      part[k] = best;
+    }
+
+    // Rings split what the staging leaves in proportion to the two stages' bytes.
+    const uint32_t rings = (227u * 1024u - geo.fixed) / 256 * 256;
+    const double f1 = geo.bits1 + geo.bits2 > 0 ? geo.bits1 / (geo.bits1 + geo.bits2) : 0.5;
+    uint32_t ring1 = (uint32_t)(rings * f1) / 128 * 128;
+    ring1 = std::min(std::max(ring1, geo.min1), rings - geo.min2);
+    const uint32_t ring2 = rings - ring1;
+
+    // ---- device memory: descriptors | CTA tables | counters | bounds | arena | lists ----
+    const uint32_t amax_words = K * (1 + kMaxSeg);
+    const size_t desc_b = sizeof(StepDesc) * K;
+    const size_t cta_b = sizeof(Cta) * (size_t)K * G;
+    const size_t ctr_b = sizeof(unsigned long long) * kCtrStride * (2 + 2 * (size_t)K);
+    const size_t amax_b = 2ull * amax_words * 16;
+    const size_t arena_b = 2ull * arena * 8;
+    const size_t list_b = sizeof(uint32_t) * K;
+    NQB_CUDA(cudaMalloc(&P->dmem, desc_b + cta_b + ctr_b + amax_b + arena_b + list_b));
     char* base = (char*)P->dmem;
     StepDesc* d_desc = (StepDesc*)base;
     Cta* d_ctas = (Cta*)(base + desc_b);
     auto* d_ctr = (unsigned long long*)(base + desc_b + cta_b);
     auto* d_amax = (unsigned*)(base + desc_b + cta_b + ctr_b);
     auto* d_arena = (long long*)(base + desc_b + cta_b + ctr_b + amax_b);
+    auto* d_list = (uint32_t*)(base + desc_b + cta_b + ctr_b + amax_b + arena_b);
     std::vector<Cta> ctas((size_t)K * G, Cta{});
     for (uint32_t k = 0; k < K; ++k) {
-      const nqb_group* g = steps[k].group;
-      std::copy(g->ctas, g->ctas + g->grid, ctas.begin() + (size_t)k * G);
+      const nqb_group* g = plan[k];
+      std::copy(g->ctas, g->ctas + g->grid, ctas.begin() + (size_t)k * G + (size_t)part[k] * Pn);
       desc[k].ctas = d_ctas + (size_t)k * G;
+    }
+    std::vector<uint32_t> flat;
+    PassParams& pp = P->params;
+    pp.list_off[0] = 0;
+    for (uint32_t i = 0; i < nsub; ++i) {
+      flat.insert(flat.end(), lists[i].begin(), lists[i].end());
+      pp.list_off[i + 1] = (uint32_t)flat.size();
     }
     NQB_CUDA(cudaMemsetAsync(d_ctr, 0, ctr_b + amax_b + arena_b, ctx->stream));
     NQB_CUDA(cudaMemcpyAsync(d_desc, desc.data(), desc_b, cudaMemcpyHostToDevice, ctx->stream));
     NQB_CUDA(cudaMemcpyAsync(d_ctas, ctas.data(), cta_b, cudaMemcpyHostToDevice, ctx->stream));
+    NQB_CUDA(cudaMemcpyAsync(d_list, flat.data(), list_b, cudaMemcpyHostToDevice, ctx->stream));
     NQB_CUDA(cudaStreamSynchronize(ctx->stream));
 
-    PassParams& pp = P->params;
     pp.desc = d_desc;
     pp.ctas = d_ctas;
     pp.K = K;
     pp.G = G;
+    pp.list = d_list;
+    pp.nsub = nsub;
+    pp.P = Pn;
     pp.ctr = d_ctr;
     pp.amax = d_amax;
     pp.amax_words = amax_words;
@@ -894,44 +1092,31 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     pp.arena_len = arena;
     pp.has_pre = has_pre ? 1 : 0;
     pp.debug = env_u32p("NQB_PASS_DEBUG", 0);
-    pp.red1_bytes = red1_b;
-    pp.red2_bytes = red2_b;
-    pp.bslot1_bytes = bslot1_b;
-    pp.bslot2_bytes = bslot2_b;
-    pp.bs2_s1_off = bs2_s1_off;
+    pp.red1_bytes = geo.red1_b;
+    pp.red2_bytes = geo.red2_b;
+    pp.bslot1_bytes = geo.bslot1_b;
+    pp.bslot2_bytes = geo.bslot2_b;
+    pp.bs2_s1_off = geo.bs2_s1_off;
     // Consumer warps per stage group.  Measured (tools/gpu_pass_ab.sh): an even
     // 6 + 6 split is best when every step is small (7B: 886 vs 841 GB/s for 4 + 8),
     // while a pass whose largest step puts > 96 KB of stage-2 bits on each CTA
     // (70B gate/up: 169 KB) is bound by the stage-2 group, and 4 + 8 gives
     // 1495 vs 1234 GB/s.
     {
-      const uint32_t w1 = max_s2_cta_bytes > 96u * 1024u ? 4u : 6u;
+      const uint32_t w1 = geo.max_s2_cta_bytes > 96u * 1024u ? 4u : 6u;
       const uint32_t ew = env_u32p("NQB_PASS_WARPS1", 0);
       pp.warps1 = ew == 4 || ew == 6 ? ew : w1;  // the kernel is instantiated for 4 and 6
     }
     pp.ring1_bytes = ring1;
     pp.ring2_bytes = ring2;
-    const uint32_t cap_kb = env_u32p("NQB_PASS_CHUNK_KB", 0);
-    // a chunk is at most cap + the largest section (16 KB); a group holds one
-    // chunk at a time, so its ring must fit one
-    // Chunks of about half a ring: a chunk's sections are the run length of every
-    // consumer warp's MMA loop (one flush per run), so longer chunks cut the
-    // per-run overhead; two chunks in flight still cover the HBM latency
-    // (measured: 70B pass 1068 -> 1240 GB/s going from ring/3 to ~32 KB chunks).
-    auto cap_of = [](uint32_t ring) {
-      return std::min<uint32_t>(40u * 1024u, (ring / 2 - 2048) / 128 * 128);
-    };
-    pp.chunk1_cap = cap_kb ? cap_kb * 1024 : cap_of(ring1);
-    pp.chunk2_cap = cap_kb ? cap_kb * 1024 : cap_of(ring2);
-    NQB_REQUIRE(pp.chunk1_cap + 16384 <= ring1 && pp.chunk2_cap + 16384 <= ring2,
-                NQB_E_VALIDATION, "NQB_PASS_CHUNK_KB too large for the shared-memory rings");
-    P->smem_bytes = fixed + rings;
+    pp.item_slabs = item_slabs;
+    P->smem_bytes = geo.fixed + rings;
     if (env_u32p("NQB_PASS_VERBOSE", 0))
       std::fprintf(stderr,
-                   "nqb pass: K=%u G=%u smem=%u head=%u red=%u+%u bslots=%ux(%u+%u) "
-                   "rings=%u+%u chunk caps=%u/%u\n",
-                   K, G, P->smem_bytes, head, red1_b, red2_b, nb, bslot1_b, bslot2_b, ring1,
-                   ring2, pp.chunk1_cap, pp.chunk2_cap);
+                   "nqb pass: K=%u G=%u partitions=%u x %u smem=%u red=%u+%u bslots=%ux(%u+%u) "
+                   "rings=%u+%u item slabs=%u warps1=%u\n",
+                   K, G, nsub, Pn, P->smem_bytes, geo.red1_b, geo.red2_b, kBSlots, geo.bslot1_b,
+                   geo.bslot2_b, ring1, ring2, item_slabs, pp.warps1);
     for (uint32_t k = 0; k < K; ++k) {
       const uint32_t esz = steps[k].f32 ? 4 : 2;
       P->x_dev.push_back(const_cast<void*>(steps[k].x));
@@ -986,6 +1171,7 @@ void pass_free(nqb_pass* P) {
   if (!P) return;
   cudaSetDevice(P->device);
   cudaFree(P->dmem);
+  for (auto* g : P->owned) group_free(g);
   delete P;
 }
 

@@ -47,6 +47,8 @@ constexpr int kCtrStride = 16;   // u64 words per counter (own 128-byte line)
 constexpr int kPassHelpers = 8;
 constexpr int kPassStamps = 24;  // trace stamps per step (16..21: consumer chunk-wait / run counters, per stage)
 constexpr int kMaxLookahead = 6;
+constexpr int kMaxSub = 8;       // SM partitions of a pass (independent steps run concurrently)
+constexpr uint32_t kPassMaxRt = 64;  // row tiles per CTA per stage in a partition's plan
 constexpr uint32_t kBSlotHead = 16;  // slot header: the two quantiser warps' sums of the values
 
 enum : uint32_t {
@@ -70,7 +72,8 @@ struct alignas(16) StepDesc {
   uint32_t amax_idx;     // 16-byte bound word (per parity) holding max|x|
   uint64_t t_off;        // this step's t region (int64 index, even)
   uint32_t t_len;        // int64 words in the region (even)
-  uint32_t pad[4];
+  uint32_t idx;          // the step's index in the pass (barriers, bounds, trace)
+  uint32_t pad[3];
 };
 static_assert(sizeof(StepDesc) % 16 == 0 && sizeof(StepDesc) <= 480, "step descriptor layout");
 constexpr uint32_t kDescSlotBytes = 512;  // descriptor + the CTA's 32-byte Cta entry at 480
@@ -85,12 +88,17 @@ struct PassParams {
   uint64_t arena_len;
   uint32_t amax_words;
   uint32_t ring1_bytes, ring2_bytes;     // stage-1 / stage-2 weight rings
-  uint32_t chunk1_cap, chunk2_cap;
+  uint32_t item_slabs;        // slabs per work item (ring chunk): one warp, one flush
   uint32_t bslot1_bytes, bslot2_bytes;   // quantised-input slots: header | B fragments (| s1)
   uint32_t red1_bytes, red2_bytes;       // per-limb row sums (row tiles of the largest stage)
   uint32_t bs2_s1_off;        // s1 slice offset in a stage-2 slot (after the t fragments)
   uint32_t warps1;            // consumer warps of the stage-1 group (4 or 6; the rest run stage 2)
   uint32_t has_pre;
+  // SM partitions: CTAs [i P, (i+1) P) run the steps list[list_off[i] .. list_off[i+1])
+  // (one partition of G CTAs unless every step is independent, pass_build)
+  const uint32_t* list;
+  uint32_t nsub, P;
+  uint32_t list_off[kMaxSub + 1];
   uint32_t debug;  // NQB_PASS_DEBUG bits (experiments only): 1 skip MMA, 2 skip quantise, 4 suspend
                    // waits, 8 skip publish/outputs, 32 no weight copies
   unsigned long long* trace;  // diagnostics: G x (kPassStamps K + 2) %globaltimer stamps
@@ -121,6 +129,7 @@ struct nqb_pass {
   // step inputs and layer outputs (nqb_pass_run_host)
   std::vector<void*> x_dev, y_dev;
   std::vector<size_t> x_bytes, y_bytes;
+  std::vector<nqb_group*> owned;  // partition plans built for this pass (freed with it)
 };
 
 namespace nqb {

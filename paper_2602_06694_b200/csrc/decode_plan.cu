@@ -50,13 +50,32 @@ __host__ __device__ __forceinline__ void unit_pos(uint32_t nq, uint32_t lane, ui
   kk = 32 * q + 16 * (i >> 1) + 4 * c + b;
 }
 
+// Bytes of one row tile over all slabs of a stage (stage 1: the CTA's slabs of m,
+// stage 2: every slab of r).
+__device__ uint32_t stage_tile_bytes(const Cta& C, bool st1, uint32_t m, uint32_t r) {
+  uint32_t b = 0;
+  if (st1)
+    for (uint32_t q = C.s1_sl0; q < (uint32_t)C.s1_sl0 + C.s1_sln; ++q) b += unit_bytes(slab_of(m, q).nq);
+  else
+    for (uint32_t q = 0, ns = nslabs(r); q < ns; ++q) b += unit_bytes(slab_of(r, q).nq);
+  return b;
+}
+
 // One block per CTA of the plan: writes that CTA's byte stream.
+// Slab-major (per-call kernel): per stage, section = slab, the CTA's row tiles
+// back to back.  Pair-major (pm, decode-pass plans): per stage, row-tile pair
+// after pair, each pair's slabs in order with the pair's two units of a slab
+// adjacent, so any run of slabs of one pair is one contiguous byte range:
+//   offset(pair p, slab i, tile j) = 2p Utot + nt_p U_i + j ub_i
+// (Utot: bytes of a tile over the stage's slabs, U_i: of its first i slabs,
+// nt_p: tiles in pair p).
 __global__ void k_relayout(const Cta* __restrict__ ctas, const Seg* __restrict__ segs,
-                           uint32_t m, RelayoutSrc src, uint32_t* __restrict__ out) {
+                           uint32_t m, RelayoutSrc src, uint32_t* __restrict__ out, int pm) {
   const Cta C = ctas[blockIdx.x];
   uint32_t* dst = out + C.stream_off / 4;
   uint32_t sec_words_off = 0;
   const uint32_t n1 = C.s1_rtn ? C.s1_sln : 0;
+  uint32_t u_cum = 0, stage_w = 0;  // pair-major: U_i of the current stage, its first word
   for (uint32_t sec = 0; sec < C.nsec; ++sec) {
     const bool st1 = sec < n1;
     const uint32_t seg = st1 ? C.s1_seg : C.s2_seg;
@@ -67,8 +86,16 @@ __global__ void k_relayout(const Cta* __restrict__ ctas, const Seg* __restrict__
     const uint32_t rt0 = st1 ? C.s1_rt0 : C.s2_rt0;
     const uint32_t unit_words = 16 * sl.nq, lane_words = sl.nq / 2;
     const uint32_t words = rtn * unit_words;
+    if (sec == n1 && sec) {  // stage 2 starts after the whole stage-1 block
+      stage_w = sec_words_off;
+      u_cum = 0;
+    }
+    const uint32_t utot = pm ? stage_tile_bytes(C, st1, m, S.r) : 0u;
     for (uint32_t x = threadIdx.x; x < words; x += blockDim.x) {
       const uint32_t t = x / unit_words, rem = x % unit_words;
+      const uint32_t nt = (t | 1u) < rtn ? 2u : 1u;
+      const uint32_t dw = pm ? stage_w + (2 * (t / 2) * utot + nt * u_cum + (t & 1) * 4 * unit_words) / 4 + rem
+                             : sec_words_off + x;
       const uint32_t lane = rem / lane_words, wl = rem % lane_words;
       uint32_t v = 0;
       for (uint32_t p = 0; p < 32; ++p) {
@@ -85,9 +112,10 @@ __global__ void k_relayout(const Cta* __restrict__ ctas, const Seg* __restrict__
         }
         v |= bit << p;
       }
-      dst[sec_words_off + x] = v;
+      dst[dw] = v;
     }
     sec_words_off += words;
+    u_cum += 4 * unit_words;
   }
 }
 
@@ -133,7 +161,9 @@ inline void split_range(uint32_t total, uint32_t parts, uint32_t idx, uint32_t& 
 
 }  // namespace
 
-nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_t count) {
+nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_t count,
+                       uint32_t grid_cap, uint32_t max_rt, bool pass_only) {
+  if (!max_rt) max_rt = kMaxRt;
   NQB_REQUIRE(count >= 1 && count <= (uint32_t)kMaxSeg, NQB_E_VALIDATION,
               "a decode group holds 1.." + std::to_string(kMaxSeg) + " layers");
   const uint32_t m = layers[0]->m;
@@ -173,7 +203,8 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
     B1tot += B1[s];
   }
 
-  const uint32_t Gmax = std::min<uint32_t>((uint32_t)ctx->num_sms, kMaxGrid);
+  uint32_t Gmax = std::min<uint32_t>((uint32_t)ctx->num_sms, kMaxGrid);
+  if (grid_cap) Gmax = std::min(Gmax, grid_cap);
   const uint32_t min_cta_bytes = env_u32("NQB_DEC_MIN_CTA_BYTES", 8192);
   uint32_t G = (uint32_t)std::min<uint64_t>(Gmax, std::max<uint64_t>(1, (Btot + min_cta_bytes - 1) /
                                                                          min_cta_bytes));
@@ -213,7 +244,7 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
         const uint32_t Gk = std::min(RT1[s], G1[s] / Gj);
         if (!Gk) continue;
         const uint32_t rt_max = (RT1[s] + Gk - 1) / Gk, sl_max = (S1 + Gj - 1) / Gj;
-        if (rt_max > (uint32_t)kMaxRt || sl_max > (uint32_t)kMaxSlabs1) continue;
+        if (rt_max > max_rt || sl_max > (uint32_t)kMaxSlabs1) continue;
         // bytes of the heaviest block (slab groups from split_range)
         uint64_t heavy = 0;
         for (uint32_t j = 0; j < Gj; ++j) {
@@ -223,9 +254,13 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
           for (uint32_t q = lo; q < lo + cnt; ++q) b += u1[q];
           heavy = std::max(heavy, b);
         }
-        // bytes streamed + the CTA's quantisation work (kQuantBytes per input)
-        const double cost = ((double)rt_max * heavy + quant_bytes * 256.0 * sl_max) *
-                            (1.0 + 1e-3 * Gj);
+        // bytes streamed + the CTA's quantisation work (kQuantBytes per input).
+        // A pass plan takes the fewest slab groups that fit: its work items are runs
+        // of one tile pair over the CTA's slabs, so long slab ranges mean long MMA
+        // runs per flush (the pass quantises in helper warps, off the MMA path).
+        const double cost = pass_only ? (double)Gj * 1e15 + (double)rt_max * heavy
+                                      : ((double)rt_max * heavy + quant_bytes * 256.0 * sl_max) *
+                                            (1.0 + 1e-3 * Gj);
         if (cost < best) {
           best = cost;
           bGk = Gk;
@@ -298,15 +333,15 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
       uint32_t given = 0;
       for (uint32_t i = 0; i < nc; ++i) {
         const double x = w[i] / ws * RT2[s];
-        k[i] = std::min<uint32_t>((uint32_t)std::floor(x), kMaxRt);
+        k[i] = std::min<uint32_t>((uint32_t)std::floor(x), max_rt);
         rem[i] = {x - k[i], i};
         given += k[i];
       }
       std::sort(rem.begin(), rem.end(), [](auto& x, auto& y) { return x.first > y.first; });
-      for (uint32_t pass = 0; given < RT2[s] && pass < 2 * kMaxRt; ++pass)
+      for (uint32_t pass = 0; given < RT2[s] && pass < 2 * max_rt; ++pass)
         for (auto& pr : rem) {
           if (given >= RT2[s]) break;
-          if (k[pr.second] < (uint32_t)kMaxRt) {
+          if (k[pr.second] < max_rt) {
             k[pr.second]++;
             given++;
           }
@@ -334,6 +369,8 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   g->m = m;
   g->R1 = R1;
   g->grid = G;
+  g->pass_only = pass_only;
+  for (uint32_t s = 0; s < count; ++s) g->layers[s] = layers[s];
   uint64_t off = 0, max_stream = 0;
   uint32_t bfrag = 0;
   std::vector<uint64_t> sbytes(G);
@@ -394,8 +431,8 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   }
   if (slot) {
     slot = (slot + 127) / 128 * 128;
-    buf = std::min(buf / slot, kMaxBars) * slot;
-    NQB_REQUIRE(buf / slot >= 2, NQB_E_DIMENSION_MISMATCH,
+    buf = std::max<uint32_t>(std::min(buf / slot, kMaxBars), pass_only ? 2 : 0) * slot;
+    NQB_REQUIRE(pass_only || buf / slot >= 2, NQB_E_DIMENSION_MISMATCH,
                 "decode ring needs two slots (NQB_DEC_SMEM_KB too small)");
     nbar = std::max<uint32_t>(nbar, buf / slot);
   }
@@ -405,7 +442,9 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   g->bfrag_bytes = (bfrag + 127) / 128 * 128;
   const uint32_t head = head_bytes(nbar);  // decode.cuh
   g->smem_bytes = head + g->bfrag_bytes + buf;
-  NQB_REQUIRE(g->smem_bytes <= 227 * 1024, NQB_E_DIMENSION_MISMATCH,
+  // a pass-only plan (larger CTA blocks, pass_build) is never run by the per-call
+  // kernel, so its per-call shared-memory footprint does not matter
+  NQB_REQUIRE(pass_only || g->smem_bytes <= 227 * 1024, NQB_E_DIMENSION_MISMATCH,
               "decode plan exceeds shared memory (" + std::to_string(g->smem_bytes) + " B)");
 
   // ---- device buffers --------------------------------------------------------
@@ -443,7 +482,8 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
     }
     NQB_CUDA(cudaMemcpyAsync(dsegs, g->seg, sizeof(Seg) * kMaxSeg, cudaMemcpyHostToDevice,
                              ctx->stream));
-    k_relayout<<<G, 256, 0, ctx->stream>>>(dctas, dsegs, m, src, (uint32_t*)g->bits);
+    k_relayout<<<G, 256, 0, ctx->stream>>>(dctas, dsegs, m, src, (uint32_t*)g->bits,
+                                           pass_only ? 1 : 0);
     NQB_LAUNCHED(ctx);
     uint32_t hmax[kMaxSeg] = {0};
     NQB_CUDA(cudaMemcpyAsync(hmax, dmax, 4 * kMaxSeg, cudaMemcpyDeviceToHost, ctx->stream));
@@ -453,7 +493,7 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
     NQB_CUDA(cudaStreamSynchronize(ctx->stream));
     for (uint32_t s = 0; s < count; ++s)
       g->seg[s].s2max = (float)host_half_to_double((uint16_t)hmax[s]);
-    dec_state_reserve(ctx, R1);
+    if (!pass_only) dec_state_reserve(ctx, R1);
   } catch (...) {
     group_free(g);
     throw;

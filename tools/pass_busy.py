@@ -56,14 +56,25 @@ def main():
     tr = p.trace().astype(np.int64)
     G, K = tr.shape[0], len(steps)
     t0 = tr[:, 0].min()
-    raw = tr[:, 1:1 + 24 * K].reshape(G, K, 24)
+    raw = tr[:, 1:1 + 24 * K].reshape(G, K, 24).astype(float)
+    # SM partitions: a CTA stamps only the steps of its own partition
+    raw[raw[:, :, 0] == 0] = np.nan
     st = (raw - t0) / 1e3
     span = (tr[:, 24 * K + 1].max() - t0) / 1e3
     kinds = ["qkv", "o", "gateup", "down"]
     out = {"model": args.model, "blocks": args.blocks, "span_us": span,
            "gbs_traced": p.algorithmic_bytes / span / 1e3}
-    s1_prev_end = np.concatenate([np.zeros((G, 1)), st[:, :-1, 1]], axis=1)
-    s2_prev_end = np.concatenate([np.zeros((G, 1)), st[:, :-1, 3]], axis=1)
+    def prev_end(col):  # the end of the CTA's previous step (its own partition's list)
+        out = np.full((G, K), np.nan)
+        for c in range(G):
+            last = 0.0
+            for k in range(K):
+                if not np.isnan(st[c, k, col]):
+                    out[c, k] = last
+                    last = st[c, k, col]
+        return out
+    s1_prev_end = prev_end(1)
+    s2_prev_end = prev_end(3)
     ph = {
         "s1_wait": st[:, :, 0] - s1_prev_end, "s1_quant": st[:, :, 7] - st[:, :, 0],
         "s1_mma": st[:, :, 8] - st[:, :, 7], "s1_pub": st[:, :, 1] - st[:, :, 8],
@@ -71,24 +82,26 @@ def main():
         "s2_mma": st[:, :, 10] - st[:, :, 9], "s2_out": st[:, :, 3] - st[:, :, 10],
         "tbar_after_s1end_max": st[:, :, 4] - st[:, :, 1].max(axis=0, keepdims=True),
         "s1_chunk_wait": raw[:, :, 16] / 1965.0, "s2_chunk_wait": raw[:, :, 17] / 1965.0,
-        "s1_chunks": (raw[:, :, 18] >> 48).astype(float), "s2_chunks": (raw[:, :, 19] >> 48).astype(float),
-        "s1_calls": ((raw[:, :, 18] >> 32) & 0xFFFF).astype(float),
-        "s2_calls": ((raw[:, :, 19] >> 32) & 0xFFFF).astype(float),
-        "s1_slabs": ((raw[:, :, 18] >> 16) & 0xFFFF).astype(float),
-        "s2_slabs": ((raw[:, :, 19] >> 16) & 0xFFFF).astype(float),
+        "s1_chunks": np.floor(raw[:, :, 18] / 2.0 ** 48), "s2_chunks": np.floor(raw[:, :, 19] / 2.0 ** 48),
+        "s1_calls": np.floor(raw[:, :, 18] / 2.0 ** 32) % 65536,
+        "s2_calls": np.floor(raw[:, :, 19] / 2.0 ** 32) % 65536,
+        "s1_slabs": np.floor(raw[:, :, 18] / 2.0 ** 16) % 65536,
+        "s2_slabs": np.floor(raw[:, :, 19] / 2.0 ** 16) % 65536,
         "s1_runpair_us": raw[:, :, 20] / 1965.0, "s2_runpair_us": raw[:, :, 21] / 1965.0,
         "s1_loop_us": raw[:, :, 22] / 1965.0, "s2_loop_us": raw[:, :, 23] / 1965.0,
     }
     for i, kd in enumerate(kinds):
         sel = [k for k in range(K) if k % 4 == i and k >= 4]
-        out[kd] = {nm: round(float(np.median(v[:, sel])), 3) for nm, v in ph.items()}
-        out[kd]["s1end_spread"] = round(float(np.median(st[:, sel, 1].max(0) - st[:, sel, 1].min(0))), 3)
-    busy1 = (ph["s1_quant"] + ph["s1_mma"] + ph["s1_pub"]).sum(1) / span
-    busy2 = (ph["s2_quant"] + ph["s2_mma"] + ph["s2_out"]).sum(1) / span
-    mma1 = ph["s1_mma"].sum(1) / span
-    mma2 = ph["s2_mma"].sum(1) / span
+        out[kd] = {nm: round(float(np.nanmedian(v[:, sel])), 3) for nm, v in ph.items()}
+        out[kd]["s1end_spread"] = round(float(np.nanmedian(np.nanmax(st[:, sel, 1], 0) -
+                                                           np.nanmin(st[:, sel, 1], 0))), 3)
+    busy1 = np.nansum(ph["s1_quant"] + ph["s1_mma"] + ph["s1_pub"], 1) / span
+    busy2 = np.nansum(ph["s2_quant"] + ph["s2_mma"] + ph["s2_out"], 1) / span
+    mma1 = np.nansum(ph["s1_mma"], 1) / span
+    mma2 = np.nansum(ph["s2_mma"], 1) / span
     out["busy"] = {"s1": float(np.median(busy1)), "s2": float(np.median(busy2)),
                    "s1_mma": float(np.median(mma1)), "s2_mma": float(np.median(mma2))}
+    out["cta_end_us"] = {"min": float((tr[:, 24 * K + 1].min() - t0) / 1e3), "max": span}
     print(json.dumps(out), flush=True)
 
 

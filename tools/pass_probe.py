@@ -49,11 +49,14 @@ def main():
     ap.add_argument("--blocks", type=int, default=0, help="override block count")
     ap.add_argument("--chained", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--sms", type=int, default=0, help="SM budget of the context (plans and pass grid)")
     args = ap.parse_args()
     import torch
 
     import paper_2602_06694_b200 as nq
     ctx = nq.context(0)
+    if args.sms:
+        ctx.set_sm_budget(args.sms)
     stream = torch.cuda.Stream()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6538.6
@@ -88,7 +91,7 @@ def main():
                 steps.append((u, x, y))
                 ls = u.layers if isinstance(u, nq.DecodeGroup) else [u]
                 nbytes += sum(algo(l.n, l.m, l.r) for l in ls) - 2 * ls[0].m * (len(ls) - 1)
-        out = {"model": model, "blocks": blocks, "bpw": bpw, "ranks": ranks,
+        out = {"model": model, "sms": args.sms, "blocks": blocks, "bpw": bpw, "ranks": ranks,
                "algo_bytes_per_pass": nbytes, "chained": args.chained}
 
         def timeit(fn, reps):
