@@ -39,6 +39,14 @@ __device__ __forceinline__ void poll_ctr(const unsigned long long* c, unsigned l
   // the data behind the barrier is read next by TMA (async proxy)
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
+// Bulk prefetch of [p, p + bytes) into L2 (no shared memory, no completion).
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  for (uint32_t o = 0; o < bytes; o += 32768u) {
+    const uint32_t n = min(32768u, bytes - o);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"((const char*)p + o), "r"(n)
+                 : "memory");
+  }
+}
 __device__ __forceinline__ void arrive_ctr(unsigned long long* c) {
   asm volatile("red.release.gpu.global.add.u64 [%0], 1;\n" ::"l"(c) : "memory");
 }
@@ -178,6 +186,37 @@ struct ChunkRec {
 };
 static_assert(sizeof(ChunkRec) <= 16, "chunk record slot");
 
+// Adds the 4 accumulator chains of one row tile to the per-limb row sums
+// red[row][kLimbs] (int32, like flush_rows but packed: kLimbs ints per row):
+// lane c adds limbs 2c, 2c+1 of rows g and g+8 with 32-bit shared atomics
+// (native; a 64-bit shared atomic add is a CAS loop on sm_100).
+__device__ __forceinline__ void flush_rows6(int (&acc)[4][4], int* red, int lane) {
+  const int g = lane >> 2, c = lane & 3;
+  if (c < (kLimbs + 1) / 2) {
+    int s[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[i] = acc[0][i] + acc[1][i] + acc[2][i] + acc[3][i];
+    int* r0 = red + g * kLimbs + 2 * c;
+    int* r1 = red + (g + 8) * kLimbs + 2 * c;
+    atomicAdd(r0, s[0]);
+    atomicAdd(r0 + 1, s[1]);
+    atomicAdd(r1, s[2]);
+    atomicAdd(r1 + 1, s[3]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0;
+}
+// sum_K bit * value of a row from its packed limb sums, and clears them
+__device__ __forceinline__ long long take_row6(int* row) {
+  unsigned long long v = 0;
+#pragma unroll
+  for (int l = 0; l < kLimbs; ++l) {
+    v += (unsigned long long)(long long)row[l] << (8 * l);
+    row[l] = 0;
+  }
+  return (long long)v >> 7;
+}
+
 // One work item resident at `base` (pair-major: the pair's units of slab a, then
 // of slab a+1, ...): its MMAs, flushed into red[] (the pair's rows).  The full
 // slabs run software-pipelined (full_run; the next slab of a tile is nt * 512
@@ -213,8 +252,8 @@ __device__ __forceinline__ void run_item(const uint8_t* base, const StageGeo& g,
     else tiles_mma<1>(unit, ub, sl.nq, lane, bv, acc);
     unit += (two ? 2u : 1u) * ub;
   }
-  flush_rows(acc[0], red + t0 * 16 * kRedStride, lane);
-  if (two) flush_rows(acc[1], red + (t0 + 1) * 16 * kRedStride, lane);
+  flush_rows6(acc[0], red + t0 * 16 * kLimbs, lane);
+  if (two) flush_rows6(acc[1], red + (t0 + 1) * 16 * kLimbs, lane);
 }
 
 // max|x| bits over x[lo, hi): binary16 magnitude bits (>= 0x7C00: non-finite)
@@ -249,6 +288,34 @@ __device__ __noinline__ uint32_t absmax_bits(const void* x, uint32_t lo, uint32_
     for (uint32_t j = i; j < min(hi, i + 8); ++j) mb = max(mb, (uint32_t)(__ldcg(xh + j) & 0x7FFFu));
   } else {
     for (uint32_t j = lo + t; j < hi; j += nt) mb = max(mb, (uint32_t)(__ldcg(xh + j) & 0x7FFFu));
+  }
+  return mb;
+}
+// max|x| bits over one 8-element unit x[a, b) (a 8-aligned; same encoding as
+// absmax_bits), inlined so several units' loads are in flight together.
+__device__ __forceinline__ uint32_t unit_absmax(const void* x, uint32_t a, uint32_t b, bool f32,
+                                                bool vec) {
+  uint32_t mb = 0;
+  if (f32) {
+    const uint32_t* xf = (const uint32_t*)x;
+    if (vec && b - a == 8) {
+      const uint4 v0 = __ldcg((const uint4*)(xf + a)), v1 = __ldcg((const uint4*)(xf + a + 4));
+      const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mb = max(mb, w[e] & 0x7FFFFFFFu);
+    } else {
+      for (uint32_t j = a; j < b; ++j) mb = max(mb, __ldcg(xf + j) & 0x7FFFFFFFu);
+    }
+    return mb >= 0x7F800000u ? 0x7F800000u : mb;
+  }
+  const unsigned short* xh = (const unsigned short*)x;
+  if (vec && b - a == 8) {
+    const uint4 v = __ldcg((const uint4*)(xh + a));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) mb = max(mb, max(w[e] & 0x7FFFu, (w[e] >> 16) & 0x7FFFu));
+  } else {
+    for (uint32_t j = a; j < b; ++j) mb = max(mb, (uint32_t)(__ldcg(xh + j) & 0x7FFFu));
   }
   return mb;
 }
@@ -298,7 +365,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   float* xmaxs = (float*)(dslots + kDescSlots * kDescSlotBytes + 256);  // max|x| of steps in flight (ring of 16)
   ChunkRec* recs1 = (ChunkRec*)((uint8_t*)xmaxs + 64);
   ChunkRec* recs2 = recs1 + kPassSlots;
-  int* red1 = (int*)(smem + pass_head_bytes());       // stage-1 row sums
+  int* red1 = (int*)(smem + pass_head_bytes());       // stage-1 row sums (kLimbs ints per row)
   int* red2 = (int*)((uint8_t*)red1 + p.red1_bytes);  // stage-2 row sums
   uint8_t* bslots1 = (uint8_t*)red2 + p.red2_bytes;   // header | B fragments of x
   constexpr uint32_t NB = kBSlots;
@@ -390,6 +457,18 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         const uint32_t k = D.idx;
         const StageGeo g = r ? stage2_geo(D, C) : stage1_geo(D, C);
         if (kTrace) PSTAMP(k, r ? 14 : 11);
+        // The weights do not depend on x: while this step streams through the
+        // ring, pull the stage's bytes of step j + ahead from HBM into L2, so the
+        // ring's copies see L2 latency (the ring alone holds too few bytes in
+        // flight to cover HBM latency at the SM's share of the bandwidth).
+        if (p.l2_ahead) {  // step 0: steps 1..ahead; later: the new edge j + ahead
+          const uint32_t hi = min(Kc - 1, j + p.l2_ahead);
+          for (uint32_t ja = j == 0 ? 1u : j + p.l2_ahead; ja <= hi; ++ja) {
+            wait_desc(ja);  // fetched ahead by sequencer 2 (ahead < kDescSlots)
+            const StageGeo ga = r ? stage2_geo(desc_of(ja), cta_of(ja)) : stage1_geo(desc_of(ja), cta_of(ja));
+            if (ga.nsec) l2_prefetch(desc_of(ja).bits + ga.src_off, ga.rtn * cum_bytes(ga, ga.nsec));
+          }
+        }
         uint64_t src = g.src_off;
         const StageItems T = stage_items(g, S);
         const uint32_t GWr = r ? kConsumerWarps - kW1 : kW1;  // items per wave
@@ -727,10 +806,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       if (!gid) {  // stage-1 publish: t rows (exact int64 reds)
         long long* Tseg = arena + D.t_off + S.t_off + (size_t)C.s1_rt0 * 16;
         for (uint32_t i = gt; i < (uint32_t)C.s1_rtn * 16; i += GT) {
-          const long long v = 2 * row_value(red + i * kRedStride) - A;
-          int4* rr = (int4*)(red + i * kRedStride);
-          rr[0] = make_int4(0, 0, 0, 0);
-          rr[1] = make_int4(0, 0, 0, 0);
+          const long long v = 2 * take_row6(red + i * kLimbs) - A;
           red_add_u64(&Tseg[i], v);
         }
       } else {  // stage-2 outputs (packed.cpp:174-190)
@@ -744,9 +820,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         uint32_t ymb = 0;
         for (uint32_t i = gt; i < (uint32_t)C.s2_rtn * 16; i += GT) {
           const uint32_t row = C.s2_rt0 * 16 + i;
-          int4* rr = (int4*)(red + i * kRedStride);
           if (row < S.n) {
-            const long long Yi = 2 * row_value(red + i * kRedStride) - A;
+            const long long Yi = 2 * take_row6(red + i * kLimbs) - A;
             double y = (double)__half2float(sc1[i]) *
                        ((double)Yi * __longlong_as_double((long long)(1023 + E) << 52));  // packed.cpp:189
             if (nonfinite) y = __longlong_as_double(0x7ff8000000000000ll);
@@ -760,9 +835,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
               ((__half*)Y)[row] = h;
               ymb = max(ymb, (uint32_t)(__half_as_ushort(h) & 0x7FFFu));
             }
+          } else {
+            (void)take_row6(red + i * kLimbs);  // padding row (zero bits): keep it clear
           }
-          rr[0] = make_int4(0, 0, 0, 0);
-          rr[1] = make_int4(0, 0, 0, 0);
         }
         if (D.flags & kStepPublish) {
 #pragma unroll
@@ -856,8 +931,8 @@ PassGeo pass_geo(uint32_t K, const std::vector<const nqb_group*>& plan, uint32_t
   q.bslot1_b = (kBSlotHead + std::max(q.bf1, 16u) + 127) / 128 * 128;
   q.bs2_s1_off = (kBSlotHead + std::max(q.bf2, 16u) + 127) / 128 * 128;
   q.bslot2_b = (q.bs2_s1_off + q.s1bytes + 127) / 128 * 128;
-  q.red1_b = q.rt1 * 16 * kRedStride * 4;
-  q.red2_b = q.rt2 * 16 * kRedStride * 4;
+  q.red1_b = (q.rt1 * 16 * 4 * kLimbs + 127) / 128 * 128;
+  q.red2_b = (q.rt2 * 16 * 4 * kLimbs + 127) / 128 * 128;
   q.fixed = pass_head_bytes() + q.red1_b + q.red2_b + kBSlots * (q.bslot1_b + q.bslot2_b);
   // a ring chunk is a wave of work items (<= 8 tile pairs over <= item_slabs
   // slabs); each ring holds at least one
@@ -1039,7 +1114,9 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     // Rings split what the staging leaves in proportion to the two stages' bytes.
     const uint32_t rings = (227u * 1024u - geo.fixed) / 256 * 256;
     const double f1 = geo.bits1 + geo.bits2 > 0 ? geo.bits1 / (geo.bits1 + geo.bits2) : 0.5;
-    uint32_t ring1 = (uint32_t)(rings * f1) / 128 * 128;
+    // NQB_PASS_RING1_PCT: stage-1 share of the rings in percent (default: bytes)
+    const uint32_t r1pct = env_u32p("NQB_PASS_RING1_PCT", 0);
+    uint32_t ring1 = (uint32_t)(rings * (r1pct ? r1pct / 100.0 : f1)) / 128 * 128;
     ring1 = std::min(std::max(ring1, geo.min1), rings - geo.min2);
     const uint32_t ring2 = rings - ring1;
 
@@ -1091,6 +1168,10 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     pp.arena = d_arena;
     pp.arena_len = arena;
     pp.has_pre = has_pre ? 1 : 0;
+    pp.pre_units = 0;
+    for (uint32_t k = 0; k < K; ++k)
+      if (desc[k].flags & kStepXPre)
+        pp.pre_units = std::max<uint32_t>(pp.pre_units, ((desc[k].m + 7) / 8 + G - 1) / G);
     pp.debug = env_u32p("NQB_PASS_DEBUG", 0);
     pp.red1_bytes = geo.red1_b;
     pp.red2_bytes = geo.red2_b;
@@ -1105,11 +1186,12 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     {
       const uint32_t w1 = geo.max_s2_cta_bytes > 96u * 1024u ? 4u : 6u;
       const uint32_t ew = env_u32p("NQB_PASS_WARPS1", 0);
-      pp.warps1 = ew == 4 || ew == 6 ? ew : w1;  // the kernel is instantiated for 4 and 6
+      pp.warps1 = ew == 3 || ew == 4 || ew == 6 ? ew : w1;  // the kernel is instantiated for 3, 4, 6
     }
     pp.ring1_bytes = ring1;
     pp.ring2_bytes = ring2;
     pp.item_slabs = item_slabs;
+    pp.l2_ahead = std::min<uint32_t>(env_u32p("NQB_PASS_L2_AHEAD", 0), kDescSlots - 4);
     P->smem_bytes = geo.fixed + rings;
     if (env_u32p("NQB_PASS_VERBOSE", 0))
       std::fprintf(stderr,
@@ -1129,7 +1211,7 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     P->stream_bytes = stream_bytes;
     P->algo_bytes = (uint64_t)algo;
     for (auto fn : {k_decode_pass<false, 6>, k_decode_pass<true, 6>, k_decode_pass<false, 4>,
-                    k_decode_pass<true, 4>})
+                    k_decode_pass<true, 4>, k_decode_pass<false, 3>, k_decode_pass<true, 3>})
       NQB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)P->smem_bytes));
     int per_sm = 0;
@@ -1160,8 +1242,11 @@ void pass_launch(nqb_context* ctx, const nqb_pass* P, unsigned long long* trace)
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const bool w4 = pp.warps1 == 4;
-  if (trace) NQB_CUDA(cudaLaunchKernelEx(&cfg, w4 ? k_decode_pass<true, 4> : k_decode_pass<true, 6>, pp));
-  else NQB_CUDA(cudaLaunchKernelEx(&cfg, w4 ? k_decode_pass<false, 4> : k_decode_pass<false, 6>, pp));
+  const bool w3 = pp.warps1 == 3;
+  if (trace)
+    NQB_CUDA(cudaLaunchKernelEx(&cfg, w3 ? k_decode_pass<true, 3> : w4 ? k_decode_pass<true, 4> : k_decode_pass<true, 6>, pp));
+  else
+    NQB_CUDA(cudaLaunchKernelEx(&cfg, w3 ? k_decode_pass<false, 3> : w4 ? k_decode_pass<false, 4> : k_decode_pass<false, 6>, pp));
   NQB_LAUNCHED(ctx);
 }
 

@@ -89,11 +89,13 @@ struct PassParams {
   uint32_t amax_words;
   uint32_t ring1_bytes, ring2_bytes;     // stage-1 / stage-2 weight rings
   uint32_t item_slabs;        // slabs per work item (ring chunk): one warp, one flush
+  uint32_t l2_ahead;          // producers prefetch a step's stage bytes into L2 this many steps ahead
   uint32_t bslot1_bytes, bslot2_bytes;   // quantised-input slots: header | B fragments (| s1)
   uint32_t red1_bytes, red2_bytes;       // per-limb row sums (row tiles of the largest stage)
   uint32_t bs2_s1_off;        // s1 slice offset in a stage-2 slot (after the t fragments)
   uint32_t warps1;            // consumer warps of the stage-1 group (4 or 6; the rest run stage 2)
   uint32_t has_pre;
+  uint32_t pre_units;         // most 8-element units of one step's input in a CTA's prepass share
   // SM partitions: CTAs [i P, (i+1) P) run the steps list[list_off[i] .. list_off[i+1])
   // (one partition of G CTAs unless every step is independent, pass_build)
   const uint32_t* list;

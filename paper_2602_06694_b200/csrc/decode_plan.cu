@@ -211,6 +211,11 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   G = std::max(G, count);
 
   const double quant_bytes = env_u32("NQB_DEC_QUANT_X100", (uint32_t)(kQuantBytes * 100)) / 100.0;
+  // measured (tools/gpu_pass_envab.sh): whole-input ranges (16 slabs) for m <= 4096
+  // (7B pass: 1274 vs 1231 GB/s for 8), 8 slabs above (70B pass: 1758 vs 1378 GB/s:
+  // the smaller quantised-x staging leaves more shared memory to the rings)
+  const uint32_t pass_slabs = std::min<uint32_t>(
+      std::max<uint32_t>(env_u32("NQB_PASS_PLAN_SLABS", m <= 4096 ? 16 : 8), 1), kMaxSlabs1);
   std::vector<Cta> ctas;
   for (;; ++G) {
     NQB_REQUIRE(G <= Gmax, NQB_E_DIMENSION_MISMATCH,
@@ -255,10 +260,12 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
           heavy = std::max(heavy, b);
         }
         // bytes streamed + the CTA's quantisation work (kQuantBytes per input).
-        // A pass plan takes the fewest slab groups that fit: its work items are runs
-        // of one tile pair over the CTA's slabs, so long slab ranges mean long MMA
-        // runs per flush (the pass quantises in helper warps, off the MMA path).
-        const double cost = pass_only ? (double)Gj * 1e15 + (double)rt_max * heavy
+        // A pass plan takes slab ranges of up to pass_slabs slabs, as long as fit: its work items are runs of one tile pair over the
+        // CTA's slabs (long runs per flush), while the quantised-x staging grows with
+        // the range (the pass quantises in helper warps, off the MMA path).
+        const double cost = pass_only ? (double)(sl_max > pass_slabs ? sl_max - pass_slabs + 64
+                                                                     : pass_slabs - sl_max) *
+                                                1e15 + (double)rt_max * heavy
                                       : ((double)rt_max * heavy + quant_bytes * 256.0 * sl_max) *
                                             (1.0 + 1e-3 * Gj);
         if (cost < best) {
