@@ -388,9 +388,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   if (tid == 0) {
     for (int s = 0; s < kPassSlots; ++s) {
       tc::mbar_init(&full1[s], 1);
-      tc::mbar_init(&empty1[s], kW1);  // a chunk is a wave: one item per warp of the group
+      // a chunk is a wave of W = GW / wave_div items, one per warp of W warps
+      tc::mbar_init(&empty1[s], kW1 / p.wave_div);
       tc::mbar_init(&full2[s], 1);
-      tc::mbar_init(&empty2[s], kConsumerWarps - kW1);
+      tc::mbar_init(&empty2[s], (kConsumerWarps - kW1) / p.wave_div);
     }
     for (int s = 0; s < kDescSlots; ++s) {
       tc::mbar_init(&dfull[s], 1);
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         }
         uint64_t src = g.src_off;
         const StageItems T = stage_items(g, S);
-        const uint32_t GWr = r ? kConsumerWarps - kW1 : kW1;  // items per wave
+        const uint32_t GWr = (r ? kConsumerWarps - kW1 : kW1) / p.wave_div;  // items per wave
         ItemCur c0{0, 0}, c1 = item_cur(T, min(GWr, T.nitems));
         uint32_t o0 = 0;
         for (uint32_t i0 = 0; i0 < T.nitems; i0 += GWr) {
@@ -747,18 +748,22 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     const StageItems T = stage_items(g, p.item_slabs);
     const uint32_t nitems = T.nitems;
     if (!nitems) return;
-    ItemCur c0{0, 0}, ci = item_cur(T, (uint32_t)gw);  // the wave's first item, this warp's
+    // waves of W items: item i is run by warp i % GW and lives in chunk i / W;
+    // W divides GW, so a warp's items sit at the same place gw % W of their
+    // waves.  In the last wave, positions past the items still wait and release.
+    const uint32_t W = (uint32_t)GW / p.wave_div, nwav = (nitems + W - 1) / W;
+    const uint32_t lead = (uint32_t)gw % W;
+    ItemCur c0 = item_cur(T, (uint32_t)gw - lead), ci = item_cur(T, (uint32_t)gw);
     unsigned long long wsum = 0, nch = 0, rsum = 0;
     const unsigned long long l0 = kTrace ? clock64() : 0ull;
-    for (uint32_t i0 = 0; i0 < nitems; i0 += GW) {
-      const uint32_t slot = chunk % kPassSlots;
+    for (uint32_t i = gw; i < nwav * W; i += GW) {
+      const uint32_t cidx = chunk + i / W, slot = cidx % kPassSlots;
       const unsigned long long w0 = kTrace ? clock64() : 0ull;
-      mbar_wait_wd(&fullr[slot], (chunk / kPassSlots) & 1, sus);
+      mbar_wait_wd(&fullr[slot], (cidx / kPassSlots) & 1, sus);
       if (kTrace) {
         wsum += clock64() - w0;
         ++nch;
       }
-      const uint32_t i = i0 + gw;
       if (i < nitems && !(p.debug & 1u)) {
         const ChunkRec cr = recs[slot];
         const uint32_t off = cur_off(g, T, ci) - cur_off(g, T, c0);
@@ -771,8 +776,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       item_advance(ci, T, GW);
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&emptyr[slot]);
-      ++chunk;
     }
+    chunk += nwav;
     if (kTrace && gw == 0 && lane == 0) {  // this warp's time waiting for chunks, and chunks
       trp[1 + kPassStamps * cur_step + 16 + gid] = wsum;
       trp[1 + kPassStamps * cur_step + 18 + gid] = (nch << 48) | (nch << 32) | ((unsigned long long)nitems << 16);
@@ -1034,7 +1039,7 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     std::vector<const nqb_group*> plan(K);
     PassGeo geo;
     {
-      const uint32_t want = chained ? 1u : std::min<uint32_t>(std::max<uint32_t>(env_u32p("NQB_PASS_SPLIT", 4), 1), kMaxSub);
+      const uint32_t want = chained ? 1u : std::min<uint32_t>(std::max<uint32_t>(env_u32p("NQB_PASS_SPLIT", kMaxSub), 1), kMaxSub);
       for (uint32_t ns = want; ns >= 1; --ns) {
         const uint32_t Pc = G / ns;
         std::vector<nqb_group*> made;
@@ -1064,6 +1069,18 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
         if (ok && !gq.fits && env_u32p("NQB_PASS_VERBOSE", 0))
           std::fprintf(stderr, "nqb pass: %u partitions: staging %u B + rings %u + %u B > 227 KB\n",
                        ns, gq.fixed, gq.min1, gq.min2);
+        // more partitions amortise the per-step chain over more bytes per CTA, but
+        // their larger row blocks take shared memory from the weight rings; a
+        // partition count is taken only if the rings keep >= NQB_PASS_MIN_RINGS_KB
+        // (default 88: 7B takes 8 partitions with 90 KB of rings, 1700 GB/s vs 1386
+        // for 4; 70B takes 2 with 112 KB, 1756 GB/s vs 1399 for 3 with 85 KB)
+        const uint32_t rings_left = ok && gq.fits ? 227u * 1024u - gq.fixed : 0u;
+        if (ok && gq.fits && ns > 1 && rings_left < env_u32p("NQB_PASS_MIN_RINGS_KB", 88) * 1024u) {
+          if (env_u32p("NQB_PASS_VERBOSE", 0))
+            std::fprintf(stderr, "nqb pass: %u partitions: rings %u B below the minimum\n", ns,
+                         rings_left);
+          gq.fits = false;
+        }
         if (ok && gq.fits) {
           nsub = ns;
           plan = pl;
@@ -1114,9 +1131,11 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     // Rings split what the staging leaves in proportion to the two stages' bytes.
     const uint32_t rings = (227u * 1024u - geo.fixed) / 256 * 256;
     const double f1 = geo.bits1 + geo.bits2 > 0 ? geo.bits1 / (geo.bits1 + geo.bits2) : 0.5;
-    // NQB_PASS_RING1_PCT: stage-1 share of the rings in percent (default: bytes)
+    // NQB_PASS_RING1_PCT: stage-1 share of the rings in percent.  Default: the
+    // stage-1 share of the bytes, at most 30 % (stage-1 waves are half the size of
+    // stage-2 waves with the 4 + 8 split; 7B: 1700 vs 1668 GB/s)
     const uint32_t r1pct = env_u32p("NQB_PASS_RING1_PCT", 0);
-    uint32_t ring1 = (uint32_t)(rings * (r1pct ? r1pct / 100.0 : f1)) / 128 * 128;
+    uint32_t ring1 = (uint32_t)(rings * (r1pct ? r1pct / 100.0 : std::min(f1, 0.30))) / 128 * 128;
     ring1 = std::min(std::max(ring1, geo.min1), rings - geo.min2);
     const uint32_t ring2 = rings - ring1;
 
@@ -1187,10 +1206,13 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       const uint32_t w1 = geo.max_s2_cta_bytes > 96u * 1024u ? 4u : 6u;
       const uint32_t ew = env_u32p("NQB_PASS_WARPS1", 0);
       pp.warps1 = ew == 3 || ew == 4 || ew == 6 ? ew : w1;  // the kernel is instantiated for 3, 4, 6
+      const uint32_t div = env_u32p("NQB_PASS_WAVE_DIV", 1);
+      pp.wave_div = (div == 2 && pp.warps1 % 2 == 0) ? 2u : 1u;
     }
     pp.ring1_bytes = ring1;
     pp.ring2_bytes = ring2;
     pp.item_slabs = item_slabs;
+    // waves of GW / wave_div items (NQB_PASS_WAVE_DIV 1 or 2; 2 needs even groups)
     pp.l2_ahead = std::min<uint32_t>(env_u32p("NQB_PASS_L2_AHEAD", 0), kDescSlots - 4);
     P->smem_bytes = geo.fixed + rings;
     if (env_u32p("NQB_PASS_VERBOSE", 0))
