@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       // a chunk is a wave of W = GW / wave_div items, one per warp of W warps
       tc::mbar_init(&empty1[s], kW1 / p.wave_div);
       tc::mbar_init(&full2[s], 1);
-      tc::mbar_init(&empty2[s], (kConsumerWarps - kW1) / p.wave_div);
+      tc::mbar_init(&empty2[s], (kConsumerWarps - kW1) / p.wave_div2);
     }
     for (int s = 0; s < kDescSlots; ++s) {
       tc::mbar_init(&dfull[s], 1);
@@ -472,15 +472,21 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         }
         uint64_t src = g.src_off;
         const StageItems T = stage_items(g, S);
-        const uint32_t GWr = (r ? kConsumerWarps - kW1 : kW1) / p.wave_div;  // items per wave
-        ItemCur c0{0, 0}, c1 = item_cur(T, min(GWr, T.nitems));
+        // items per wave; stage 2: whole row tiles (tile-major, row-complete items)
+        const uint32_t GWr = r ? (kConsumerWarps - kW1) / p.wave_div2 : kW1 / p.wave_div;
+        const uint32_t nit = r ? (g.nsec ? g.rtn : 0u) : T.nitems;
+        ItemCur c1 = item_cur(T, min(GWr, T.nitems));
         uint32_t o0 = 0;
-        for (uint32_t i0 = 0; i0 < T.nitems; i0 += GWr) {
-          const uint32_t o1 = cur_off(g, T, c1);
-          const uint32_t sb = o1 - o0;
-          o0 = o1;
-          item_advance(c1, T, GWr);
-          (void)c0;
+        for (uint32_t i0 = 0; i0 < nit; i0 += GWr) {
+          uint32_t sb;
+          if (r) {
+            sb = min(GWr, nit - i0) * T.utot;
+          } else {
+            const uint32_t o1 = cur_off(g, T, c1);
+            sb = o1 - o0;
+            o0 = o1;
+            item_advance(c1, T, GWr);
+          }
           const uint64_t start = ring_place(pos, sb, RB);
           // wait for the slot and for every older chunk this range overwrites: chunks
           // are placed monotonically, so [start, pos) reaches older chunk c's bytes
@@ -786,6 +792,96 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     }
   };
 
+  // Stage 2, row-complete items: an item is one row tile over all slabs of r
+  // (tile-major layout), so the warp that runs it holds the tile's complete row
+  // sums and writes the outputs itself (packed.cpp:174-190): no shared row sums,
+  // no group-wide epilogue after the MMAs.  Waves of W = GW / wave_div2 tiles.
+  auto rc_stage = [&](const StageGeo& g, const StepDesc& D, const Cta& C, uint32_t j, long long A,
+                      const uint8_t* bs) {
+    const uint32_t nitems = g.nsec ? g.rtn : 0u;
+    if (!nitems) return;
+    const uint32_t utot = cum_bytes(g, g.nsec);
+    const Seg& S = D.seg[C.s2_seg];
+    const float xmax = xmaxs[j % 16];
+    const int ea = act_exponent(S.s2max, xmax);
+    const bool nonfinite = is_inf(xmax);
+    const int E = t_shift(D.m) + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
+    const double scale = __longlong_as_double((long long)(1023 + E) << 52);
+    const bool yf32 = D.flags & kStepYF32;
+    const __half* sc1 = (const __half*)(bs + p.bs2_s1_off);
+    void* Y = D.y[C.s2_seg];
+    const uint8_t* bf = bs + kBSlotHead;
+    const uint32_t W = (uint32_t)GW / p.wave_div2, nwav = (nitems + W - 1) / W;
+    uint32_t F, rem;
+    slab_split(g.K, F, rem);
+    const uint32_t nfull = min(F, g.nsec);
+    const uint32_t gq = lane >> 2, cq = lane & 3;
+    uint32_t ymb = 0;
+    for (uint32_t i = gw; i < nwav * W; i += GW) {
+      const uint32_t cidx = chunk + i / W, slot = cidx % kPassSlots;
+      mbar_wait_wd(&fullr[slot], (cidx / kPassSlots) & 1, sus);
+      if (i < nitems && !(p.debug & 1u)) {
+        int acc[2][4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[0][q][0] = acc[0][q][1] = acc[0][q][2] = acc[0][q][3] = 0;
+        const uint8_t* unit = ring + recs[slot].off + (i % W) * utot;
+        if (nfull) {
+          const uint8_t* bp = bf + (gq * 4 + cq) * 16;
+          full_run<1>(unit, 512u, bp, nfull, lane, gq < (uint32_t)kLimbs, acc);
+          unit += 512u * nfull;
+        }
+        for (uint32_t s = nfull; s < g.nsec; ++s) {  // the 128 / 64 tails
+          uint2 bv[8];
+          const Slab sl = slab_of(g.K, s);
+          load_b(bf, 0, sl, gq, cq, bv);
+          tiles_mma<1>(unit, unit_bytes(sl.nq), sl.nq, lane, bv, acc);
+          unit += unit_bytes(sl.nq);
+        }
+        // row sums: lane c holds limbs 2c, 2c+1 of rows g, g+8; combine the quad
+        unsigned long long v0 = 0, v1 = 0;
+        if (cq < (kLimbs + 1) / 2) {
+          int sm[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sm[e] = acc[0][0][e] + acc[0][1][e] + acc[0][2][e] + acc[0][3][e];
+          v0 = ((unsigned long long)(long long)sm[0] << (16 * cq)) +
+               ((unsigned long long)(long long)sm[1] << (16 * cq + 8));
+          v1 = ((unsigned long long)(long long)sm[2] << (16 * cq)) +
+               ((unsigned long long)(long long)sm[3] << (16 * cq + 8));
+        }
+        v0 += __shfl_xor_sync(~0u, v0, 1);
+        v1 += __shfl_xor_sync(~0u, v1, 1);
+        v0 += __shfl_xor_sync(~0u, v0, 2);
+        v1 += __shfl_xor_sync(~0u, v1, 2);
+        if (cq < 2 && !(p.debug & 8u)) {
+          const uint32_t rl = i * 16 + gq + 8 * cq, row = C.s2_rt0 * 16 + rl;
+          if (row < S.n) {
+            const long long Yi = 2 * ((long long)(cq ? v1 : v0) >> 7) - A;
+            double y = (double)__half2float(sc1[rl]) * ((double)Yi * scale);  // packed.cpp:189
+            if (nonfinite) y = __longlong_as_double(0x7ff8000000000000ll);
+            if (yf32) {
+              const float yo = (float)y;
+              ((float*)Y)[row] = yo;
+              const uint32_t b = __float_as_uint(yo) & 0x7FFFFFFFu;
+              ymb = max(ymb, b >= 0x7F800000u ? 0x7F800000u : b);
+            } else {
+              const __half h = __float2half_rn((float)y);
+              ((__half*)Y)[row] = h;
+              ymb = max(ymb, (uint32_t)(__half_as_ushort(h) & 0x7FFFu));
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&emptyr[slot]);
+    }
+    chunk += nwav;
+    if (D.flags & kStepPublish) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ymb = max(ymb, __shfl_xor_sync(~0u, ymb, o));
+      if (lane == 0 && ymb) atomicMax(amax + 4 * ((size_t)K + (size_t)D.idx * kMaxSeg + C.s2_seg), ymb);
+    }
+  };
+
   // Both groups run the same loop (one copy of the MMA code in the kernel):
   // group 0 does stage 1 of step k (x -> t), group 1 stage 2 (t -> y).
   for (uint32_t j = 0; j < Kc; ++j) {
@@ -803,52 +899,17 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     const StageGeo g = gid ? stage2_geo(D, C) : stage1_geo(D, C);
     const long long A = ((const long long*)bs)[0] + ((const long long*)bs)[1];
     cur_step = k;
-    mma_stage(g, bs + kBSlotHead);
+    if (gid == 0) mma_stage(g, bs + kBSlotHead);
+    else rc_stage(g, D, C, j, A, bs);
     group_sync(gid, GT);
     if (kTrace && gt == 0) PSTAMP(k, gid ? 10 : 8);
-    if (g.nsec && !(p.debug & 8u)) {
-      const Seg& S = D.seg[gid ? C.s2_seg : C.s1_seg];
-      if (!gid) {  // stage-1 publish: t rows (exact int64 reds)
+    if (g.nsec && !(p.debug & 8u) && gid == 0) {
+      const Seg& S = D.seg[C.s1_seg];
+      {  // stage-1 publish: t rows (exact int64 reds)
         long long* Tseg = arena + D.t_off + S.t_off + (size_t)C.s1_rt0 * 16;
         for (uint32_t i = gt; i < (uint32_t)C.s1_rtn * 16; i += GT) {
           const long long v = 2 * take_row6(red + i * kLimbs) - A;
           red_add_u64(&Tseg[i], v);
-        }
-      } else {  // stage-2 outputs (packed.cpp:174-190)
-        const float xmax = xmaxs[j % 16];
-        const int ea = act_exponent(S.s2max, xmax);
-        const bool nonfinite = is_inf(xmax);
-        const int E = t_shift(D.m) + ea - kFix;  // t = T2 * 2^sh * 2^(ea - kFix)
-        const bool yf32 = D.flags & kStepYF32;
-        const __half* sc1 = (const __half*)(bs + p.bs2_s1_off);
-        void* Y = D.y[C.s2_seg];
-        uint32_t ymb = 0;
-        for (uint32_t i = gt; i < (uint32_t)C.s2_rtn * 16; i += GT) {
-          const uint32_t row = C.s2_rt0 * 16 + i;
-          if (row < S.n) {
-            const long long Yi = 2 * take_row6(red + i * kLimbs) - A;
-            double y = (double)__half2float(sc1[i]) *
-                       ((double)Yi * __longlong_as_double((long long)(1023 + E) << 52));  // packed.cpp:189
-            if (nonfinite) y = __longlong_as_double(0x7ff8000000000000ll);
-            if (yf32) {
-              const float yo = (float)y;
-              ((float*)Y)[row] = yo;
-              const uint32_t b = __float_as_uint(yo) & 0x7FFFFFFFu;
-              ymb = max(ymb, b >= 0x7F800000u ? 0x7F800000u : b);
-            } else {
-              const __half h = __float2half_rn((float)y);
-              ((__half*)Y)[row] = h;
-              ymb = max(ymb, (uint32_t)(__half_as_ushort(h) & 0x7FFFu));
-            }
-          } else {
-            (void)take_row6(red + i * kLimbs);  // padding row (zero bits): keep it clear
-          }
-        }
-        if (D.flags & kStepPublish) {
-#pragma unroll
-          for (int o = 16; o; o >>= 1) ymb = max(ymb, __shfl_xor_sync(~0u, ymb, o));
-          if (lane == 0 && ymb)
-            atomicMax(amax + 4 * ((size_t)K + (size_t)k * kMaxSeg + C.s2_seg), ymb);
         }
       }
     }
@@ -898,6 +959,8 @@ struct PassGeo {
   uint64_t max_s2_cta_bytes = 0;
   uint32_t bslot1_b = 0, bs2_s1_off = 0, bslot2_b = 0, red1_b = 0, red2_b = 0, fixed = 0;
   uint32_t min1 = 0, min2 = 0;  // smallest rings
+  uint32_t utot2 = 0;           // bytes of one stage-2 row tile over all slabs of r (largest)
+  uint32_t div2 = 1;            // stage-2 wave divisor
   bool fits = false;
 };
 
@@ -921,6 +984,9 @@ PassGeo pass_geo(uint32_t K, const std::vector<const nqb_group*>& plan, uint32_t
       if (C.s2_rtn) {
         uint64_t b2 = 0;
         const uint32_t r2 = g->seg[C.s2_seg].r;
+        uint32_t tb = 0;
+        for (uint32_t i = 0, ns = nslabs(r2); i < ns; ++i) tb += unit_bytes(slab_of(r2, i).nq);
+        q.utot2 = std::max(q.utot2, tb);
         for (uint32_t i = 0, ns = nslabs(r2); i < ns; ++i)
           b2 += (uint64_t)C.s2_rtn * unit_bytes(slab_of(r2, i).nq);
         q.max_s2_cta_bytes = std::max<uint64_t>(q.max_s2_cta_bytes, b2);
@@ -937,11 +1003,14 @@ PassGeo pass_geo(uint32_t K, const std::vector<const nqb_group*>& plan, uint32_t
   q.bs2_s1_off = (kBSlotHead + std::max(q.bf2, 16u) + 127) / 128 * 128;
   q.bslot2_b = (q.bs2_s1_off + q.s1bytes + 127) / 128 * 128;
   q.red1_b = (q.rt1 * 16 * 4 * kLimbs + 127) / 128 * 128;
-  q.red2_b = (q.rt2 * 16 * 4 * kLimbs + 127) / 128 * 128;
+  q.red2_b = 0;  // stage 2 runs row-complete items: no shared row sums
   q.fixed = pass_head_bytes() + q.red1_b + q.red2_b + kBSlots * (q.bslot1_b + q.bslot2_b);
   // a ring chunk is a wave of work items (<= 8 tile pairs over <= item_slabs
-  // slabs); each ring holds at least one
-  q.min1 = q.min2 = std::max<uint32_t>(24u * 1024u, 8 * 1024u * item_slabs);
+  // slabs; stage 2: <= 8 whole row tiles, halved when that passes 40 KB); each
+  // ring holds at least one
+  q.div2 = 8u * q.utot2 > 40u * 1024u ? 2u : 1u;
+  q.min1 = std::max<uint32_t>(24u * 1024u, 8 * 1024u * item_slabs);
+  q.min2 = std::max<uint32_t>(24u * 1024u, 8u / q.div2 * q.utot2);
   q.fits = q.fixed + q.min1 + q.min2 <= 227u * 1024u;
   return q;
 }
@@ -1208,6 +1277,8 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       pp.warps1 = ew == 3 || ew == 4 || ew == 6 ? ew : w1;  // the kernel is instantiated for 3, 4, 6
       const uint32_t div = env_u32p("NQB_PASS_WAVE_DIV", 1);
       pp.wave_div = (div == 2 && pp.warps1 % 2 == 0) ? 2u : 1u;
+      const uint32_t div2 = env_u32p("NQB_PASS_WAVE_DIV2", geo.div2);
+      pp.wave_div2 = (div2 == 2 && (kConsumerWarps - pp.warps1) % 2 == 0) ? 2u : 1u;
     }
     pp.ring1_bytes = ring1;
     pp.ring2_bytes = ring2;

@@ -89,7 +89,8 @@ struct PassParams {
   uint32_t amax_words;
   uint32_t ring1_bytes, ring2_bytes;     // stage-1 / stage-2 weight rings
   uint32_t item_slabs;        // slabs per work item (ring chunk): one warp, one flush
-  uint32_t wave_div;          // a ring chunk holds (group warps) / wave_div work items
+  uint32_t wave_div;          // a stage-1 ring chunk holds (group warps) / wave_div work items
+  uint32_t wave_div2;         // a stage-2 ring chunk holds (group warps) / wave_div2 row tiles
   uint32_t l2_ahead;          // producers prefetch a step's stage bytes into L2 this many steps ahead
   uint32_t bslot1_bytes, bslot2_bytes;   // quantised-input slots: header | B fragments (| s1)
   uint32_t red1_bytes, red2_bytes;       // per-limb row sums (row tiles of the largest stage)

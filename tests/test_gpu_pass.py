@@ -134,23 +134,22 @@ def test_pass_tails_and_fp32(nq, chk):
         assert rel(got[0].cpu().numpy(), want) <= TIGHT_TOL
 
 
-@pytest.mark.parametrize("chunk_kb", ["8", "20"])
-def test_pass_small_chunks_wrap_the_ring(nq, chk, chunk_kb, monkeypatch):
-    """Tiny chunks: many ring slots in flight, wrap-around, slot reuse."""
-    import torch
-    monkeypatch.setenv("NQB_PASS_CHUNK_KB", chunk_kb)
-    rng = np.random.default_rng(int(chunk_kb))
-    steps, host, keep = block_model(nq, rng, (2048, 5504, 900, 1300), torch.float16, True)
-    run_and_check(nq, chk, steps, host)
-
-
-def test_pass_chunking_is_bitwise_invariant(nq, chk, monkeypatch):
-    """Outputs do not depend on how the weight stream is cut into ring chunks."""
+@pytest.mark.parametrize("env", [
+    {"NQB_PASS_SPLIT": "1"},
+    {"NQB_PASS_SPLIT": "2", "NQB_PASS_ITEM_SLABS": "1"},
+    {"NQB_PASS_SPLIT": "8", "NQB_PASS_ITEM_SLABS": "3", "NQB_PASS_WAVE_DIV": "2",
+     "NQB_PASS_WAVE_DIV2": "2", "NQB_PASS_MIN_RINGS_KB": "0"},
+    {"NQB_PASS_PLAN_SLABS": "2", "NQB_PASS_RING1_PCT": "50", "NQB_PASS_WARPS1": "6"},
+])
+def test_pass_work_split_is_bitwise_invariant(nq, chk, env, monkeypatch):
+    """Outputs do not depend on the SM partitions, the pass plans, the work items or
+    the ring waves (small rings wrap and reuse slots many times)."""
     import torch
     rng = np.random.default_rng(21)
-    steps, host, keep = block_model(nq, rng, (1024, 2752, 400, 600), torch.float16, False)
-    _, a = run_and_check(nq, chk, steps, host, oracle_check=False)
-    monkeypatch.setenv("NQB_PASS_CHUNK_KB", "4")
+    steps, host, keep = block_model(nq, rng, (2048, 5504, 900, 1300), torch.float16, False)
+    _, a = run_and_check(nq, chk, steps, host)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     _, b = run_and_check(nq, chk, steps, host, oracle_check=False)
     for x, y in zip(a, b):
         for u, v in zip(x, y):
