@@ -106,69 +106,6 @@ __device__ __forceinline__ uint32_t cum_bytes(const StageGeo& g, uint32_t i) {
   return bytes;
 }
 
-// Work items of a stage: (row-tile pair, run of <= S slabs), pair-major; item i
-// is ring chunk (stage chunk base + i) and goes to consumer warp (chunk % GW).
-struct Item {
-  uint32_t pr, a, b, nt;
-};
-__device__ __forceinline__ Item item_of(const StageGeo& g, uint32_t S, uint32_t i) {
-  const uint32_t ipp = (g.nsec + S - 1) / S;
-  Item it;
-  it.pr = i / ipp;
-  it.a = (i % ipp) * S;
-  it.b = min(g.nsec, it.a + S);
-  it.nt = 2 * it.pr + 1 < g.rtn ? 2u : 1u;
-  return it;
-}
-__device__ __forceinline__ uint32_t items_of(const StageGeo& g, uint32_t S) {
-  return g.nsec ? (g.rtn + 1) / 2 * ((g.nsec + S - 1) / S) : 0u;
-}
-// Item cursor for walking a stage's items in steps of a wave (no divisions in
-// the loop): item i = pr * ipp + h.
-struct ItemCur {
-  uint32_t pr, h;
-};
-struct StageItems {
-  uint32_t S, ipp, nitems, nf, utot;  // slabs per item, items per pair, items, full slabs, tile bytes
-};
-__device__ __forceinline__ StageItems stage_items(const StageGeo& g, uint32_t S) {
-  StageItems t;
-  t.S = S;
-  t.ipp = g.nsec ? (g.nsec + S - 1) / S : 1u;
-  t.nitems = items_of(g, S);
-  uint32_t F, rem;
-  slab_split(g.K, F, rem);
-  t.nf = F > g.slab0 ? min(F - g.slab0, g.nsec) : 0u;
-  t.utot = cum_bytes(g, g.nsec);
-  return t;
-}
-__device__ __forceinline__ ItemCur item_cur(const StageItems& t, uint32_t i) {
-  return ItemCur{i / t.ipp, i % t.ipp};
-}
-__device__ __forceinline__ void item_advance(ItemCur& c, const StageItems& t, uint32_t n) {
-  c.h += n;
-  while (c.h >= t.ipp) {
-    c.h -= t.ipp;
-    ++c.pr;
-  }
-}
-// byte offset of the item at cursor c in the stage's pair-major stream (past the
-// last pair: the stage's bytes)
-__device__ __forceinline__ uint32_t cur_off(const StageGeo& g, const StageItems& t, const ItemCur& c) {
-  const uint32_t npair = (g.rtn + 1) / 2;
-  if (c.pr >= npair) return g.rtn * t.utot;
-  const uint32_t a = c.h * t.S, nt = 2 * c.pr + 1 < g.rtn ? 2u : 1u;
-  return 2 * c.pr * t.utot + nt * (a <= t.nf ? 512u * a : cum_bytes(g, a));
-}
-
-// Byte offset of item i in the stage's pair-major stream (i = items: the end).
-__device__ __forceinline__ uint32_t item_off(const StageGeo& g, uint32_t S, uint32_t i,
-                                             uint32_t utot) {
-  if (i >= items_of(g, S)) return g.rtn * utot;
-  const Item it = item_of(g, S, i);
-  return 2 * it.pr * utot + it.nt * cum_bytes(g, it.a);
-}
-
 // Ring placement shared by producer and consumers: chunks never wrap.
 __device__ __forceinline__ uint64_t ring_place(uint64_t& pos, uint32_t bytes, uint32_t ring) {
   const uint32_t off = (uint32_t)(pos % ring);
@@ -185,76 +122,6 @@ struct ChunkRec {
   uint32_t i0;       // first work item of the wave
 };
 static_assert(sizeof(ChunkRec) <= 16, "chunk record slot");
-
-// Adds the 4 accumulator chains of one row tile to the per-limb row sums
-// red[row][kLimbs] (int32, like flush_rows but packed: kLimbs ints per row):
-// lane c adds limbs 2c, 2c+1 of rows g and g+8 with 32-bit shared atomics
-// (native; a 64-bit shared atomic add is a CAS loop on sm_100).
-__device__ __forceinline__ void flush_rows6(int (&acc)[4][4], int* red, int lane) {
-  const int g = lane >> 2, c = lane & 3;
-  if (c < (kLimbs + 1) / 2) {
-    int s[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) s[i] = acc[0][i] + acc[1][i] + acc[2][i] + acc[3][i];
-    int* r0 = red + g * kLimbs + 2 * c;
-    int* r1 = red + (g + 8) * kLimbs + 2 * c;
-    atomicAdd(r0, s[0]);
-    atomicAdd(r0 + 1, s[1]);
-    atomicAdd(r1, s[2]);
-    atomicAdd(r1 + 1, s[3]);
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0;
-}
-// sum_K bit * value of a row from its packed limb sums, and clears them
-__device__ __forceinline__ long long take_row6(int* row) {
-  unsigned long long v = 0;
-#pragma unroll
-  for (int l = 0; l < kLimbs; ++l) {
-    v += (unsigned long long)(long long)row[l] << (8 * l);
-    row[l] = 0;
-  }
-  return (long long)v >> 7;
-}
-
-// One work item resident at `base` (pair-major: the pair's units of slab a, then
-// of slab a+1, ...): its MMAs, flushed into red[] (the pair's rows).  The full
-// slabs run software-pipelined (full_run; the next slab of a tile is nt * 512
-// bytes on), then the 128 / 64 tails.
-__device__ __forceinline__ void run_item(const uint8_t* base, const StageGeo& g, uint32_t pr,
-                                         uint32_t a, uint32_t b, const uint8_t* bfrag, int* red) {
-  const int lane = threadIdx.x & 31;
-  int acc[2][4][4];
-#pragma unroll
-  for (int j = 0; j < 2; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[j][q][0] = acc[j][q][1] = acc[j][q][2] = acc[j][q][3] = 0;
-  const uint32_t gq = lane >> 2, c = lane & 3;
-  const uint32_t t0 = 2 * pr;
-  const bool two = t0 + 1 < g.rtn;
-  uint32_t F, rem;
-  slab_split(g.K, F, rem);
-  const uint32_t sl0 = g.slab0 + a;  // absolute slab of the item's first slab
-  const uint32_t nfull = F > sl0 ? min(F - sl0, b - a) : 0u;
-  const uint8_t* unit = base;
-  if (nfull) {
-    const uint8_t* bp = bfrag + kBytesPerK * (256 * sl0 - g.klo) + (gq * 4 + c) * 16;
-    if (two) full_run<2>(unit, 1024u, bp, nfull, lane, gq < (uint32_t)kLimbs, acc);
-    else full_run<1>(unit, 512u, bp, nfull, lane, gq < (uint32_t)kLimbs, acc);
-    unit += (two ? 1024u : 512u) * nfull;
-  }
-  for (uint32_t s = a + nfull; s < b; ++s) {  // the 128 / 64 tails
-    uint2 bv[8];
-    const Slab sl = slab_of(g.K, g.slab0 + s);
-    const uint32_t ub = unit_bytes(sl.nq);
-    load_b(bfrag, g.klo, sl, gq, c, bv);
-    if (two) tiles_mma<2>(unit, ub, sl.nq, lane, bv, acc);
-    else tiles_mma<1>(unit, ub, sl.nq, lane, bv, acc);
-    unit += (two ? 2u : 1u) * ub;
-  }
-  flush_rows6(acc[0], red + t0 * 16 * kLimbs, lane);
-  if (two) flush_rows6(acc[1], red + (t0 + 1) * 16 * kLimbs, lane);
-}
 
 // max|x| bits over x[lo, hi): binary16 magnitude bits (>= 0x7C00: non-finite)
 // or |fp32| bits (non-finite -> +Inf bits), so every bound is an ordered uint.
@@ -365,9 +232,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   float* xmaxs = (float*)(dslots + kDescSlots * kDescSlotBytes + 256);  // max|x| of steps in flight (ring of 16)
   ChunkRec* recs1 = (ChunkRec*)((uint8_t*)xmaxs + 64);
   ChunkRec* recs2 = recs1 + kPassSlots;
-  int* red1 = (int*)(smem + pass_head_bytes());       // stage-1 row sums (kLimbs ints per row)
-  int* red2 = (int*)((uint8_t*)red1 + p.red1_bytes);  // stage-2 row sums
-  uint8_t* bslots1 = (uint8_t*)red2 + p.red2_bytes;   // header | B fragments of x
+  uint8_t* bslots1 = smem + pass_head_bytes();       // header | B fragments of x
   constexpr uint32_t NB = kBSlots;
   uint8_t* bslots2 = bslots1 + NB * p.bslot1_bytes;  // header | B fragments of t | s1 slice
   uint8_t* ring1 = bslots2 + NB * p.bslot2_bytes;
@@ -444,7 +309,6 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       if (lane != 0) return;
       const int r = role == 0 ? 0 : 1;
       const uint32_t RB = r ? p.ring2_bytes : p.ring1_bytes;
-      const uint32_t S = p.item_slabs;
       uint64_t* fullr = r ? full2 : full1;
       uint64_t* emptyr = r ? empty2 : empty1;
       ChunkRec* recs = r ? recs2 : recs1;
@@ -471,22 +335,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
           }
         }
         uint64_t src = g.src_off;
-        const StageItems T = stage_items(g, S);
-        // items per wave; stage 2: whole row tiles (tile-major, row-complete items)
+        // waves of whole row tiles (tile-major, row-complete items), contiguous
+        const uint32_t utot = cum_bytes(g, g.nsec);
         const uint32_t GWr = r ? (kConsumerWarps - kW1) / p.wave_div2 : kW1 / p.wave_div;
-        const uint32_t nit = r ? (g.nsec ? g.rtn : 0u) : T.nitems;
-        ItemCur c1 = item_cur(T, min(GWr, T.nitems));
-        uint32_t o0 = 0;
+        const uint32_t nit = g.nsec ? g.rtn : 0u;
         for (uint32_t i0 = 0; i0 < nit; i0 += GWr) {
-          uint32_t sb;
-          if (r) {
-            sb = min(GWr, nit - i0) * T.utot;
-          } else {
-            const uint32_t o1 = cur_off(g, T, c1);
-            sb = o1 - o0;
-            o0 = o1;
-            item_advance(c1, T, GWr);
-          }
+          const uint32_t sb = min(GWr, nit - i0) * utot;
           const uint64_t start = ring_place(pos, sb, RB);
           // wait for the slot and for every older chunk this range overwrites: chunks
           // are placed monotonically, so [start, pos) reaches older chunk c's bytes
@@ -717,9 +571,6 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   const int GW = gid ? kConsumerWarps - W1 : W1;  // warps in this group
   const uint32_t GT = 32u * GW;                   // threads in this group
   const int gt = tid - gid * 32 * W1;
-  int* const red = gid ? red2 : red1;
-  for (uint32_t i = gt; i < (gid ? p.red2_bytes : p.red1_bytes) / 16; i += GT)
-    ((int4*)red)[i] = make_int4(0, 0, 0, 0);
   // ---- |x| prepass: this CTA's share of every independent input, one grid barrier
   if (p.has_pre) {
     for (uint32_t k = tid; k < K; k += kConsumerThreads) {
@@ -746,62 +597,23 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
   uint64_t* const emptyr = gid ? empty2 : empty1;
   const ChunkRec* const recs = gid ? recs2 : recs1;
   const uint8_t* const ring = gid ? ring2 : ring1;
-  // A ring chunk is a wave of GW consecutive work items (pair-major, so one
-  // contiguous byte range); warp w runs item w of each wave and flushes once per
-  // item (a tile pair over a run of up to item_slabs slabs).
   uint32_t cur_step = 0;
-  auto mma_stage = [&](const StageGeo& g, const uint8_t* bf) {
-    const StageItems T = stage_items(g, p.item_slabs);
-    const uint32_t nitems = T.nitems;
-    if (!nitems) return;
-    // waves of W items: item i is run by warp i % GW and lives in chunk i / W;
-    // W divides GW, so a warp's items sit at the same place gw % W of their
-    // waves.  In the last wave, positions past the items still wait and release.
-    const uint32_t W = (uint32_t)GW / p.wave_div, nwav = (nitems + W - 1) / W;
-    const uint32_t lead = (uint32_t)gw % W;
-    ItemCur c0 = item_cur(T, (uint32_t)gw - lead), ci = item_cur(T, (uint32_t)gw);
-    unsigned long long wsum = 0, nch = 0, rsum = 0;
-    const unsigned long long l0 = kTrace ? clock64() : 0ull;
-    for (uint32_t i = gw; i < nwav * W; i += GW) {
-      const uint32_t cidx = chunk + i / W, slot = cidx % kPassSlots;
-      const unsigned long long w0 = kTrace ? clock64() : 0ull;
-      mbar_wait_wd(&fullr[slot], (cidx / kPassSlots) & 1, sus);
-      if (kTrace) {
-        wsum += clock64() - w0;
-        ++nch;
-      }
-      if (i < nitems && !(p.debug & 1u)) {
-        const ChunkRec cr = recs[slot];
-        const uint32_t off = cur_off(g, T, ci) - cur_off(g, T, c0);
-        const uint32_t a = ci.h * T.S;
-        const unsigned long long r0 = kTrace ? clock64() : 0ull;
-        run_item(ring + cr.off + off, g, ci.pr, a, min(g.nsec, a + T.S), bf, red);
-        if (kTrace) rsum += clock64() - r0;
-      }
-      item_advance(c0, T, GW);
-      item_advance(ci, T, GW);
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&emptyr[slot]);
-    }
-    chunk += nwav;
-    if (kTrace && gw == 0 && lane == 0) {  // this warp's time waiting for chunks, and chunks
-      trp[1 + kPassStamps * cur_step + 16 + gid] = wsum;
-      trp[1 + kPassStamps * cur_step + 18 + gid] = (nch << 48) | (nch << 32) | ((unsigned long long)nitems << 16);
-      trp[1 + kPassStamps * cur_step + 20 + gid] = rsum;
-      trp[1 + kPassStamps * cur_step + 22 + gid] = clock64() - l0;  // the whole chunk loop
-    }
-  };
-
-  // Stage 2, row-complete items: an item is one row tile over all slabs of r
-  // (tile-major layout), so the warp that runs it holds the tile's complete row
-  // sums and writes the outputs itself (packed.cpp:174-190): no shared row sums,
-  // no group-wide epilogue after the MMAs.  Waves of W = GW / wave_div2 tiles.
+  // Row-complete work items: an item is one row tile of the stage over all of
+  // the CTA's slabs (tile-major layout), so the warp that runs it holds the
+  // tile's complete row sums (packed.cpp:174-190): stage 1 publishes its t rows
+  // with int64 reds, stage 2 writes its outputs; no shared row sums, no
+  // group-wide epilogue after the MMAs.  A ring chunk is a wave of W = GW /
+  // wave_div consecutive tiles (one contiguous copy); tile i is run by warp
+  // i % GW, so W dividing GW puts each warp's tiles at the same place of their
+  // waves, and in the last wave the positions past the tiles still release.
   auto rc_stage = [&](const StageGeo& g, const StepDesc& D, const Cta& C, uint32_t j, long long A,
                       const uint8_t* bs) {
     const uint32_t nitems = g.nsec ? g.rtn : 0u;
     if (!nitems) return;
     const uint32_t utot = cum_bytes(g, g.nsec);
-    const Seg& S = D.seg[C.s2_seg];
+    const Seg& S = D.seg[gid ? C.s2_seg : C.s1_seg];
+    // stage 1: the tile's t rows are published with exact int64 reds
+    long long* Tseg = arena + D.t_off + S.t_off + (size_t)C.s1_rt0 * 16;
     const float xmax = xmaxs[j % 16];
     const int ea = act_exponent(S.s2max, xmax);
     const bool nonfinite = is_inf(xmax);
@@ -811,10 +623,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     const __half* sc1 = (const __half*)(bs + p.bs2_s1_off);
     void* Y = D.y[C.s2_seg];
     const uint8_t* bf = bs + kBSlotHead;
-    const uint32_t W = (uint32_t)GW / p.wave_div2, nwav = (nitems + W - 1) / W;
+    const uint32_t W = (uint32_t)GW / (gid ? p.wave_div2 : p.wave_div), nwav = (nitems + W - 1) / W;
     uint32_t F, rem;
     slab_split(g.K, F, rem);
-    const uint32_t nfull = min(F, g.nsec);
+    const uint32_t nfull = F > g.slab0 ? min(F - g.slab0, g.nsec) : 0u;
     const uint32_t gq = lane >> 2, cq = lane & 3;
     uint32_t ymb = 0;
     for (uint32_t i = gw; i < nwav * W; i += GW) {
@@ -826,14 +638,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         for (int q = 0; q < 4; ++q) acc[0][q][0] = acc[0][q][1] = acc[0][q][2] = acc[0][q][3] = 0;
         const uint8_t* unit = ring + recs[slot].off + (i % W) * utot;
         if (nfull) {
-          const uint8_t* bp = bf + (gq * 4 + cq) * 16;
+          const uint8_t* bp = bf + kBytesPerK * (256 * g.slab0 - g.klo) + (gq * 4 + cq) * 16;
           full_run<1>(unit, 512u, bp, nfull, lane, gq < (uint32_t)kLimbs, acc);
           unit += 512u * nfull;
         }
         for (uint32_t s = nfull; s < g.nsec; ++s) {  // the 128 / 64 tails
           uint2 bv[8];
-          const Slab sl = slab_of(g.K, s);
-          load_b(bf, 0, sl, gq, cq, bv);
+          const Slab sl = slab_of(g.K, g.slab0 + s);
+          load_b(bf, g.klo, sl, gq, cq, bv);
           tiles_mma<1>(unit, unit_bytes(sl.nq), sl.nq, lane, bv, acc);
           unit += unit_bytes(sl.nq);
         }
@@ -852,7 +664,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
         v1 += __shfl_xor_sync(~0u, v1, 1);
         v0 += __shfl_xor_sync(~0u, v0, 2);
         v1 += __shfl_xor_sync(~0u, v1, 2);
-        if (cq < 2 && !(p.debug & 8u)) {
+        if (cq < 2 && !(p.debug & 8u) && gid == 0) {
+          const uint32_t rl = i * 16 + gq + 8 * cq;
+          red_add_u64(&Tseg[rl], 2 * ((long long)(cq ? v1 : v0) >> 7) - A);
+        } else if (cq < 2 && !(p.debug & 8u)) {
           const uint32_t rl = i * 16 + gq + 8 * cq, row = C.s2_rt0 * 16 + rl;
           if (row < S.n) {
             const long long Yi = 2 * ((long long)(cq ? v1 : v0) >> 7) - A;
@@ -875,7 +690,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
       if (lane == 0) tc::mbar_arrive(&emptyr[slot]);
     }
     chunk += nwav;
-    if (D.flags & kStepPublish) {
+    if (gid && (D.flags & kStepPublish)) {
 #pragma unroll
       for (int o = 16; o; o >>= 1) ymb = max(ymb, __shfl_xor_sync(~0u, ymb, o));
       if (lane == 0 && ymb) atomicMax(amax + 4 * ((size_t)K + (size_t)D.idx * kMaxSeg + C.s2_seg), ymb);
@@ -899,20 +714,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_decode_pass(const __grid_co
     const StageGeo g = gid ? stage2_geo(D, C) : stage1_geo(D, C);
     const long long A = ((const long long*)bs)[0] + ((const long long*)bs)[1];
     cur_step = k;
-    if (gid == 0) mma_stage(g, bs + kBSlotHead);
-    else rc_stage(g, D, C, j, A, bs);
-    group_sync(gid, GT);
+    rc_stage(g, D, C, j, A, bs);
     if (kTrace && gt == 0) PSTAMP(k, gid ? 10 : 8);
-    if (g.nsec && !(p.debug & 8u) && gid == 0) {
-      const Seg& S = D.seg[C.s1_seg];
-      {  // stage-1 publish: t rows (exact int64 reds)
-        long long* Tseg = arena + D.t_off + S.t_off + (size_t)C.s1_rt0 * 16;
-        for (uint32_t i = gt; i < (uint32_t)C.s1_rtn * 16; i += GT) {
-          const long long v = 2 * take_row6(red + i * kLimbs) - A;
-          red_add_u64(&Tseg[i], v);
-        }
-      }
-    }
     group_sync(gid, GT);  // reds / outputs happen-before the sequencer's release
     if (gt == 0) {
       if (kTrace) PSTAMP(k, gid ? 3 : 1);
@@ -954,17 +757,17 @@ namespace {
 // Geometry of a pass over a given set of plans (one per step), and the
 // shared-memory split it needs.
 struct PassGeo {
-  uint32_t bf1 = 0, bf2 = 0, s1bytes = 16, rt1 = 1, rt2 = 1, maxsec1 = 0, maxsec2 = 0;
+  uint32_t bf1 = 0, bf2 = 0, s1bytes = 16;
   double bits1 = 0, bits2 = 0;
   uint64_t max_s2_cta_bytes = 0;
-  uint32_t bslot1_b = 0, bs2_s1_off = 0, bslot2_b = 0, red1_b = 0, red2_b = 0, fixed = 0;
+  uint32_t bslot1_b = 0, bs2_s1_off = 0, bslot2_b = 0, fixed = 0;
   uint32_t min1 = 0, min2 = 0;  // smallest rings
-  uint32_t utot2 = 0;           // bytes of one stage-2 row tile over all slabs of r (largest)
-  uint32_t div2 = 1;            // stage-2 wave divisor
+  uint32_t utot1 = 0, utot2 = 0;  // bytes of one row tile over a stage's slabs (largest)
+  uint32_t div1 = 1, div2 = 1;    // wave divisors
   bool fits = false;
 };
 
-PassGeo pass_geo(uint32_t K, const std::vector<const nqb_group*>& plan, uint32_t item_slabs) {
+PassGeo pass_geo(uint32_t K, const std::vector<const nqb_group*>& plan) {
   PassGeo q;
   for (uint32_t k = 0; k < K; ++k) {
     const nqb_group* g = plan[k];
@@ -979,7 +782,7 @@ PassGeo pass_geo(uint32_t K, const std::vector<const nqb_group*>& plan, uint32_t
         const Slab last = slab_of(g->m, C.s1_sl0 + C.s1_sln - 1);
         const uint32_t nk1 = last.k0 + 32 * last.nq - slab_of(g->m, C.s1_sl0).k0;
         q.bf1 = std::max(q.bf1, kBytesPerK * nk1);
-        q.maxsec1 = std::max<uint32_t>(q.maxsec1, C.s1_rtn * 512u);
+        q.utot1 = std::max(q.utot1, 2u * nk1);  // one row tile over the CTA's slabs
       }
       if (C.s2_rtn) {
         uint64_t b2 = 0;
@@ -990,26 +793,22 @@ PassGeo pass_geo(uint32_t K, const std::vector<const nqb_group*>& plan, uint32_t
         for (uint32_t i = 0, ns = nslabs(r2); i < ns; ++i)
           b2 += (uint64_t)C.s2_rtn * unit_bytes(slab_of(r2, i).nq);
         q.max_s2_cta_bytes = std::max<uint64_t>(q.max_s2_cta_bytes, b2);
-        q.maxsec2 = std::max<uint32_t>(q.maxsec2, C.s2_rtn * 512u);
       }
       q.s1bytes = std::max<uint32_t>(q.s1bytes, 32u * C.s2_rtn);
-      q.rt1 = std::max<uint32_t>(q.rt1, C.s1_rtn);
-      q.rt2 = std::max<uint32_t>(q.rt2, C.s2_rtn);
     }
   }
-  // Shared memory: head | row sums (stage 1, 2) | quantised-x slots | quantised-t
-  // slots | stage-1 ring | stage-2 ring.
+  // Shared memory: head | quantised-x slots | quantised-t slots | stage-1 ring |
+  // stage-2 ring.
   q.bslot1_b = (kBSlotHead + std::max(q.bf1, 16u) + 127) / 128 * 128;
   q.bs2_s1_off = (kBSlotHead + std::max(q.bf2, 16u) + 127) / 128 * 128;
   q.bslot2_b = (q.bs2_s1_off + q.s1bytes + 127) / 128 * 128;
-  q.red1_b = (q.rt1 * 16 * 4 * kLimbs + 127) / 128 * 128;
-  q.red2_b = 0;  // stage 2 runs row-complete items: no shared row sums
-  q.fixed = pass_head_bytes() + q.red1_b + q.red2_b + kBSlots * (q.bslot1_b + q.bslot2_b);
-  // a ring chunk is a wave of work items (<= 8 tile pairs over <= item_slabs
-  // slabs; stage 2: <= 8 whole row tiles, halved when that passes 40 KB); each
-  // ring holds at least one
+  q.fixed = pass_head_bytes() + kBSlots * (q.bslot1_b + q.bslot2_b);
+  // a ring chunk is a wave of whole row tiles, one per warp of the group (<= 6
+  // for stage 1, <= 8 for stage 2), halved when that passes 40 KB; each ring
+  // holds at least one
+  q.div1 = 6u * q.utot1 > 40u * 1024u ? 2u : 1u;
   q.div2 = 8u * q.utot2 > 40u * 1024u ? 2u : 1u;
-  q.min1 = std::max<uint32_t>(24u * 1024u, 8 * 1024u * item_slabs);
+  q.min1 = std::max<uint32_t>(24u * 1024u, 6u / q.div1 * q.utot1);
   q.min2 = std::max<uint32_t>(24u * 1024u, 8u / q.div2 * q.utot2);
   q.fits = q.fixed + q.min1 + q.min2 <= 227u * 1024u;
   return q;
@@ -1103,7 +902,6 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     // pass keeps one partition of G CTAs (the steps run one after the other).
     // The pass runs on its own plans (pair-major stream layout, k_relayout; the
     // groups' per-call plans stay untouched), one per distinct group.
-    const uint32_t item_slabs = std::min<uint32_t>(std::max<uint32_t>(env_u32p("NQB_PASS_ITEM_SLABS", 4), 1), 64);
     uint32_t nsub = 0;
     std::vector<const nqb_group*> plan(K);
     PassGeo geo;
@@ -1134,7 +932,7 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
             std::fprintf(stderr, "nqb pass: %u partitions: plan failed: %s\n", ns, f.msg.c_str());
         }
         PassGeo gq;
-        if (ok) gq = pass_geo(K, pl, item_slabs);
+        if (ok) gq = pass_geo(K, pl);
         if (ok && !gq.fits && env_u32p("NQB_PASS_VERBOSE", 0))
           std::fprintf(stderr, "nqb pass: %u partitions: staging %u B + rings %u + %u B > 227 KB\n",
                        ns, gq.fixed, gq.min1, gq.min2);
@@ -1261,8 +1059,6 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       if (desc[k].flags & kStepXPre)
         pp.pre_units = std::max<uint32_t>(pp.pre_units, ((desc[k].m + 7) / 8 + G - 1) / G);
     pp.debug = env_u32p("NQB_PASS_DEBUG", 0);
-    pp.red1_bytes = geo.red1_b;
-    pp.red2_bytes = geo.red2_b;
     pp.bslot1_bytes = geo.bslot1_b;
     pp.bslot2_bytes = geo.bslot2_b;
     pp.bs2_s1_off = geo.bs2_s1_off;
@@ -1275,23 +1071,23 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       const uint32_t w1 = geo.max_s2_cta_bytes > 96u * 1024u ? 4u : 6u;
       const uint32_t ew = env_u32p("NQB_PASS_WARPS1", 0);
       pp.warps1 = ew == 3 || ew == 4 || ew == 6 ? ew : w1;  // the kernel is instantiated for 3, 4, 6
-      const uint32_t div = env_u32p("NQB_PASS_WAVE_DIV", 1);
+      const uint32_t div = env_u32p("NQB_PASS_WAVE_DIV", pp.warps1 * geo.utot1 > 40u * 1024u ? 2u : 1u);
       pp.wave_div = (div == 2 && pp.warps1 % 2 == 0) ? 2u : 1u;
       const uint32_t div2 = env_u32p("NQB_PASS_WAVE_DIV2", geo.div2);
       pp.wave_div2 = (div2 == 2 && (kConsumerWarps - pp.warps1) % 2 == 0) ? 2u : 1u;
     }
     pp.ring1_bytes = ring1;
     pp.ring2_bytes = ring2;
-    pp.item_slabs = item_slabs;
     // waves of GW / wave_div items (NQB_PASS_WAVE_DIV 1 or 2; 2 needs even groups)
     pp.l2_ahead = std::min<uint32_t>(env_u32p("NQB_PASS_L2_AHEAD", 0), kDescSlots - 4);
     P->smem_bytes = geo.fixed + rings;
     if (env_u32p("NQB_PASS_VERBOSE", 0))
       std::fprintf(stderr,
-                   "nqb pass: K=%u G=%u partitions=%u x %u smem=%u red=%u+%u bslots=%ux(%u+%u) "
-                   "rings=%u+%u item slabs=%u warps1=%u\n",
-                   K, G, nsub, Pn, P->smem_bytes, geo.red1_b, geo.red2_b, kBSlots, geo.bslot1_b,
-                   geo.bslot2_b, ring1, ring2, item_slabs, pp.warps1);
+                   "nqb pass: K=%u G=%u partitions=%u x %u smem=%u bslots=%ux(%u+%u) "
+                   "rings=%u+%u tile bytes=%u/%u waves=%u/%u warps1=%u\n",
+                   K, G, nsub, Pn, P->smem_bytes, kBSlots, geo.bslot1_b, geo.bslot2_b, ring1, ring2,
+                   geo.utot1, geo.utot2, pp.warps1 / pp.wave_div, (kConsumerWarps - pp.warps1) / pp.wave_div2,
+                   pp.warps1);
     for (uint32_t k = 0; k < K; ++k) {
       const uint32_t esz = steps[k].f32 ? 4 : 2;
       P->x_dev.push_back(const_cast<void*>(steps[k].x));

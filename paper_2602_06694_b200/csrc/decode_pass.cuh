@@ -47,7 +47,7 @@ constexpr int kCtrStride = 16;   // u64 words per counter (own 128-byte line)
 constexpr int kPassHelpers = 8;
 constexpr int kPassStamps = 24;  // trace stamps per step (16..21: consumer chunk-wait / run counters, per stage)
 constexpr int kMaxLookahead = 6;
-constexpr int kMaxSub = 8;       // SM partitions of a pass (independent steps run concurrently)
+constexpr int kMaxSub = 16;      // SM partitions of a pass (independent steps run concurrently)
 constexpr uint32_t kPassMaxRt = 128;  // row tiles per CTA per stage in a partition's plan
 constexpr uint32_t kBSlotHead = 16;  // slot header: the two quantiser warps' sums of the values
 
@@ -88,12 +88,10 @@ struct PassParams {
   uint64_t arena_len;
   uint32_t amax_words;
   uint32_t ring1_bytes, ring2_bytes;     // stage-1 / stage-2 weight rings
-  uint32_t item_slabs;        // slabs per work item (ring chunk): one warp, one flush
   uint32_t wave_div;          // a stage-1 ring chunk holds (group warps) / wave_div work items
   uint32_t wave_div2;         // a stage-2 ring chunk holds (group warps) / wave_div2 row tiles
   uint32_t l2_ahead;          // producers prefetch a step's stage bytes into L2 this many steps ahead
   uint32_t bslot1_bytes, bslot2_bytes;   // quantised-input slots: header | B fragments (| s1)
-  uint32_t red1_bytes, red2_bytes;       // per-limb row sums (row tiles of the largest stage)
   uint32_t bs2_s1_off;        // s1 slice offset in a stage-2 slot (after the t fragments)
   uint32_t warps1;            // consumer warps of the stage-1 group (4 or 6; the rest run stage 2)
   uint32_t has_pre;

@@ -63,19 +63,17 @@ __device__ uint32_t stage_tile_bytes(const Cta& C, bool st1, uint32_t m, uint32_
 
 // One block per CTA of the plan: writes that CTA's byte stream.
 // Slab-major (per-call kernel): per stage, section = slab, the CTA's row tiles
-// back to back.  Decode-pass plans (pm): stage 1 pair-major, row-tile pair after
-// pair, each pair's slabs in order with the pair's two units of a slab adjacent,
-// so any run of slabs of one pair is one contiguous byte range:
-//   offset(pair p, slab i, tile j) = 2p Utot + nt_p U_i + j ub_i
-// (Utot: bytes of a tile over the stage's slabs, U_i: of its first i slabs,
-// nt_p: tiles in pair p); stage 2 tile-major, offset(tile t, slab i) = t Utot + U_i.
+// back to back.  Decode-pass plans (pm): per stage tile-major, each row tile's
+// slabs in order, so one tile of a stage is one contiguous byte range:
+//   offset(tile t, slab i) = t Utot + U_i
+// (Utot: bytes of a tile over the stage's slabs, U_i: of its first i slabs).
 __global__ void k_relayout(const Cta* __restrict__ ctas, const Seg* __restrict__ segs,
                            uint32_t m, RelayoutSrc src, uint32_t* __restrict__ out, int pm) {
   const Cta C = ctas[blockIdx.x];
   uint32_t* dst = out + C.stream_off / 4;
   uint32_t sec_words_off = 0;
   const uint32_t n1 = C.s1_rtn ? C.s1_sln : 0;
-  uint32_t u_cum = 0, stage_w = 0;  // pair-major: U_i of the current stage, its first word
+  uint32_t u_cum = 0, stage_w = 0;  // tile-major: U_i of the current stage, its first word
   for (uint32_t sec = 0; sec < C.nsec; ++sec) {
     const bool st1 = sec < n1;
     const uint32_t seg = st1 ? C.s1_seg : C.s2_seg;
@@ -93,12 +91,9 @@ __global__ void k_relayout(const Cta* __restrict__ ctas, const Seg* __restrict__
     const uint32_t utot = pm ? stage_tile_bytes(C, st1, m, S.r) : 0u;
     for (uint32_t x = threadIdx.x; x < words; x += blockDim.x) {
       const uint32_t t = x / unit_words, rem = x % unit_words;
-      const uint32_t nt = (t | 1u) < rtn ? 2u : 1u;
-      // pair-major for stage 1; tile-major (pairs of one tile) for stage 2, whose
-      // work items are whole rows tiles (decode_pass.cu, row-complete items)
-      const uint32_t dw = !pm ? sec_words_off + x
-                        : st1 ? stage_w + (2 * (t / 2) * utot + nt * u_cum + (t & 1) * 4 * unit_words) / 4 + rem
-                              : stage_w + (t * utot + u_cum) / 4 + rem;
+      // tile-major: a decode-pass work item is one whole row tile of a stage
+      // (decode_pass.cu, row-complete items)
+      const uint32_t dw = !pm ? sec_words_off + x : stage_w + (t * utot + u_cum) / 4 + rem;
       const uint32_t lane = rem / lane_words, wl = rem % lane_words;
       uint32_t v = 0;
       for (uint32_t p = 0; p < 32; ++p) {
