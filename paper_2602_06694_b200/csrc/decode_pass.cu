@@ -888,230 +888,268 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
     }
   }
 
-  auto* P = new nqb_pass();
-  P->device = ctx->device;
-  P->K = K;
-  P->G = G;
-  try {
-    // ---- SM partitions.  When no step reads or overwrites another step's output,
-    // the steps are independent: the grid splits into nsub partitions of P CTAs
-    // and each runs its share of the steps on plans built for P CTAs, so every CTA
-    // sees nsub times the bytes per step and the per-step handoff chain (x
-    // quantisation, t barrier, epilogues) is amortised over that much more work
-    // (measured: a 7B pass on 74 SMs runs at 77 % of the rate on 148).  A chained
-    // pass keeps one partition of G CTAs (the steps run one after the other).
-    // The pass runs on its own plans (pair-major stream layout, k_relayout; the
-    // groups' per-call plans stay untouched), one per distinct group.
-    uint32_t nsub = 0;
-    std::vector<const nqb_group*> plan(K);
-    PassGeo geo;
-    {
-      const uint32_t want = chained ? 1u : std::min<uint32_t>(std::max<uint32_t>(env_u32p("NQB_PASS_SPLIT", kMaxSub), 1), kMaxSub);
-      for (uint32_t ns = want; ns >= 1; --ns) {
-        const uint32_t Pc = G / ns;
-        std::vector<nqb_group*> made;
-        std::vector<const nqb_group*> pl(K);
-        bool ok = Pc >= 8 || ns == 1;
-        try {
-          std::vector<std::pair<const nqb_group*, nqb_group*>> memo;
-          for (uint32_t k = 0; k < K && ok; ++k) {
-            const nqb_group* g = steps[k].group;
-            nqb_group* h = nullptr;
-            for (auto& pr : memo)
-              if (pr.first == g) h = pr.second;
-            if (!h) {
-              h = group_build(ctx, g->layers, g->nseg, Pc, kPassMaxRt, true);
-              made.push_back(h);
-              memo.push_back({g, h});
-            }
-            pl[k] = h;
-          }
-        } catch (const nqb::Failure& f) {
-          ok = false;
-          if (env_u32p("NQB_PASS_VERBOSE", 0))
-            std::fprintf(stderr, "nqb pass: %u partitions: plan failed: %s\n", ns, f.msg.c_str());
+  // ---- SM partitions.  When no step reads or overwrites another step's output,
+  // the steps are independent: the grid splits into nsub partitions of P CTAs
+  // and each runs its share of the steps on plans built for P CTAs, so every CTA
+  // sees nsub times the bytes per step and the per-step handoff chain (x
+  // quantisation, t barrier, t quantisation) is amortised over that much more
+  // work.  A chained pass keeps one partition of G CTAs (the steps run one after
+  // the other).  The pass runs on its own plans (tile-major stream layout,
+  // k_relayout; the groups' per-call plans stay untouched), one per distinct group.
+  const std::vector<StepDesc> desc0 = desc;
+  auto build_with = [&](uint32_t nsub, const std::vector<const nqb_group*>& plan, const PassGeo& geo,
+                        std::vector<nqb_group*> owned) -> nqb_pass* {
+    std::vector<StepDesc> desc = desc0;
+    auto* P = new nqb_pass();
+    P->device = ctx->device;
+    P->K = K;
+    P->G = G;
+    P->owned = std::move(owned);
+    try {
+      const uint32_t Pn = G / nsub;
+      NQB_REQUIRE(geo.fits, NQB_E_DIMENSION_MISMATCH,
+                  "decode pass: staging buffers leave no room for the weight rings");
+
+      // ---- per-step plan data, t regions, algorithmic bytes ----
+      uint64_t arena = 0, stream_bytes = 0;
+      double algo = 0;
+      std::vector<uint64_t> load(nsub, 0);
+      std::vector<std::vector<uint32_t>> lists(nsub);
+      std::vector<uint32_t> part(K, 0);
+      for (uint32_t k = 0; k < K; ++k) {
+        const nqb_group* g = plan[k];
+        NQB_REQUIRE(g->grid <= Pn, NQB_E_INTERNAL, "decode plan larger than its partition");
+        StepDesc& D = desc[k];
+        D.bits = g->bits;
+        D.R1 = g->R1;
+        const uint32_t esz = steps[k].f32 ? 4 : 2;
+        for (uint32_t q = 0; q < g->nseg; ++q) {
+          D.seg[q] = g->seg[q];
+          algo += (double)g->r[q] * (g->n[q] + g->m) / 8.0 + 2.0 * (g->n[q] + g->m) + esz * g->n[q];
         }
-        PassGeo gq;
-        if (ok) gq = pass_geo(K, pl);
-        if (ok && !gq.fits && env_u32p("NQB_PASS_VERBOSE", 0))
-          std::fprintf(stderr, "nqb pass: %u partitions: staging %u B + rings %u + %u B > 227 KB\n",
-                       ns, gq.fixed, gq.min1, gq.min2);
-        // more partitions amortise the per-step chain over more bytes per CTA, but
-        // their larger row blocks take shared memory from the weight rings; a
-        // partition count is taken only if the rings keep >= NQB_PASS_MIN_RINGS_KB
-        // (default 88: 7B takes 8 partitions with 90 KB of rings, 1700 GB/s vs 1386
-        // for 4; 70B takes 2 with 112 KB, 1756 GB/s vs 1399 for 3 with 85 KB)
-        const uint32_t rings_left = ok && gq.fits ? 227u * 1024u - gq.fixed : 0u;
-        if (ok && gq.fits && ns > 1 && rings_left < env_u32p("NQB_PASS_MIN_RINGS_KB", 88) * 1024u) {
-          if (env_u32p("NQB_PASS_VERBOSE", 0))
-            std::fprintf(stderr, "nqb pass: %u partitions: rings %u B below the minimum\n", ns,
-                         rings_left);
-          gq.fits = false;
+        algo += (double)esz * g->m;
+        stream_bytes += g->stream_bytes;
+        D.t_off = arena;
+        D.t_len = (g->R1 + 3) & ~1u;  // even, plus the odd-start overhang of a segment copy
+        arena += D.t_len;
+        // partition: the least-loaded one (steps stay in pass order inside it)
+        uint32_t best = 0;
+        for (uint32_t i = 1; i < nsub; ++i)
+          if (load[i] < load[best]) best = i;
+        load[best] += g->stream_bytes;
+        lists[best].push_back(k);
+        part[k] = best;
+      }
+
+      // Rings split what the staging leaves in proportion to the two stages' bytes.
+      const uint32_t rings = (227u * 1024u - geo.fixed) / 256 * 256;
+      const double f1 = geo.bits1 + geo.bits2 > 0 ? geo.bits1 / (geo.bits1 + geo.bits2) : 0.5;
+      // NQB_PASS_RING1_PCT: stage-1 share of the rings in percent.  Default: the
+      // stage-1 share of the bytes, at most 30 % (stage-1 waves are half the size of
+      // stage-2 waves with the 4 + 8 split; 7B: 1700 vs 1668 GB/s)
+      const uint32_t r1pct = env_u32p("NQB_PASS_RING1_PCT", 0);
+      uint32_t ring1 = (uint32_t)(rings * (r1pct ? r1pct / 100.0 : std::min(f1, 0.30))) / 128 * 128;
+      ring1 = std::min(std::max(ring1, geo.min1), rings - geo.min2);
+      const uint32_t ring2 = rings - ring1;
+
+      // ---- device memory: descriptors | CTA tables | counters | bounds | arena | lists ----
+      const uint32_t amax_words = K * (1 + kMaxSeg);
+      const size_t desc_b = sizeof(StepDesc) * K;
+      const size_t cta_b = sizeof(Cta) * (size_t)K * G;
+      const size_t ctr_b = sizeof(unsigned long long) * kCtrStride * (2 + 2 * (size_t)K);
+      const size_t amax_b = 2ull * amax_words * 16;
+      const size_t arena_b = 2ull * arena * 8;
+      const size_t list_b = sizeof(uint32_t) * K;
+      NQB_CUDA(cudaMalloc(&P->dmem, desc_b + cta_b + ctr_b + amax_b + arena_b + list_b));
+      char* base = (char*)P->dmem;
+      StepDesc* d_desc = (StepDesc*)base;
+      Cta* d_ctas = (Cta*)(base + desc_b);
+      auto* d_ctr = (unsigned long long*)(base + desc_b + cta_b);
+      auto* d_amax = (unsigned*)(base + desc_b + cta_b + ctr_b);
+      auto* d_arena = (long long*)(base + desc_b + cta_b + ctr_b + amax_b);
+      auto* d_list = (uint32_t*)(base + desc_b + cta_b + ctr_b + amax_b + arena_b);
+      std::vector<Cta> ctas((size_t)K * G, Cta{});
+      for (uint32_t k = 0; k < K; ++k) {
+        const nqb_group* g = plan[k];
+        std::copy(g->ctas, g->ctas + g->grid, ctas.begin() + (size_t)k * G + (size_t)part[k] * Pn);
+        desc[k].ctas = d_ctas + (size_t)k * G;
+      }
+      std::vector<uint32_t> flat;
+      PassParams& pp = P->params;
+      pp.list_off[0] = 0;
+      for (uint32_t i = 0; i < nsub; ++i) {
+        flat.insert(flat.end(), lists[i].begin(), lists[i].end());
+        pp.list_off[i + 1] = (uint32_t)flat.size();
+      }
+      NQB_CUDA(cudaMemsetAsync(d_ctr, 0, ctr_b + amax_b + arena_b, ctx->stream));
+      NQB_CUDA(cudaMemcpyAsync(d_desc, desc.data(), desc_b, cudaMemcpyHostToDevice, ctx->stream));
+      NQB_CUDA(cudaMemcpyAsync(d_ctas, ctas.data(), cta_b, cudaMemcpyHostToDevice, ctx->stream));
+      NQB_CUDA(cudaMemcpyAsync(d_list, flat.data(), list_b, cudaMemcpyHostToDevice, ctx->stream));
+      NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+
+      pp.desc = d_desc;
+      pp.ctas = d_ctas;
+      pp.K = K;
+      pp.G = G;
+      pp.list = d_list;
+      pp.nsub = nsub;
+      pp.P = Pn;
+      pp.ctr = d_ctr;
+      pp.amax = d_amax;
+      pp.amax_words = amax_words;
+      pp.arena = d_arena;
+      pp.arena_len = arena;
+      pp.has_pre = has_pre ? 1 : 0;
+      pp.pre_units = 0;
+      for (uint32_t k = 0; k < K; ++k)
+        if (desc[k].flags & kStepXPre)
+          pp.pre_units = std::max<uint32_t>(pp.pre_units, ((desc[k].m + 7) / 8 + G - 1) / G);
+      pp.debug = env_u32p("NQB_PASS_DEBUG", 0);
+      pp.bslot1_bytes = geo.bslot1_b;
+      pp.bslot2_bytes = geo.bslot2_b;
+      pp.bs2_s1_off = geo.bs2_s1_off;
+      // Consumer warps per stage group.  Measured (tools/gpu_pass_ab.sh): an even
+      // 6 + 6 split is best when every step is small (7B: 886 vs 841 GB/s for 4 + 8),
+      // while a pass whose largest step puts > 96 KB of stage-2 bits on each CTA
+      // (70B gate/up: 169 KB) is bound by the stage-2 group, and 4 + 8 gives
+      // 1495 vs 1234 GB/s.
+      {
+        const uint32_t w1 = geo.max_s2_cta_bytes > 96u * 1024u ? 4u : 6u;
+        const uint32_t ew = env_u32p("NQB_PASS_WARPS1", 0);
+        pp.warps1 = ew == 3 || ew == 4 || ew == 6 ? ew : w1;  // the kernel is instantiated for 3, 4, 6
+        const uint32_t div = env_u32p("NQB_PASS_WAVE_DIV", pp.warps1 * geo.utot1 > 40u * 1024u ? 2u : 1u);
+        pp.wave_div = (div == 2 && pp.warps1 % 2 == 0) ? 2u : 1u;
+        const uint32_t div2 = env_u32p("NQB_PASS_WAVE_DIV2", geo.div2);
+        pp.wave_div2 = (div2 == 2 && (kConsumerWarps - pp.warps1) % 2 == 0) ? 2u : 1u;
+      }
+      pp.ring1_bytes = ring1;
+      pp.ring2_bytes = ring2;
+      // waves of GW / wave_div items (NQB_PASS_WAVE_DIV 1 or 2; 2 needs even groups)
+      pp.l2_ahead = std::min<uint32_t>(env_u32p("NQB_PASS_L2_AHEAD", 0), kDescSlots - 4);
+      P->smem_bytes = geo.fixed + rings;
+      if (env_u32p("NQB_PASS_VERBOSE", 0))
+        std::fprintf(stderr,
+                     "nqb pass: K=%u G=%u partitions=%u x %u smem=%u bslots=%ux(%u+%u) "
+                     "rings=%u+%u tile bytes=%u/%u waves=%u/%u warps1=%u\n",
+                     K, G, nsub, Pn, P->smem_bytes, kBSlots, geo.bslot1_b, geo.bslot2_b, ring1, ring2,
+                     geo.utot1, geo.utot2, pp.warps1 / pp.wave_div, (kConsumerWarps - pp.warps1) / pp.wave_div2,
+                     pp.warps1);
+      for (uint32_t k = 0; k < K; ++k) {
+        const uint32_t esz = steps[k].f32 ? 4 : 2;
+        P->x_dev.push_back(const_cast<void*>(steps[k].x));
+        P->x_bytes.push_back((size_t)desc[k].m * esz);
+        for (uint32_t q = 0; q < desc[k].nseg; ++q) {
+          P->y_dev.push_back(steps[k].y[q]);
+          P->y_bytes.push_back((size_t)desc[k].seg[q].n * esz);
         }
-        if (ok && gq.fits) {
-          nsub = ns;
-          plan = pl;
-          geo = gq;
-          P->owned = made;
-          break;
+      }
+      P->stream_bytes = stream_bytes;
+      P->algo_bytes = (uint64_t)algo;
+      for (auto fn : {k_decode_pass<false, 6>, k_decode_pass<true, 6>, k_decode_pass<false, 4>,
+                      k_decode_pass<true, 4>, k_decode_pass<false, 3>, k_decode_pass<true, 3>})
+        NQB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)P->smem_bytes));
+      int per_sm = 0;
+      NQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_pass<false, 6>,
+                                                             kPassThreads, P->smem_bytes));
+      NQB_REQUIRE(per_sm >= 1, NQB_E_INTERNAL, "decode pass kernel does not fit an SM");
+    } catch (...) {
+      pass_free(P);
+      throw;
+    }
+    return P;
+  };
+
+  // Candidate partition counts, largest first.  Which count is fastest depends on
+  // how the plans and the rings come out (measured, same box: 7B 12 partitions
+  // 1973 GB/s, 14: 1523, 16: 1650; 70B 5: 2472, 6: 2123, 8: 2163), so by default
+  // (NQB_PASS_TUNE=1) the builder times each candidate that fits (three launches on
+  // the context's stream, outputs overwritten by the caller's first launch) and
+  // keeps the fastest; NQB_PASS_TUNE=0 takes the first that fits.
+  const uint32_t want = chained ? 1u : std::min<uint32_t>(std::max<uint32_t>(env_u32p("NQB_PASS_SPLIT", kMaxSub), 1), kMaxSub);
+  const bool tune = !chained && env_u32p("NQB_PASS_TUNE", 1) != 0;
+  const bool verbose = env_u32p("NQB_PASS_VERBOSE", 0) != 0;
+  static const uint32_t kCands[] = {16, 12, 8, 6, 5, 4, 3, 2, 1};
+  nqb_pass* best = nullptr;
+  float best_ms = 0.f;
+  for (uint32_t ns : kCands) {
+    if (ns > want) continue;
+    if (best && !tune) break;
+    const uint32_t Pc = G / ns;
+    std::vector<nqb_group*> made;
+    std::vector<const nqb_group*> pl(K);
+    bool ok = Pc >= 8 || ns == 1;
+    try {
+      std::vector<std::pair<const nqb_group*, nqb_group*>> memo;
+      for (uint32_t k = 0; k < K && ok; ++k) {
+        const nqb_group* g = steps[k].group;
+        nqb_group* h = nullptr;
+        for (auto& pr : memo)
+          if (pr.first == g) h = pr.second;
+        if (!h) {
+          h = group_build(ctx, g->layers, g->nseg, Pc, kPassMaxRt, true);
+          made.push_back(h);
+          memo.push_back({g, h});
         }
-        for (auto* h : made) group_free(h);
+        pl[k] = h;
       }
+    } catch (const nqb::Failure& f) {
+      ok = false;
+      if (verbose) std::fprintf(stderr, "nqb pass: %u partitions: plan failed: %s\n", ns, f.msg.c_str());
     }
-    NQB_REQUIRE(nsub >= 1, NQB_E_DIMENSION_MISMATCH,
-                "decode pass: no partition of the grid fits the steps' plans in shared memory");
-    const uint32_t Pn = G / nsub;
-    NQB_REQUIRE(geo.fits, NQB_E_DIMENSION_MISMATCH,
-                "decode pass: staging buffers leave no room for the weight rings");
-
-    // ---- per-step plan data, t regions, algorithmic bytes ----
-    uint64_t arena = 0, stream_bytes = 0;
-    double algo = 0;
-    std::vector<uint64_t> load(nsub, 0);
-    std::vector<std::vector<uint32_t>> lists(nsub);
-    std::vector<uint32_t> part(K, 0);
-    for (uint32_t k = 0; k < K; ++k) {
-      const nqb_group* g = plan[k];
-      NQB_REQUIRE(g->grid <= Pn, NQB_E_INTERNAL, "decode plan larger than its partition");
-      StepDesc& D = desc[k];
-      D.bits = g->bits;
-      D.R1 = g->R1;
-      const uint32_t esz = steps[k].f32 ? 4 : 2;
-      for (uint32_t q = 0; q < g->nseg; ++q) {
-        D.seg[q] = g->seg[q];
-        algo += (double)g->r[q] * (g->n[q] + g->m) / 8.0 + 2.0 * (g->n[q] + g->m) + esz * g->n[q];
-      }
-      algo += (double)esz * g->m;
-      stream_bytes += g->stream_bytes;
-      D.t_off = arena;
-      D.t_len = (g->R1 + 3) & ~1u;  // even, plus the odd-start overhang of a segment copy
-      arena += D.t_len;
-      // partition: the least-loaded one (steps stay in pass order inside it)
-      uint32_t best = 0;
-      for (uint32_t i = 1; i < nsub; ++i)
-        if (load[i] < load[best]) best = i;
-      load[best] += g->stream_bytes;
-      lists[best].push_back(k);
-      part[k] = best;
+    PassGeo gq;
+    if (ok) gq = pass_geo(K, pl);
+    if (ok && !gq.fits && verbose)
+      std::fprintf(stderr, "nqb pass: %u partitions: staging %u B + rings %u + %u B > 227 KB\n", ns,
+                   gq.fixed, gq.min1, gq.min2);
+    // more partitions amortise the per-step chain over more bytes per CTA, but
+    // their larger blocks take shared memory from the weight rings: a partition
+    // count must leave >= NQB_PASS_MIN_RINGS_KB (default 88) of rings
+    const uint32_t rings_left = ok && gq.fits ? 227u * 1024u - gq.fixed : 0u;
+    if (ok && gq.fits && ns > 1 && rings_left < env_u32p("NQB_PASS_MIN_RINGS_KB", 88) * 1024u) {
+      if (verbose) std::fprintf(stderr, "nqb pass: %u partitions: rings %u B below the minimum\n", ns, rings_left);
+      gq.fits = false;
     }
-
-    // Rings split what the staging leaves in proportion to the two stages' bytes.
-    const uint32_t rings = (227u * 1024u - geo.fixed) / 256 * 256;
-    const double f1 = geo.bits1 + geo.bits2 > 0 ? geo.bits1 / (geo.bits1 + geo.bits2) : 0.5;
-    // NQB_PASS_RING1_PCT: stage-1 share of the rings in percent.  Default: the
-    // stage-1 share of the bytes, at most 30 % (stage-1 waves are half the size of
-    // stage-2 waves with the 4 + 8 split; 7B: 1700 vs 1668 GB/s)
-    const uint32_t r1pct = env_u32p("NQB_PASS_RING1_PCT", 0);
-    uint32_t ring1 = (uint32_t)(rings * (r1pct ? r1pct / 100.0 : std::min(f1, 0.30))) / 128 * 128;
-    ring1 = std::min(std::max(ring1, geo.min1), rings - geo.min2);
-    const uint32_t ring2 = rings - ring1;
-
-    // ---- device memory: descriptors | CTA tables | counters | bounds | arena | lists ----
-    const uint32_t amax_words = K * (1 + kMaxSeg);
-    const size_t desc_b = sizeof(StepDesc) * K;
-    const size_t cta_b = sizeof(Cta) * (size_t)K * G;
-    const size_t ctr_b = sizeof(unsigned long long) * kCtrStride * (2 + 2 * (size_t)K);
-    const size_t amax_b = 2ull * amax_words * 16;
-    const size_t arena_b = 2ull * arena * 8;
-    const size_t list_b = sizeof(uint32_t) * K;
-    NQB_CUDA(cudaMalloc(&P->dmem, desc_b + cta_b + ctr_b + amax_b + arena_b + list_b));
-    char* base = (char*)P->dmem;
-    StepDesc* d_desc = (StepDesc*)base;
-    Cta* d_ctas = (Cta*)(base + desc_b);
-    auto* d_ctr = (unsigned long long*)(base + desc_b + cta_b);
-    auto* d_amax = (unsigned*)(base + desc_b + cta_b + ctr_b);
-    auto* d_arena = (long long*)(base + desc_b + cta_b + ctr_b + amax_b);
-    auto* d_list = (uint32_t*)(base + desc_b + cta_b + ctr_b + amax_b + arena_b);
-    std::vector<Cta> ctas((size_t)K * G, Cta{});
-    for (uint32_t k = 0; k < K; ++k) {
-      const nqb_group* g = plan[k];
-      std::copy(g->ctas, g->ctas + g->grid, ctas.begin() + (size_t)k * G + (size_t)part[k] * Pn);
-      desc[k].ctas = d_ctas + (size_t)k * G;
+    if (!(ok && gq.fits)) {
+      for (auto* h : made) group_free(h);
+      continue;
     }
-    std::vector<uint32_t> flat;
-    PassParams& pp = P->params;
-    pp.list_off[0] = 0;
-    for (uint32_t i = 0; i < nsub; ++i) {
-      flat.insert(flat.end(), lists[i].begin(), lists[i].end());
-      pp.list_off[i + 1] = (uint32_t)flat.size();
+    nqb_pass* Pc_pass = build_with(ns, pl, gq, std::move(made));
+    if (!tune) {
+      best = Pc_pass;
+      break;
     }
-    NQB_CUDA(cudaMemsetAsync(d_ctr, 0, ctr_b + amax_b + arena_b, ctx->stream));
-    NQB_CUDA(cudaMemcpyAsync(d_desc, desc.data(), desc_b, cudaMemcpyHostToDevice, ctx->stream));
-    NQB_CUDA(cudaMemcpyAsync(d_ctas, ctas.data(), cta_b, cudaMemcpyHostToDevice, ctx->stream));
-    NQB_CUDA(cudaMemcpyAsync(d_list, flat.data(), list_b, cudaMemcpyHostToDevice, ctx->stream));
-    NQB_CUDA(cudaStreamSynchronize(ctx->stream));
-
-    pp.desc = d_desc;
-    pp.ctas = d_ctas;
-    pp.K = K;
-    pp.G = G;
-    pp.list = d_list;
-    pp.nsub = nsub;
-    pp.P = Pn;
-    pp.ctr = d_ctr;
-    pp.amax = d_amax;
-    pp.amax_words = amax_words;
-    pp.arena = d_arena;
-    pp.arena_len = arena;
-    pp.has_pre = has_pre ? 1 : 0;
-    pp.pre_units = 0;
-    for (uint32_t k = 0; k < K; ++k)
-      if (desc[k].flags & kStepXPre)
-        pp.pre_units = std::max<uint32_t>(pp.pre_units, ((desc[k].m + 7) / 8 + G - 1) / G);
-    pp.debug = env_u32p("NQB_PASS_DEBUG", 0);
-    pp.bslot1_bytes = geo.bslot1_b;
-    pp.bslot2_bytes = geo.bslot2_b;
-    pp.bs2_s1_off = geo.bs2_s1_off;
-    // Consumer warps per stage group.  Measured (tools/gpu_pass_ab.sh): an even
-    // 6 + 6 split is best when every step is small (7B: 886 vs 841 GB/s for 4 + 8),
-    // while a pass whose largest step puts > 96 KB of stage-2 bits on each CTA
-    // (70B gate/up: 169 KB) is bound by the stage-2 group, and 4 + 8 gives
-    // 1495 vs 1234 GB/s.
-    {
-      const uint32_t w1 = geo.max_s2_cta_bytes > 96u * 1024u ? 4u : 6u;
-      const uint32_t ew = env_u32p("NQB_PASS_WARPS1", 0);
-      pp.warps1 = ew == 3 || ew == 4 || ew == 6 ? ew : w1;  // the kernel is instantiated for 3, 4, 6
-      const uint32_t div = env_u32p("NQB_PASS_WAVE_DIV", pp.warps1 * geo.utot1 > 40u * 1024u ? 2u : 1u);
-      pp.wave_div = (div == 2 && pp.warps1 % 2 == 0) ? 2u : 1u;
-      const uint32_t div2 = env_u32p("NQB_PASS_WAVE_DIV2", geo.div2);
-      pp.wave_div2 = (div2 == 2 && (kConsumerWarps - pp.warps1) % 2 == 0) ? 2u : 1u;
+    float ms = 0.f;
+    try {
+      cudaEvent_t e0, e1;
+      NQB_CUDA(cudaEventCreate(&e0));
+      NQB_CUDA(cudaEventCreate(&e1));
+      pass_launch(ctx, Pc_pass, nullptr);
+      NQB_CUDA(cudaEventRecord(e0, ctx->stream));
+      pass_launch(ctx, Pc_pass, nullptr);
+      pass_launch(ctx, Pc_pass, nullptr);
+      NQB_CUDA(cudaEventRecord(e1, ctx->stream));
+      NQB_CUDA(cudaEventSynchronize(e1));
+      NQB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    } catch (...) {
+      pass_free(Pc_pass);
+      if (best) pass_free(best);
+      throw;
     }
-    pp.ring1_bytes = ring1;
-    pp.ring2_bytes = ring2;
-    // waves of GW / wave_div items (NQB_PASS_WAVE_DIV 1 or 2; 2 needs even groups)
-    pp.l2_ahead = std::min<uint32_t>(env_u32p("NQB_PASS_L2_AHEAD", 0), kDescSlots - 4);
-    P->smem_bytes = geo.fixed + rings;
-    if (env_u32p("NQB_PASS_VERBOSE", 0))
-      std::fprintf(stderr,
-                   "nqb pass: K=%u G=%u partitions=%u x %u smem=%u bslots=%ux(%u+%u) "
-                   "rings=%u+%u tile bytes=%u/%u waves=%u/%u warps1=%u\n",
-                   K, G, nsub, Pn, P->smem_bytes, kBSlots, geo.bslot1_b, geo.bslot2_b, ring1, ring2,
-                   geo.utot1, geo.utot2, pp.warps1 / pp.wave_div, (kConsumerWarps - pp.warps1) / pp.wave_div2,
-                   pp.warps1);
-    for (uint32_t k = 0; k < K; ++k) {
-      const uint32_t esz = steps[k].f32 ? 4 : 2;
-      P->x_dev.push_back(const_cast<void*>(steps[k].x));
-      P->x_bytes.push_back((size_t)desc[k].m * esz);
-      for (uint32_t q = 0; q < desc[k].nseg; ++q) {
-        P->y_dev.push_back(steps[k].y[q]);
-        P->y_bytes.push_back((size_t)desc[k].seg[q].n * esz);
-      }
+    if (verbose) std::fprintf(stderr, "nqb pass: %u partitions: %.1f us per launch\n", ns, ms * 500.f);
+    if (!best || ms < best_ms) {
+      if (best) pass_free(best);
+      best = Pc_pass;
+      best_ms = ms;
+    } else {
+      pass_free(Pc_pass);
     }
-    P->stream_bytes = stream_bytes;
-    P->algo_bytes = (uint64_t)algo;
-    for (auto fn : {k_decode_pass<false, 6>, k_decode_pass<true, 6>, k_decode_pass<false, 4>,
-                    k_decode_pass<true, 4>, k_decode_pass<false, 3>, k_decode_pass<true, 3>})
-      NQB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)P->smem_bytes));
-    int per_sm = 0;
-    NQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_pass<false, 6>,
-                                                           kPassThreads, P->smem_bytes));
-    NQB_REQUIRE(per_sm >= 1, NQB_E_INTERNAL, "decode pass kernel does not fit an SM");
-  } catch (...) {
-    pass_free(P);
-    throw;
   }
-  return P;
+  NQB_REQUIRE(best != nullptr, NQB_E_DIMENSION_MISMATCH,
+              "decode pass: no partition of the grid fits the steps' plans in shared memory");
+  return best;
 }
 
 void pass_launch(nqb_context* ctx, const nqb_pass* P, unsigned long long* trace) {

@@ -48,7 +48,7 @@ constexpr int kPassHelpers = 8;
 constexpr int kPassStamps = 24;  // trace stamps per step (16..21: consumer chunk-wait / run counters, per stage)
 constexpr int kMaxLookahead = 6;
 constexpr int kMaxSub = 16;      // SM partitions of a pass (independent steps run concurrently)
-constexpr uint32_t kPassMaxRt = 128;  // row tiles per CTA per stage in a partition's plan
+constexpr uint32_t kPassMaxRt = 1024;  // row tiles per CTA per stage in a partition's plan (no shared row sums)
 constexpr uint32_t kBSlotHead = 16;  // slot header: the two quantiser warps' sums of the values
 
 enum : uint32_t {
