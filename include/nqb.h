@@ -238,6 +238,18 @@ int nqb_pass_free(nqb_pass* pass);
  * host. */
 int nqb_pass_run_host(nqb_context* ctx, const nqb_pass* pass, const void* const* hx,
                       void* const* hy);
+/* The same with the host buffers bound once (a serving loop's pinned or
+ * registered token buffers): nqb_pass_io_create resolves every buffer's device
+ * alias and uploads the two copy lists; nqb_pass_io_run then moves the inputs,
+ * launches the pass and moves the outputs with three launches and one
+ * synchronisation, no per-call host work.  Every non-NULL buffer must be
+ * page-locked (cudaHostAlloc / torch pin_memory) or registered with
+ * nqb_host_register (NQB_E_VALIDATION otherwise: use nqb_pass_run_host). */
+typedef struct nqb_pass_io nqb_pass_io;
+int nqb_pass_io_create(nqb_context* ctx, const nqb_pass* pass, const void* const* hx,
+                       void* const* hy, nqb_pass_io** out);
+int nqb_pass_io_run(nqb_context* ctx, const nqb_pass_io* io);
+int nqb_pass_io_free(nqb_pass_io* io);
 /* Bits streamed per launch, and the algorithmic bytes of the pass: per layer
  * r(n+m)/8 + 2(n+m) scales + y, plus x once per step. */
 uint64_t nqb_pass_stream_bytes(const nqb_pass* pass);

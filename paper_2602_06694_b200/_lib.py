@@ -118,6 +118,9 @@ PROTOTYPES = {
     "nqb_pass_launch": (C.c_int, [P, P]),
     "nqb_pass_free": (C.c_int, [P]),
     "nqb_pass_run_host": (C.c_int, [P, P, P, P]),
+    "nqb_pass_io_create": (C.c_int, [P, P, P, P, P]),
+    "nqb_pass_io_run": (C.c_int, [P, P]),
+    "nqb_pass_io_free": (C.c_int, [P]),
     "nqb_pass_stream_bytes": (U64, [P]),
     "nqb_pass_algorithmic_bytes": (U64, [P]),
     "nqb_debug_pass_trace": (C.c_int, [P, P, P, PU32]),

@@ -905,6 +905,93 @@ int nqb_pass_free(nqb_pass* pass) {
 // every step, in step order) receives that layer's output, and the call returns
 // when the outputs are on the host.  Pinned host buffers make the copies
 // asynchronous DMA; pageable ones go through the driver's staging.
+}  // extern "C"
+
+// Bound host I/O of a pass (nqb_pass_io_*): the copy lists live on the device.
+struct nqb_pass_io {
+  int device = 0;
+  const nqb_pass* pass = nullptr;
+  nqb::CopyJob* d_in = nullptr;
+  nqb::CopyJob* d_out = nullptr;
+  uint32_t n_in = 0, n_out = 0;
+};
+
+extern "C" {
+
+int nqb_pass_io_create(nqb_context* ctx, const nqb_pass* pass, const void* const* hx,
+                       void* const* hy, nqb_pass_io** out) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_REQUIRE(pass != nullptr && out != nullptr, NQB_E_VALIDATION, "null argument");
+  NQB_REQUIRE(pass->device == ctx->device, NQB_E_VALIDATION, "decode pass lives on another device");
+  *out = nullptr;
+  std::vector<CopyJob> in, outj;
+  for (uint32_t k = 0; hx && k < pass->K; ++k) {
+    if (!hx[k]) continue;
+    void* mapped = host_alias(ctx, hx[k], pass->x_bytes[k]);
+    NQB_REQUIRE(mapped != nullptr, NQB_E_VALIDATION,
+                "pass io: host input is not page-locked or registered (use nqb_pass_run_host)");
+    in.push_back(CopyJob{pass->x_dev[k], mapped, pass->x_bytes[k]});
+  }
+  for (size_t i = 0; hy && i < pass->y_dev.size(); ++i) {
+    if (!hy[i]) continue;
+    void* mapped = host_alias(ctx, hy[i], pass->y_bytes[i]);
+    NQB_REQUIRE(mapped != nullptr, NQB_E_VALIDATION,
+                "pass io: host output is not page-locked or registered (use nqb_pass_run_host)");
+    outj.push_back(CopyJob{mapped, pass->y_dev[i], pass->y_bytes[i]});
+  }
+  auto* io = new nqb_pass_io();
+  io->device = ctx->device;
+  io->pass = pass;
+  try {
+    NQB_CUDA(cudaMalloc(&io->d_in, sizeof(CopyJob) * std::max<size_t>(in.size(), 1)));
+    NQB_CUDA(cudaMalloc(&io->d_out, sizeof(CopyJob) * std::max<size_t>(outj.size(), 1)));
+    if (!in.empty())
+      NQB_CUDA(cudaMemcpy(io->d_in, in.data(), sizeof(CopyJob) * in.size(), cudaMemcpyHostToDevice));
+    if (!outj.empty())
+      NQB_CUDA(cudaMemcpy(io->d_out, outj.data(), sizeof(CopyJob) * outj.size(), cudaMemcpyHostToDevice));
+  } catch (...) {
+    cudaFree(io->d_in);
+    cudaFree(io->d_out);
+    delete io;
+    throw;
+  }
+  io->n_in = (uint32_t)in.size();
+  io->n_out = (uint32_t)outj.size();
+  *out = io;
+  API_END
+}
+
+int nqb_pass_io_run(nqb_context* ctx, const nqb_pass_io* io) {
+  API_BEGIN
+  check_ctx(ctx);
+  NQB_REQUIRE(io != nullptr, NQB_E_VALIDATION, "null pass io");
+  NQB_REQUIRE(io->device == ctx->device, NQB_E_VALIDATION, "pass io lives on another device");
+  const uint32_t cap = 4u * (uint32_t)ctx->num_sms;
+  if (io->n_in) {
+    k_copy_jobs<<<std::min(io->n_in, cap), 256, 0, ctx->stream>>>(io->d_in, io->n_in);
+    NQB_LAUNCHED(ctx);
+  }
+  pass_launch(ctx, io->pass, nullptr);
+  if (io->n_out) {
+    k_copy_jobs<<<std::min(io->n_out, cap), 256, 0, ctx->stream>>>(io->d_out, io->n_out);
+    NQB_LAUNCHED(ctx);
+  }
+  NQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+int nqb_pass_io_free(nqb_pass_io* io) {
+  API_BEGIN
+  if (io) {
+    cudaSetDevice(io->device);
+    cudaFree(io->d_in);
+    cudaFree(io->d_out);
+    delete io;
+  }
+  API_END
+}
+
 int nqb_pass_run_host(nqb_context* ctx, const nqb_pass* pass, const void* const* hx,
                       void* const* hy) {
   API_BEGIN

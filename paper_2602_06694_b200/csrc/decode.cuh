@@ -174,7 +174,8 @@ namespace nqb {
 // decode-pass kernel only: row-tile blocks above kMaxRt and the pair-major
 // stream layout (k_relayout); group_gemv refuses it.
 nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_t count,
-                       uint32_t grid_cap = 0, uint32_t max_rt = 0, bool pass_only = false);
+                       uint32_t grid_cap = 0, uint32_t max_rt = 0, bool pass_only = false,
+                       uint32_t plan_slabs = 0);
 void group_free(nqb_group* g);
 // decode.cu
 void group_gemv(nqb_context* ctx, const nqb_group* g, const void* d_x, int x_f32,

@@ -160,7 +160,7 @@ inline void split_range(uint32_t total, uint32_t parts, uint32_t idx, uint32_t& 
 }  // namespace
 
 nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_t count,
-                       uint32_t grid_cap, uint32_t max_rt, bool pass_only) {
+                       uint32_t grid_cap, uint32_t max_rt, bool pass_only, uint32_t plan_slabs) {
   if (!max_rt) max_rt = kMaxRt;
   NQB_REQUIRE(count >= 1 && count <= (uint32_t)kMaxSeg, NQB_E_VALIDATION,
               "a decode group holds 1.." + std::to_string(kMaxSeg) + " layers");
@@ -213,7 +213,8 @@ nqb_group* group_build(nqb_context* ctx, const nqb_layer* const* layers, uint32_
   // (7B pass: 1274 vs 1231 GB/s for 8), 8 slabs above (70B pass: 1758 vs 1378 GB/s:
   // the smaller quantised-x staging leaves more shared memory to the rings)
   const uint32_t pass_slabs = std::min<uint32_t>(
-      std::max<uint32_t>(env_u32("NQB_PASS_PLAN_SLABS", m <= 4096 ? 16 : 8), 1), kMaxSlabs1);
+      std::max<uint32_t>(env_u32("NQB_PASS_PLAN_SLABS", plan_slabs ? plan_slabs : m <= 4096 ? 16 : 8), 1),
+      kMaxSlabs1);
   std::vector<Cta> ctas;
   for (;; ++G) {
     NQB_REQUIRE(G <= Gmax, NQB_E_DIMENSION_MISMATCH,

@@ -559,6 +559,42 @@ class DecodeGroup:
         _check(fn(self.ctx.handle, self.handle, C.c_void_p(x.data_ptr()), arr), "group gemv")
 
 
+class PassHostIO:
+    """Host buffers bound to a DecodePass (nqb_pass_io_create); run() is one pass
+    end to end (inputs up, the pass, outputs down, synchronous)."""
+
+    def __init__(self, dpass, xs, ys):
+        self.dpass, self.ctx = dpass, dpass.ctx
+        ny = sum(len(k[2]) for k in dpass._keep)
+        if len(xs) != dpass.steps or len(ys) != ny:
+            raise DimensionMismatch(f"host_io: {len(xs)} inputs / {len(ys)} outputs for "
+                                    f"{dpass.steps} steps / {ny} layers")
+        for (unit, x, outs), hxk in zip(dpass._keep, xs):
+            if hxk is not None and hxk.nbytes != x.numel() * x.element_size():
+                raise DimensionMismatch("host_io: host input size differs from the step input")
+        self._arrays = (list(xs), list(ys))  # keep the buffers alive while bound
+        hx = (C.c_void_p * len(xs))(*[None if x is None else x.ctypes.data for x in xs])
+        hy = (C.c_void_p * ny)(*[None if y is None else y.ctypes.data for y in ys])
+        h = C.c_void_p()
+        _check(self.ctx.lib.nqb_pass_io_create(self.ctx.handle, dpass.handle, hx, hy, C.byref(h)),
+               "nqb_pass_io_create")
+        self.handle = h
+
+    def run(self):
+        _check(self.ctx.lib.nqb_pass_io_run(self.ctx.handle, self.handle), "nqb_pass_io_run")
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.ctx.lib.nqb_pass_io_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 class DecodePass:
     """A whole decode pass as ONE launch of the persistent decode-pass kernel
     (nqb_pass).  `steps` is a list of (group_or_layer, x, ys):
@@ -623,6 +659,13 @@ class DecodePass:
         hy = (C.c_void_p * ny)(*[None if y is None else y.ctypes.data for y in ys])
         _check(self.ctx.lib.nqb_pass_run_host(self.ctx.handle, self.handle, hx, hy),
                "nqb_pass_run_host")
+
+    def host_io(self, xs, ys):
+        """Binds page-locked (pinned or registered) host buffers once, like
+        run_host's arguments; the returned PassHostIO.run() then moves the inputs,
+        runs the pass and moves the outputs with no per-call host work
+        (nqb_pass_io_*)."""
+        return PassHostIO(self, xs, ys)
 
     def launch(self):
         """Enqueues the pass on torch's current stream."""

@@ -259,3 +259,39 @@ def test_pass_run_host_registered_and_pageable_agree(nq, chk):
             for a in hx + hy:
                 ctx.unregister_host(a)
     p.free()
+
+
+def test_pass_host_io_bound_buffers(nq, chk):
+    """nqb_pass_io_*: pinned and registered host buffers bound once give the device
+    pass's outputs bit for bit on every run; pageable buffers are refused."""
+    import torch
+    rng = np.random.default_rng(34)
+    steps, host, keep = block_model(nq, rng, (1024, 2752, 400, 600), torch.float16, False)
+    p = nq.DecodePass(steps)
+    p.launch()
+    torch.cuda.synchronize()
+    want = [y.cpu().numpy().copy() for _, _, ys in steps for y in ys]
+    ctx = p.ctx
+    hx = [x.cpu().pin_memory().numpy() for _, x, _ in steps]
+    hy = [torch.empty(w.shape, dtype=torch.float16).pin_memory().numpy() for w in want]
+    io = p.host_io(hx, hy)
+    for _ in range(3):
+        for a in hy:
+            a[...] = 0
+        io.run()
+        for a, b in zip(hy, want):
+            assert np.array_equal(a.view(np.uint16), b.view(np.uint16))
+    io.close()
+    hxr = [x.cpu().numpy().copy() for _, x, _ in steps]  # pageable, then registered
+    with pytest.raises(nq.Error):
+        p.host_io(hxr, hy)
+    for a in hxr:
+        ctx.register_host(a)
+    io = p.host_io(hxr, hy)
+    io.run()
+    for a, b in zip(hy, want):
+        assert np.array_equal(a.view(np.uint16), b.view(np.uint16))
+    io.close()
+    for a in hxr:
+        ctx.unregister_host(a)
+    p.free()
