@@ -692,13 +692,13 @@ def main():
         extra["per_call_graph"] = per_call_graph_gbs(nq, ctx, torch, stream, pass_steps, step_bytes)
         achieved = step_bytes * args.steps / secs / 1e9
         traffic = None
-        tp = os.path.join(ROOT, "profiles", "r02b_decode_pass", "traffic.json")
+        tp = os.path.join(ROOT, "profiles", "r02c_decode_pass", "traffic.json")
         if os.path.exists(tp):  # ncu dram__bytes_read+write of one launch of this same pass
             traffic = json.load(open(tp))["dram_bytes_per_launch"]
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic,
                 "traffic_note": "ncu dram bytes of one k_decode_pass launch of this pass "
-                                "(profiles/r02b_decode_pass/traffic.json); algorithmic bytes per "
+                                "(profiles/r02c_decode_pass/traffic.json); algorithmic bytes per "
                                 "launch = algorithmic_bytes_per_step",
                 "peak_source": peak_kind,
                 "kernel": "nqb::dec::k_decode_pass (persistent decode pass: one launch per step, "
