@@ -947,8 +947,19 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       // NQB_PASS_RING1_PCT: stage-1 share of the rings in percent.  Default: the
       // stage-1 share of the bytes, at most 30 % (stage-1 waves are half the size of
       // stage-2 waves with the 4 + 8 split; 7B: 1700 vs 1668 GB/s)
+      // Stage-1 consumer warps and wave size (decided here: they size the rings).
+      // The split is 4 + 8 when the largest step puts more than 96 KB of stage-2
+      // bits on a CTA (measured, 70B: 1495 vs 1234 GB/s), else 6 + 6; stage-1 waves
+      // are halved when they pass 24 KB (7B, 8 KB tiles: 2059 vs 1967 GB/s with a
+      // 40 % stage-1 ring share; 70B's 4 KB tiles keep whole waves)
+      const uint32_t ew = env_u32p("NQB_PASS_WARPS1", 0);
+      const uint32_t warps1 = ew == 3 || ew == 4 || ew == 6 ? ew
+                              : geo.max_s2_cta_bytes > 96u * 1024u ? 4u : 6u;
+      const uint32_t div1e = env_u32p("NQB_PASS_WAVE_DIV", warps1 * geo.utot1 > 24u * 1024u ? 2u : 1u);
+      const uint32_t div1 = (div1e == 2 && warps1 % 2 == 0) ? 2u : 1u;
       const uint32_t r1pct = env_u32p("NQB_PASS_RING1_PCT", 0);
-      uint32_t ring1 = (uint32_t)(rings * (r1pct ? r1pct / 100.0 : std::min(f1, 0.30))) / 128 * 128;
+      const double share1 = r1pct ? r1pct / 100.0 : div1 == 2 ? 0.40 : std::min(f1, 0.30);
+      uint32_t ring1 = (uint32_t)(rings * share1) / 128 * 128;
       ring1 = std::min(std::max(ring1, geo.min1), rings - geo.min2);
       const uint32_t ring2 = rings - ring1;
 
@@ -1014,11 +1025,8 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       // (70B gate/up: 169 KB) is bound by the stage-2 group, and 4 + 8 gives
       // 1495 vs 1234 GB/s.
       {
-        const uint32_t w1 = geo.max_s2_cta_bytes > 96u * 1024u ? 4u : 6u;
-        const uint32_t ew = env_u32p("NQB_PASS_WARPS1", 0);
-        pp.warps1 = ew == 3 || ew == 4 || ew == 6 ? ew : w1;  // the kernel is instantiated for 3, 4, 6
-        const uint32_t div = env_u32p("NQB_PASS_WAVE_DIV", pp.warps1 * geo.utot1 > 40u * 1024u ? 2u : 1u);
-        pp.wave_div = (div == 2 && pp.warps1 % 2 == 0) ? 2u : 1u;
+        pp.warps1 = warps1;  // the kernel is instantiated for 3, 4 and 6
+        pp.wave_div = div1;
         const uint32_t div2 = env_u32p("NQB_PASS_WAVE_DIV2", geo.div2);
         pp.wave_div2 = (div2 == 2 && (kConsumerWarps - pp.warps1) % 2 == 0) ? 2u : 1u;
       }
