@@ -914,6 +914,7 @@ struct nqb_pass_io {
   nqb::CopyJob* d_in = nullptr;
   nqb::CopyJob* d_out = nullptr;
   uint32_t n_in = 0, n_out = 0;
+  void* d_desc = nullptr;  // descriptors with outputs redirected to mapped host memory (or null)
 };
 
 extern "C" {
@@ -933,12 +934,27 @@ int nqb_pass_io_create(nqb_context* ctx, const nqb_pass* pass, const void* const
                 "pass io: host input is not page-locked or registered (use nqb_pass_run_host)");
     in.push_back(CopyJob{pass->x_dev[k], mapped, pass->x_bytes[k]});
   }
-  for (size_t i = 0; hy && i < pass->y_dev.size(); ++i) {
-    if (!hy[i]) continue;
-    void* mapped = host_alias(ctx, hy[i], pass->y_bytes[i]);
-    NQB_REQUIRE(mapped != nullptr, NQB_E_VALIDATION,
-                "pass io: host output is not page-locked or registered (use nqb_pass_run_host)");
-    outj.push_back(CopyJob{mapped, pass->y_dev[i], pass->y_bytes[i]});
+  // Outputs no later step reads are written by the pass straight into the mapped
+  // host buffers (a patched copy of the step descriptors), overlapping the PCIe
+  // writes with the pass; the others come back through the copy kernel.
+  const bool direct = std::getenv("NQB_PASS_IO_DIRECT_Y") == nullptr ||
+                      std::strtoul(std::getenv("NQB_PASS_IO_DIRECT_Y"), nullptr, 10) != 0;
+  std::vector<uint8_t> patched = pass->desc_host;
+  auto* D = (dec::StepDesc*)patched.data();
+  bool any_direct = false;
+  for (uint32_t k = 0, i = 0; k < pass->K; ++k) {
+    for (uint32_t q = 0; q < D[k].nseg; ++q, ++i) {
+      if (!hy || !hy[i]) continue;
+      void* mapped = host_alias(ctx, hy[i], pass->y_bytes[i]);
+      NQB_REQUIRE(mapped != nullptr, NQB_E_VALIDATION,
+                  "pass io: host output is not page-locked or registered (use nqb_pass_run_host)");
+      if (direct && !(D[k].flags & dec::kStepPublish)) {
+        D[k].y[q] = mapped;
+        any_direct = true;
+      } else {
+        outj.push_back(CopyJob{mapped, pass->y_dev[i], pass->y_bytes[i]});
+      }
+    }
   }
   auto* io = new nqb_pass_io();
   io->device = ctx->device;
@@ -950,9 +966,14 @@ int nqb_pass_io_create(nqb_context* ctx, const nqb_pass* pass, const void* const
       NQB_CUDA(cudaMemcpy(io->d_in, in.data(), sizeof(CopyJob) * in.size(), cudaMemcpyHostToDevice));
     if (!outj.empty())
       NQB_CUDA(cudaMemcpy(io->d_out, outj.data(), sizeof(CopyJob) * outj.size(), cudaMemcpyHostToDevice));
+    if (any_direct) {
+      NQB_CUDA(cudaMalloc(&io->d_desc, patched.size()));
+      NQB_CUDA(cudaMemcpy(io->d_desc, patched.data(), patched.size(), cudaMemcpyHostToDevice));
+    }
   } catch (...) {
     cudaFree(io->d_in);
     cudaFree(io->d_out);
+    cudaFree(io->d_desc);
     delete io;
     throw;
   }
@@ -972,7 +993,7 @@ int nqb_pass_io_run(nqb_context* ctx, const nqb_pass_io* io) {
     k_copy_jobs<<<std::min(io->n_in, cap), 256, 0, ctx->stream>>>(io->d_in, io->n_in);
     NQB_LAUNCHED(ctx);
   }
-  pass_launch(ctx, io->pass, nullptr);
+  pass_launch(ctx, io->pass, nullptr, io->d_desc);
   if (io->n_out) {
     k_copy_jobs<<<std::min(io->n_out, cap), 256, 0, ctx->stream>>>(io->d_out, io->n_out);
     NQB_LAUNCHED(ctx);
@@ -987,6 +1008,7 @@ int nqb_pass_io_free(nqb_pass_io* io) {
     cudaSetDevice(io->device);
     cudaFree(io->d_in);
     cudaFree(io->d_out);
+    cudaFree(io->d_desc);
     delete io;
   }
   API_END

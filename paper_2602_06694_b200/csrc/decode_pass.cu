@@ -1052,6 +1052,7 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
         }
       }
       P->stream_bytes = stream_bytes;
+      P->desc_host.assign((const uint8_t*)desc.data(), (const uint8_t*)(desc.data() + K));
       P->algo_bytes = (uint64_t)algo;
       for (auto fn : {k_decode_pass<false, 6>, k_decode_pass<true, 6>, k_decode_pass<false, 4>,
                       k_decode_pass<true, 4>, k_decode_pass<false, 3>, k_decode_pass<true, 3>})
@@ -1163,9 +1164,11 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
   return best;
 }
 
-void pass_launch(nqb_context* ctx, const nqb_pass* P, unsigned long long* trace) {
+void pass_launch(nqb_context* ctx, const nqb_pass* P, unsigned long long* trace,
+                 const void* desc_override) {
   NQB_REQUIRE(P->device == ctx->device, NQB_E_VALIDATION, "decode pass lives on another device");
   PassParams pp = P->params;
+  if (desc_override) pp.desc = (const StepDesc*)desc_override;
   pp.trace = trace;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P->G);

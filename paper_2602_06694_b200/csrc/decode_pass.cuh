@@ -132,6 +132,7 @@ struct nqb_pass {
   std::vector<void*> x_dev, y_dev;
   std::vector<size_t> x_bytes, y_bytes;
   std::vector<nqb_group*> owned;  // partition plans built for this pass (freed with it)
+  std::vector<uint8_t> desc_host;  // the step descriptors as uploaded (nqb_pass_io patches y)
 };
 
 namespace nqb {
@@ -142,7 +143,10 @@ struct PassStepIn {
   int f32;
 };
 nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps);
-void pass_launch(nqb_context* ctx, const nqb_pass* p, unsigned long long* trace);
+// desc_override: a patched copy of the step descriptors (nqb_pass_io: outputs
+// written straight to mapped host memory), or null
+void pass_launch(nqb_context* ctx, const nqb_pass* p, unsigned long long* trace,
+                 const void* desc_override = nullptr);
 void pass_free(nqb_pass* p);
 uint32_t pass_trace_words(const nqb_pass* p);  // nqb_debug_pass_trace stamps
 }  // namespace nqb

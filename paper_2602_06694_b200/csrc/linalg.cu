@@ -728,10 +728,14 @@ static void launch_power_stream(nqb_context* ctx, PowerArgs& a, uint32_t grid) {
   // Row pairs per step (>= 2 slots: dispatch condition).  Three rows per step
   // (NQB_POWER_RS3=1, six slots) measured slower: 42.4k vs 39.2k cycles per
   // iteration at 4096^2 (registers: the 24 kept values spill).
+  // (only instantiated where it can run: CPT <= 8)
   const bool three = CPT <= 8 && nslots >= 6 && getenv_flag("NQB_POWER_RS3");
   nslots = three ? nslots / 3 * 3 : (nslots & ~1u);
   const size_t smem = (size_t)nslots * row_bytes;
-  auto kern = three ? k_power_stream<CPT, 3> : k_power_stream<CPT, 2>;
+  auto kern = k_power_stream<CPT, 2>;
+  if constexpr (CPT <= 8) {
+    if (three) kern = k_power_stream<CPT, 3>;
+  }
   NQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {&a, &nslots, (void*)&row_bytes};
   // grid_sync's monotonic counter must start at a multiple of this grid
