@@ -1057,7 +1057,7 @@ nqb_pass* pass_build(nqb_context* ctx, uint32_t K, const PassStepIn* steps) {
       for (auto fn : {k_decode_pass<false, 6>, k_decode_pass<true, 6>, k_decode_pass<false, 4>,
                       k_decode_pass<true, 4>, k_decode_pass<false, 3>, k_decode_pass<true, 3>})
         NQB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)P->smem_bytes));
+                                      227 * 1024));  // the ceiling: passes may be built concurrently
       int per_sm = 0;
       NQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_pass<false, 6>,
                                                              kPassThreads, P->smem_bytes));
