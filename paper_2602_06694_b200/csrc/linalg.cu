@@ -25,7 +25,13 @@
 #include "common.cuh"
 #include "tc_common.cuh"
 
+#include <mutex>
+
 namespace nqb {
+
+// serialises cudaFuncSetAttribute + launch of the power kernels across threads
+static std::mutex g_attr_mutex;
+
 
 void dgemm(nqb_context*, bool, bool, uint32_t, uint32_t, uint32_t, double, const double*,
            uint32_t, const double*, uint32_t, double, double*, uint32_t);
@@ -736,11 +742,11 @@ static void launch_power_stream(nqb_context* ctx, PowerArgs& a, uint32_t grid) {
   if constexpr (CPT <= 8) {
     if (three) kern = k_power_stream<CPT, 3>;
   }
-  // the attribute is per function, not per launch: set the ceiling (the same value
-  // from every thread), so concurrent contexts launching with different smem sizes
-  // never see a lower bound another thread just set (cudaErrorInvalidValue)
-  NQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-  (void)smem;
+  // the attribute is per function, not per launch: concurrent contexts (one per
+  // worker thread) must not set a smaller bound between another thread's set and
+  // its launch (cudaErrorInvalidValue), so set + launch hold one lock
+  std::lock_guard<std::mutex> attr_lock(g_attr_mutex);
+  NQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {&a, &nslots, (void*)&row_bytes};
   // grid_sync's monotonic counter must start at a multiple of this grid
   NQB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
@@ -761,11 +767,11 @@ template <int CPT, int RB, bool WSMEM>
 static void launch_power_t(nqb_context* ctx, PowerArgs& a, uint32_t grid) {
   const size_t smem = sizeof(double) * (a.cols + (WSMEM ? (size_t)CPT * PI_THREADS : 0));
   auto kern = k_power<CPT, RB, WSMEM>;
-  // the attribute is per function, not per launch: set the ceiling (the same value
-  // from every thread), so concurrent contexts launching with different smem sizes
-  // never see a lower bound another thread just set (cudaErrorInvalidValue)
-  NQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-  (void)smem;
+  // the attribute is per function, not per launch: concurrent contexts (one per
+  // worker thread) must not set a smaller bound between another thread's set and
+  // its launch (cudaErrorInvalidValue), so set + launch hold one lock
+  std::lock_guard<std::mutex> attr_lock(g_attr_mutex);
+  NQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {&a};
   // grid_sync's monotonic counter must start at a multiple of this grid
   NQB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
